@@ -1,0 +1,160 @@
+/*
+ * specmd_b200.h -- C ABI of the B200-native expert-cached MoE layer step.
+ *
+ * This is the drop-in boundary for the path the reference implements in
+ * pure Python (expertsim, /root/reference/pkg/src/expertsim):
+ *
+ *   reference symbol (file:line)                         replaced by
+ *   -----------------------------------------------------------------------
+ *   routing.softmax_rows / topk_indices / route_event     esim_router_launch
+ *     (routing.py:22-35, 109-161)
+ *   engine.Simulation._aggregate_demand (engine.py:578)   esim_router_launch
+ *   prefetch.predict_event (prefetch.py:67-107)           esim_router_launch
+ *   engine.Simulation.run / _run_layer / _handle_demand   esim_replay_launch
+ *     / _fetch / _submit_prefetches / _settle
+ *     (engine.py:422-748), eviction.* (eviction.py:29-294),
+ *     miss.resolve_miss (miss.py:82-140),
+ *     prefetch.watchdog_step (prefetch.py:163-221),
+ *     engine.CacheState / Channel (engine.py:188-370),
+ *     metrics.classify_miss (metrics.py:46-57)
+ *   engine.run_simulation (engine.py:751)                 esim_run_host
+ *   (no reference equivalent: the paper's real system)    esim_ffn_* /
+ *                                                         esim_layer_step_*
+ *
+ * Conventions: plain pointers and sizes, no torch types. Functions return
+ * 0 on success and a negative code on failure; esim_last_error() returns
+ * the thread-local message. Codes: -1 config (ConfigError), -2 runtime
+ * invariant (RuntimeError), -3 CUDA error, -4 capacity of an output buffer.
+ * Device pointers are marked d_; streams are cudaStream_t passed as void*.
+ */
+#ifndef SPECMD_B200_H
+#define SPECMD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- enums (strings in the reference) -------------------------------- */
+enum { ESIM_FP16 = 0, ESIM_INT8 = 1, ESIM_INT4 = 2, ESIM_INT2 = 3 };          /* models.py:21-26 */
+enum { ESIM_ROUTE_STANDARD = 0, ESIM_ROUTE_CACHE_AWARE = 1 };                  /* routing.py:16-17 */
+enum { ESIM_EV_LRU = 0, ESIM_EV_LFU, ESIM_EV_LHU, ESIM_EV_FLD, ESIM_EV_SB, ESIM_EV_LS }; /* eviction.py:297 */
+enum { ESIM_PF_NONE = 0, ESIM_PF_TOPK, ESIM_PF_SCORE, ESIM_PF_ORACLE };        /* prefetch.py:22-27 */
+enum { ESIM_MISS_FETCH = 0, ESIM_MISS_FETCH_LOW, ESIM_MISS_FETCH_PRIORITY,
+       ESIM_MISS_DROP, ESIM_MISS_SUBST };                                      /* miss.py:18-24 */
+enum { ESIM_REC_ACCESS = 1, ESIM_REC_EVICT, ESIM_REC_PREFETCH, ESIM_REC_PREDICTION,
+       ESIM_REC_ROUTE, ESIM_REC_PASS };                                        /* metrics.py:62-128 */
+
+#define ESIM_FLAG_FULL_LOG 1   /* emit every EsimRec (else counters + digest only) */
+#define ESIM_MAX_E 256         /* experts per layer supported by the device path */
+#define ESIM_MAX_K 16
+
+/* One simulation config, resolved to integers/doubles on the host
+ * (SimConfig engine.py:82-97 + HardwareSpec models.py:126-145 after
+ * resolve_capacity models.py:148-165). */
+typedef struct {
+    int32_t num_layers, experts, top_k, n_precisions;
+    int32_t precisions[4];        /* ladder, largest first (ModelSpec.precisions) */
+    int64_t expert_bytes[4];      /* by precision code; 0 = not available */
+    int64_t capacity_bytes;       /* resolved capacity */
+    int64_t bandwidth;            /* bytes/s; 0 = infinitely fast link */
+    int64_t compute_us;           /* per_layer_compute_us */
+    int32_t working_prec;
+    int32_t routing;
+    double  lam;
+    int32_t eviction;
+    int32_t prefetch;
+    double  sb_decay, overfetch, percentile;
+    int32_t miss;
+    int32_t drop_rank_threshold;
+    double  subst_tolerance, degrade_percentile;
+    int32_t flags;
+    int32_t trace_id;             /* which router/trace buffer set this point replays */
+} EsimConfig;                     /* 168 bytes */
+
+/* One event-log record, 64 bytes; field mapping per kind is documented in
+ * paper_2602_03921_b200/records.py:decode_records. */
+typedef struct {
+    int32_t kind, pass_id, layer, i0, i1, i2, i3, i4;
+    int64_t t0, t1, t2;
+    double  x0;
+} EsimRec;
+
+/* Report vector: everything metrics.build_report (metrics.py:190-316)
+ * needs, accumulated in log order. Per-layer counters live in a separate
+ * [L][ESIM_PL_FIELDS] int64 array. */
+typedef struct {
+    int64_t totals[15];           /* metrics.TOTAL_FIELDS order */
+    int64_t ttft_us, total_us, decode_us, sync_overhead_us, passes, decode_passes;
+    int64_t rows_total, faithful_rows, modified_rows;
+    int64_t pf_tp, pf_pred_total, pf_dem_total, pf_records, pf_empty, pf_prec_parts, pf_rec_parts;
+    int64_t ls_forced, ls_unforced, ls_refusals;
+    int64_t n_recs, n_pred_experts;
+    uint64_t digest;              /* FNV-1a over the canonical record stream */
+    double  original_mass, executed_mass, pf_prec_sum, pf_rec_sum;
+    int64_t status;               /* 0 ok, else negative error code */
+    int64_t pad[3];
+} EsimCounters;                   /* 360 bytes */
+
+#define ESIM_PL_FIELDS 10         /* demanded hits misses compulsory collision capacity dropped substituted pred_size_sum pred_count */
+
+/* Router output for one trace, policy independent under standard routing
+ * (SURVEY.md section 7 decision 2). Event ev = pass*L + layer. Buffers are
+ * sized by the caller: demands [n_events][E], rows [n_rows_total][K]. */
+typedef struct {
+    int32_t n_passes, num_layers, experts, top_k;
+    int64_t n_events, n_rows_total;
+    const int32_t *pass_tokens;   /* [n_passes] */
+    const int32_t *pass_kind;     /* [n_passes] 0 prefill 1 decode */
+    const int64_t *row_offset;    /* [n_events+1] first token row of each event */
+    const float   *logits;        /* [n_rows_total][E] */
+} EsimTraceDesc;
+
+typedef struct {
+    /* per event demand list, sorted (rank, -gate, expert)  engine.py:578-594 */
+    int32_t *n_dem;               /* [n_events] */
+    int32_t *dem_expert;          /* [n_events][E] */
+    int32_t *dem_rank;            /* [n_events][E] */
+    float   *dem_gate;            /* [n_events][E] */
+    double  *dem_summed;          /* [n_events][E] */
+    int32_t *dem_tokens;          /* [n_events][E] */
+    double  *sel_mass;            /* [n_events] sum of sum(weights) in row order */
+    /* per row top-k (selected == original under standard routing) */
+    int16_t *row_sel;             /* [n_rows_total][K] */
+    float   *row_w;               /* [n_rows_total][K] */
+    /* per event next-layer prediction when this event is the target (prefetch.py:67-107) */
+    int32_t *n_pred;              /* [n_events] */
+    int32_t *pred_expert;         /* [n_events][E] */
+    float   *pred_score;          /* [n_events][E] */
+    int32_t *pred_clamped;        /* [n_events] */
+} EsimRouterOut;
+
+const char *esim_last_error(void);
+int esim_version(void);
+
+/* Fused router over a whole trace (device buffers), one CTA per event. */
+int esim_router_launch(const EsimTraceDesc *d_trace_host_desc, const EsimRouterOut *d_out,
+                       int32_t pred_mode, double overfetch, double percentile, void *stream);
+
+/* Replay n grid points (d_cfg[n]) against router outputs; trace_id in each
+ * config indexes the arrays of descriptors. Outputs: d_counters[n],
+ * d_per_layer[n][L][ESIM_PL_FIELDS], and when ESIM_FLAG_FULL_LOG is set,
+ * d_recs[n][rec_cap] and d_pred_experts[n][pe_cap]. */
+int esim_replay_launch(const EsimConfig *d_cfg, int32_t n_points,
+                       const EsimTraceDesc *traces, const EsimRouterOut *routers, int32_t n_traces,
+                       EsimCounters *d_counters, int64_t *d_per_layer,
+                       EsimRec *d_recs, int64_t rec_cap, int32_t *d_pred_experts, int64_t pe_cap,
+                       void *stream);
+
+/* End-to-end host API (run_simulation): host trace + host configs in, host
+ * counters/records out; copies, router and replay on the device. */
+int esim_run_host(const EsimConfig *cfg, int32_t n_points,
+                  const EsimTraceDesc *traces, int32_t n_traces,
+                  EsimCounters *counters, int64_t *per_layer,
+                  EsimRec *recs, int64_t rec_cap, int32_t *pred_experts, int64_t pe_cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECMD_B200_H */

@@ -1,0 +1,121 @@
+"""Prefetcher plug-in surface (mirror of expertsim/prefetch.py:1-221).
+
+Prediction (topk / score-percentile / oracle over the NEXT layer's router
+scores, unioned over token rows) runs inside the fused router kernel
+(csrc/router.cu). The watchdog's two sweeps run inside the replay kernel
+(csrc/replay.cu). Prediction noise is host input preparation: it consumes
+numpy's PCG64 stream in the reference's order (prefetch.py:110-136,
+engine.py:661-666) and is applied to the device predictions before replay.
+"""
+from __future__ import annotations
+
+import math
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+
+from .models import ConfigError
+
+NONE = "none"
+TOPK = "topk"
+SCORE = "score"
+ORACLE = "oracle"
+PREFETCH_MODES = (NONE, TOPK, SCORE, ORACLE)
+PREFETCH_CODE = {m: i for i, m in enumerate(PREFETCH_MODES)}
+
+
+def nearest_rank_percentile(values, p: float) -> float:
+    """Nearest-rank percentile (prefetch.py:30-36)."""
+    if not 0.0 <= p < 100.0:
+        raise ConfigError(f"percentile must be in [0, 100), got {p}")
+    v = np.sort(np.asarray(values), kind="stable")
+    return float(v[max(1, math.ceil(p / 100.0 * v.shape[0])) - 1])
+
+
+def predict_event(next_logits, k: int, mode: str, overfetch: float = 1.0, percentile: float = 80.0):
+    """(predictions, clamped) for one event, computed on the device."""
+    if mode not in (TOPK, SCORE, ORACLE):
+        raise ConfigError(f"unknown prefetch mode {mode!r}")
+    if mode == TOPK and overfetch <= 0:
+        raise ConfigError(f"overfetch must be positive, got {overfetch}")
+    from . import _device
+    return _device.predict_event(np.asarray(next_logits, dtype=np.float32), k, mode, overfetch, percentile)
+
+
+def apply_prediction_noise(predictions, num_experts: int, noise: float, rng: np.random.Generator):
+    """Swap each prediction for a random unchosen expert with probability
+    `noise`; scores ride along; noise 0 draws nothing (prefetch.py:110-136)."""
+    if noise == 0.0 or not predictions:
+        return predictions
+    if not 0.0 <= noise <= 1.0:
+        raise ConfigError(f"prediction noise must be in [0, 1], got {noise}")
+    chosen = {e for e, _ in predictions}
+    out = []
+    for e, s in predictions:
+        if rng.random() < noise:
+            pool = [x for x in range(num_experts) if x not in chosen]
+            if pool:
+                pick = pool[rng.integers(len(pool))]
+                chosen.discard(e)
+                chosen.add(pick)
+                e = pick
+        out.append((e, s))
+    return out
+
+
+@dataclass
+class PrefetchRequest:
+    target_layer: int
+    expert: int
+    score: float
+    submit_us: int
+
+
+class PrefetchQueue:
+    """FIFO of submitted requests (prefetch.py:147-160)."""
+
+    def __init__(self) -> None:
+        self._q: deque = deque()
+
+    def submit(self, req: PrefetchRequest) -> None:
+        self._q.append(req)
+
+    def __len__(self) -> int:
+        return len(self._q)
+
+    def pop(self) -> PrefetchRequest:
+        return self._q.popleft()
+
+
+def noised_prediction_stream(offsets, experts, scores, clamped, num_layers: int, n_passes: int,
+                             num_experts: int, noise: float, seed: int):
+    """Apply prediction noise to a whole trace's prediction stream.
+
+    Inputs are the per-event predictions (event = pass*L + layer, each event
+    as a TARGET layer). The reference draws noise in submission order --
+    pass by pass, layer 0..L-2 predicting layer+1 -- from one
+    default_rng(seed) (engine.py:413, 653-666); this replays that order and
+    returns new (offsets, experts, scores, clamped) arrays.
+    """
+    rng = np.random.default_rng(seed)
+    n_events = num_layers * n_passes
+    out_e, out_s = [], []
+    new_off = np.zeros(n_events + 1, np.int32)
+    lists: dict = {}
+    for p in range(n_passes):
+        for layer in range(num_layers - 1):
+            ev = p * num_layers + layer + 1
+            a, b = int(offsets[ev]), int(offsets[ev + 1])
+            preds = [(int(experts[i]), float(scores[i])) for i in range(a, b)]
+            lists[ev] = apply_prediction_noise(preds, num_experts, noise, rng)
+    pos = 0
+    for ev in range(n_events):
+        new_off[ev] = pos
+        for e, s in lists.get(ev, []):
+            out_e.append(e)
+            out_s.append(s)
+            pos += 1
+    new_off[n_events] = pos
+    return (new_off, np.asarray(out_e, np.int32), np.asarray(out_s, np.float32),
+            np.asarray(clamped, np.int32).copy())
