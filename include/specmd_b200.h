@@ -133,25 +133,38 @@ typedef struct {
 const char *esim_last_error(void);
 int esim_version(void);
 
-/* Fused router over a whole trace (device buffers), one CTA per event. */
-int esim_router_launch(const EsimTraceDesc *d_trace_host_desc, const EsimRouterOut *d_out,
+/* Fused router over a whole trace: one CTA per event. `trace` and `out`
+ * are host structs holding DEVICE pointers. pred_mode/overfetch/percentile
+ * select the next-layer predictor (prefetch.py:67-107). */
+int esim_router_launch(const EsimTraceDesc *trace, const EsimRouterOut *out,
                        int32_t pred_mode, double overfetch, double percentile, void *stream);
 
-/* Replay n grid points (d_cfg[n]) against router outputs; trace_id in each
- * config indexes the arrays of descriptors. Outputs: d_counters[n],
- * d_per_layer[n][L][ESIM_PL_FIELDS], and when ESIM_FLAG_FULL_LOG is set,
- * d_recs[n][rec_cap] and d_pred_experts[n][pe_cap]. */
-int esim_replay_launch(const EsimConfig *d_cfg, int32_t n_points,
-                       const EsimTraceDesc *traces, const EsimRouterOut *routers, int32_t n_traces,
-                       EsimCounters *d_counters, int64_t *d_per_layer,
-                       EsimRec *d_recs, int64_t rec_cap, int32_t *d_pred_experts, int64_t pe_cap,
-                       void *stream);
+/* Plug-in kernels behind routing.softmax_rows / topk_indices (routing.py:22-35):
+ * one warp per row, numpy-exact. Device pointers. */
+int esim_softmax_launch(const float *d_x, int32_t rows, int32_t experts, float *d_out, void *stream);
+int esim_topk_launch(const float *d_scores, int32_t rows, int32_t experts, int32_t k, int32_t *d_idx, void *stream);
 
-/* End-to-end host API (run_simulation): host trace + host configs in, host
- * counters/records out; copies, router and replay on the device. */
-int esim_run_host(const EsimConfig *cfg, int32_t n_points,
-                  const EsimTraceDesc *traces, int32_t n_traces,
-                  EsimCounters *counters, int64_t *per_layer,
+/* Shared memory one replayed grid point needs (for the host's grouping). */
+int esim_replay_smem_per_point(const EsimConfig *h_cfg, int32_t n, int32_t max_tokens, int32_t pl_stride);
+
+/* Replay n grid points, one warp each. h_cfg/d_cfg: the same configs on
+ * host (launch sizing) and device; cfg.trace_id indexes d_traces/d_routers
+ * (device arrays of descriptors). Outputs (device): counters[n],
+ * per_layer[n][pl_stride][ESIM_PL_FIELDS], and with ESIM_FLAG_FULL_LOG,
+ * recs[n][rec_cap] + pred_experts[n][pe_cap]. max_tokens = largest token
+ * count of any event (cache-aware scratch). warps_per_cta 0 = auto. */
+int esim_replay_launch(const EsimConfig *h_cfg, const EsimConfig *d_cfg, int32_t n,
+                       const EsimTraceDesc *d_traces, const EsimRouterOut *d_routers, int32_t max_tokens,
+                       EsimCounters *d_counters, int64_t *d_per_layer, int32_t pl_stride,
+                       EsimRec *d_recs, int64_t rec_cap, int32_t *d_pred_experts, int64_t pe_cap,
+                       int32_t warps_per_cta, void *stream);
+
+/* End-to-end host API (engine.run_simulation over many configs): host
+ * traces (host pointers) and configs in; router + replay on the device;
+ * host counters/per-layer/records out. Synchronous. Configs sharing a
+ * trace_id must share the predictor (prefetch mode/overfetch/percentile). */
+int esim_run_host(const EsimConfig *cfg, int32_t n, const EsimTraceDesc *traces, int32_t n_traces,
+                  EsimCounters *counters, int64_t *per_layer, int32_t pl_stride,
                   EsimRec *recs, int64_t rec_cap, int32_t *pred_experts, int64_t pe_cap);
 
 #ifdef __cplusplus

@@ -1,0 +1,366 @@
+"""Device side of the host API: loads libspecmd_b200.so (in-tree, sm_100a)
+and drives the router and replay kernels through the C ABI.
+
+PyTorch is plumbing here: device memory (torch tensors), streams and
+events. All routing, directory, victim-selection and channel logic runs in
+the CUDA kernels. There is no CPU fallback: without the library or a GPU
+every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from .metrics import report_from_counters
+from .models import ConfigError
+from .prefetch import PREFETCH_CODE, noised_prediction_stream
+from .records import REC_DTYPE, decode_records
+from .routing import RoutingDecision
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libspecmd_b200.so")
+_lib = None
+
+
+def lib():
+    """The loaded C-ABI library (raises if missing: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2602_03921_b200.build` "
+                               "(the CUDA path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.esim_last_error.restype = C.c_char_p
+        L.esim_router_launch.argtypes = [vp, vp, i32, f64, f64, vp]
+        L.esim_replay_launch.argtypes = [vp, vp, i32, vp, vp, i32, vp, vp, i32, vp, i64, vp, i64, i32, vp]
+        L.esim_replay_smem_per_point.argtypes = [vp, i32, i32, i32]
+        L.esim_run_host.argtypes = [vp, i32, vp, i32, vp, vp, i32, vp, i64, vp, i64]
+        L.esim_softmax_launch.argtypes = [vp, i32, i32, vp, vp]
+        L.esim_topk_launch.argtypes = [vp, i32, i32, i32, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("the specmd_b200 device path needs a CUDA GPU (no CPU fallback)")
+    return torch
+
+
+def _check(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    msg = lib().esim_last_error().decode()
+    if rc == -1:
+        raise ConfigError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed ({rc}): {msg}")
+
+
+def _stream():
+    return _torch().cuda.current_stream().cuda_stream
+
+
+# ---------------------------------------------------------------------------
+# device-resident trace + router output
+# ---------------------------------------------------------------------------
+class DeviceTrace:
+    """A PackedTrace uploaded to HBM, plus its EsimTraceDesc."""
+
+    def __init__(self, pk, non_blocking: bool = False):
+        torch = _torch()
+        dev = torch.device("cuda")
+        self.pk = pk
+
+        def up(a):
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            if non_blocking:
+                t = t.pin_memory()
+            return t.to(dev, non_blocking=non_blocking)
+
+        self.pass_tokens = up(pk.pass_tokens)
+        self.pass_kind = up(pk.pass_kind)
+        self.row_offset = up(pk.row_offset)
+        self.logits = up(pk.logits)
+        self.desc = _abi.EsimTraceDesc(
+            pk.n_passes, pk.num_layers, pk.experts, pk.top_k, pk.n_events, int(pk.row_offset[-1]),
+            self.pass_tokens.data_ptr(), self.pass_kind.data_ptr(), self.row_offset.data_ptr(),
+            self.logits.data_ptr())
+        self.max_tokens = int(pk.pass_tokens.max()) if pk.n_passes else 0
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.pass_tokens, self.pass_kind, self.row_offset,
+                                                          self.logits))
+
+
+class RouterOut:
+    """Router output buffers for one DeviceTrace (EsimRouterOut)."""
+
+    FIELDS = ("n_dem", "dem_expert", "dem_rank", "dem_gate", "dem_summed", "dem_tokens", "sel_mass",
+              "row_sel", "row_w", "n_pred", "pred_expert", "pred_score", "pred_clamped")
+
+    def __init__(self, dt: DeviceTrace):
+        torch = _torch()
+        pk = dt.pk
+        ne, E, K, rows = pk.n_events, pk.experts, pk.top_k, int(pk.row_offset[-1])
+        z = lambda n, dt_: torch.empty(max(n, 1), dtype=dt_, device="cuda")  # noqa: E731
+        self.t = {
+            "n_dem": z(ne, torch.int32), "dem_expert": z(ne * E, torch.int32), "dem_rank": z(ne * E, torch.int32),
+            "dem_gate": z(ne * E, torch.float32), "dem_summed": z(ne * E, torch.float64),
+            "dem_tokens": z(ne * E, torch.int32), "sel_mass": z(ne, torch.float64),
+            "row_sel": z(rows * K, torch.int16), "row_w": z(rows * K, torch.float32),
+            "n_pred": z(ne, torch.int32), "pred_expert": z(ne * E, torch.int32),
+            "pred_score": z(ne * E, torch.float32), "pred_clamped": z(ne, torch.int32),
+        }
+        self.refresh()
+
+    def refresh(self) -> None:
+        self.desc = _abi.EsimRouterOut(*[self.t[f].data_ptr() for f in self.FIELDS])
+
+    def with_predictions(self, n_pred, pred_expert, pred_score, pred_clamped) -> "RouterOut":
+        """A copy sharing the demand stream but with host-supplied predictions."""
+        torch = _torch()
+        other = object.__new__(RouterOut)
+        other.t = dict(self.t)
+        other.t["n_pred"] = torch.from_numpy(np.ascontiguousarray(n_pred, np.int32)).cuda()
+        other.t["pred_expert"] = torch.from_numpy(np.ascontiguousarray(pred_expert, np.int32)).cuda()
+        other.t["pred_score"] = torch.from_numpy(np.ascontiguousarray(pred_score, np.float32)).cuda()
+        other.t["pred_clamped"] = torch.from_numpy(np.ascontiguousarray(pred_clamped, np.int32)).cuda()
+        other.refresh()
+        return other
+
+
+def route_trace(dt: DeviceTrace, prefetch: str, overfetch: float, percentile: float, stream=None) -> RouterOut:
+    """Launch the fused router kernel over every event of the trace."""
+    out = RouterOut(dt)
+    rc = lib().esim_router_launch(C.addressof(dt.desc), C.addressof(out.desc), PREFETCH_CODE[prefetch],
+                                  float(overfetch), float(percentile), stream or _stream())
+    _check(rc, "router")
+    return out
+
+
+def _noised(dt: DeviceTrace, ro: RouterOut, cfg) -> RouterOut:
+    """Apply numpy-PCG64 prediction noise (engine.py:661-666) to the device predictions."""
+    pk = dt.pk
+    E = pk.experts
+    n_pred = ro.t["n_pred"].cpu().numpy()[:pk.n_events]
+    pe = ro.t["pred_expert"].cpu().numpy()[:pk.n_events * E].reshape(pk.n_events, E)
+    ps = ro.t["pred_score"].cpu().numpy()[:pk.n_events * E].reshape(pk.n_events, E)
+    cl = ro.t["pred_clamped"].cpu().numpy()[:pk.n_events]
+    off = np.zeros(pk.n_events + 1, np.int32)
+    np.cumsum(n_pred, out=off[1:])
+    flat_e = np.concatenate([pe[i, :n_pred[i]] for i in range(pk.n_events)]) if pk.n_events else pe[:0, 0]
+    flat_s = np.concatenate([ps[i, :n_pred[i]] for i in range(pk.n_events)]) if pk.n_events else ps[:0, 0]
+    noff, ne_, ns_, ncl = noised_prediction_stream(off, flat_e, flat_s, cl, pk.num_layers, pk.n_passes, E,
+                                                   cfg.prefetch_noise, cfg.seed)
+    npred = np.diff(noff).astype(np.int32)
+    pe2 = np.zeros((pk.n_events, E), np.int32)
+    ps2 = np.zeros((pk.n_events, E), np.float32)
+    for i in range(pk.n_events):
+        pe2[i, :npred[i]] = ne_[noff[i]:noff[i + 1]]
+        ps2[i, :npred[i]] = ns_[noff[i]:noff[i + 1]]
+    return ro.with_predictions(npred, pe2.ravel(), ps2.ravel(), ncl)
+
+
+# ---------------------------------------------------------------------------
+# replay
+# ---------------------------------------------------------------------------
+@dataclass
+class SimResult:
+    report: dict
+    log: list | None
+    counters: object
+    per_layer: np.ndarray
+
+
+def rec_capacity(pk) -> tuple[int, int]:
+    rows = int(pk.row_offset[-1])
+    return 64 + pk.n_events * (6 + 12 * pk.experts) + rows * pk.top_k * 2, pk.n_events * pk.experts
+
+
+class ReplayBatch:
+    """A set of grid points staged on the device for (repeated) replay.
+
+    Points are grouped by model geometry so each launch sizes shared memory
+    for its own model; groups run back to back on one stream."""
+
+    def __init__(self, cfgs, traces, full_log: bool = False, stream=None):
+        torch = _torch()
+        self.cfgs, self.traces, self.full_log = list(cfgs), list(traces), full_log
+        self.dtraces: dict = {}
+        self.stream = stream
+        streams = {}
+        for cfg, tr in zip(self.cfgs, self.traces):
+            key = id(tr)
+            if key not in self.dtraces:
+                self.dtraces[key] = DeviceTrace(tr.packed())
+            skey = (key, cfg.prefetch, cfg.overfetch, cfg.percentile,
+                    (cfg.prefetch_noise, cfg.seed) if cfg.prefetch != "none" and cfg.prefetch_noise > 0 else None)
+            if skey not in streams:
+                dt = self.dtraces[key]
+                ro = route_trace(dt, cfg.prefetch, cfg.overfetch, cfg.percentile, stream)
+                if skey[4] is not None:
+                    ro = _noised(dt, ro, cfg)
+                streams[skey] = (len(streams), dt, ro)
+        self.sets = list(streams.values())
+        torch.cuda.synchronize()
+        self.d_traces = self._blob([s[1].desc for s in self.sets])
+        self.d_routers = self._blob([s[2].desc for s in self.sets])
+        skeys = list(streams.keys())
+        self.ccfg = []
+        for cfg, tr in zip(self.cfgs, self.traces):
+            skey = (id(tr), cfg.prefetch, cfg.overfetch, cfg.percentile,
+                    (cfg.prefetch_noise, cfg.seed) if cfg.prefetch != "none" and cfg.prefetch_noise > 0 else None)
+            self.ccfg.append(cfg.to_c(skeys.index(skey), full_log))
+        n = len(self.ccfg)
+        self.Lmax = max(c.num_layers for c in self.ccfg)
+        groups: dict = {}
+        for i, c in enumerate(self.ccfg):
+            groups.setdefault((c.num_layers, c.experts), []).append(i)
+        self.groups = list(groups.values())
+        self.order = [i for g in self.groups for i in g]
+        harr = (_abi.EsimConfig * n)(*[self.ccfg[i] for i in self.order])
+        self.h_cfg = harr
+        self.d_cfg = torch.frombuffer(bytearray(harr), dtype=torch.uint8).cuda()
+        self.counters = torch.zeros(n * C.sizeof(_abi.EsimCounters), dtype=torch.uint8, device="cuda")
+        self.per_layer = torch.zeros(n * self.Lmax * _abi.ESIM_PL_FIELDS, dtype=torch.int64, device="cuda")
+        self.max_tokens = max(s[1].max_tokens for s in self.sets)
+        if full_log:
+            caps = [rec_capacity(s[1].pk) for s in self.sets]
+            self.rec_cap = max(c[0] for c in caps)
+            self.pe_cap = max(c[1] for c in caps)
+            self.recs = torch.zeros(n * self.rec_cap * 64, dtype=torch.uint8, device="cuda")
+            self.pexp = torch.zeros(n * self.pe_cap, dtype=torch.int32, device="cuda")
+        else:
+            self.rec_cap = self.pe_cap = 0
+            self.recs = self.pexp = None
+
+    @staticmethod
+    def _blob(structs):
+        torch = _torch()
+        raw = b"".join(bytes(s) for s in structs)
+        return torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
+
+    def launch(self, stream=None, warps_per_cta: int = 0) -> None:
+        st = stream or self.stream or _stream()
+        csz = C.sizeof(_abi.EsimConfig)
+        cntsz = C.sizeof(_abi.EsimCounters)
+        base = 0
+        for g in self.groups:
+            n = len(g)
+            hptr = C.addressof(self.h_cfg) + base * csz
+            rc = lib().esim_replay_launch(
+                hptr, self.d_cfg.data_ptr() + base * csz, n, self.d_traces.data_ptr(), self.d_routers.data_ptr(),
+                self.max_tokens, self.counters.data_ptr() + base * cntsz,
+                self.per_layer.data_ptr() + base * self.Lmax * _abi.ESIM_PL_FIELDS * 8, self.Lmax,
+                self.recs.data_ptr() + base * self.rec_cap * 64 if self.full_log else None, self.rec_cap,
+                self.pexp.data_ptr() + base * self.pe_cap * 4 if self.full_log else None, self.pe_cap,
+                warps_per_cta, st)
+            _check(rc, "replay")
+            base += n
+
+    def results(self) -> list:
+        """Counters / per-layer / logs back to host, in the caller's point order."""
+        torch = _torch()
+        torch.cuda.synchronize()
+        n = len(self.ccfg)
+        raw = self.counters.cpu().numpy().tobytes()
+        cs = [_abi.EsimCounters.from_buffer_copy(raw[i * 360:(i + 1) * 360]) for i in range(n)]
+        pl = self.per_layer.cpu().numpy().reshape(n, self.Lmax, _abi.ESIM_PL_FIELDS)
+        if self.full_log:
+            recs = self.recs.cpu().numpy().view(REC_DTYPE).reshape(n, self.rec_cap)
+            pexp = self.pexp.cpu().numpy().reshape(n, self.pe_cap)
+        out = [None] * n
+        for pos, i in enumerate(self.order):
+            c = cs[pos]
+            if c.status != 0:
+                code = int(c.status)
+                if code == -1:
+                    raise ConfigError("replay: an expert exceeds the cache capacity")
+                raise RuntimeError(f"replay failed on point {i} (status {code})")
+            cfg = self.cfgs[i]
+            L = cfg.model.num_layers
+            log = decode_records(recs[pos][:c.n_recs], pexp[pos]) if self.full_log else None
+            rep = report_from_counters(cfg.echo(), L, cfg.hardware.per_layer_compute_us, c, pl[pos][:L])
+            out[i] = SimResult(rep, log, c, pl[pos][:L].copy())
+        return out
+
+
+def run_simulations(cfgs, traces, full_log: bool = False) -> list:
+    """Replay each (config, trace) pair on the device; results in input order."""
+    from .engine import check_geometry
+    for cfg, tr in zip(cfgs, traces):
+        check_geometry(cfg, tr)
+    b = ReplayBatch(cfgs, traces, full_log=full_log)
+    b.launch()
+    return b.results()
+
+
+# ---------------------------------------------------------------------------
+# plug-in functions (routing / prefetch) on the device
+# ---------------------------------------------------------------------------
+def softmax(x: np.ndarray) -> np.ndarray:
+    torch = _torch()
+    if x.ndim == 1:
+        x = x[None, :]
+    d = torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+    out = torch.empty_like(d)
+    _check(lib().esim_softmax_launch(d.data_ptr(), x.shape[0], x.shape[1], out.data_ptr(), _stream()), "softmax")
+    return out.cpu().numpy()
+
+
+def topk(scores: np.ndarray, k: int) -> list:
+    torch = _torch()
+    s = np.ascontiguousarray(np.asarray(scores, np.float32).reshape(1, -1))
+    d = torch.from_numpy(s).cuda()
+    idx = torch.empty(k, dtype=torch.int32, device="cuda")
+    _check(lib().esim_topk_launch(d.data_ptr(), 1, s.shape[1], k, idx.data_ptr(), _stream()), "topk")
+    return [int(i) for i in idx.cpu().numpy()]
+
+
+def _single_event_trace(logits: np.ndarray, k: int):
+    from .models import ModelSpec
+    from .trace import _from_packed
+    x = np.ascontiguousarray(logits, np.float32)
+    if x.ndim == 1:
+        x = x[None, :]
+    spec = ModelSpec("event", 1, x.shape[1], k, 1)
+    return _from_packed(spec, [x.shape[0]], [0], x, {})
+
+
+def route_event(logits, k, policy, lam, cached, delta, layer) -> list:
+    if policy != "standard":
+        raise NotImplementedError("standalone cache-aware route_event: use Simulation (replay kernel routes it)")
+    tr = _single_event_trace(logits, k)
+    dt = DeviceTrace(tr.packed())
+    ro = route_trace(dt, "none", 1.0, 80.0)
+    rows = int(tr.packed().row_offset[-1])
+    sel = ro.t["row_sel"].cpu().numpy()[:rows * k].reshape(rows, k)
+    w = ro.t["row_w"].cpu().numpy()[:rows * k].reshape(rows, k)
+    out = []
+    for r in range(rows):
+        idx = [int(i) for i in sel[r]]
+        ws = [float(v) for v in w[r]]
+        out.append(RoutingDecision(idx, ws, list(idx), list(ws), False))
+    return out
+
+
+def predict_event(next_logits, k, mode, overfetch, percentile):
+    tr = _single_event_trace(next_logits, k)
+    dt = DeviceTrace(tr.packed())
+    ro = route_trace(dt, mode, overfetch, percentile)
+    E = dt.pk.experts
+    n = int(ro.t["n_pred"].cpu().numpy()[0])
+    pe = ro.t["pred_expert"].cpu().numpy()[:n]
+    ps = ro.t["pred_score"].cpu().numpy()[:n]
+    clamped = bool(ro.t["pred_clamped"].cpu().numpy()[0]) if mode == "topk" else False
+    if mode == "topk":
+        clamped = math.ceil(k * overfetch) > E
+    return [(int(e), float(s)) for e, s in zip(pe, ps)], clamped

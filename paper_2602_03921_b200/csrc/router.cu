@@ -1,0 +1,282 @@
+// router.cu -- fused router kernel: softmax + stable top-k routing, demand
+// aggregation and the next-layer prefetch predictor, one CTA per trace
+// event, one warp per token row.
+//
+// Reference computation (all bit-exact):
+//   routing.softmax_rows / topk_indices / route_event   routing.py:22-35, 109-142
+//   engine.Simulation._aggregate_demand                 engine.py:578-594
+//   RouteRec selected/original mass (builtin sum)       engine.py:630-631
+//   prefetch.predict_event (topk / score / oracle)      prefetch.py:39-107
+// The output is policy independent under standard routing, so one launch
+// serves every replayed grid point of the trace.
+//
+// HBM roofline: each event reads T*E*4 B of logits once and writes
+// T*k*6 B of selections plus <= E demand / prediction records.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/specmd_b200.h"
+#include "numpy_f32.cuh"
+
+namespace esim {
+
+struct RouterArgs {
+    EsimTraceDesc tr;
+    EsimRouterOut out;
+    int pred_mode;      // ESIM_PF_*
+    int pred_count;     // topk predictor: min(ceil(k*overfetch), E)
+    int pred_clamped;   // topk predictor: ceil(k*overfetch) > E
+    int pct_rank;       // score predictor: nearest rank (1-based), host-computed in double
+};
+
+constexpr int kRouterWarps = 8;
+
+// warp argmax over the row in smem, ties to the lower index; `taken` is the
+// per-lane bitmask of already-chosen elements (element i owned by lane i%32,
+// bit i/32). Returns the winning index (uniform across the warp).
+__device__ __forceinline__ int warp_argmax(const float* s, int E, int lane, uint32_t taken) {
+    float bv = -1.0f;
+    int bi = 0x7fffffff;
+    for (int i = lane, j = 0; i < E; i += 32, j++) {
+        if (taken & (1u << j)) continue;
+        float v = s[i];
+        if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    }
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    return bi;
+}
+
+__global__ void __launch_bounds__(kRouterWarps * 32)
+router_kernel(RouterArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int E = a.tr.experts, K = a.tr.top_k;
+    const int64_t ev = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* rowbuf = reinterpret_cast<float*>(smem) + warp * E;             // [warps][E]
+    unsigned* best = reinterpret_cast<unsigned*>(smem) + kRouterWarps * E;  // [E] prediction union
+    int* cnt = reinterpret_cast<int*>(best + E);                            // [2]
+
+    const int64_t r0 = a.tr.row_offset[ev], r1 = a.tr.row_offset[ev + 1];
+    const int T = (int)(r1 - r0);
+    for (int i = threadIdx.x; i < E; i += blockDim.x) best[i] = 0u;
+    if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
+    __syncthreads();
+
+    const int nsel = a.pred_mode == ESIM_PF_TOPK ? max(K, a.pred_count) : K;
+    for (int r = warp; r < T; r += kRouterWarps) {
+        const float* x = a.tr.logits + (r0 + r) * (int64_t)E;
+        float m = -__int_as_float(0x7f800000);
+        for (int i = lane; i < E; i += 32) { float v = x[i]; rowbuf[i] = v; m = fmaxf(m, v); }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        for (int i = lane; i < E; i += 32) rowbuf[i] = np_expf(__fsub_rn(rowbuf[i], m));
+        __syncwarp();
+        float S = __fadd_rn(0.0f, warp_pw_sum(rowbuf, E, lane));
+        __syncwarp();
+        for (int i = lane; i < E; i += 32) rowbuf[i] = __fdiv_rn(rowbuf[i], S);
+        __syncwarp();
+
+        // stable top-nsel: repeated warp argmax (score desc, index asc)
+        uint32_t taken = 0;
+        int16_t* sel = a.out.row_sel + (r0 + r) * K;
+        float* w = a.out.row_w + (r0 + r) * K;
+        for (int j = 0; j < nsel; j++) {
+            int b = warp_argmax(rowbuf, E, lane, taken);
+            if ((b & 31) == lane) taken |= 1u << (b >> 5);
+            if (lane == 0) {
+                if (j < K) { sel[j] = (int16_t)b; w[j] = rowbuf[b]; }
+                bool pred = (a.pred_mode == ESIM_PF_TOPK && j < a.pred_count) ||
+                            (a.pred_mode == ESIM_PF_ORACLE && j < K);
+                if (pred) atomicMax(&best[b], __float_as_uint(rowbuf[b]) + 1u);
+            }
+        }
+        if (a.pred_mode == ESIM_PF_SCORE) {
+            // nearest-rank percentile: the value at sorted position pct_rank-1
+            float thr = 0.0f;
+            bool found = false;
+            for (int i = lane; i < E; i += 32) {
+                float v = rowbuf[i];
+                int less = 0, le = 0;
+                for (int j = 0; j < E; j++) { float u = rowbuf[j]; less += (u < v); le += (u <= v); }
+                if (less <= a.pct_rank - 1 && a.pct_rank - 1 < le) { thr = v; found = true; }
+            }
+            unsigned who = __ballot_sync(0xffffffffu, found);
+            thr = __shfl_sync(0xffffffffu, thr, __ffs(who) - 1);
+            for (int i = lane; i < E; i += 32)
+                if (rowbuf[i] > thr) atomicMax(&best[i], __float_as_uint(rowbuf[i]) + 1u);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // ---- predictions for this event as a target: sort (-score, expert) ----
+    const int64_t eb = ev * E;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        unsigned ke = best[e];
+        if (!ke) continue;
+        int pos = 0;
+        for (int j = 0; j < E; j++) {
+            unsigned kj = best[j];
+            pos += (kj > ke) || (kj == ke && kj && j < e);
+        }
+        a.out.pred_expert[eb + pos] = e;
+        a.out.pred_score[eb + pos] = __uint_as_float(ke - 1u);
+        atomicAdd(&cnt[0], 1);
+    }
+
+    // ---- demand aggregation (engine.py:578-594) -------------------------
+    // pass 1: per expert best (lowest) rank and max gate -> smem (reuses the
+    // row buffers); pass 2: sort key (rank, -gate, expert) -> position, and
+    // the row-ordered fp64 sum (plain +=, engine.py:592) + token count.
+    __syncthreads();
+    float* gate_s = reinterpret_cast<float*>(smem);
+    int* rank_s = reinterpret_cast<int*>(smem) + E;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        int rank = 0x7fffffff;
+        float gate = -1.0f;
+        for (int r = 0; r < T; r++) {
+            const int16_t* sel = a.out.row_sel + (r0 + r) * K;
+            for (int j = 0; j < K; j++)
+                if (sel[j] == e) {
+                    rank = min(rank, j + 1);
+                    gate = fmaxf(gate, a.out.row_w[(r0 + r) * K + j]);
+                }
+        }
+        gate_s[e] = gate;
+        rank_s[e] = rank;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const int rk = rank_s[e];
+        if (rk == 0x7fffffff) continue;
+        const float g = gate_s[e];
+        int pos = 0;
+        for (int j = 0; j < E; j++) {
+            int rj = rank_s[j];
+            if (rj == 0x7fffffff || j == e) continue;
+            float gj = gate_s[j];
+            pos += (rj < rk) || (rj == rk && (gj > g || (gj == g && j < e)));
+        }
+        int tok = 0;
+        double summed = 0.0;
+        for (int r = 0; r < T; r++) {
+            const int16_t* sel = a.out.row_sel + (r0 + r) * K;
+            for (int j = 0; j < K; j++)
+                if (sel[j] == e) {
+                    double wv = (double)a.out.row_w[(r0 + r) * K + j];
+                    summed = tok ? __dadd_rn(summed, wv) : wv;
+                    tok++;
+                }
+        }
+        a.out.dem_expert[eb + pos] = e;
+        a.out.dem_rank[eb + pos] = rk;
+        a.out.dem_gate[eb + pos] = g;
+        a.out.dem_summed[eb + pos] = summed;
+        a.out.dem_tokens[eb + pos] = tok;
+        atomicAdd(&cnt[1], 1);
+    }
+    __syncthreads();
+
+    // ---- RouteRec mass: sum(sum(dec.weights) for dec) with builtin sum ---
+    if (threadIdx.x == 0) {
+        PySum outer;
+        outer.init();
+        for (int r = 0; r < T; r++) {
+            PySum in;
+            in.init();
+            for (int j = 0; j < K; j++) in.add((double)a.out.row_w[(r0 + r) * K + j]);
+            outer.add(in.value());
+        }
+        a.out.sel_mass[ev] = outer.value();
+        a.out.n_pred[ev] = cnt[0];
+        a.out.n_dem[ev] = cnt[1];
+        a.out.pred_clamped[ev] = (a.pred_mode == ESIM_PF_TOPK) ? a.pred_clamped : 0;
+    }
+}
+
+}  // namespace esim
+
+// host launcher (declared in capi.cu)
+cudaError_t esim_router_launch_impl(const EsimTraceDesc& tr, const EsimRouterOut& out, int pred_mode,
+                                    int pred_count, int pred_clamped, int pct_rank, cudaStream_t st) {
+    esim::RouterArgs a{tr, out, pred_mode, pred_count, pred_clamped, pct_rank};
+    size_t smem = (size_t)(esim::kRouterWarps * tr.experts + tr.experts) * 4 + 16;
+    if (tr.n_events == 0) return cudaSuccess;
+    esim::router_kernel<<<(unsigned)tr.n_events, esim::kRouterWarps * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// standalone plug-in kernels: routing.softmax_rows and routing.topk_indices
+// (routing.py:22-35) over a (rows, E) matrix, one warp per row
+// ---------------------------------------------------------------------------
+namespace esim {
+__global__ void softmax_rows_kernel(const float* __restrict__ x, int rows, int E, float* __restrict__ out) {
+    extern __shared__ float sbuf[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (r >= rows) return;
+    float* buf = sbuf + warp * E;
+    float m = -__int_as_float(0x7f800000);
+    for (int i = lane; i < E; i += 32) { float v = x[(int64_t)r * E + i]; buf[i] = v; m = fmaxf(m, v); }
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int i = lane; i < E; i += 32) buf[i] = np_expf(__fsub_rn(buf[i], m));
+    __syncwarp();
+    float S = __fadd_rn(0.0f, warp_pw_sum(buf, E, lane));
+    for (int i = lane; i < E; i += 32) out[(int64_t)r * E + i] = __fdiv_rn(buf[i], S);
+}
+
+__global__ void topk_rows_kernel(const float* __restrict__ s, int rows, int E, int k, int32_t* __restrict__ idx) {
+    extern __shared__ float sbuf[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (r >= rows) return;
+    float* buf = sbuf + warp * E;
+    for (int i = lane; i < E; i += 32) buf[i] = s[(int64_t)r * E + i];
+    __syncwarp();
+    uint32_t taken = 0;
+    for (int j = 0; j < k; j++) {
+        // stable argsort of -scores: larger first, ties to the lower index;
+        // NaN-free inputs assumed (router scores)
+        float bv = -__int_as_float(0x7f800000);
+        int bi = 0x7fffffff;
+        for (int i = lane, t = 0; i < E; i += 32, t++) {
+            if (taken & (1u << t)) continue;
+            float v = buf[i];
+            if (bi == 0x7fffffff || v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+        }
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        if (lane == 0) idx[(int64_t)r * k + j] = bi;
+    }
+}
+}  // namespace esim
+
+extern "C" int esim_softmax_launch(const float* d_x, int32_t rows, int32_t E, float* d_out, void* stream) {
+    if (E < 1 || E > ESIM_MAX_E) return -1;
+    int wpb = 4;
+    int blocks = (rows + wpb - 1) / wpb;
+    if (blocks == 0) return 0;
+    esim::softmax_rows_kernel<<<blocks, wpb * 32, wpb * E * 4, (cudaStream_t)stream>>>(d_x, rows, E, d_out);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+extern "C" int esim_topk_launch(const float* d_s, int32_t rows, int32_t E, int32_t k, int32_t* d_idx, void* stream) {
+    if (E < 1 || E > ESIM_MAX_E || k < 1 || k > E) return -1;
+    int wpb = 4;
+    int blocks = (rows + wpb - 1) / wpb;
+    if (blocks == 0) return 0;
+    esim::topk_rows_kernel<<<blocks, wpb * 32, wpb * E * 4, (cudaStream_t)stream>>>(d_s, rows, E, k, d_idx);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
