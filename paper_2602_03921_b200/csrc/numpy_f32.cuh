@@ -67,15 +67,16 @@ __device__ __forceinline__ float warp_pw_block(const float* a, int n, int lane) 
     return res;
 }
 
-// full recursive pairwise sum (n up to 1024), whole warp participates
-__device__ inline float warp_pw_sum(const float* a, int n, int lane) {
+// numpy pairwise sum for n <= 256 (ESIM_MAX_E): blocks of <= 128 are
+// summed directly; larger n split once at n2 = n/2 - (n/2)%8 (numpy's
+// recursion, which never nests deeper for n <= 256). No recursion on the
+// device: the stack size stays statically known.
+__device__ __forceinline__ float warp_pw_sum(const float* a, int n, int lane) {
     if (n <= 128) return warp_pw_block(a, n, lane);
-    // explicit stack over the numpy recursion: n2 = n/2 - (n/2)%8
-    // n <= 1024 -> at most 3 levels; emulate with small recursion
     int n2 = n / 2;
     n2 -= n2 % 8;
-    float lo = warp_pw_sum(a, n2, lane);
-    float hi = warp_pw_sum(a + n2, n - n2, lane);
+    float lo = warp_pw_block(a, n2, lane);
+    float hi = warp_pw_block(a + n2, n - n2, lane);
     return __fadd_rn(lo, hi);
 }
 

@@ -763,13 +763,9 @@ __device__ int warp_topk(const float* s, int E, int K, int lane, int16_t* out) {
     return 0;
 }
 
-// numpy DOUBLE_pairwise_sum of one float32 row cast to float64 (lanes 0..7 accumulate)
-__device__ double warp_pw_sum_f64(const float* a, int n, int lane) {
-    if (n > 128) {
-        int n2 = n / 2;
-        n2 -= n2 % 8;
-        return __dadd_rn(warp_pw_sum_f64(a, n2, lane), warp_pw_sum_f64(a + n2, n - n2, lane));
-    }
+// numpy DOUBLE_pairwise_sum of one float32 row cast to float64 (lanes 0..7
+// accumulate); n <= 256 splits at most once, so no recursion.
+__device__ __forceinline__ double warp_pw_block_f64(const float* a, int n, int lane) {
     if (n < 8) {
         double res = 0.0;
         for (int i = 0; i < n; i++) res = __dadd_rn(res, (double)a[i]);
@@ -787,6 +783,13 @@ __device__ double warp_pw_sum_f64(const float* a, int n, int lane) {
     double res = __shfl_sync(FULL, r, 0);
     for (int i = lim; i < n; i++) res = __dadd_rn(res, (double)a[i]);
     return res;
+}
+
+__device__ __forceinline__ double warp_pw_sum_f64(const float* a, int n, int lane) {
+    if (n <= 128) return warp_pw_block_f64(a, n, lane);
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(warp_pw_block_f64(a, n2, lane), warp_pw_block_f64(a + n2, n - n2, lane));
 }
 
 __device__ int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int64_t rows_before) {
