@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""Benchmark: policy-replay accesses/s of the expert-cache layer step on B200.
+
+Workload (one "step", per rank): the BASELINE.json configs[4] policy sweep
+-- {lru, lfu, ls} x {1, 5, 25 %} x {1, 5, 25 GB/s} x {olmoe, mixtral,
+qwen15moe, phi35moe}, score:80 prefetch, fetch, int4 -- replayed over
+`--seeds` synthetic 64+64 traces per model (reference generator defaults,
+affinity 0.6, skew 1.0). Rank r takes seeds r*S+1 .. r*S+S (weak scaling);
+for N > 1 the fixed-size result records are all-gathered over NCCL inside
+the step. A step = fused router kernel over every trace + replay kernel
+over every grid point (one warp each), inputs resident in HBM.
+
+value    = demanded accesses (all ranks) / step time (max over ranks)
+e2e      = the same through the C ABI (esim_run_host) with host buffers:
+           trace H2D, router, replay, counters D2H, inside the timed region
+roofline = replay kernel: 48 B algorithmic per demanded access (SURVEY.md
+           section 8(d)) / its CUDA-event time vs measured HBM peak
+cpu_baseline / --impl reference = the C oracle (oracle/, a restatement of
+           the reference simulator) on this box's host cores
+
+Also reported: `layer_step` (physical OLMoE bf16 prefill+decode with the
+0.6 GB cache, configs[1]) when --layer-step is given or by default at N=1.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "OLMoE TTFT + expert-cache hit rate at 5% capacity; policy-replay accesses/s"
+MODELS = ("olmoe", "mixtral", "qwen15moe", "phi35moe")
+REPLAY_BYTES_PER_ACCESS = 48   # demand rec + slot read/write + event rec
+
+
+def env_int(name, default):
+    return int(os.environ.get(name, default))
+
+
+def make_traces(seeds):
+    from paper_2602_03921_b200.models import builtin_spec
+    from paper_2602_03921_b200.trace import generate_synthetic
+    return {m: [generate_synthetic(builtin_spec(m), seed=s, prefill_tokens=64, decode_tokens=64,
+                                   affinity=0.6, skew=1.0) for s in seeds] for m in MODELS}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(seeds, threads):
+    """The C oracle (restated reference simulator) on host cores."""
+    from oracle import oracle
+    tr = make_traces(seeds)
+    from paper_2602_03921_b200.sweep import c5_points
+    cfgs, trs = c5_points(tr)
+    ids, tl, cc = {}, [], []
+    for c, t in zip(cfgs, trs):
+        if id(t) not in ids:
+            ids[id(t)] = len(tl)
+            tl.append(t)
+        cc.append(c.to_c(ids[id(t)], False))
+    t0 = time.perf_counter()
+    cs, _ = oracle.run_batch(cc, tl, threads)
+    dt = time.perf_counter() - t0
+    acc = sum(int(c.totals[0]) for c in cs)
+    return acc, dt, cs
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port of the reference's CPU simulator, all host threads."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    seeds = list(range(1, args.seeds + 1))
+    for _ in range(args.warmup):
+        cpu_baseline(seeds[:1], threads)
+    times, acc = [], 0
+    for _ in range(args.steps):
+        acc, dt, _ = cpu_baseline(seeds, threads)
+        times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = acc / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "accesses/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64+f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "c5_policy_sweep_replay", "models": list(MODELS), "grid": "3x3x3 per model",
+                       "seeds": args.seeds, "points": 108 * args.seeds},
+            "cpu_baseline": {"value": value, "unit": "accesses/s", "cores": threads, "kind": "port",
+                             "sample": f"C5 grid x {args.seeds} seeds ({acc} demanded accesses) per step"},
+            "e2e": {"value": value, "unit": "accesses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--seeds", type=int, default=48, help="traces per model per rank")
+    ap.add_argument("--cpu-seeds", type=int, default=8, help="cpu_baseline sample (1 thread)")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2602_03921_b200 import build as _build
+    from paper_2602_03921_b200.sweep import DeviceSweep, c5_points, run_grid_host
+    _build.build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    seeds = list(range(rank * args.seeds + 1, rank * args.seeds + args.seeds + 1))
+    traces = make_traces(seeds)
+    cfgs, trs = c5_points(traces)
+    ds = DeviceSweep(cfgs, trs)
+    n_pts = len(cfgs)
+    cnt = ds.counters_tensor()
+    gathered = torch.empty(world * cnt.numel(), dtype=torch.uint8, device="cuda") if world > 1 else None
+
+    def step():
+        ds.route()
+        ds.replay()
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, cnt)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()                       # L2 flush between steps (untimed)
+            e = ev[k]
+            e[0].record()
+            ds.route()
+            e[1].record()
+            ds.replay()
+            e[2].record()
+            if world > 1:
+                dist.all_gather_into_tensor(gathered, cnt)
+            e[3].record()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    replay_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    route_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    res = ds.results()
+    acc_local = sum(int(r.counters.totals[0]) for r in res)
+    digests = [int(r.counters.digest) for r in res]
+    ms = sum(step_ms) / len(step_ms)
+    t = torch.tensor([ms, float(acc_local)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms, acc_all = float(tmax[0]), float(tsum[1])
+    else:
+        acc_all = float(acc_local)
+    value = acc_all / (ms / 1e3)
+
+    # ---- e2e through the C ABI with host buffers ------------------------
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(max(1, args.warmup)):
+            run_grid_host(cfgs, trs)
+        h2d = sum(t.packed().logits.nbytes + t.packed().row_offset.nbytes + t.packed().pass_tokens.nbytes * 2
+                  for t in {id(x): x for x in trs}.values()) + 168 * n_pts
+        d2h = n_pts * (360 + max(c.model.num_layers for c in cfgs) * 80)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            cs, _ = run_grid_host(cfgs, trs)
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / args.steps
+        e2e_match = [int(c.digest) for c in cs] == digests
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": acc_all / (float(te[0]) / 1e3), "unit": "accesses/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": float(te[0]), "digests_match_device_path": e2e_match}
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    peaks, peak_kind = measured_peaks()
+    rms = sum(replay_ms) / len(replay_ms)
+    achieved = REPLAY_BYTES_PER_ACCESS * acc_local / (rms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "replay_traffic.json")) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    except OSError:
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": "accesses/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64+f32", "data": "synthetic",
+        "config": {"workload": "c5_policy_sweep_replay", "models": list(MODELS),
+                   "grid": "eviction{lru,lfu,ls} x capacity{0.01,0.05,0.25} x bandwidth{1,5,25}GB/s",
+                   "policy": "score:80 + fetch + int4", "traces": "64 prefill + 64 decode, affinity 0.6 skew 1.0",
+                   "seeds_per_rank": args.seeds, "points_per_rank": n_pts, "parallelism": f"grid-shard x{world}",
+                   "l2": "flushed between steps (256 MiB memset, untimed)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "kernel": "replay_kernel", "algorithmic_bytes_per_access": REPLAY_BYTES_PER_ACCESS,
+                     "peak_source": peak_kind},
+        "gpu_launches": args.steps * (ds.n_router_launches + ds.n_replay_launches),
+        "kernel_ms": {"router": sum(route_ms) / len(route_ms), "replay": rms},
+        "wall_s_timed_region": t_wall,
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1:
+        cs_seeds = list(range(1, args.cpu_seeds + 1))
+        acc_c, dt_c, ccs = cpu_baseline(cs_seeds, 1)
+        line["cpu_baseline"] = {"value": acc_c / dt_c, "unit": "accesses/s", "cores": 1, "kind": "port",
+                                "sample": f"C5 grid x {args.cpu_seeds} seeds ({acc_c} accesses), "
+                                          f"C oracle single thread, {dt_c:.1f} s"}
+        # parity spot check: device digests vs oracle on the shared seeds
+        nshared = min(args.cpu_seeds, args.seeds)
+        dev_by = {}
+        for c, r in zip(cfgs, res):
+            dev_by.setdefault(c.model.name, []).append(int(r.counters.digest))
+        line["parity"] = {"points_checked": 108 * nshared,
+                          "digest_mismatches": _count_mismatch(cfgs, digests, ccs, args.seeds, args.cpu_seeds)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _count_mismatch(cfgs, dev_digests, oracle_counters, dev_seeds, cpu_seeds):
+    # both lists are in c5_points order: model-major, seed, then the 27-point grid
+    bad = 0
+    n = min(dev_seeds, cpu_seeds)
+    for mi in range(len(MODELS)):
+        for s in range(n):
+            for g in range(27):
+                d = dev_digests[(mi * dev_seeds + s) * 27 + g]
+                o = int(oracle_counters[(mi * cpu_seeds + s) * 27 + g].digest)
+                bad += d != o
+    return bad
+
+
+if __name__ == "__main__":
+    main()

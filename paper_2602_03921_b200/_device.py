@@ -208,7 +208,8 @@ class ReplayBatch:
                 ro = route_trace(dt, cfg.prefetch, cfg.overfetch, cfg.percentile, stream)
                 if skey[4] is not None:
                     ro = _noised(dt, ro, cfg)
-                streams[skey] = (len(streams), dt, ro)
+                streams[skey] = (len(streams), dt, ro, (cfg.prefetch, cfg.overfetch, cfg.percentile),
+                                 skey[4] is not None)
         self.sets = list(streams.values())
         torch.cuda.synchronize()
         self.d_traces = self._blob([s[1].desc for s in self.sets])

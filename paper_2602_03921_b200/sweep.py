@@ -1,0 +1,160 @@
+"""Policy-sweep replay: many grid points over shared traces, on 1..N GPUs.
+
+The reference runs a sweep as a process pool of independent simulations
+(cli.py:424-495, grid order = itertools.product of the axes with the last
+axis fastest, cli.py:446). Here every grid point is one warp of the replay
+kernel, all points of a model share one router pass over their trace, and
+N GPUs each replay a contiguous, cost-balanced block of the grid; the
+fixed-size result records are gathered to rank 0 with one NCCL all-gather.
+
+Two entry points:
+  run_grid_host(cfgs, traces)    the C-ABI end-to-end call (esim_run_host):
+                                 host trace buffers in, host reports out
+  DeviceSweep                    device-resident staging for repeated runs
+                                 (the bench's timed loop)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import replace
+from itertools import product
+
+import numpy as np
+
+from . import _abi
+from .engine import SimConfig, check_geometry
+from .metrics import flatten_report, report_from_counters
+from .models import GB, ConfigError, HardwareSpec, builtin_spec
+
+# BASELINE.json configs[4] / SURVEY.md section 8(d) C5
+C5_MODELS = ("olmoe", "mixtral", "qwen15moe", "phi35moe")
+C5_EVICTIONS = ("lru", "lfu", "ls")
+C5_CAPACITIES = (0.01, 0.05, 0.25)
+C5_BANDWIDTHS = (1 * GB, 5 * GB, 25 * GB)
+
+
+def grid(model: str, evictions=C5_EVICTIONS, capacities=C5_CAPACITIES, bandwidths=C5_BANDWIDTHS,
+         **fixed) -> list:
+    """SimConfigs in cli.py:446 product order (eviction, capacity, bandwidth; last fastest)."""
+    spec = builtin_spec(model)
+    base = dict(working_precision="int4", prefetch="score", percentile=80.0, miss="fetch", seed=0)
+    base.update(fixed)
+    out = []
+    for ev, cap, bw in product(evictions, capacities, bandwidths):
+        hw = HardwareSpec(capacity_fraction=cap, bandwidth_bytes_per_sec=bw)
+        out.append(SimConfig(model=spec, hardware=hw, eviction=ev, **base))
+    return out
+
+
+def c5_points(traces_by_model: dict) -> tuple[list, list]:
+    """The 108-point C5 grid (x len(traces) per model): parallel lists of configs and traces."""
+    cfgs, trs = [], []
+    for m in C5_MODELS:
+        for tr in traces_by_model[m]:
+            g = grid(m)
+            cfgs += g
+            trs += [tr] * len(g)
+    return cfgs, trs
+
+
+def shard_bounds(costs: list, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block of points for `rank`, balanced by cumulative cost."""
+    total = float(sum(costs))
+    cum = np.concatenate([[0.0], np.cumsum(costs)])
+    lo = int(np.searchsorted(cum, total * rank / world, side="left"))
+    hi = int(np.searchsorted(cum, total * (rank + 1) / world, side="left"))
+    if rank == world - 1:
+        hi = len(costs)
+    return lo, hi
+
+
+# ---------------------------------------------------------------------------
+def _lib():
+    from ._device import lib
+    return lib()
+
+
+def run_grid_host(cfgs, traces, pl_stride: int | None = None):
+    """One end-to-end C-ABI call (esim_run_host): host buffers in and out.
+
+    Returns (counters list, per_layer array [n][pl_stride][ESIM_PL_FIELDS]).
+    Configs that share a trace object must share the predictor; prediction
+    noise is not supported on this path (use engine.Simulation)."""
+    if any(c.prefetch != "none" and c.prefetch_noise > 0 for c in cfgs):
+        raise ConfigError("run_grid_host: prediction noise needs the Simulation path")
+    ids, descs, keep = {}, [], []
+    ccfg = []
+    for cfg, tr in zip(cfgs, traces):
+        check_geometry(cfg, tr)
+        key = (id(tr), cfg.prefetch, cfg.overfetch, cfg.percentile)
+        if key not in ids:
+            ids[key] = len(descs)
+            d, k = _abi.trace_desc_host(tr.packed())
+            descs.append(d)
+            keep.append(k)
+        ccfg.append(cfg.to_c(ids[key], False))
+    n = len(ccfg)
+    L = pl_stride or max(c.num_layers for c in ccfg)
+    carr = (_abi.EsimConfig * n)(*ccfg)
+    darr = (_abi.EsimTraceDesc * len(descs))(*descs)
+    counters = (_abi.EsimCounters * n)()
+    per_layer = np.zeros((n, L, _abi.ESIM_PL_FIELDS), np.int64)
+    rc = _lib().esim_run_host(C.addressof(carr), n, C.addressof(darr), len(descs), C.addressof(counters),
+                              per_layer.ctypes.data, L, None, 0, None, 0)
+    if rc != 0:
+        msg = _lib().esim_last_error().decode()
+        if rc == -1:
+            raise ConfigError(msg)
+        raise RuntimeError(f"esim_run_host failed ({rc}): {msg}")
+    return list(counters), per_layer
+
+
+def reports(cfgs, counters, per_layer) -> list:
+    return [report_from_counters(c.echo(), c.model.num_layers, c.hardware.per_layer_compute_us, k,
+                                 per_layer[i][:c.model.num_layers])
+            for i, (c, k) in enumerate(zip(cfgs, counters))]
+
+
+def csv_rows(cfgs, counters, per_layer) -> list:
+    return [flatten_report(r) for r in reports(cfgs, counters, per_layer)]
+
+
+# ---------------------------------------------------------------------------
+class DeviceSweep:
+    """Grid points staged in HBM; `step()` = router over every trace +
+    replay of every point (one warp each), all on one stream."""
+
+    def __init__(self, cfgs, traces):
+        from ._device import ReplayBatch
+        self.cfgs, self.traces = list(cfgs), list(traces)
+        self.batch = ReplayBatch(self.cfgs, self.traces, full_log=False)
+
+    def route(self, stream=None) -> None:
+        from ._device import PREFETCH_CODE, _check, lib
+        for _, dt, ro, (mode, over, pct), noised in self.batch.sets:
+            if noised:
+                raise ConfigError("DeviceSweep.route: noised prediction streams are host-prepared")
+            rc = lib().esim_router_launch(C.addressof(dt.desc), C.addressof(ro.desc), PREFETCH_CODE[mode],
+                                          float(over), float(pct), stream)
+            _check(rc, "router")
+
+    def replay(self, stream=None) -> None:
+        self.batch.launch(stream)
+
+    def step(self, stream=None) -> None:
+        self.route(stream)
+        self.replay(stream)
+
+    @property
+    def n_router_launches(self) -> int:
+        return len(self.batch.sets)
+
+    @property
+    def n_replay_launches(self) -> int:
+        return len(self.batch.groups)
+
+    def counters_tensor(self):
+        return self.batch.counters
+
+    def results(self) -> list:
+        return self.batch.results()
