@@ -47,6 +47,7 @@ enum { ESIM_REC_ACCESS = 1, ESIM_REC_EVICT, ESIM_REC_PREFETCH, ESIM_REC_PREDICTI
        ESIM_REC_ROUTE, ESIM_REC_PASS };                                        /* metrics.py:62-128 */
 
 #define ESIM_FLAG_FULL_LOG 1   /* emit every EsimRec (else counters + digest only) */
+#define ESIM_FLAG_NO_DIGEST 2  /* skip the record-stream digest (counters only) */
 #define ESIM_MAX_E 256         /* experts per layer supported by the device path */
 #define ESIM_MAX_K 16
 
@@ -145,19 +146,23 @@ int esim_softmax_launch(const float *d_x, int32_t rows, int32_t experts, float *
 int esim_topk_launch(const float *d_scores, int32_t rows, int32_t experts, int32_t k, int32_t *d_idx, void *stream);
 
 /* Shared memory one replayed grid point needs (for the host's grouping). */
-int esim_replay_smem_per_point(const EsimConfig *h_cfg, int32_t n, int32_t max_tokens, int32_t pl_stride);
+int esim_replay_smem_per_point(const EsimConfig *h_cfg, int32_t n, int32_t max_tokens, int32_t pl_stride,
+                               int32_t queue_cap);
 
 /* Replay n grid points, one warp each. h_cfg/d_cfg: the same configs on
  * host (launch sizing) and device; cfg.trace_id indexes d_traces/d_routers
  * (device arrays of descriptors). Outputs (device): counters[n],
  * per_layer[n][pl_stride][ESIM_PL_FIELDS], and with ESIM_FLAG_FULL_LOG,
  * recs[n][rec_cap] + pred_experts[n][pe_cap]. max_tokens = largest token
- * count of any event (cache-aware scratch). warps_per_cta 0 = auto. */
+ * count of any event (cache-aware scratch). warps_per_cta 0 = auto.
+ * queue_cap: channel ring entries; 0 = default (64), -1 = exact bound
+ * (resident slots + 1). A point whose channel outgrows the ring stops with
+ * counters.status = -5; the caller re-launches it with queue_cap = -1. */
 int esim_replay_launch(const EsimConfig *h_cfg, const EsimConfig *d_cfg, int32_t n,
                        const EsimTraceDesc *d_traces, const EsimRouterOut *d_routers, int32_t max_tokens,
                        EsimCounters *d_counters, int64_t *d_per_layer, int32_t pl_stride,
                        EsimRec *d_recs, int64_t rec_cap, int32_t *d_pred_experts, int64_t pe_cap,
-                       int32_t warps_per_cta, void *stream);
+                       int32_t warps_per_cta, int32_t queue_cap, void *stream);
 
 /* End-to-end host API (engine.run_simulation over many configs): host
  * traces (host pointers) and configs in; router + replay on the device;

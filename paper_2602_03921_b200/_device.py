@@ -23,7 +23,7 @@ from .records import REC_DTYPE, decode_records
 from .routing import RoutingDecision
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libspecmd_b200.so")
+LIB_PATH = os.environ.get("ESIM_LIB") or os.path.join(HERE, "lib", "libspecmd_b200.so")
 _lib = None
 
 
@@ -38,8 +38,8 @@ def lib():
         vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
         L.esim_last_error.restype = C.c_char_p
         L.esim_router_launch.argtypes = [vp, vp, i32, f64, f64, vp]
-        L.esim_replay_launch.argtypes = [vp, vp, i32, vp, vp, i32, vp, vp, i32, vp, i64, vp, i64, i32, vp]
-        L.esim_replay_smem_per_point.argtypes = [vp, i32, i32, i32]
+        L.esim_replay_launch.argtypes = [vp, vp, i32, vp, vp, i32, vp, vp, i32, vp, i64, vp, i64, i32, i32, vp]
+        L.esim_replay_smem_per_point.argtypes = [vp, i32, i32, i32, i32]
         L.esim_run_host.argtypes = [vp, i32, vp, i32, vp, vp, i32, vp, i64, vp, i64]
         L.esim_softmax_launch.argtypes = [vp, i32, i32, vp, vp]
         L.esim_topk_launch.argtypes = [vp, i32, i32, i32, vp, vp]
@@ -191,7 +191,7 @@ class ReplayBatch:
     Points are grouped by model geometry so each launch sizes shared memory
     for its own model; groups run back to back on one stream."""
 
-    def __init__(self, cfgs, traces, full_log: bool = False, stream=None):
+    def __init__(self, cfgs, traces, full_log: bool = False, stream=None, digest: bool = True):
         torch = _torch()
         self.cfgs, self.traces, self.full_log = list(cfgs), list(traces), full_log
         self.dtraces: dict = {}
@@ -219,7 +219,10 @@ class ReplayBatch:
         for cfg, tr in zip(self.cfgs, self.traces):
             skey = (id(tr), cfg.prefetch, cfg.overfetch, cfg.percentile,
                     (cfg.prefetch_noise, cfg.seed) if cfg.prefetch != "none" and cfg.prefetch_noise > 0 else None)
-            self.ccfg.append(cfg.to_c(skeys.index(skey), full_log))
+            cc = cfg.to_c(skeys.index(skey), full_log)
+            if not digest:
+                cc.flags |= _abi.ESIM_FLAG_NO_DIGEST
+            self.ccfg.append(cc)
         n = len(self.ccfg)
         self.Lmax = max(c.num_layers for c in self.ccfg)
         groups: dict = {}
@@ -249,13 +252,30 @@ class ReplayBatch:
         raw = b"".join(bytes(s) for s in structs)
         return torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
 
-    def launch(self, stream=None, warps_per_cta: int = 0) -> None:
-        st = stream or self.stream or _stream()
+    def launch(self, stream=None, warps_per_cta: int = 0, queue_cap: int = 0) -> None:
+        """Replay every group; groups run concurrently on forked streams
+        (each group's launch sizes shared memory for its own model)."""
+        torch = _torch()
+        cur = torch.cuda.current_stream() if stream is None else stream
+        st_handle = cur.cuda_stream if hasattr(cur, "cuda_stream") else cur
+        if not hasattr(self, "_streams"):
+            self._streams = [torch.cuda.Stream() for _ in self.groups]
+            self._fork = torch.cuda.Event()
+            self._joins = [torch.cuda.Event() for _ in self.groups]
+        single = len(self.groups) == 1 or not hasattr(cur, "cuda_stream")
+        if not single:
+            self._fork.record(cur)
         csz = C.sizeof(_abi.EsimConfig)
         cntsz = C.sizeof(_abi.EsimCounters)
         base = 0
-        for g in self.groups:
+        for gi, g in enumerate(self.groups):
             n = len(g)
+            if single:
+                sh = st_handle
+            else:
+                gs = self._streams[gi]
+                gs.wait_event(self._fork)
+                sh = gs.cuda_stream
             hptr = C.addressof(self.h_cfg) + base * csz
             rc = lib().esim_replay_launch(
                 hptr, self.d_cfg.data_ptr() + base * csz, n, self.d_traces.data_ptr(), self.d_routers.data_ptr(),
@@ -263,9 +283,13 @@ class ReplayBatch:
                 self.per_layer.data_ptr() + base * self.Lmax * _abi.ESIM_PL_FIELDS * 8, self.Lmax,
                 self.recs.data_ptr() + base * self.rec_cap * 64 if self.full_log else None, self.rec_cap,
                 self.pexp.data_ptr() + base * self.pe_cap * 4 if self.full_log else None, self.pe_cap,
-                warps_per_cta, st)
+                warps_per_cta, queue_cap, sh)
             _check(rc, "replay")
+            if not single:
+                self._joins[gi].record(self._streams[gi])
+                cur.wait_event(self._joins[gi])
             base += n
+        self._queue_cap = queue_cap
 
     def results(self) -> list:
         """Counters / per-layer / logs back to host, in the caller's point order."""
@@ -274,6 +298,9 @@ class ReplayBatch:
         n = len(self.ccfg)
         raw = self.counters.cpu().numpy().tobytes()
         cs = [_abi.EsimCounters.from_buffer_copy(raw[i * 360:(i + 1) * 360]) for i in range(n)]
+        if any(c.status == -5 for c in cs) and getattr(self, "_queue_cap", 0) != -1:
+            self.launch(queue_cap=-1)             # channel outgrew the default ring: exact bound
+            return self.results()
         pl = self.per_layer.cpu().numpy().reshape(n, self.Lmax, _abi.ESIM_PL_FIELDS)
         if self.full_log:
             recs = self.recs.cpu().numpy().view(REC_DTYPE).reshape(n, self.rec_cap)

@@ -21,8 +21,8 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     const EsimRouterOut* d_routers, EsimCounters* d_counters,
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
-                                    int warps_per_cta, cudaStream_t st);
-int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca);
+                                    bool has_cnt, int warps_per_cta, cudaStream_t st);
+int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt);
 
 static thread_local std::string g_err;
 
@@ -61,10 +61,12 @@ extern "C" int esim_router_launch(const EsimTraceDesc* tr, const EsimRouterOut* 
     return 0;
 }
 
-struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca; };
+struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca, has_cnt; };
 
-static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stride, Sizing* z) {
-    Sizing s{0, 1, 2, 0, 0, 0, 0, false};
+// queue_cap 0 = default ring size (64 entries, overflow -> status -5 and the
+// caller re-launches with the exact bound queue_cap = -1: slots + 1)
+static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stride, int queue_cap, Sizing* z) {
+    Sizing s{0, 1, 2, 0, 0, 0, 0, false, false};
     for (int i = 0; i < n; i++) {
         const EsimConfig& c = h[i];
         if (c.experts > ESIM_MAX_E || c.top_k > ESIM_MAX_K) return fail(-1, "geometry exceeds device limits");
@@ -81,8 +83,10 @@ static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stri
         s.Emax = std::max(s.Emax, c.experts);
         s.Kmax = std::max(s.Kmax, c.top_k);
         if (c.routing == ESIM_ROUTE_CACHE_AWARE) s.ca = true;
+        if (c.eviction == ESIM_EV_LFU || c.eviction == ESIM_EV_LHU) s.has_cnt = true;
     }
-    s.Q = s.S + 1;
+    if (s.S > 4095) return fail(-1, "more than 4095 resident experts per cache is not supported by the device directory");
+    s.Q = queue_cap > 0 ? std::min(queue_cap, s.S + 1) : queue_cap < 0 ? s.S + 1 : std::min(64, s.S + 1);
     s.Tmax = s.ca ? std::max(1, max_tokens) : 0;
     if (pl_stride < s.Lmax) return fail(-1, "per-layer stride smaller than num_layers");
     s.Lmax = pl_stride;
@@ -91,31 +95,31 @@ static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stri
 }
 
 extern "C" int esim_replay_smem_per_point(const EsimConfig* h_cfg, int32_t n, int32_t max_tokens,
-                                          int32_t pl_stride) {
+                                          int32_t pl_stride, int32_t queue_cap) {
     Sizing z;
-    int rc = replay_sizing(h_cfg, n, max_tokens, pl_stride, &z);
+    int rc = replay_sizing(h_cfg, n, max_tokens, pl_stride, queue_cap, &z);
     if (rc) return rc;
-    return esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca);
+    return esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt);
 }
 
 extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_cfg, int32_t n,
                                   const EsimTraceDesc* d_traces, const EsimRouterOut* d_routers, int32_t max_tokens,
                                   EsimCounters* d_counters, int64_t* d_per_layer, int32_t pl_stride,
                                   EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp, int64_t pe_cap,
-                                  int32_t warps_per_cta, void* stream) {
+                                  int32_t warps_per_cta, int32_t queue_cap, void* stream) {
     if (n <= 0) return 0;
     Sizing z;
-    int rc = replay_sizing(h_cfg, n, max_tokens, pl_stride, &z);
+    int rc = replay_sizing(h_cfg, n, max_tokens, pl_stride, queue_cap, &z);
     if (rc) return rc;
-    int per = esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca);
+    int per = esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt);
     const int budget = 227 * 1024;
     int w = warps_per_cta > 0 ? warps_per_cta : 4;
     while (w > 1 && per * w > budget) w--;
     if (per * w > budget) return fail(-1, "replay state of one grid point exceeds shared memory (" +
                                               std::to_string(per) + " B)");
     cudaError_t e = esim_replay_launch_impl(d_cfg, n, d_traces, d_routers, d_counters, d_per_layer, d_recs, rec_cap,
-                                            d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, w,
-                                            (cudaStream_t)stream);
+                                            d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
+                                            w, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "replay launch");
     return 0;
 }
@@ -240,7 +244,7 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
     int rc = esim_replay_launch(cfg, (EsimConfig*)(base + cfg_off), n, (EsimTraceDesc*)(base + td_off),
                                 (EsimRouterOut*)(base + rd_off), max_tokens, (EsimCounters*)(base + cnt_off),
                                 (int64_t*)(base + pl_off), pl_stride, recs ? (EsimRec*)(base + rec_off) : nullptr,
-                                rec_cap, recs ? (int32_t*)(base + pe_off) : nullptr, pe_cap, 0, C.st);
+                                rec_cap, recs ? (int32_t*)(base + pe_off) : nullptr, pe_cap, 0, 0, C.st);
     if (rc) return rc;
     cudaMemcpyAsync(counters, base + cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, C.st);
     cudaMemcpyAsync(per_layer, base + pl_off, sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS,
@@ -251,6 +255,24 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
     }
     e = cudaStreamSynchronize(C.st);
     if (e != cudaSuccess) return cuda_fail(e, "esim_run_host");
+    bool overflow = false;
+    for (int i = 0; i < n; i++) overflow |= counters[i].status == -5;
+    if (overflow) {   // channel deeper than the default ring: replay again with the exact bound
+        rc = esim_replay_launch(cfg, (EsimConfig*)(base + cfg_off), n, (EsimTraceDesc*)(base + td_off),
+                                (EsimRouterOut*)(base + rd_off), max_tokens, (EsimCounters*)(base + cnt_off),
+                                (int64_t*)(base + pl_off), pl_stride, recs ? (EsimRec*)(base + rec_off) : nullptr,
+                                rec_cap, recs ? (int32_t*)(base + pe_off) : nullptr, pe_cap, 0, -1, C.st);
+        if (rc) return rc;
+        cudaMemcpyAsync(counters, base + cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, C.st);
+        cudaMemcpyAsync(per_layer, base + pl_off, sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS,
+                        cudaMemcpyDeviceToHost, C.st);
+        if (recs) {
+            cudaMemcpyAsync(recs, base + rec_off, sizeof(EsimRec) * n * rec_cap, cudaMemcpyDeviceToHost, C.st);
+            cudaMemcpyAsync(pred_experts, base + pe_off, sizeof(int32_t) * n * pe_cap, cudaMemcpyDeviceToHost, C.st);
+        }
+        e = cudaStreamSynchronize(C.st);
+        if (e != cudaSuccess) return cuda_fail(e, "esim_run_host");
+    }
     for (int i = 0; i < n; i++)
         if (counters[i].status) {
             int s = (int)counters[i].status;

@@ -13,30 +13,38 @@
 //   classify_miss / ResidencyHistory                      metrics.py:32-57
 //   route_event (cache_aware, DeltaAvgState)              routing.py:60-90, 143-161
 //
-// Device-native structures instead of the reference's containers: the
-// directory is flat shared-memory arrays indexed by ident = layer*E+expert
-// plus a slot table of residents carrying one 64-bit policy key; every
-// victim choice is a warp argmin over the slot table (LS: class bit | gen,
-// LRU: stamp, LFU: count then touch, FLD: cyclic distance, SB: fp64 signal).
-// The channel is a ring buffer whose retiming is a warp max-plus scan.
-// Scalars are computed redundantly by all 32 lanes (warp-uniform control
-// flow); lane 0 owns counters and record output.
+// Device-native structures instead of the reference's containers:
+//  * directory: one packed 16-bit word per ident (ident = layer*E + expert):
+//    bit15 in-flight, bit12 resident, bits13-14 precision, bits0-11 slot;
+//    an int16 miss history per ident; a slot table of residents, each with
+//    one 64-bit policy key; a free-slot stack;
+//  * victim selection: a warp argmin over the slot table (LS: class|gen,
+//    LRU: stamp, LFU: count then touch, FLD: cyclic distance, SB: fp64);
+//  * channel: a ring buffer [head][demands/promoted][pending prefetches]
+//    whose retiming is a warp max-plus scan; capacity is a launch parameter
+//    (overflow -> status -5, the host re-launches with the exact bound).
+// Every helper is force-inlined so the warp-uniform scalars (clock, byte
+// accounting, queue cursors, digest) stay in registers, redundantly
+// computed by all 32 lanes; counters live in shared memory owned by lane 0.
 #include <cuda_runtime.h>
 #include <cstdint>
 
 #include "../../include/specmd_b200.h"
 #include "numpy_f32.cuh"
 
+#define DFI __device__ __forceinline__
+
 namespace esim {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint64_t FNV_OFFSET = 0xcbf29ce484222325ULL;
 constexpr uint64_t FNV_PRIME = 0x100000001b3ULL;
+constexpr int STATUS_QUEUE_OVERFLOW = -5;
 
 struct ReplayArgs {
     const EsimConfig* cfg;
     int n_points;
-    const EsimTraceDesc* traces;   // device copies of the descriptors (device pointers inside)
+    const EsimTraceDesc* traces;   // device array of descriptors (device pointers inside)
     const EsimRouterOut* routers;
     EsimCounters* counters;
     int64_t* per_layer;            // [n][Lmax][ESIM_PL_FIELDS]
@@ -45,32 +53,43 @@ struct ReplayArgs {
     int32_t* pexp;
     int64_t pe_cap;
     int N, S, Q, Lmax, Emax, Tmax, Kmax;  // smem sizing (max over points)
+    int has_cnt;                   // any LFU/LHU point (per-ident counts)
     int warps_per_cta;
     int point_bytes;
 };
 
-// shared-memory layout of one point (offsets in bytes, 8-byte aligned blocks)
+// lane-0 owned counters (shared memory)
+struct Ctr {                       // 32-bit counts: native ATOMS.ADD (64-bit is a CAS loop)
+    uint32_t totals[15];
+    uint32_t rows_total, faithful, modified;
+    uint32_t pf_tp, pf_pred, pf_dem, pf_records, pf_empty, pf_prec_parts, pf_rec_parts;
+    uint32_t ls_forced, ls_refusals;
+    uint32_t passes, decode_passes;
+    int64_t sync_overhead, decode_us, ttft, total;   // lane-0 plain updates
+    double ps[8];                  // Neumaier (f, c) pairs: orig, exec, prec, rec
+};
+
 struct Layout {
-    int key, q_submit, q_start, q_comp, dsum;          // 8-byte arrays
-    int cnt, rscore, q_score, pl, demmask, ca_w, dem_gate, dem_summed;  // 4/8-byte
-    int hist, slot_of, res_ident, q_ident, ca_sel;     // 2-byte
-    int st, q_flags, tofetch, ca_mod, dem_rank;        // 1-byte
-    int ca_row, dem_expert, dem_tokens, lsc;
+    int key, q_submit, q_comp, dsum, ctr, dem_summed;     // 8-byte
+    int cnt, rscore, q_score, pl, demmask, lsc, ca_w, ca_row, dem_gate, dem_tokens, dem_expert, dem_rank;  // 4-byte
+    int rs, hist, res_ident, fs, q_ident, ca_sel;         // 2-byte
+    int q_flags, tofetch, ca_mod;                         // 1-byte
     int total;
 };
 
 __host__ __device__ inline int al8(int x) { return (x + 7) & ~7; }
 
-__host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E, int T, int K, bool ca) {
+__host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E, int T, int K, bool ca,
+                                              bool has_cnt) {
     Layout l;
     int o = 0;
     l.key = o; o += al8(S * 8);
     l.q_submit = o; o += al8(Q * 8);
-    l.q_start = o; o += al8(Q * 8);
     l.q_comp = o; o += al8(Q * 8);
-    l.dsum = o; o += al8(L * 8);
+    l.dsum = o; o += al8(ca ? L * 8 : 0);
+    l.ctr = o; o += al8((int)sizeof(Ctr));
     l.dem_summed = o; o += al8(ca ? E * 8 : 0);
-    l.cnt = o; o += al8(N * 4);
+    l.cnt = o; o += al8(has_cnt ? N * 4 : 0);
     l.rscore = o; o += al8(S * 4);
     l.q_score = o; o += al8(Q * 4);
     l.pl = o; o += al8(L * ESIM_PL_FIELDS * 4);
@@ -81,298 +100,349 @@ __host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E,
     l.dem_gate = o; o += al8(ca ? E * 4 : 0);
     l.dem_tokens = o; o += al8(ca ? E * 4 : 0);
     l.dem_expert = o; o += al8(ca ? E * 4 : 0);
+    l.dem_rank = o; o += al8(ca ? E * 4 : 0);
+    l.rs = o; o += al8(N * 2);
     l.hist = o; o += al8(N * 2);
-    l.slot_of = o; o += al8(N * 2);
     l.res_ident = o; o += al8(S * 2);
+    l.fs = o; o += al8(S * 2);
     l.q_ident = o; o += al8(Q * 2);
     l.ca_sel = o; o += al8(ca ? T * K * 2 : 0);
-    l.st = o; o += al8(N);
     l.q_flags = o; o += al8(Q);
     l.tofetch = o; o += al8(E);
     l.ca_mod = o; o += al8(ca ? T : 0);
-    l.dem_rank = o; o += al8(ca ? E * 4 : 0);
     l.total = o;
     return l;
 }
 
-// status bits in st[]: bits 0-2 = resident precision + 1, bit 7 = in flight
-constexpr uint8_t ST_INFLIGHT = 0x80;
+// packed directory word
+constexpr uint16_t RS_INF = 0x8000, RS_RES = 0x1000;
+DFI bool rs_res(uint16_t w) { return w & RS_RES; }
+DFI int rs_prec(uint16_t w) { return (w >> 13) & 3; }
+DFI int rs_slot(uint16_t w) { return w & 0x0FFF; }
+DFI uint16_t rs_make(int prec, int slot) { return (uint16_t)(RS_RES | (prec << 13) | slot); }
 
 struct Pt {
-    // config
     const EsimConfig* c;
-    int L, E, K, N, S, Q;
+    int L, E, K, S, Q;
     int pol, lane;
-    int64_t cap, bw;
-    int64_t dur[4];
-    // smem arrays
-    uint8_t* st;
-    int16_t* hist;
-    int16_t* slot_of;
-    int32_t* cnt;
-    int16_t* res_ident;
+    int64_t cap;
+    int64_t dur0, dur1, dur2, dur3, eb0, eb1, eb2, eb3;   // by precision code (registers, not an array)
+    // shared memory
     uint64_t* key;
+    int64_t *q_submit, *q_comp;
+    double* dsum;
+    Ctr* ctr;
+    double* dem_summed_s;
+    int32_t* cnt;
     float* rscore;
-    int16_t* q_ident;
-    uint8_t* q_flags;
     float* q_score;
-    int64_t *q_submit, *q_start, *q_comp;
     int32_t* pl;
     uint32_t* demmask;
-    uint8_t* tofetch;
-    double* dsum;
     float* lsc;
-    // cache-aware scratch
-    int16_t* ca_sel;
     float* ca_w;
-    uint8_t* ca_mod;
     float* ca_row;
+    float* dem_gate_s;
+    int32_t* dem_tokens_s;
     int32_t* dem_expert_s;
     int32_t* dem_rank_s;
-    float* dem_gate_s;
-    double* dem_summed_s;
-    int32_t* dem_tokens_s;
-    // scalars (warp-uniform)
+    uint16_t* rs;
+    int16_t* hist;
+    int16_t* res_ident;
+    uint16_t* fs;
+    int16_t* q_ident;
+    int16_t* ca_sel;
+    uint8_t* q_flags;
+    uint8_t* tofetch;
+    uint8_t* ca_mod;
+    // warp-uniform scalars
     int64_t now, resident_bytes, reserved_bytes;
-    int qh, qn, nA;
-    uint64_t seq;        // LRU stamp / LFU touch / LS gen counter
+    int qh, qn, nA, fs_top;
+    uint64_t seq;
+    uint64_t digest;
+    bool digest_on;
+    uint32_t pf_ev[5];              // prefetch submitted/started/completed/skipped/dropped (registers)
+    uint32_t n_evict, n_forced;
+    int64_t n_recs, n_pe;
     int pass_id, layer;
-    // outputs
-    EsimCounters* C;     // global, lane 0 writes at the end
-    EsimCounters acc;    // lane-0 accumulators live in registers of every lane (uniform)
+    int err;
+    // record output
     EsimRec* recs;
     int64_t rec_cap;
     int32_t* pexp;
     int64_t pe_cap;
     bool full;
-    int err;
-    PySum ps_orig, ps_exec, ps_prec, ps_rec;
 };
 
-__device__ __forceinline__ int qphys(const Pt& p, int i) {
+DFI int64_t pdur(const Pt& p, int c) { return c == 0 ? p.dur0 : c == 1 ? p.dur1 : c == 2 ? p.dur2 : p.dur3; }
+DFI int64_t peb(const Pt& p, int c) { return c == 0 ? p.eb0 : c == 1 ? p.eb1 : c == 2 ? p.eb2 : p.eb3; }
+
+DFI int qphys(const Pt& p, int i) {
     int x = p.qh + i;
     return x >= p.Q ? x - p.Q : x;
 }
 
-__device__ __forceinline__ uint64_t fnv_word(uint64_t h, uint64_t w) { return (h ^ w) * FNV_PRIME; }
+// fire-and-forget shared-memory atomics: lane 0 never waits on a counter RMW
+DFI void ctr_add(Pt& p, uint32_t& f, uint32_t v) {
+    if (p.lane == 0) f += v;
+}
+DFI void pl_add(Pt& p, int idx, int v) {
+    if (p.lane == 0) p.pl[idx] += v;
+}
+
+DFI void ps_add(Pt& p, int which, double x) {
+    if (p.lane == 0) {
+        double f = p.ctr->ps[2 * which], c = p.ctr->ps[2 * which + 1];
+        double t = __dadd_rn(f, x);
+        if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+        else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+        p.ctr->ps[2 * which] = t;
+        p.ctr->ps[2 * which + 1] = c;
+    }
+}
 
 // ---------------------------------------------------------------------------
-// record output
+// record output + digest
+// digest: mix = sum_i w_i * K_i over the record's 8 words (t0 skipped for
+// predictions), h = ((h ^ mix) * P) ^ (>> 29); prediction experts chained.
 // ---------------------------------------------------------------------------
-__device__ void emit(Pt& p, EsimRec& r, const int32_t* pe, int npe) {
-    const uint64_t* w = reinterpret_cast<const uint64_t*>(&r);
-    uint64_t h = p.acc.digest;
-    #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        if (r.kind == ESIM_REC_PREDICTION && i == 4) continue;
-        h = fnv_word(h, w[i]);
+#define KMIX0 0x9E3779B97F4A7C15ULL
+#define KMIX1 0xBF58476D1CE4E5B9ULL
+#define KMIX2 0x94D049BB133111EBULL
+#define KMIX3 0xD6E8FEB86659FD93ULL
+#define KMIX4 0xA0761D6478BD642FULL
+#define KMIX5 0xE7037ED1A0B428DBULL
+#define KMIX6 0x8EBC6AF09C88C6E3ULL
+#define KMIX7 0x589965CC75374CC3ULL
+
+DFI uint64_t w2(int32_t a, int32_t b) { return (uint64_t)(uint32_t)a | ((uint64_t)(uint32_t)b << 32); }
+
+DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0, int64_t t1,
+              int64_t t2, double x0, const int32_t* pe = nullptr, int npe = 0) {
+    if (p.digest_on) {
+    uint64_t mix = w2(kind, p.pass_id) * KMIX0 + w2(layer, i0) * KMIX1 + w2(i1, i2) * KMIX2 +
+                   w2(i3, i4) * KMIX3 + (uint64_t)t1 * KMIX5 + (uint64_t)t2 * KMIX6 +
+                   (uint64_t)__double_as_longlong(x0) * KMIX7;
+    if (kind != ESIM_REC_PREDICTION) mix += (uint64_t)t0 * KMIX4;
+    uint64_t h = (p.digest ^ mix) * FNV_PRIME;
+    h ^= h >> 29;
+    for (int j = 0; j < npe; j++) h = (h ^ (uint64_t)(uint32_t)pe[j]) * FNV_PRIME;
+    p.digest = h;
     }
-    for (int j = 0; j < npe; j++) h = fnv_word(h, (uint64_t)(uint32_t)pe[j]);
-    p.acc.digest = h;
     if (p.full) {
-        int64_t n = p.acc.n_recs, m = p.acc.n_pred_experts;
+        const int64_t n = p.n_recs, m = p.n_pe;
         if (n < p.rec_cap && m + npe <= p.pe_cap) {
-            if (r.kind == ESIM_REC_PREDICTION) r.t0 = m;
-            if (p.lane == 0) p.recs[n] = r;
+            if (p.lane == 0) {
+                EsimRec r;
+                r.kind = kind; r.pass_id = p.pass_id; r.layer = layer;
+                r.i0 = i0; r.i1 = i1; r.i2 = i2; r.i3 = i3; r.i4 = i4;
+                r.t0 = kind == ESIM_REC_PREDICTION ? m : t0; r.t1 = t1; r.t2 = t2; r.x0 = x0;
+                p.recs[n] = r;
+            }
             for (int j = p.lane; j < npe; j += 32) p.pexp[m + j] = pe[j];
         } else if (!p.err) {
             p.err = -4;
         }
     }
-    p.acc.n_recs++;
-    p.acc.n_pred_experts += npe;
+    p.n_recs++;
+    p.n_pe += npe;
 }
 
-__device__ __forceinline__ void rec_prefetch(Pt& p, int ev, int target, int expert, int64_t t, float score,
-                                             int reason) {
-    EsimRec r;
-    r.kind = ESIM_REC_PREFETCH; r.pass_id = p.pass_id; r.layer = p.layer;
-    r.i0 = ev; r.i1 = target; r.i2 = expert; r.i3 = reason; r.i4 = 0;
-    r.t0 = t; r.t1 = 0; r.t2 = 0; r.x0 = (double)score;
-    emit(p, r, nullptr, 0);
-    p.acc.totals[10 + ev]++;
+DFI void rec_prefetch(Pt& p, int ev, int target, int expert, int64_t t, float score, int reason) {
+    emit(p, ESIM_REC_PREFETCH, p.layer, ev, target, expert, reason, 0, t, 0, 0, (double)score);
+    p.pf_ev[ev]++;                  // ev is a compile-time constant at every call site
 }
 
 // ---------------------------------------------------------------------------
-// policies: note_* update the slot key; victim = warp argmin
+// policies (eviction.py:29-294) on slot keys
 // ---------------------------------------------------------------------------
-constexpr uint64_t LS_CURRENT = 1ull << 62;
+constexpr uint64_t LS_CURRENT = 1ull << 50;   // stamps stay below 2^50; key << 12 fits 64 bits
+constexpr uint64_t KEY_FREE = 0x000FFFFFFFFFFFFFull; // free-slot key: above every live LRU/LS key,
+                                                     // also after begin_pass clears bit 50
 
-__device__ __forceinline__ uint64_t order_double(double d) {
-    uint64_t b = (uint64_t)__double_as_longlong(d);
+DFI uint64_t order_double(double d) {
+    const uint64_t b = (uint64_t)__double_as_longlong(d);
     return (b >> 63) ? ~b : (b | (1ull << 63));
 }
 
-// admit / access / prefetch-hit bookkeeping on a resident's slot (all lanes call; lane 0 writes)
-__device__ void pol_touch_ls(Pt& p, int slot) {
-    uint64_t k = p.key[slot];
-    if (k & LS_CURRENT) return;                              // first touch of the pass fixed it
-    uint64_t nk = LS_CURRENT | (p.seq++);
-    __syncwarp();
-    if (p.lane == 0) p.key[slot] = nk;
+DFI void set_key(Pt& p, int slot, uint64_t k) {
+    if (p.lane == 0) p.key[slot] = k;
     __syncwarp();
 }
 
-__device__ void pol_note_admit(Pt& p, int ident, int slot) {
-    uint64_t nk = 0;
-    switch (p.pol) {
-    case ESIM_EV_LRU: nk = p.seq++; break;                    // move_to_end
-    case ESIM_EV_LFU: case ESIM_EV_LHU: nk = p.seq++; break;  // touch; count setdefault 0
-    case ESIM_EV_FLD: nk = 0; break;
-    case ESIM_EV_SB: nk = __double_as_longlong(0.0); break;   // new residency starts at 0
-    case ESIM_EV_LS: nk = LS_CURRENT | (p.seq++); break;      // untracked -> current
-    }
-    if (p.lane == 0) p.key[slot] = nk;
+DFI void ls_touch(Pt& p, int slot) {                                  // eviction.py:245-250
+    if (p.key[slot] & LS_CURRENT) return;                              // first touch fixed it
     __syncwarp();
+    set_key(p, slot, LS_CURRENT | (p.seq++));
 }
 
-__device__ void pol_note_access(Pt& p, int ident, int slot, bool has_gate, double gate, int prec) {
+DFI void note_admit(Pt& p, int slot) {
+    uint64_t nk;
     switch (p.pol) {
-    case ESIM_EV_LRU: {
-        uint64_t nk = p.seq++;
-        if (p.lane == 0) p.key[slot] = nk;
-        break;
+    case ESIM_EV_LRU: case ESIM_EV_LFU: case ESIM_EV_LHU: nk = p.seq++; break;   // move_to_end / touch
+    case ESIM_EV_LS: nk = LS_CURRENT | (p.seq++); break;                         // untracked -> current
+    default: nk = 0; break;                                                      // FLD; SB signal 0.0
     }
+    set_key(p, slot, nk);
+}
+
+DFI void note_access(Pt& p, int ident, int slot, bool has_gate, double gate, int prec) {
+    switch (p.pol) {
+    case ESIM_EV_LRU: set_key(p, slot, p.seq++); break;
     case ESIM_EV_LFU: case ESIM_EV_LHU: {
-        int step = 1;
-        if (p.pol == ESIM_EV_LHU) step = (prec == p.c->precisions[0]) ? 1 : 0;
-        uint64_t nk = p.seq++;
-        if (p.lane == 0) { p.cnt[ident] += step; p.key[slot] = nk; }
+        const int step = (p.pol == ESIM_EV_LFU || prec == p.c->precisions[0]) ? 1 : 0;
+        if (p.lane == 0) p.cnt[ident] += step;
+        set_key(p, slot, p.seq++);
         break;
     }
-    case ESIM_EV_FLD: break;
     case ESIM_EV_SB:
         if (has_gate) {
-            double s = __longlong_as_double((long long)p.key[slot]);
-            double ns = __dadd_rn(s, gate);
+            const double s = __longlong_as_double((long long)p.key[slot]);
             __syncwarp();
-            if (p.lane == 0) p.key[slot] = (uint64_t)__double_as_longlong(ns);
+            set_key(p, slot, (uint64_t)__double_as_longlong(__dadd_rn(s, gate)));
         }
         break;
-    case ESIM_EV_LS: pol_touch_ls(p, slot); break;
+    case ESIM_EV_LS: ls_touch(p, slot); break;
+    default: break;
     }
-    __syncwarp();
 }
 
-// warp argmin over residents. Returns the victim slot or -1.
-__device__ int select_victim(Pt& p, bool forced) {
-    uint64_t bk = ~0ull;
-    uint32_t bi = 0xffffffffu;
-    int c = p.layer;
-    for (int s = p.lane; s < p.S; s += 32) {
-        int id = p.res_ident[s];
-        if (id < 0) continue;
-        uint64_t k;
-        uint32_t tie = (uint32_t)id;
-        switch (p.pol) {
-        case ESIM_EV_LRU: case ESIM_EV_LS: k = p.key[s]; break;
-        case ESIM_EV_LFU: case ESIM_EV_LHU:
-            k = ((uint64_t)(uint32_t)p.cnt[id] << 32) | (uint32_t)p.key[s];
-            break;
-        case ESIM_EV_FLD: {
-            int l = id / p.E, e = id - l * p.E;
-            int d = ((l - c) % p.L + p.L) % p.L;
-            k = (uint64_t)(p.L - 1 - d);
-            tie = (uint32_t)(e * p.L + l);
-            break;
-        }
-        default: k = order_double(__longlong_as_double((long long)p.key[s])); break;  // SB
-        }
-        if (k < bk || (k == bk && tie < bi)) { bk = k; bi = tie; }
-    }
-    int bs = -1;
+// warp argmin over residents; returns the victim slot or -1 (select_victim).
+// Every policy's order is total, so one 64-bit key per slot with the slot
+// index in the low 12 bits reduces in a single shuffle chain:
+//   LRU / LS   (class | stamp) << 12 | slot      stamps are unique
+//   LFU / LHU  count:20 | touch:32 | slot:12      touches are unique
+//   FLD        (L-1-dist):8 | expert:16 | layer:16 | slot:12
+//   SB         two stages: min signal, then min ident among equal signals
+DFI uint64_t warp_min_u64(uint64_t v) {
     #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        uint64_t ok = __shfl_xor_sync(FULL, bk, o);
-        uint32_t oi = __shfl_xor_sync(FULL, bi, o);
-        if (ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+        const uint64_t w = __shfl_xor_sync(FULL, v, o);
+        v = w < v ? w : v;
     }
-    if (bi == 0xffffffffu) return -1;
-    int ident = (int)bi;
-    if (p.pol == ESIM_EV_FLD) { int e = ident / p.L, l = ident - e * p.L; ident = l * p.E + e; }
-    if (p.pol == ESIM_EV_LS) {
-        if (bk & LS_CURRENT) {                               // no stale resident left
-            if (!forced) { p.acc.ls_refusals++; return -1; }
-            p.acc.ls_forced++;
+    return v;
+}
+
+DFI int select_victim(Pt& p, bool forced) {
+    const int c = p.layer;
+    uint64_t best = ~0ull;
+    if (p.pol == ESIM_EV_SB) {
+        uint64_t bsig = ~0ull;
+        for (int s = p.lane; s < p.S; s += 32)
+            if (p.res_ident[s] >= 0) {
+                const uint64_t k = order_double(__longlong_as_double((long long)p.key[s]));
+                bsig = k < bsig ? k : bsig;
+            }
+        bsig = warp_min_u64(bsig);
+        if (bsig == ~0ull) return -1;
+        for (int s = p.lane; s < p.S; s += 32) {
+            const int id = p.res_ident[s];
+            if (id >= 0 && order_double(__longlong_as_double((long long)p.key[s])) == bsig) {
+                const uint64_t k = ((uint64_t)id << 12) | (uint64_t)s;
+                best = k < best ? k : best;
+            }
         }
+        best = warp_min_u64(best);
+        return (int)(best & 0xFFF);
     }
-    bs = p.slot_of[ident];
-    return bs;
+    if (p.pol == ESIM_EV_LRU || p.pol == ESIM_EV_LS) {               // branch-free: free slots hold KEY_FREE
+        #pragma unroll 4
+        for (int s = p.lane; s < p.S; s += 32) {
+            const uint64_t k = (p.key[s] << 12) | (uint64_t)s;
+            best = k < best ? k : best;
+        }
+        best = warp_min_u64(best);
+        if ((best >> 12) >= (KEY_FREE & ~LS_CURRENT)) return -1;
+        if (p.pol == ESIM_EV_LS && ((best >> 12) & LS_CURRENT)) {
+            if (!forced) { ctr_add(p, p.ctr->ls_refusals, 1); return -1; }
+            ctr_add(p, p.ctr->ls_forced, 1);
+        }
+        return (int)(best & 0xFFF);
+    }
+    for (int s = p.lane; s < p.S; s += 32) {
+        const int id = p.res_ident[s];
+        if (id < 0) continue;
+        uint64_t k;
+        if (p.pol == ESIM_EV_LFU || p.pol == ESIM_EV_LHU) {
+            k = ((uint64_t)(uint32_t)p.cnt[id] << 44) | ((uint64_t)(uint32_t)p.key[s] << 12) | (uint64_t)s;
+        } else {                                                          // FLD
+            const int l = id / p.E, e = id - l * p.E;
+            int d = l - c;
+            d = d < 0 ? d + p.L : d;
+            k = ((uint64_t)(p.L - 1 - d) << 44) | ((uint64_t)e << 28) | ((uint64_t)l << 12) | (uint64_t)s;
+        }
+        best = k < best ? k : best;
+    }
+    best = warp_min_u64(best);
+    if (best == ~0ull) return -1;
+    if (p.pol == ESIM_EV_LS && ((best >> 12) & LS_CURRENT)) {           // no stale resident left
+        if (!forced) { ctr_add(p, p.ctr->ls_refusals, 1); return -1; }
+        ctr_add(p, p.ctr->ls_forced, 1);
+    }
+    return (int)(best & 0xFFF);
 }
 
 // ---------------------------------------------------------------------------
-// cache + history
+// cache
 // ---------------------------------------------------------------------------
-__device__ int alloc_slot(Pt& p) {
-    for (int base = 0; base < p.S; base += 32) {
-        int s = base + p.lane;
-        bool fr = s < p.S && p.res_ident[s] < 0;
-        unsigned m = __ballot_sync(FULL, fr);
-        if (m) return base + __ffs(m) - 1;
-    }
-    return -1;
-}
-
-__device__ void evict(Pt& p, int slot, int cause, bool forced) {          // engine.py:451-460
-    int ident = p.res_ident[slot];
-    int prec = (p.st[ident] & 7) - 1;
-    p.resident_bytes -= p.c->expert_bytes[prec];
+DFI void evict(Pt& p, int slot, int cause, bool forced) {                 // engine.py:451-460
+    const int ident = p.res_ident[slot];
+    const int prec = rs_prec(p.rs[ident]);
+    p.resident_bytes -= peb(p, prec);
     __syncwarp();
     if (p.lane == 0) {
-        p.st[ident] = 0;
+        p.rs[ident] = 0;
         p.hist[ident] = (int16_t)p.pass_id;
         p.res_ident[slot] = -1;
-        p.slot_of[ident] = -1;
+        p.key[slot] = KEY_FREE;
+        p.fs[p.fs_top] = (uint16_t)slot;
     }
     __syncwarp();
-    EsimRec r;
-    r.kind = ESIM_REC_EVICT; r.pass_id = p.pass_id; r.layer = p.layer;
-    r.i0 = ident / p.E; r.i1 = ident % p.E; r.i2 = prec; r.i3 = cause; r.i4 = forced ? 1 : 0;
-    r.t0 = r.t1 = r.t2 = 0; r.x0 = 0.0;
-    emit(p, r, nullptr, 0);
-    p.acc.totals[8]++;
-    if (forced) p.acc.totals[9]++;
+    p.fs_top++;
+    emit(p, ESIM_REC_EVICT, p.layer, ident / p.E, ident % p.E, prec, cause, forced ? 1 : 0, 0, 0, 0, 0.0);
+    p.n_evict++;
+    p.n_forced += forced ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------
-// channel: ring buffer [head][A: demands/promoted][B: pending prefetches]
+// channel
 // ---------------------------------------------------------------------------
-struct QEntry { int16_t ident; uint8_t flags; float score; int64_t submit, start, comp; };
+struct QEntry { int16_t ident; uint8_t flags; float score; int64_t submit, comp; };
 
-__device__ __forceinline__ QEntry q_load(const Pt& p, int i) {
-    int x = qphys(p, i);
+DFI QEntry q_load(const Pt& p, int i) {
+    const int x = qphys(p, i);
     QEntry e;
     e.ident = p.q_ident[x]; e.flags = p.q_flags[x]; e.score = p.q_score[x];
-    e.submit = p.q_submit[x]; e.start = p.q_start[x]; e.comp = p.q_comp[x];
+    e.submit = p.q_submit[x]; e.comp = p.q_comp[x];
     return e;
 }
-__device__ __forceinline__ void q_store(Pt& p, int i, const QEntry& e) {
-    int x = qphys(p, i);
+DFI void q_store(Pt& p, int i, const QEntry& e) {
+    const int x = qphys(p, i);
     p.q_ident[x] = e.ident; p.q_flags[x] = e.flags; p.q_score[x] = e.score;
-    p.q_submit[x] = e.submit; p.q_start[x] = e.start; p.q_comp[x] = e.comp;
+    p.q_submit[x] = e.submit; p.q_comp[x] = e.comp;
 }
 
-// open a hole at logical index `at` (shift [at, qn) right by one)
-__device__ void q_open(Pt& p, int at) {
+// open a hole at logical index `at` (shift [at, qn) right by one); false on overflow
+DFI bool q_open(Pt& p, int at) {
+    if (p.qn >= p.Q) { p.err = STATUS_QUEUE_OVERFLOW; return false; }
     for (int hi = p.qn; hi > at; hi -= 32) {
-        int lo = max(at, hi - 32);
-        int i = lo + p.lane;
+        const int lo = max(at, hi - 32);
+        const int i = lo + p.lane;
         QEntry e;
-        bool act = i < hi;
+        const bool act = i < hi;
         if (act) e = q_load(p, i);
         __syncwarp();
         if (act) q_store(p, i + 1, e);
         __syncwarp();
     }
     p.qn++;
+    return true;
 }
 
-// close logical index `at` (shift (at, qn) left by one)
-__device__ void q_close(Pt& p, int at) {
+DFI void q_close(Pt& p, int at) {
     for (int lo = at + 1; lo < p.qn; lo += 32) {
-        int i = lo + p.lane;
+        const int i = lo + p.lane;
         QEntry e;
-        bool act = i < p.qn;
+        const bool act = i < p.qn;
         if (act) e = q_load(p, i);
         __syncwarp();
         if (act) q_store(p, i - 1, e);
@@ -381,176 +451,176 @@ __device__ void q_close(Pt& p, int at) {
     p.qn--;
 }
 
-__device__ __forceinline__ int64_t entry_dur(const Pt& p, uint8_t flags) { return p.dur[(flags >> 2) & 3]; }
-
-// start_i = max(comp_{i-1}, submit_i); comp_i = start_i + dur_i for i >= from (>=1):
-// a warp inclusive scan of x -> max(x + a, b) maps (engine.py:283-288)
-__device__ void retime(Pt& p, int from) {
+// comp_i = max(comp_{i-1}, submit_i) + dur_i for i >= from >= 1 (engine.py:283-288):
+// a warp inclusive scan composing x -> max(x + a, b)
+DFI void retime(Pt& p, int from) {
     if (from < 1) from = 1;
     if (from >= p.qn) return;
     int64_t carry = p.q_comp[qphys(p, from - 1)];
     for (int base = from; base < p.qn; base += 32) {
-        int i = base + p.lane;
-        bool act = i < p.qn;
-        int64_t a = 0, b = INT64_MIN / 4, d = 0, sub = 0;
+        const int i = base + p.lane;
+        const bool act = i < p.qn;
+        int64_t a = 0, b = INT64_MIN / 4;
+        int x = 0;
         if (act) {
-            int x = qphys(p, i);
-            d = entry_dur(p, p.q_flags[x]);
-            sub = p.q_submit[x];
+            x = qphys(p, i);
+            const int64_t d = pdur(p, (p.q_flags[x] >> 2) & 3);
             a = d;
-            b = sub + d;
+            b = p.q_submit[x] + d;
         }
         #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int64_t pa = __shfl_up_sync(FULL, a, o);
-            int64_t pb = __shfl_up_sync(FULL, b, o);
+            const int64_t pa = __shfl_up_sync(FULL, a, o);
+            const int64_t pb = __shfl_up_sync(FULL, b, o);
             if (p.lane >= o) { b = max(pb + a, b); a = pa + a; }
         }
-        int64_t comp = max(carry + a, b);
+        const int64_t comp = max(carry + a, b);
         __syncwarp();
-        if (act) {
-            int x = qphys(p, i);
-            p.q_comp[x] = comp;
-            p.q_start[x] = comp - d;
-        }
-        int last = min(31, p.qn - 1 - base);
+        if (act) p.q_comp[x] = comp;
+        const int last = min(31, p.qn - 1 - base);
         carry = __shfl_sync(FULL, comp, last);
         __syncwarp();
     }
 }
 
-__device__ int q_find(const Pt& p, int ident) {
+DFI int q_find(const Pt& p, int ident) {
     for (int base = 0; base < p.qn; base += 32) {
-        int i = base + p.lane;
-        bool hit = i < p.qn && p.q_ident[qphys(p, i)] == ident;
-        unsigned m = __ballot_sync(FULL, hit);
+        const int i = base + p.lane;
+        const bool hit = i < p.qn && p.q_ident[qphys(p, i)] == ident;
+        const unsigned m = __ballot_sync(FULL, hit);
         if (m) return base + __ffs(m) - 1;
     }
     return -1;
 }
 
-__device__ void settle(Pt& p) {                                           // engine.py:422-442
+DFI void settle(Pt& p) {                                                   // engine.py:422-442
     while (p.qn > 0) {
-        int h = p.qh;
-        int64_t comp = p.q_comp[h];
+        const int h = p.qh;
+        const int64_t comp = p.q_comp[h];
         if (comp > p.now) break;
-        int ident = p.q_ident[h];
-        uint8_t fl = p.q_flags[h];
-        float score = p.q_score[h];
-        int prec = (fl >> 2) & 3;
-        int64_t nb = p.c->expert_bytes[prec];
+        const int ident = p.q_ident[h];
+        const uint8_t fl = p.q_flags[h];
+        const float score = p.q_score[h];
+        const int prec = (fl >> 2) & 3;
+        const int64_t nb = peb(p, prec);
+        if (p.fs_top <= 0) { p.err = -2; return; }
+        const int slot = p.fs[p.fs_top - 1];
         __syncwarp();
+        p.fs_top--;
         p.qh = (p.qh + 1 == p.Q) ? 0 : p.qh + 1;
         p.qn--;
         if (p.nA > 0) p.nA--;
         p.reserved_bytes -= nb;
         p.resident_bytes += nb;
-        int slot = alloc_slot(p);
-        if (slot < 0) { p.err = -2; return; }
         if (p.lane == 0) {
-            p.st[ident] = (uint8_t)(prec + 1);
-            p.slot_of[ident] = (int16_t)slot;
+            p.rs[ident] = rs_make(prec, slot);
             p.res_ident[slot] = (int16_t)ident;
             p.rscore[slot] = score;
             if (p.hist[ident] == -2) p.hist[ident] = -1;
         }
         __syncwarp();
         if (p.resident_bytes + p.reserved_bytes > p.cap && !p.err) p.err = -2;
-        pol_note_admit(p, ident, slot);
+        note_admit(p, slot);
         if (fl & 1) rec_prefetch(p, 2, ident / p.E, ident % p.E, comp, score, 0);
     }
 }
 
-__device__ __forceinline__ void advance_to(Pt& p, int64_t t) { p.now = t; settle(p); }
+DFI void advance_to(Pt& p, int64_t t) {
+    p.now = t;
+    settle(p);
+}
 
-// _fetch (engine.py:463-510). Returns blocked us, or -1 for None.
-__device__ int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
-    int64_t nb = p.c->expert_bytes[prec];
+// _fetch (engine.py:463-510): blocked us, or -1 for None
+DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
+    const int64_t nb = peb(p, prec);
     if (nb > p.cap) {
         if (!final) return -1;
         p.err = -1;
         return 0;
     }
     while (p.cap - p.resident_bytes - p.reserved_bytes < nb && !p.err) {
-        int v = select_victim(p, final);
+        const int v = select_victim(p, final);
         if (v >= 0) { evict(p, v, 0, final); continue; }
         if (!final) return -1;
-        int nB = p.qn - 1 - p.nA;                                 // pending prefetches
-        if (p.qn > 1 && nB > 0) {                                 // cancel newest (= queue tail)
-            QEntry e = q_load(p, p.qn - 1);
+        if (p.qn > 1 && p.qn - 1 - p.nA > 0) {                           // cancel newest pending = tail
+            const QEntry e = q_load(p, p.qn - 1);
             __syncwarp();
             p.qn--;
-            p.reserved_bytes -= p.c->expert_bytes[(e.flags >> 2) & 3];
-            if (p.lane == 0) p.st[e.ident] &= (uint8_t)~ST_INFLIGHT;
+            p.reserved_bytes -= peb(p, (e.flags >> 2) & 3);
+            if (p.lane == 0) p.rs[e.ident] = 0;
             __syncwarp();
             rec_prefetch(p, 4, e.ident / p.E, e.ident % p.E, p.now, e.score, 4);
             continue;
         }
         if (p.qn == 0) { p.err = -2; return 0; }
-        int64_t nd = p.q_comp[p.qh];
+        const int64_t nd = p.q_comp[p.qh];
         advance_to(p, nd > p.now ? nd : p.now);
     }
     if (p.err) return 0;
     p.reserved_bytes += nb;
-    int at = p.qn > 0 ? 1 + p.nA : 0;
-    q_open(p, at);
+    const int at = p.qn > 0 ? 1 + p.nA : 0;
+    if (!q_open(p, at)) return 0;
     QEntry e;
     e.ident = (int16_t)ident; e.flags = (uint8_t)(prec << 2); e.score = gate;
-    e.submit = p.now;
-    e.start = p.now; e.comp = p.now + p.dur[prec];
-    if (p.lane == 0) { q_store(p, at, e); p.st[ident] |= ST_INFLIGHT; }
+    e.submit = p.now; e.comp = p.now + pdur(p, prec);
+    if (p.lane == 0) { q_store(p, at, e); p.rs[ident] = RS_INF; }
     __syncwarp();
     if (at > 0) p.nA++;
     retime(p, at);
-    int64_t comp = p.q_comp[qphys(p, at)];
-    int64_t blocked = comp - p.now;
+    const int64_t comp = p.q_comp[qphys(p, at)];
+    const int64_t blocked = comp - p.now;
     advance_to(p, comp);
     return blocked;
 }
 
-__device__ void access_rec(Pt& p, int expert, int tokens, int rank, int outcome, int mclass, int64_t blocked,
-                           double wd, int prec, int sub) {
-    EsimRec r;
-    r.kind = ESIM_REC_ACCESS; r.pass_id = p.pass_id; r.layer = p.layer;
-    r.i0 = expert; r.i1 = tokens; r.i2 = rank;
-    r.i3 = outcome | ((mclass < 0 ? 0xFF : mclass) << 8) | ((prec + 1) << 16);
-    r.i4 = sub; r.t0 = blocked; r.t1 = 0; r.t2 = 0; r.x0 = wd;
-    emit(p, r, nullptr, 0);
-    p.acc.totals[0]++;
-    p.acc.sync_overhead_us += blocked;
-    int32_t* pl = p.pl + p.layer * ESIM_PL_FIELDS;
-    int f = outcome == 0 ? 1 : (outcome <= 2 ? 2 : (outcome == 3 ? 6 : 7));
-    if (outcome == 0) p.acc.totals[1]++;
-    else if (outcome <= 2) { p.acc.totals[2]++; p.acc.totals[3 + mclass]++; }
-    else if (outcome == 3) p.acc.totals[6]++;
-    else p.acc.totals[7]++;
+DFI void access_rec(Pt& p, int expert, int tokens, int rank, int outcome, int mclass, int64_t blocked, double wd,
+                    int prec, int sub) {
+    emit(p, ESIM_REC_ACCESS, p.layer, expert, tokens, rank,
+         outcome | ((mclass < 0 ? 0xFF : mclass) << 8) | ((prec + 1) << 16), sub, blocked, 0, 0, wd);
+    // per-layer counters only; totals[0..7] are their sums (formed at the end)
     if (p.lane == 0) {
+        int32_t* pl = p.pl + p.layer * ESIM_PL_FIELDS;
         pl[0]++;
-        pl[f]++;
+        pl[outcome == 0 ? 1 : outcome <= 2 ? 2 : outcome == 3 ? 6 : 7]++;
         if (outcome == 1 || outcome == 2) pl[3 + mclass]++;
+        if (blocked) p.ctr->sync_overhead += blocked;
     }
 }
 
-// _handle_demand + resolve_miss. Returns outcome code (0 hit 1 fetch 2 wait 3 drop 4 subst), -1 error.
-__device__ int handle_demand(Pt& p, int expert, int rank, float gate, double summed, int tokens,
-                             const float* layer_scores, int nd, int64_t& blocked, double& wd) {
+// nearest-rank percentile (prefetch.py:30-36) of n floats in smem, warp-parallel
+DFI float warp_nearest_rank(const float* v, int n, long rank, int lane) {
+    float thr = 0.0f;
+    bool found = false;
+    for (int i = lane; i < n; i += 32) {
+        const float x = v[i];
+        int less = 0, le = 0;
+        for (int j = 0; j < n; j++) { const float u = v[j]; less += u < x; le += u <= x; }
+        if (less <= rank - 1 && rank - 1 < le) { thr = x; found = true; }
+    }
+    const unsigned who = __ballot_sync(FULL, found);
+    return __shfl_sync(FULL, thr, __ffs(who) - 1);
+}
+
+// _handle_demand + resolve_miss: outcome 0 hit 1 fetch 2 wait 3 drop 4 subst, -1 error
+DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, int tokens, int nd,
+                      int64_t& blocked, double& wd) {
     const EsimConfig* cfg = p.c;
-    int ident = p.layer * p.E + expert;
-    blocked = 0; wd = 0.0;
-    uint8_t st = p.st[ident];
-    if (st & 7) {
-        int prec = (st & 7) - 1;
-        int slot = p.slot_of[ident];
-        pol_note_access(p, ident, slot, true, (double)gate, prec);
+    const int ident = p.layer * p.E + expert;
+    blocked = 0;
+    wd = 0.0;
+    const uint16_t w = p.rs[ident];
+    if (rs_res(w)) {
+        const int prec = rs_prec(w), slot = rs_slot(w);
+        note_access(p, ident, slot, true, (double)gate, prec);
         if (p.lane == 0) p.rscore[slot] = gate;
         __syncwarp();
         access_rec(p, expert, tokens, rank, 0, -1, 0, 0.0, prec, -1);
         return 0;
     }
-    int h = p.hist[ident];
-    int mclass = h == -2 ? 0 : (h == p.pass_id ? 1 : 2);
-    if (st & ST_INFLIGHT) {                                              // promote + wait
-        int idx = q_find(p, ident);
+    const int h = p.hist[ident];
+    const int mclass = h == -2 ? 0 : (h == p.pass_id ? 1 : 2);
+    if (w & RS_INF) {                                                     // promote + wait (engine.py:526-537)
+        const int idx = q_find(p, ident);
         QEntry e = q_load(p, idx);
         e.flags |= 2;
         __syncwarp();
@@ -559,7 +629,7 @@ __device__ int handle_demand(Pt& p, int expert, int rank, float gate, double sum
             if (p.lane == 0) p.q_flags[qphys(p, 0)] = e.flags;
             __syncwarp();
         } else {
-            bool inA = idx <= p.nA;
+            const bool inA = idx <= p.nA;
             q_close(p, idx);
             if (inA) p.nA--;
             at = 1 + p.nA;
@@ -569,12 +639,12 @@ __device__ int handle_demand(Pt& p, int expert, int rank, float gate, double sum
             p.nA++;
             retime(p, min(idx, at));
         }
-        int prec = (e.flags >> 2) & 3;
-        int64_t comp = p.q_comp[qphys(p, at)];
+        const int prec = (e.flags >> 2) & 3;
+        const int64_t comp = p.q_comp[qphys(p, at)];
         blocked = comp - p.now;
         advance_to(p, comp);
-        int slot = p.slot_of[ident];
-        pol_note_access(p, ident, slot, true, (double)gate, prec);
+        const int slot = rs_slot(p.rs[ident]);
+        note_access(p, ident, slot, true, (double)gate, prec);
         if (p.lane == 0) p.rscore[slot] = gate;
         __syncwarp();
         access_rec(p, expert, tokens, rank, 2, mclass, blocked, 0.0, prec, -1);
@@ -585,33 +655,36 @@ __device__ int handle_demand(Pt& p, int expert, int rank, float gate, double sum
         access_rec(p, expert, tokens, rank, 3, -1, 0, wd, -1, -1);
         return 3;
     }
-    if (cfg->miss == ESIM_MISS_SUBST) {                                  // find_substitute miss.py:66-79
+    if (cfg->miss == ESIM_MISS_SUBST) {                                   // find_substitute (miss.py:66-79)
         double bd = 0.0;
         int be = -1;
         for (int e0 = 0; e0 < p.E; e0 += 32) {
-            int e = e0 + p.lane;
+            const int e = e0 + p.lane;
             double diff = 0.0;
             bool ok = false;
             if (e < p.E) {
-                int id = p.layer * p.E + e;
-                if (p.st[id] & 7) {
-                    diff = fabs((double)p.rscore[p.slot_of[id]] - (double)gate);
+                const uint16_t ww = p.rs[p.layer * p.E + e];
+                if (rs_res(ww)) {
+                    diff = fabs(__dsub_rn((double)p.rscore[rs_slot(ww)], (double)gate));
                     ok = diff <= cfg->subst_tolerance;
                 }
             }
+            int ce = ok ? e : 0x7fffffff;
             #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                double od = __shfl_xor_sync(FULL, diff, o);
-                int oe = __shfl_xor_sync(FULL, ok ? e : -1, o);
-                bool ook = oe >= 0;
-                if (ook && (!ok || od < diff || (od == diff && oe < e))) { diff = od; e = oe; ok = true; }
+                const double od = __shfl_xor_sync(FULL, diff, o);
+                const int oe = __shfl_xor_sync(FULL, ce, o);
+                if (oe != 0x7fffffff && (ce == 0x7fffffff || od < diff || (od == diff && oe < ce))) {
+                    diff = od;
+                    ce = oe;
+                }
             }
-            if (ok && (be < 0 || diff < bd)) { bd = diff; be = e; }
+            if (ce != 0x7fffffff && (be < 0 || diff < bd)) { bd = diff; be = ce; }
         }
         if (be >= 0) {
-            int sid = p.layer * p.E + be;
-            int sp = (p.st[sid] & 7) - 1;
-            pol_note_access(p, sid, p.slot_of[sid], false, 0.0, sp);
+            const uint16_t sw = p.rs[p.layer * p.E + be];
+            const int sp = rs_prec(sw);
+            note_access(p, p.layer * p.E + be, rs_slot(sw), false, 0.0, sp);
             wd = -summed;
             access_rec(p, expert, tokens, rank, 4, -1, 0, wd, sp, be);
             return 4;
@@ -625,25 +698,14 @@ __device__ int handle_demand(Pt& p, int expert, int rank, float gate, double sum
     } else if (cfg->miss == ESIM_MISS_FETCH_PRIORITY) {
         int start = 0;
         if (cfg->n_precisions > 1 && nd > 0) {
-            // nearest-rank percentile of layer_scores (float64 compare)
             long rk = (long)ceil(cfg->degrade_percentile / 100.0 * (double)nd);
             if (rk < 1) rk = 1;
-            float thr = 0.0f;
-            bool found = false;
-            for (int i = p.lane; i < nd; i += 32) {
-                float v = layer_scores[i];
-                int less = 0, le = 0;
-                for (int j = 0; j < nd; j++) { float u = layer_scores[j]; less += u < v; le += u <= v; }
-                if (less <= rk - 1 && rk - 1 < le) { thr = v; found = true; }
-            }
-            unsigned who = __ballot_sync(FULL, found);
-            thr = __shfl_sync(FULL, thr, __ffs(who) - 1);
+            const float thr = warp_nearest_rank(p.lsc, nd, rk, p.lane);
             if ((double)gate < (double)thr) start = 1;
         }
         for (int i = start; i < cfg->n_precisions; i++) {
-            bool fin = i == cfg->n_precisions - 1;
             prec = cfg->precisions[i];
-            b = do_fetch(p, ident, gate, prec, fin);
+            b = do_fetch(p, ident, gate, prec, i == cfg->n_precisions - 1);
             if (b >= 0 || p.err) break;
         }
         if (b < 0 && !p.err) p.err = -2;
@@ -651,8 +713,8 @@ __device__ int handle_demand(Pt& p, int expert, int rank, float gate, double sum
         b = do_fetch(p, ident, gate, prec, true);
     }
     if (p.err) return -1;
-    int slot = p.slot_of[ident];
-    pol_note_access(p, ident, slot, true, (double)gate, prec);
+    const int slot = rs_slot(p.rs[ident]);
+    note_access(p, ident, slot, true, (double)gate, prec);
     if (p.lane == 0) p.rscore[slot] = gate;
     __syncwarp();
     blocked = b;
@@ -660,31 +722,27 @@ __device__ int handle_demand(Pt& p, int expert, int rank, float gate, double sum
     return 1;
 }
 
-// _submit_prefetches + watchdog_step for submitting layer `layer`
-__device__ void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
-    int target = p.layer + 1;
-    int n = R.n_pred[tev];
+// _submit_prefetches + watchdog_step (engine.py:651-725, prefetch.py:163-221)
+DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
+    const int target = p.layer + 1;
+    const int n = R.n_pred[tev];
     const int32_t* pe = R.pred_expert + tev * p.E;
     const float* ps = R.pred_score + tev * p.E;
-    EsimRec r;
-    r.kind = ESIM_REC_PREDICTION; r.pass_id = p.pass_id; r.layer = p.layer;
-    r.i0 = target; r.i1 = n; r.i2 = R.pred_clamped[tev]; r.i3 = 0; r.i4 = 0;
-    r.t0 = 0; r.t1 = 0; r.t2 = 0; r.x0 = 0.0;
-    emit(p, r, pe, n);
-    if (p.lane == 0) { p.pl[target * ESIM_PL_FIELDS + 8] += n; p.pl[target * ESIM_PL_FIELDS + 9] += 1; }
+    emit(p, ESIM_REC_PREDICTION, p.layer, target, n, R.pred_clamped[tev], 0, 0, 0, 0, 0, 0.0, pe, n);
+    pl_add(p, target * ESIM_PL_FIELDS + 8, n);
+    pl_add(p, target * ESIM_PL_FIELDS + 9, 1);
     for (int j = 0; j < n; j++) rec_prefetch(p, 0, target, pe[j], p.now, ps[j], 0);
-    int wp = p.c->working_prec;
-    int64_t nb = p.c->expert_bytes[wp];
-    // sweep 1 (FIFO): residents are marked (LS touch), in-flight skipped
+    const int wp = p.c->working_prec;
+    const int64_t nb = peb(p, wp);
     int nt = 0;
-    for (int j = 0; j < n; j++) {
-        int e = pe[j];
-        int ident = target * p.E + e;
-        uint8_t st = p.st[ident];
-        if (st & 7) {
-            if (p.pol == ESIM_EV_LS) pol_touch_ls(p, p.slot_of[ident]);
+    for (int j = 0; j < n; j++) {                                         // sweep 1
+        const int e = pe[j];
+        const int ident = target * p.E + e;
+        const uint16_t w = p.rs[ident];
+        if (rs_res(w)) {
+            if (p.pol == ESIM_EV_LS) ls_touch(p, rs_slot(w));
             rec_prefetch(p, 3, target, e, p.now, ps[j], 1);
-        } else if (st & ST_INFLIGHT) {
+        } else if (w & RS_INF) {
             rec_prefetch(p, 3, target, e, p.now, ps[j], 2);
         } else {
             if (p.lane == 0) p.tofetch[nt] = (uint8_t)j;
@@ -692,40 +750,36 @@ __device__ void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
         }
     }
     __syncwarp();
-    // sweep 2: evict unforced or drop; reserve; append behind the tail
-    for (int t = 0; t < nt && !p.err; t++) {
-        int j = p.tofetch[t];
-        int e = pe[j];
-        float sc = ps[j];
-        int ident = target * p.E + e;
+    for (int t = 0; t < nt && !p.err; t++) {                              // sweep 2
+        const int j = p.tofetch[t];
+        const int e = pe[j];
+        const float sc = ps[j];
+        const int ident = target * p.E + e;
         bool refused = false;
         while (p.cap - p.resident_bytes - p.reserved_bytes < nb) {
-            int v = select_victim(p, false);
+            const int v = select_victim(p, false);
             if (v < 0) { rec_prefetch(p, 4, target, e, p.now, sc, 3); refused = true; break; }
             evict(p, v, 1, false);
         }
         if (refused) continue;
+        if (p.qn >= p.Q) { p.err = STATUS_QUEUE_OVERFLOW; return; }
         p.reserved_bytes += nb;
         QEntry q;
         q.ident = (int16_t)ident; q.flags = (uint8_t)(1 | (wp << 2)); q.score = sc; q.submit = p.now;
-        int64_t tail = p.qn ? p.q_comp[qphys(p, p.qn - 1)] : p.now;
-        q.start = p.qn ? (p.now > tail ? p.now : tail) : p.now;
-        q.comp = q.start + p.dur[wp];
-        int at = p.qn;
+        int64_t start = p.now;
+        if (p.qn) { const int64_t tail = p.q_comp[qphys(p, p.qn - 1)]; start = p.now > tail ? p.now : tail; }
+        q.comp = start + pdur(p, wp);
+        const int at = p.qn;
         __syncwarp();
-        if (p.lane == 0) { q_store(p, at, q); p.st[ident] |= ST_INFLIGHT; }
+        if (p.lane == 0) { q_store(p, at, q); p.rs[ident] = RS_INF; }
         __syncwarp();
         p.qn++;
         rec_prefetch(p, 1, target, e, p.now, sc, 0);
     }
 }
 
-// ---- cache-aware routing in the loop (routing.py:143-161) ----------------
-// Per row: original softmax/top-k, bias = f32(lam * mean) on this layer's
-// resident experts, re-softmax, re-top-k; DeltaAvg mean updated after the
-// row with the fp64 pairwise row sum. Fills the smem demand arrays and the
-// per-row selection; returns the demand count.
-__device__ float warp_softmax(float* buf, int E, int lane) {
+// ---- cache-aware routing inside the loop (routing.py:143-161) -------------
+DFI void warp_softmax(float* buf, int E, int lane) {
     float m = -__int_as_float(0x7f800000);
     for (int i = lane; i < E; i += 32) m = fmaxf(m, buf[i]);
     #pragma unroll
@@ -733,45 +787,42 @@ __device__ float warp_softmax(float* buf, int E, int lane) {
     __syncwarp();
     for (int i = lane; i < E; i += 32) buf[i] = np_expf(__fsub_rn(buf[i], m));
     __syncwarp();
-    float S = __fadd_rn(0.0f, warp_pw_sum(buf, E, lane));
+    const float S = __fadd_rn(0.0f, warp_pw_sum(buf, E, lane));
     __syncwarp();
     for (int i = lane; i < E; i += 32) buf[i] = __fdiv_rn(buf[i], S);
     __syncwarp();
-    return S;
 }
 
-__device__ int warp_topk(const float* s, int E, int K, int lane, int16_t* out) {
+DFI void warp_topk(const float* s, int E, int K, int lane, int16_t* out) {
     uint32_t taken = 0;
     for (int j = 0; j < K; j++) {
         float bv = -1.0f;
         int bi = 0x7fffffff;
         for (int i = lane, t = 0; i < E; i += 32, t++) {
             if (taken & (1u << t)) continue;
-            float v = s[i];
+            const float v = s[i];
             if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
         }
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            float ov = __shfl_xor_sync(FULL, bv, o);
-            int oi = __shfl_xor_sync(FULL, bi, o);
+            const float ov = __shfl_xor_sync(FULL, bv, o);
+            const int oi = __shfl_xor_sync(FULL, bi, o);
             if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
         }
         if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
         if (lane == 0) out[j] = (int16_t)bi;
     }
     __syncwarp();
-    return 0;
 }
 
-// numpy DOUBLE_pairwise_sum of one float32 row cast to float64 (lanes 0..7
-// accumulate); n <= 256 splits at most once, so no recursion.
-__device__ __forceinline__ double warp_pw_block_f64(const float* a, int n, int lane) {
+// numpy DOUBLE_pairwise_sum of a float32 row cast to float64; n <= 256 splits at most once
+DFI double warp_pw_block_f64(const float* a, int n, int lane) {
     if (n < 8) {
         double res = 0.0;
         for (int i = 0; i < n; i++) res = __dadd_rn(res, (double)a[i]);
         return res;
     }
-    int lim = n - (n % 8);
+    const int lim = n - (n % 8);
     double r = 0.0;
     if (lane < 8) {
         r = (double)a[lane];
@@ -785,54 +836,52 @@ __device__ __forceinline__ double warp_pw_block_f64(const float* a, int n, int l
     return res;
 }
 
-__device__ __forceinline__ double warp_pw_sum_f64(const float* a, int n, int lane) {
+DFI double warp_pw_sum_f64(const float* a, int n, int lane) {
     if (n <= 128) return warp_pw_block_f64(a, n, lane);
     int n2 = n / 2;
     n2 -= n2 % 8;
     return __dadd_rn(warp_pw_block_f64(a, n2, lane), warp_pw_block_f64(a + n2, n - n2, lane));
 }
 
-__device__ int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int64_t rows_before) {
+// route one event with the cache-aware bias; fills the smem demand arrays
+// (indexed by expert) and dem_expert_s (sorted order); returns the demand count
+DFI int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int64_t rows_before) {
     const int E = p.E, K = p.K, l = p.layer;
     const float* X = tr.logits + tr.row_offset[ev] * (int64_t)E;
     float* buf = p.ca_row;
     bool any_cached = false;
-    for (int e = p.lane; e < E; e += 32) any_cached |= (p.st[l * E + e] & 7) != 0;
+    for (int e = p.lane; e < E; e += 32) any_cached |= rs_res(p.rs[l * E + e]);
     any_cached = __any_sync(FULL, any_cached);
     int16_t orig[ESIM_MAX_K];
     for (int r = 0; r < T; r++) {
         const float* x = X + (int64_t)r * E;
-        // original scores and top-k
         for (int i = p.lane; i < E; i += 32) buf[i] = x[i];
         __syncwarp();
-        warp_softmax(buf, E, p.lane);
-        warp_topk(buf, E, K, p.lane, p.ca_sel + r * K);       // temp: original selection
+        warp_softmax(buf, E, p.lane);                                     // original scores
+        warp_topk(buf, E, K, p.lane, p.ca_sel + r * K);
         for (int j = 0; j < K; j++) orig[j] = p.ca_sel[r * K + j];
         const int64_t dcount = (rows_before + r) * (int64_t)E;
-        double mean = dcount ? __ddiv_rn(p.dsum[l], (double)dcount) : 0.0;
-        // keep the original scores (weights are read at the biased selection)
+        const double mean = dcount ? __ddiv_rn(p.dsum[l], (double)dcount) : 0.0;
         __syncwarp();
-        for (int i = p.lane; i < E; i += 32) p.dem_gate_s[i] = buf[i];
+        for (int i = p.lane; i < E; i += 32) p.dem_gate_s[i] = buf[i];     // keep original scores
         __syncwarp();
+        const bool bias_on = p.c->lam != 0.0 && mean != 0.0 && any_cached;
+        const float bias = __double2float_rn(__dmul_rn(p.c->lam, mean));
         for (int i = p.lane; i < E; i += 32) {
             float v = x[i];
-            if (p.c->lam != 0.0 && mean != 0.0 && any_cached && (p.st[l * E + i] & 7)) {
-                float bias = __double2float_rn(__dmul_rn(p.c->lam, mean));
-                v = __fadd_rn(v, bias);
-            }
+            if (bias_on && rs_res(p.rs[l * E + i])) v = __fadd_rn(v, bias);
             buf[i] = v;
         }
         __syncwarp();
         warp_softmax(buf, E, p.lane);
         warp_topk(buf, E, K, p.lane, p.ca_sel + r * K);
-        // DeltaAvg update with this row (after the bias)
-        for (int i = p.lane; i < E; i += 32) buf[i] = x[i];
+        for (int i = p.lane; i < E; i += 32) buf[i] = x[i];                // DeltaAvg update after the row
         __syncwarp();
-        double rs = __dadd_rn(0.0, warp_pw_sum_f64(buf, E, p.lane));
-        if (p.lane == 0) p.dsum[l] = __dadd_rn(p.dsum[l], rs);
+        const double rsum = __dadd_rn(0.0, warp_pw_sum_f64(buf, E, p.lane));
+        if (p.lane == 0) p.dsum[l] = __dadd_rn(p.dsum[l], rsum);
         bool same = true;
         for (int a = 0; a < K; a++) {
-            int s = p.ca_sel[r * K + a];
+            const int s = p.ca_sel[r * K + a];
             bool f = false;
             for (int b = 0; b < K; b++) f |= (s == orig[b]);
             same &= f;
@@ -843,62 +892,59 @@ __device__ int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int
         }
         __syncwarp();
     }
-    // aggregate demands (engine.py:578-594) from the biased selection
-    int nd = 0;
-    for (int e0 = 0; e0 < E; e0 += 32) {
-        int e = e0 + p.lane;
+    for (int e0 = 0; e0 < E; e0 += 32) {                                  // _aggregate_demand
+        const int e = e0 + p.lane;
+        if (e >= E) continue;
         int rank = 0x7fffffff, tok = 0;
         float gate = -1.0f;
         double summed = 0.0;
-        if (e < E) {
-            for (int r = 0; r < T; r++)
-                for (int j = 0; j < K; j++)
-                    if (p.ca_sel[r * K + j] == e) {
-                        float wv = p.ca_w[r * K + j];
-                        rank = min(rank, j + 1);
-                        gate = fmaxf(gate, wv);
-                        summed = tok ? __dadd_rn(summed, (double)wv) : (double)wv;
-                        tok++;
-                    }
-            p.dem_rank_s[e] = tok ? rank : 0x7fffffff;
-            p.dem_gate_s[e] = gate;
-            p.dem_summed_s[e] = summed;
-            p.dem_tokens_s[e] = tok;
-        }
+        for (int r = 0; r < T; r++)
+            for (int j = 0; j < K; j++)
+                if (p.ca_sel[r * K + j] == e) {
+                    const float wv = p.ca_w[r * K + j];
+                    rank = min(rank, j + 1);
+                    gate = fmaxf(gate, wv);
+                    summed = tok ? __dadd_rn(summed, (double)wv) : (double)wv;
+                    tok++;
+                }
+        p.dem_rank_s[e] = tok ? rank : 0x7fffffff;
+        p.dem_gate_s[e] = gate;
+        p.dem_summed_s[e] = summed;
+        p.dem_tokens_s[e] = tok;
     }
     __syncwarp();
-    // order by (rank, -gate, expert): position of each present expert
     int cnt = 0;
-    for (int e0 = 0; e0 < E; e0 += 32) {
-        int e = e0 + p.lane;
+    for (int e0 = 0; e0 < E; e0 += 32) {                                  // order (rank, -gate, expert)
+        const int e = e0 + p.lane;
         int pos = -1;
         if (e < E && p.dem_rank_s[e] != 0x7fffffff) {
-            int rk = p.dem_rank_s[e];
-            float g = p.dem_gate_s[e];
+            const int rk = p.dem_rank_s[e];
+            const float g = p.dem_gate_s[e];
             pos = 0;
             for (int j = 0; j < E; j++) {
-                int rj = p.dem_rank_s[j];
+                const int rj = p.dem_rank_s[j];
                 if (rj == 0x7fffffff || j == e) continue;
-                float gj = p.dem_gate_s[j];
+                const float gj = p.dem_gate_s[j];
                 pos += (rj < rk) || (rj == rk && (gj > g || (gj == g && j < e)));
             }
         }
         cnt += __popc(__ballot_sync(FULL, pos >= 0));
-        if (e < E) reinterpret_cast<int*>(p.ca_row)[e] = pos;   // routing done: reuse as int scratch
+        if (e < E) reinterpret_cast<int*>(p.ca_row)[e] = pos;            // routing done: int scratch
     }
     __syncwarp();
-    nd = cnt;
-    // scatter into sorted order: dem_expert_s holds the sorted expert list
     for (int e = p.lane; e < E; e += 32) {
-        int pos = reinterpret_cast<int*>(p.ca_row)[e];
+        const int pos = reinterpret_cast<int*>(p.ca_row)[e];
         if (pos >= 0) p.dem_expert_s[pos] = e;
     }
     __syncwarp();
-    return nd;
+    return cnt;
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) replay_kernel(ReplayArgs A) {
+#ifndef ESIM_REPLAY_MINB
+#define ESIM_REPLAY_MINB 1
+#endif
+__global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int wid = threadIdx.x >> 5;
     const int pid = blockIdx.x * A.warps_per_cta + wid;
@@ -908,31 +954,37 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs A) {
     const EsimRouterOut R = A.routers[cfg->trace_id];
     unsigned char* base = smem_raw + (size_t)wid * A.point_bytes;
     const bool ca = cfg->routing == ESIM_ROUTE_CACHE_AWARE;
-    Layout lay = make_layout(A.N, A.S, A.Q, A.Lmax, A.Emax, A.Tmax, A.Kmax, A.Tmax > 0);
+    const Layout lay = make_layout(A.N, A.S, A.Q, A.Lmax, A.Emax, A.Tmax, A.Kmax, A.Tmax > 0, A.has_cnt != 0);
 
     Pt p;
     p.c = cfg;
-    p.L = cfg->num_layers; p.E = cfg->experts; p.K = cfg->top_k; p.N = p.L * p.E;
+    p.L = cfg->num_layers; p.E = cfg->experts; p.K = cfg->top_k;
+    const int N = p.L * p.E;
     p.lane = threadIdx.x & 31;
     p.pol = cfg->eviction;
-    p.cap = cfg->capacity_bytes; p.bw = cfg->bandwidth;
+    p.cap = cfg->capacity_bytes;
+    const int64_t bw = cfg->bandwidth;
     int64_t minb = INT64_MAX;
+    int64_t durs[4], ebs[4];
+    #pragma unroll
     for (int i = 0; i < 4; i++) {
-        int64_t nb = cfg->expert_bytes[i];
-        p.dur[i] = (p.bw == 0 || nb == 0) ? 0 : (nb * 1000000 + p.bw - 1) / p.bw;
+        const int64_t nb = cfg->expert_bytes[i];
+        ebs[i] = nb;
+        durs[i] = (bw == 0 || nb == 0) ? 0 : (nb * 1000000 + bw - 1) / bw;
         if (nb > 0 && nb < minb) minb = nb;
     }
+    p.eb0 = ebs[0]; p.eb1 = ebs[1]; p.eb2 = ebs[2]; p.eb3 = ebs[3];
+    p.dur0 = durs[0]; p.dur1 = durs[1]; p.dur2 = durs[2]; p.dur3 = durs[3];
     int64_t slots = p.cap / minb;
-    if (slots > p.N) slots = p.N;
+    if (slots > N) slots = N;
     if (slots > A.S) slots = A.S;
     p.S = (int)slots;
-    p.Q = p.S + 1;
-    if (p.Q > A.Q) p.Q = A.Q;
+    p.Q = A.Q;
     p.key = reinterpret_cast<uint64_t*>(base + lay.key);
     p.q_submit = reinterpret_cast<int64_t*>(base + lay.q_submit);
-    p.q_start = reinterpret_cast<int64_t*>(base + lay.q_start);
     p.q_comp = reinterpret_cast<int64_t*>(base + lay.q_comp);
     p.dsum = reinterpret_cast<double*>(base + lay.dsum);
+    p.ctr = reinterpret_cast<Ctr*>(base + lay.ctr);
     p.dem_summed_s = reinterpret_cast<double*>(base + lay.dem_summed);
     p.cnt = reinterpret_cast<int32_t*>(base + lay.cnt);
     p.rscore = reinterpret_cast<float*>(base + lay.rscore);
@@ -945,49 +997,61 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs A) {
     p.dem_gate_s = reinterpret_cast<float*>(base + lay.dem_gate);
     p.dem_tokens_s = reinterpret_cast<int32_t*>(base + lay.dem_tokens);
     p.dem_expert_s = reinterpret_cast<int32_t*>(base + lay.dem_expert);
+    p.dem_rank_s = reinterpret_cast<int32_t*>(base + lay.dem_rank);
+    p.rs = reinterpret_cast<uint16_t*>(base + lay.rs);
     p.hist = reinterpret_cast<int16_t*>(base + lay.hist);
-    p.slot_of = reinterpret_cast<int16_t*>(base + lay.slot_of);
     p.res_ident = reinterpret_cast<int16_t*>(base + lay.res_ident);
+    p.fs = reinterpret_cast<uint16_t*>(base + lay.fs);
     p.q_ident = reinterpret_cast<int16_t*>(base + lay.q_ident);
     p.ca_sel = reinterpret_cast<int16_t*>(base + lay.ca_sel);
-    p.st = base + lay.st;
     p.q_flags = base + lay.q_flags;
     p.tofetch = base + lay.tofetch;
     p.ca_mod = base + lay.ca_mod;
-    p.dem_rank_s = reinterpret_cast<int32_t*>(base + lay.dem_rank);
 
-    for (int i = p.lane; i < p.N; i += 32) { p.st[i] = 0; p.hist[i] = -2; p.slot_of[i] = -1; p.cnt[i] = 0; }
-    for (int i = p.lane; i < p.S; i += 32) { p.res_ident[i] = -1; p.key[i] = 0; }
+    const bool lfu = p.pol == ESIM_EV_LFU || p.pol == ESIM_EV_LHU;
+    for (int i = p.lane; i < N; i += 32) {
+        p.rs[i] = 0;
+        p.hist[i] = -2;
+        if (lfu) p.cnt[i] = 0;
+    }
+    for (int i = p.lane; i < p.S; i += 32) { p.res_ident[i] = -1; p.key[i] = KEY_FREE; p.fs[i] = (uint16_t)(p.S - 1 - i); }
     for (int i = p.lane; i < p.L * ESIM_PL_FIELDS; i += 32) p.pl[i] = 0;
-    for (int i = p.lane; i < p.L; i += 32) p.dsum[i] = 0.0;
+    if (ca) for (int i = p.lane; i < p.L; i += 32) p.dsum[i] = 0.0;
+    {
+        uint32_t* cw = reinterpret_cast<uint32_t*>(p.ctr);
+        for (int i = p.lane; i < (int)(sizeof(Ctr) / 4); i += 32) cw[i] = 0;
+    }
     __syncwarp();
     p.now = 0; p.resident_bytes = 0; p.reserved_bytes = 0;
-    p.qh = 0; p.qn = 0; p.nA = 0; p.seq = 0;
+    p.qh = 0; p.qn = 0; p.nA = 0; p.fs_top = p.S; p.seq = 0;
+    p.digest = FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
+    p.n_evict = 0; p.n_forced = 0;
+    #pragma unroll
+    for (int i = 0; i < 5; i++) p.pf_ev[i] = 0;
     p.err = 0;
     p.full = (cfg->flags & ESIM_FLAG_FULL_LOG) && A.recs != nullptr;
+    p.digest_on = (cfg->flags & ESIM_FLAG_NO_DIGEST) == 0;
     p.recs = A.recs + (int64_t)pid * A.rec_cap;
     p.rec_cap = A.rec_cap;
     p.pexp = A.pexp + (int64_t)pid * A.pe_cap;
     p.pe_cap = A.pe_cap;
-    memset(&p.acc, 0, sizeof(p.acc));
-    p.acc.digest = FNV_OFFSET;
-    p.ps_orig.init(); p.ps_exec.init(); p.ps_prec.init(); p.ps_rec.init();
     if (ca && (p.E > A.Emax || A.Tmax == 0)) p.err = -1;
-    int64_t rows_before = 0;   // token rows of earlier passes (DeltaAvg counts, routing.py:83-90)
+    if (lfu && !A.has_cnt) p.err = -1;
+    int64_t rows_before = 0;
 
     for (int pass = 0; pass < tr.n_passes && !p.err; pass++) {
         p.pass_id = pass;
-        // begin_pass (eviction.py:37-45): LS current -> stale, SB decay
-        if (p.pol == ESIM_EV_LS) {
+        if (p.pol == ESIM_EV_LS) {                                        // begin_pass (eviction.py:262-268)
             for (int s = p.lane; s < p.S; s += 32) p.key[s] &= ~LS_CURRENT;
-        } else if (p.pol == ESIM_EV_SB) {
+        } else if (p.pol == ESIM_EV_SB) {                                 // eviction.py:195-197
             for (int s = p.lane; s < p.S; s += 32)
                 if (p.res_ident[s] >= 0)
                     p.key[s] = (uint64_t)__double_as_longlong(
                         __dmul_rn(__longlong_as_double((long long)p.key[s]), cfg->sb_decay));
         }
         __syncwarp();
-        int64_t pstart = p.now, pblocked = 0;
+        const int64_t pstart = p.now;
+        int64_t pblocked = 0;
         for (int l = 0; l < p.L && !p.err; l++) {
             p.layer = l;
             const int64_t ev = (int64_t)pass * p.L + l;
@@ -999,49 +1063,38 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs A) {
             const double* d_sum;
             if (ca) {
                 nd = route_cache_aware(p, tr, ev, T, rows_before);
-                d_exp = p.dem_expert_s;
-                // gather sorted arrays (rank/gate/sum/tokens are indexed by expert)
-                d_rank = p.dem_rank_s; d_gate = p.dem_gate_s; d_sum = p.dem_summed_s; d_tok = p.dem_tokens_s;
+                d_exp = p.dem_expert_s; d_rank = p.dem_rank_s; d_gate = p.dem_gate_s;
+                d_sum = p.dem_summed_s; d_tok = p.dem_tokens_s;
             } else {
                 nd = R.n_dem[ev];
-                d_exp = R.dem_expert + ev * p.E;
-                d_rank = R.dem_rank + ev * p.E;
-                d_gate = R.dem_gate + ev * p.E;
-                d_sum = R.dem_summed + ev * p.E;
-                d_tok = R.dem_tokens + ev * p.E;
+                d_exp = R.dem_expert + ev * p.E; d_rank = R.dem_rank + ev * p.E; d_gate = R.dem_gate + ev * p.E;
+                d_sum = R.dem_summed + ev * p.E; d_tok = R.dem_tokens + ev * p.E;
             }
-            // layer scores in demand order (for fetch_priority); reuse the tofetch area? use a
-            // register-free path: read gate by position
-            float* lscores = p.lsc;
-            if (cfg->miss == ESIM_MISS_FETCH_PRIORITY) {
-                for (int i = p.lane; i < nd; i += 32) {
-                    int e = d_exp[i];
-                    lscores[i] = ca ? d_gate[e] : d_gate[i];
-                }
+            if (cfg->miss == ESIM_MISS_FETCH_PRIORITY) {                  // layer scores in demand order
+                for (int i = p.lane; i < nd; i += 32) p.lsc[i] = ca ? d_gate[d_exp[i]] : d_gate[i];
                 __syncwarp();
             }
-            // prefetch precision/recall for this (pass, layer) as a target (metrics.py:150-187)
-            if (cfg->prefetch != ESIM_PF_NONE && l >= 1) {
+            if (cfg->prefetch != ESIM_PF_NONE && l >= 1) {                // prefetch P/R (metrics.py:150-187)
                 for (int i = p.lane; i < (p.E + 31) / 32; i += 32) p.demmask[i] = 0;
                 __syncwarp();
                 for (int i = p.lane; i < nd; i += 32) atomicOr(&p.demmask[d_exp[i] >> 5], 1u << (d_exp[i] & 31));
                 __syncwarp();
-                int np = R.n_pred[ev];
+                const int np = R.n_pred[ev];
                 int inter = 0;
                 for (int j = p.lane; j < np; j += 32) {
-                    int e = R.pred_expert[ev * p.E + j];
+                    const int e = R.pred_expert[ev * p.E + j];
                     inter += (p.demmask[e >> 5] >> (e & 31)) & 1;
                 }
                 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) inter += __shfl_xor_sync(FULL, inter, o);
-                p.acc.pf_tp += inter;
-                p.acc.pf_pred_total += np;
-                p.acc.pf_dem_total += nd;
-                p.acc.pf_records++;
-                if (np) { p.ps_prec.add(__ddiv_rn((double)inter, (double)np)); p.acc.pf_prec_parts++; }
-                else p.acc.pf_empty++;
-                p.ps_rec.add(__ddiv_rn((double)inter, (double)nd));
-                p.acc.pf_rec_parts++;
+                if (p.lane == 0) {
+                    Ctr* c = p.ctr;
+                    c->pf_tp += inter; c->pf_pred += np; c->pf_dem += nd; c->pf_records++;
+                    if (np) c->pf_prec_parts++; else c->pf_empty++;
+                    c->pf_rec_parts++;
+                }
+                if (np) ps_add(p, 2, __ddiv_rn((double)inter, (double)np));
+                ps_add(p, 3, __ddiv_rn((double)inter, (double)nd));
             }
             int64_t blocked = 0;
             double wdelta = 0.0;
@@ -1051,11 +1104,11 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs A) {
                 __syncwarp();
             }
             for (int i = 0; i < nd && !p.err; i++) {
-                int e = d_exp[i];
-                int k = ca ? e : i;
+                const int e = d_exp[i];
+                const int k = ca ? e : i;
                 int64_t b;
                 double wd;
-                int oc = handle_demand(p, e, d_rank[k], d_gate[k], d_sum[k], d_tok[k], lscores, nd, b, wd);
+                const int oc = handle_demand(p, e, d_rank[k], d_gate[k], d_sum[k], d_tok[k], nd, b, wd);
                 blocked += b;
                 wdelta = __dadd_rn(wdelta, wd);
                 if (oc == 3 || oc == 4) {
@@ -1065,33 +1118,28 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs A) {
                 }
             }
             if (p.err) break;
-            // RouteRec (engine.py:625-643)
-            int faithful = T, nmod = 0;
-            if (ca) {
+            int faithful = T, nmod = 0;                                   // RouteRec (engine.py:625-643)
+            if (ca || any_aff) {
+                const int16_t* rsel = ca ? p.ca_sel : R.row_sel + tr.row_offset[ev] * p.K;
                 int bad = 0;
                 for (int r = p.lane; r < T; r += 32) {
-                    bool hit = p.ca_mod[r] != 0;
-                    nmod += p.ca_mod[r];
+                    bool hit = ca && p.ca_mod[r] != 0;
+                    if (ca) nmod += p.ca_mod[r];
                     if (any_aff)
-                        for (int j = 0; j < p.K; j++) { int s = p.ca_sel[r * p.K + j]; hit |= (p.demmask[s >> 5] >> (s & 31)) & 1; }
+                        for (int j = 0; j < p.K; j++) {
+                            const int s = rsel[r * p.K + j];
+                            hit |= (p.demmask[s >> 5] >> (s & 31)) & 1;
+                        }
                     bad += hit;
                 }
                 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) { bad += __shfl_xor_sync(FULL, bad, o); nmod += __shfl_xor_sync(FULL, nmod, o); }
-                faithful = T - bad;
-            } else if (any_aff) {
-                int bad = 0;
-                const int16_t* rs = R.row_sel + tr.row_offset[ev] * p.K;
-                for (int r = p.lane; r < T; r += 32) {
-                    bool hit = false;
-                    for (int j = 0; j < p.K; j++) { int s = rs[r * p.K + j]; hit |= (p.demmask[s >> 5] >> (s & 31)) & 1; }
-                    bad += hit;
+                for (int o = 16; o > 0; o >>= 1) {
+                    bad += __shfl_xor_sync(FULL, bad, o);
+                    nmod += __shfl_xor_sync(FULL, nmod, o);
                 }
-                #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(FULL, bad, o);
                 faithful = T - bad;
             }
-            double origm = R.sel_mass[ev];
+            const double origm = R.sel_mass[ev];
             double selm = origm;
             if (ca) {
                 PySum outer;
@@ -1104,67 +1152,85 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs A) {
                 }
                 selm = outer.value();
             }
-            double exm = __dadd_rn(selm, wdelta);
-            {
-                EsimRec r;
-                r.kind = ESIM_REC_ROUTE; r.pass_id = pass; r.layer = l;
-                r.i0 = T; r.i1 = faithful; r.i2 = nmod; r.i3 = 0; r.i4 = 0;
-                r.t0 = 0; r.t1 = __double_as_longlong(origm); r.t2 = __double_as_longlong(exm); r.x0 = selm;
-                emit(p, r, nullptr, 0);
+            const double exm = __dadd_rn(selm, wdelta);
+            emit(p, ESIM_REC_ROUTE, l, T, faithful, nmod, 0, 0, 0, __double_as_longlong(origm),
+                 __double_as_longlong(exm), selm);
+            if (p.lane == 0) {
+                p.ctr->rows_total += T; p.ctr->faithful += faithful; p.ctr->modified += nmod;
             }
-            p.acc.rows_total += T; p.acc.faithful_rows += faithful; p.acc.modified_rows += nmod;
-            p.ps_orig.add(origm);
-            p.ps_exec.add(exm);
+            ps_add(p, 0, origm);
+            ps_add(p, 1, exm);
             if (cfg->prefetch != ESIM_PF_NONE && l + 1 < p.L) submit_prefetches(p, R, ev + 1);
             advance_to(p, p.now + cfg->compute_us);
             pblocked += blocked;
         }
         if (p.err) break;
-        EsimRec r;
-        r.kind = ESIM_REC_PASS; r.pass_id = pass; r.layer = 0;
-        r.i0 = tr.pass_kind[pass]; r.i1 = tr.pass_tokens[pass]; r.i2 = 0; r.i3 = 0; r.i4 = 0;
-        r.t0 = pstart; r.t1 = p.now; r.t2 = pblocked; r.x0 = 0.0;
-        emit(p, r, nullptr, 0);
-        p.acc.passes++;
-        if (pass == 0) p.acc.ttft_us = p.now;
-        p.acc.total_us = p.now;
-        if (tr.pass_kind[pass] == 1) { p.acc.decode_passes++; p.acc.decode_us += p.now - pstart; }
+        emit(p, ESIM_REC_PASS, 0, tr.pass_kind[pass], tr.pass_tokens[pass], 0, 0, 0, pstart, p.now, pblocked, 0.0);
+        if (p.lane == 0) {
+            Ctr* c = p.ctr;
+            c->passes++;
+            if (pass == 0) c->ttft = p.now;
+            c->total = p.now;
+            if (tr.pass_kind[pass] == 1) { c->decode_passes++; c->decode_us += p.now - pstart; }
+        }
         rows_before += tr.pass_tokens[pass];
     }
-    p.acc.original_mass = p.ps_orig.value();
-    p.acc.executed_mass = p.ps_exec.value();
-    p.acc.pf_prec_sum = p.ps_prec.value();
-    p.acc.pf_rec_sum = p.ps_rec.value();
-    p.acc.status = p.err;
     __syncwarp();
-    if (p.lane == 0) A.counters[pid] = p.acc;
+    if (p.lane == 0) {
+        const Ctr* c = p.ctr;
+        EsimCounters* o = &A.counters[pid];
+        for (int i = 0; i < 8; i++) {
+            int64_t t = 0;
+            for (int l = 0; l < p.L; l++) t += p.pl[l * ESIM_PL_FIELDS + i];
+            o->totals[i] = t;
+        }
+        o->totals[8] = p.n_evict;
+        o->totals[9] = p.n_forced;
+        for (int i = 0; i < 5; i++) o->totals[10 + i] = p.pf_ev[i];
+        o->ttft_us = c->ttft; o->total_us = c->total; o->decode_us = c->decode_us;
+        o->sync_overhead_us = c->sync_overhead; o->passes = c->passes; o->decode_passes = c->decode_passes;
+        o->rows_total = c->rows_total; o->faithful_rows = c->faithful; o->modified_rows = c->modified;
+        o->pf_tp = c->pf_tp; o->pf_pred_total = c->pf_pred; o->pf_dem_total = c->pf_dem;
+        o->pf_records = c->pf_records; o->pf_empty = c->pf_empty; o->pf_prec_parts = c->pf_prec_parts;
+        o->pf_rec_parts = c->pf_rec_parts;
+        o->ls_forced = c->ls_forced; o->ls_unforced = 0; o->ls_refusals = c->ls_refusals;
+        o->n_recs = p.n_recs; o->n_pred_experts = p.n_pe; o->digest = p.digest;
+        double* vo = &o->original_mass;
+        for (int i = 0; i < 4; i++) {
+            const double f = c->ps[2 * i], cc = c->ps[2 * i + 1];
+            vo[i] = (cc != 0.0 && isfinite(cc)) ? __dadd_rn(f, cc) : f;
+        }
+        o->status = p.err;
+        o->pad[0] = o->pad[1] = o->pad[2] = 0;
+    }
     int64_t* plo = A.per_layer + (int64_t)pid * A.Lmax * ESIM_PL_FIELDS;
-    for (int i = p.lane; i < p.L * ESIM_PL_FIELDS; i += 32) plo[i] = p.pl[i];
+    for (int i = p.lane; i < A.Lmax * ESIM_PL_FIELDS; i += 32) plo[i] = i < p.L * ESIM_PL_FIELDS ? p.pl[i] : 0;
 }
 
 }  // namespace esim
 
-int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca) {
-    return esim::make_layout(N, S, Q, L, E, T, K, ca).total;
+int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt) {
+    return esim::make_layout(N, S, Q, L, E, T, K, ca, has_cnt).total;
 }
 
 cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTraceDesc* d_traces,
                                     const EsimRouterOut* d_routers, EsimCounters* d_counters,
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
-                                    int warps_per_cta, cudaStream_t st) {
+                                    bool has_cnt, int warps_per_cta, cudaStream_t st) {
     esim::ReplayArgs a;
     a.cfg = d_cfg; a.n_points = n; a.traces = d_traces; a.routers = d_routers;
     a.counters = d_counters; a.per_layer = d_per_layer; a.recs = d_recs; a.rec_cap = rec_cap;
     a.pexp = d_pexp; a.pe_cap = pe_cap;
     a.N = N; a.S = S; a.Q = Q; a.Lmax = Lmax; a.Emax = Emax; a.Tmax = Tmax; a.Kmax = Kmax;
+    a.has_cnt = has_cnt ? 1 : 0;
     a.warps_per_cta = warps_per_cta;
-    a.point_bytes = esim::make_layout(N, S, Q, Lmax, Emax, Tmax, Kmax, Tmax > 0).total;
-    size_t smem = (size_t)a.point_bytes * warps_per_cta;
+    a.point_bytes = esim::make_layout(N, S, Q, Lmax, Emax, Tmax, Kmax, Tmax > 0, has_cnt).total;
+    const size_t smem = (size_t)a.point_bytes * warps_per_cta;
     cudaError_t e = cudaFuncSetAttribute(esim::replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    int blocks = (n + warps_per_cta - 1) / warps_per_cta;
+    const int blocks = (n + warps_per_cta - 1) / warps_per_cta;
     esim::replay_kernel<<<blocks, 32 * warps_per_cta, smem, st>>>(a);
     return cudaGetLastError();
 }

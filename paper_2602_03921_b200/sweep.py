@@ -124,10 +124,10 @@ class DeviceSweep:
     """Grid points staged in HBM; `step()` = router over every trace +
     replay of every point (one warp each), all on one stream."""
 
-    def __init__(self, cfgs, traces):
+    def __init__(self, cfgs, traces, digest: bool = True):
         from ._device import ReplayBatch
         self.cfgs, self.traces = list(cfgs), list(traces)
-        self.batch = ReplayBatch(self.cfgs, self.traces, full_log=False)
+        self.batch = ReplayBatch(self.cfgs, self.traces, full_log=False, digest=digest)
 
     def route(self, stream=None) -> None:
         from ._device import PREFETCH_CODE, _check, lib

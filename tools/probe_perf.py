@@ -23,10 +23,10 @@ acc = sum(c.totals[0] for c in cs)
 out["oracle_1thr_s"] = dt1; out["accesses_seed1"] = acc; out["oracle_1thr_acc_s"] = acc / dt1
 t0 = time.perf_counter(); cs16, _ = oracle.run_batch(ccfg, tl, os.cpu_count()); dtn = time.perf_counter() - t0
 out["oracle_nthr_s"] = dtn; out["oracle_nthr_acc_s"] = acc / dtn; out["threads"] = os.cpu_count()
-for S in (1, 4, 16, 48):
+for S, dg in ((1, True), (16, True), (48, True), (48, False), (96, True)):
     tt = traces(list(range(1, S + 1)))
     cfgs, trs = c5_points(tt)
-    ds = DeviceSweep(cfgs, trs)
+    ds = DeviceSweep(cfgs, trs, digest=dg)
     st = torch.cuda.current_stream()
     for _ in range(2): ds.step()
     torch.cuda.synchronize()
@@ -34,9 +34,9 @@ for S in (1, 4, 16, 48):
     e0.record(); ds.route(); e1.record(); ds.replay(); e2.record(); torch.cuda.synchronize()
     res = ds.results()
     a = sum(r.counters.totals[0] for r in res)
-    out[f"S{S}"] = {"points": len(cfgs), "accesses": a, "route_ms": e0.elapsed_time(e1), "replay_ms": e1.elapsed_time(e2),
+    out[f"S{S}{dg}"] = {"points": len(cfgs), "accesses": a, "route_ms": e0.elapsed_time(e1), "replay_ms": e1.elapsed_time(e2),
                     "acc_per_s": a / (e0.elapsed_time(e2) / 1e3)}
-    print(S, out[f"S{S}"], flush=True)
+    print(S, dg, out[f"S{S}{dg}"], flush=True)
 # digest check vs oracle for S=1
 ds = DeviceSweep(*c5_points(t1)); ds.step(); res = ds.results()
 out["digest_match_seed1"] = all(r.counters.digest == c.digest for r, c in zip(res, cs))
