@@ -230,6 +230,8 @@ def main():
     # ---- e2e through the C ABI with host buffers ------------------------
     e2e = None
     if not args.no_e2e:
+        from paper_2602_03921_b200.sweep import pin_traces
+        pin_traces(trs)                     # inputs live in pinned host memory
         for _ in range(max(1, args.warmup)):
             run_grid_host(cfgs, trs)
         h2d = sum(t.packed().logits.nbytes + t.packed().row_offset.nbytes + t.packed().pass_tokens.nbytes * 2

@@ -30,6 +30,7 @@
 #ifndef SPECMD_B200_H
 #define SPECMD_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -132,6 +133,10 @@ typedef struct {
 } EsimRouterOut;
 
 const char *esim_last_error(void);
+/* Page-lock / release a caller-owned host buffer (trace arrays) so that
+ * esim_run_host's host->device copies run as asynchronous DMA. */
+int esim_host_register(void *ptr, size_t bytes);
+int esim_host_unregister(void *ptr);
 int esim_version(void);
 
 /* Fused router over a whole trace: one CTA per event. `trace` and `out`
@@ -139,6 +144,18 @@ int esim_version(void);
  * select the next-layer predictor (prefetch.py:67-107). */
 int esim_router_launch(const EsimTraceDesc *trace, const EsimRouterOut *out,
                        int32_t pred_mode, double overfetch, double percentile, void *stream);
+
+/* The same over many traces in ONE launch (one CTA per event of every
+ * trace). Device arrays: traces[n], outs[n], params[n][4] = {pred_mode,
+ * pred_count, pred_clamped, pct_rank} (see esim_predictor_params), prefix[n+1]
+ * event prefix sums. */
+int esim_router_launch_batch(const EsimTraceDesc *d_traces, const EsimRouterOut *d_outs,
+                             const int32_t *d_params, const int64_t *d_prefix, int32_t n_traces,
+                             int64_t total_events, int32_t max_experts, void *stream);
+/* Host helper: the predictor constants the router uses, computed in double
+ * exactly as the reference does (prefetch.py:35, 48). out[4] as above. */
+int esim_predictor_params(int32_t top_k, int32_t experts, int32_t pred_mode, double overfetch,
+                          double percentile, int32_t *out4);
 
 /* Plug-in kernels behind routing.softmax_rows / topk_indices (routing.py:22-35):
  * one warp per row, numpy-exact. Device pointers. */
@@ -155,9 +172,10 @@ int esim_replay_smem_per_point(const EsimConfig *h_cfg, int32_t n, int32_t max_t
  * per_layer[n][pl_stride][ESIM_PL_FIELDS], and with ESIM_FLAG_FULL_LOG,
  * recs[n][rec_cap] + pred_experts[n][pe_cap]. max_tokens = largest token
  * count of any event (cache-aware scratch). warps_per_cta 0 = auto.
- * queue_cap: channel ring entries; 0 = default (64), -1 = exact bound
- * (resident slots + 1). A point whose channel outgrows the ring stops with
- * counters.status = -5; the caller re-launches it with queue_cap = -1. */
+ * queue_cap: channel ring entries; <= 0 = the exact bound (resident slots
+ * + 1, cannot overflow). A smaller positive cap saves shared memory; a point
+ * whose channel outgrows it stops with counters.status = -5 and must be
+ * re-launched with queue_cap = 0. */
 int esim_replay_launch(const EsimConfig *h_cfg, const EsimConfig *d_cfg, int32_t n,
                        const EsimTraceDesc *d_traces, const EsimRouterOut *d_routers, int32_t max_tokens,
                        EsimCounters *d_counters, int64_t *d_per_layer, int32_t pl_stride,

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -35,6 +37,18 @@ static int cuda_fail(cudaError_t e, const char* where) {
 }
 
 extern "C" const char* esim_last_error(void) { return g_err.c_str(); }
+
+// page-lock a caller buffer so the host API's copies are true async DMA
+extern "C" int esim_host_register(void* p, size_t bytes) {
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) { cudaGetLastError(); return 0; }
+    return e == cudaSuccess ? 0 : cuda_fail(e, "cudaHostRegister");
+}
+extern "C" int esim_host_unregister(void* p) {
+    cudaError_t e = cudaHostUnregister(p);
+    if (e == cudaErrorHostMemoryNotRegistered) { cudaGetLastError(); return 0; }
+    return e == cudaSuccess ? 0 : cuda_fail(e, "cudaHostUnregister");
+}
 extern "C" int esim_version(void) { return 1; }
 
 // predictor constants resolved on the host exactly as the reference does in
@@ -47,6 +61,14 @@ static void predictor_consts(int k, int E, double overfetch, double percentile, 
     *count = (int)std::min<double>(c, (double)E);
     long r = (long)std::ceil(percentile / 100.0 * (double)E);
     *rank = (int)std::max<long>(1, r);
+}
+
+extern "C" int esim_predictor_params(int32_t k, int32_t E, int32_t mode, double overfetch, double percentile,
+                                     int32_t* out4) {
+    int count, clamped, rank;
+    predictor_consts(k, E, overfetch, percentile, &count, &clamped, &rank);
+    out4[0] = mode; out4[1] = count; out4[2] = clamped; out4[3] = rank;
+    return 0;
 }
 
 extern "C" int esim_router_launch(const EsimTraceDesc* tr, const EsimRouterOut* out, int32_t pred_mode,
@@ -63,8 +85,10 @@ extern "C" int esim_router_launch(const EsimTraceDesc* tr, const EsimRouterOut* 
 
 struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca, has_cnt; };
 
-// queue_cap 0 = default ring size (64 entries, overflow -> status -5 and the
-// caller re-launches with the exact bound queue_cap = -1: slots + 1)
+// queue_cap <= 0: the exact bound (resident slots + 1 entries: every queued
+// transfer holds a reservation of >= the smallest expert, so the channel can
+// never outgrow it). A positive cap trades shared memory for the risk of
+// status -5, which the caller resolves by re-launching with the bound.
 static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stride, int queue_cap, Sizing* z) {
     Sizing s{0, 1, 2, 0, 0, 0, 0, false, false};
     for (int i = 0; i < n; i++) {
@@ -86,7 +110,7 @@ static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stri
         if (c.eviction == ESIM_EV_LFU || c.eviction == ESIM_EV_LHU) s.has_cnt = true;
     }
     if (s.S > 4095) return fail(-1, "more than 4095 resident experts per cache is not supported by the device directory");
-    s.Q = queue_cap > 0 ? std::min(queue_cap, s.S + 1) : queue_cap < 0 ? s.S + 1 : std::min(64, s.S + 1);
+    s.Q = queue_cap > 0 ? std::min(queue_cap, s.S + 1) : s.S + 1;
     s.Tmax = s.ca ? std::max(1, max_tokens) : 0;
     if (pl_stride < s.Lmax) return fail(-1, "per-layer stride smaller than num_layers");
     s.Lmax = pl_stride;
@@ -127,6 +151,10 @@ extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_c
 // ---------------------------------------------------------------------------
 // end-to-end host API: host buffers in, host results out
 // ---------------------------------------------------------------------------
+extern "C" int esim_router_launch_batch(const EsimTraceDesc* d_traces, const EsimRouterOut* d_outs,
+                                        const int32_t* d_params, const int64_t* d_prefix, int32_t n_traces,
+                                        int64_t total_events, int32_t max_experts, void* stream);
+
 namespace {
 struct DevBuf {
     void* p = nullptr;
@@ -142,9 +170,27 @@ struct DevBuf {
     }
 };
 
+struct HostBuf {                        // grow-only pinned staging
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMallocHost(&p, n);
+        if (e == cudaSuccess) cap = n;
+        return e;
+    }
+};
+
 struct HostCtx {
+    HostBuf stage;
     cudaStream_t st = nullptr;
-    std::vector<DevBuf> bufs;
+    std::vector<cudaStream_t> gs;       // one per geometry group (concurrent replays)
+    std::vector<cudaEvent_t> ge;
+    cudaEvent_t routed = nullptr;
+    DevBuf slab;
 };
 
 HostCtx& ctx() {
@@ -160,51 +206,81 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
                              int64_t rec_cap, int32_t* pred_experts, int64_t pe_cap) {
     HostCtx& C = ctx();
     cudaError_t e;
+    const bool prof = getenv("ESIM_PROFILE_HOST") != nullptr;
+    auto now_ms = []() { return std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double t_start = now_ms();
     if (!C.st) {
-        e = cudaStreamCreateWithFlags(&C.st, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return cuda_fail(e, "stream");
+        if ((e = cudaStreamCreateWithFlags(&C.st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+        if ((e = cudaEventCreateWithFlags(&C.routed, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
     }
-    // predictor params per trace: taken from the first config that uses it
-    std::vector<int> pmode(n_traces, 0);
-    std::vector<double> pover(n_traces, 1.0), ppct(n_traces, 80.0);
+    if (n <= 0) return 0;
+    // predictor per trace (taken from the first config using it)
+    std::vector<int32_t> params(4 * n_traces, 0);
     std::vector<char> seen(n_traces, 0);
+    std::vector<double> pover(n_traces), ppct(n_traces);
     for (int i = 0; i < n; i++) {
-        int t = cfg[i].trace_id;
+        const int t = cfg[i].trace_id;
         if (t < 0 || t >= n_traces) return fail(-1, "trace_id out of range");
-        if (!seen[t]) { seen[t] = 1; pmode[t] = cfg[i].prefetch; pover[t] = cfg[i].overfetch; ppct[t] = cfg[i].percentile; }
-        else if (pmode[t] != cfg[i].prefetch || pover[t] != cfg[i].overfetch || ppct[t] != cfg[i].percentile)
+        if (!seen[t]) {
+            seen[t] = 1;
+            pover[t] = cfg[i].overfetch;
+            ppct[t] = cfg[i].percentile;
+            esim_predictor_params(traces[t].top_k, traces[t].experts, cfg[i].prefetch, cfg[i].overfetch,
+                                  cfg[i].percentile, &params[4 * t]);
+        } else if (params[4 * t] != cfg[i].prefetch || pover[t] != cfg[i].overfetch || ppct[t] != cfg[i].percentile) {
             return fail(-1, "configs sharing a trace_id must share the predictor");
+        }
     }
-    // one device slab: traces, router outputs, configs, outputs
+    // geometry groups (stable), each replayed on its own stream with its own shared-memory sizing
+    std::vector<int> order(n);
+    for (int i = 0; i < n; i++) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return std::make_pair(cfg[a].num_layers, cfg[a].experts) < std::make_pair(cfg[b].num_layers, cfg[b].experts);
+    });
+    std::vector<std::pair<int, int>> groups;   // [begin, end) in `order`
+    for (int i = 0; i < n; i++) {
+        if (i == 0 || cfg[order[i]].num_layers != cfg[order[i - 1]].num_layers ||
+            cfg[order[i]].experts != cfg[order[i - 1]].experts)
+            groups.push_back({i, i + 1});
+        else
+            groups.back().second = i + 1;
+    }
+    std::vector<EsimConfig> pcfg(n);
+    for (int i = 0; i < n; i++) pcfg[i] = cfg[order[i]];
+    // one device slab: traces, router outputs, tables, configs, outputs
     size_t total = 0;
     std::vector<size_t> toff(n_traces), roff(n_traces);
-    int max_tokens = 0;
+    std::vector<int64_t> prefix(n_traces + 1, 0);
+    int max_tokens = 0, max_e = 1;
     for (int t = 0; t < n_traces; t++) {
         const EsimTraceDesc& d = traces[t];
-        int64_t ne = d.n_events, nr = d.n_rows_total, E = d.experts, K = d.top_k;
+        const int64_t ne = d.n_events, nr = d.n_rows_total, E = d.experts, K = d.top_k;
         toff[t] = total;
         total += al256(d.n_passes * 4) * 2 + al256((ne + 1) * 8) + al256(nr * E * 4);
         roff[t] = total;
         total += al256(ne * 4) * 3 + al256(ne * E * 4) * 6 + al256(ne * E * 8) + al256(ne * 8) +
-                 al256(nr * K * 2) + al256(nr * K * 4) + al256(ne * 4);
+                 al256(nr * K * 2) + al256(nr * K * 4);
+        prefix[t + 1] = prefix[t] + ne;
+        max_e = std::max(max_e, (int)E);
         for (int p = 0; p < d.n_passes; p++) max_tokens = std::max(max_tokens, d.pass_tokens[p]);
     }
-    size_t cfg_off = total; total += al256(sizeof(EsimConfig) * n);
-    size_t td_off = total; total += al256(sizeof(EsimTraceDesc) * n_traces);
-    size_t rd_off = total; total += al256(sizeof(EsimRouterOut) * n_traces);
-    size_t cnt_off = total; total += al256(sizeof(EsimCounters) * n);
-    size_t pl_off = total; total += al256(sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS);
-    size_t rec_off = total; total += recs ? al256(sizeof(EsimRec) * n * rec_cap) : 0;
-    size_t pe_off = total; total += recs ? al256(sizeof(int32_t) * n * pe_cap) : 0;
-    if (C.bufs.empty()) C.bufs.resize(1);
-    e = C.bufs[0].ensure(total);
-    if (e != cudaSuccess) return cuda_fail(e, "device alloc");
-    char* base = (char*)C.bufs[0].p;
+    const size_t cfg_off = total; total += al256(sizeof(EsimConfig) * n);
+    const size_t td_off = total; total += al256(sizeof(EsimTraceDesc) * n_traces);
+    const size_t rd_off = total; total += al256(sizeof(EsimRouterOut) * n_traces);
+    const size_t par_off = total; total += al256(sizeof(int32_t) * 4 * n_traces);
+    const size_t pre_off = total; total += al256(sizeof(int64_t) * (n_traces + 1));
+    const size_t cnt_off = total; total += al256(sizeof(EsimCounters) * n);
+    const size_t pl_off = total; total += al256(sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS);
+    const size_t rec_off = total; total += recs ? al256(sizeof(EsimRec) * n * rec_cap) : 0;
+    const size_t pe_off = total; total += recs ? al256(sizeof(int32_t) * n * pe_cap) : 0;
+    if ((e = C.slab.ensure(total)) != cudaSuccess) return cuda_fail(e, "device alloc");
+    char* base = (char*)C.slab.p;
     std::vector<EsimTraceDesc> dtr(n_traces);
     std::vector<EsimRouterOut> dro(n_traces);
     for (int t = 0; t < n_traces; t++) {
         const EsimTraceDesc& h = traces[t];
-        int64_t ne = h.n_events, nr = h.n_rows_total, E = h.experts, K = h.top_k;
+        const int64_t ne = h.n_events, nr = h.n_rows_total, E = h.experts, K = h.top_k;
         char* q = base + toff[t];
         EsimTraceDesc d = h;
         auto put = [&](const void* src, size_t bytes) -> void* {
@@ -219,8 +295,8 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
         d.logits = (const float*)put(h.logits, nr * E * 4);
         dtr[t] = d;
         char* r = base + roff[t];
-        EsimRouterOut o;
         auto take = [&](size_t bytes) -> void* { void* x = r; r += al256(bytes); return x; };
+        EsimRouterOut o;
         o.n_dem = (int32_t*)take(ne * 4);
         o.n_pred = (int32_t*)take(ne * 4);
         o.pred_clamped = (int32_t*)take(ne * 4);
@@ -235,49 +311,92 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
         o.row_sel = (int16_t*)take(nr * K * 2);
         o.row_w = (float*)take(nr * K * 4);
         dro[t] = o;
-        int rc = esim_router_launch(&d, &o, pmode[t], pover[t], ppct[t], C.st);
-        if (rc) return rc;
     }
-    cudaMemcpyAsync(base + cfg_off, cfg, sizeof(EsimConfig) * n, cudaMemcpyHostToDevice, C.st);
+    cudaMemcpyAsync(base + cfg_off, pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice, C.st);
     cudaMemcpyAsync(base + td_off, dtr.data(), sizeof(EsimTraceDesc) * n_traces, cudaMemcpyHostToDevice, C.st);
     cudaMemcpyAsync(base + rd_off, dro.data(), sizeof(EsimRouterOut) * n_traces, cudaMemcpyHostToDevice, C.st);
-    int rc = esim_replay_launch(cfg, (EsimConfig*)(base + cfg_off), n, (EsimTraceDesc*)(base + td_off),
-                                (EsimRouterOut*)(base + rd_off), max_tokens, (EsimCounters*)(base + cnt_off),
-                                (int64_t*)(base + pl_off), pl_stride, recs ? (EsimRec*)(base + rec_off) : nullptr,
-                                rec_cap, recs ? (int32_t*)(base + pe_off) : nullptr, pe_cap, 0, 0, C.st);
-    if (rc) return rc;
-    cudaMemcpyAsync(counters, base + cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, C.st);
-    cudaMemcpyAsync(per_layer, base + pl_off, sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS,
-                    cudaMemcpyDeviceToHost, C.st);
-    if (recs) {
-        cudaMemcpyAsync(recs, base + rec_off, sizeof(EsimRec) * n * rec_cap, cudaMemcpyDeviceToHost, C.st);
-        cudaMemcpyAsync(pred_experts, base + pe_off, sizeof(int32_t) * n * pe_cap, cudaMemcpyDeviceToHost, C.st);
+    cudaMemcpyAsync(base + par_off, params.data(), sizeof(int32_t) * 4 * n_traces, cudaMemcpyHostToDevice, C.st);
+    cudaMemcpyAsync(base + pre_off, prefix.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice, C.st);
+    double t_h2d = now_ms();
+    if (prof) { cudaStreamSynchronize(C.st); fprintf(stderr, "[esim_run_host] setup+h2d enqueue %.2f ms, h2d done %.2f ms\n", t_h2d - t_start, now_ms() - t_start); }
+    int rc = esim_router_launch_batch((EsimTraceDesc*)(base + td_off), (EsimRouterOut*)(base + rd_off),
+                                      (int32_t*)(base + par_off), (int64_t*)(base + pre_off), n_traces,
+                                      prefix[n_traces], max_e, C.st);
+    if (rc) return cuda_fail(cudaGetLastError(), "router batch");
+    while (C.gs.size() < groups.size()) {
+        cudaStream_t s2;
+        cudaEvent_t e2;
+        if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+        if ((e = cudaEventCreateWithFlags(&e2, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+        C.gs.push_back(s2);
+        C.ge.push_back(e2);
     }
-    e = cudaStreamSynchronize(C.st);
-    if (e != cudaSuccess) return cuda_fail(e, "esim_run_host");
-    bool overflow = false;
-    for (int i = 0; i < n; i++) overflow |= counters[i].status == -5;
-    if (overflow) {   // channel deeper than the default ring: replay again with the exact bound
-        rc = esim_replay_launch(cfg, (EsimConfig*)(base + cfg_off), n, (EsimTraceDesc*)(base + td_off),
-                                (EsimRouterOut*)(base + rd_off), max_tokens, (EsimCounters*)(base + cnt_off),
-                                (int64_t*)(base + pl_off), pl_stride, recs ? (EsimRec*)(base + rec_off) : nullptr,
-                                rec_cap, recs ? (int32_t*)(base + pe_off) : nullptr, pe_cap, 0, -1, C.st);
-        if (rc) return rc;
-        cudaMemcpyAsync(counters, base + cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, C.st);
-        cudaMemcpyAsync(per_layer, base + pl_off, sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS,
-                        cudaMemcpyDeviceToHost, C.st);
-        if (recs) {
-            cudaMemcpyAsync(recs, base + rec_off, sizeof(EsimRec) * n * rec_cap, cudaMemcpyDeviceToHost, C.st);
-            cudaMemcpyAsync(pred_experts, base + pe_off, sizeof(int32_t) * n * pe_cap, cudaMemcpyDeviceToHost, C.st);
+    auto replay_groups = [&](int queue_cap, const std::vector<char>& which) -> int {
+        cudaEventRecord(C.routed, C.st);
+        for (size_t g = 0; g < groups.size(); g++) {
+            if (!which[g]) continue;
+            const int b = groups[g].first, m = groups[g].second - b;
+            cudaStreamWaitEvent(C.gs[g], C.routed, 0);
+            int r2 = esim_replay_launch(pcfg.data() + b, (EsimConfig*)(base + cfg_off) + b, m,
+                                        (EsimTraceDesc*)(base + td_off), (EsimRouterOut*)(base + rd_off), max_tokens,
+                                        (EsimCounters*)(base + cnt_off) + b,
+                                        (int64_t*)(base + pl_off) + (size_t)b * pl_stride * ESIM_PL_FIELDS, pl_stride,
+                                        recs ? (EsimRec*)(base + rec_off) + (size_t)b * rec_cap : nullptr, rec_cap,
+                                        recs ? (int32_t*)(base + pe_off) + (size_t)b * pe_cap : nullptr, pe_cap, 0,
+                                        queue_cap, C.gs[g]);
+            if (r2) return r2;
+            cudaEventRecord(C.ge[g], C.gs[g]);
+            cudaStreamWaitEvent(C.st, C.ge[g], 0);
         }
-        e = cudaStreamSynchronize(C.st);
-        if (e != cudaSuccess) return cuda_fail(e, "esim_run_host");
+        return 0;
+    };
+    if (prof) { cudaStreamSynchronize(C.st); fprintf(stderr, "[esim_run_host] router done %.2f ms\n", now_ms() - t_start); }
+    std::vector<char> all(groups.size(), 1);
+    if ((rc = replay_groups(0, all))) return rc;
+    if (prof) { cudaStreamSynchronize(C.st); fprintf(stderr, "[esim_run_host] replay done %.2f ms (%zu groups)\n", now_ms() - t_start, groups.size()); }
+    const size_t pls = (size_t)pl_stride * ESIM_PL_FIELDS;
+    const size_t st_cnt = al256(sizeof(EsimCounters) * n), st_pl = al256(sizeof(int64_t) * n * pls);
+    const size_t st_rec = recs ? al256(sizeof(EsimRec) * n * rec_cap) : 0;
+    const size_t st_pe = recs ? al256(sizeof(int32_t) * n * pe_cap) : 0;
+    if ((e = C.stage.ensure(st_cnt + st_pl + st_rec + st_pe)) != cudaSuccess) return cuda_fail(e, "pinned staging");
+    EsimCounters* pc = (EsimCounters*)C.stage.p;
+    int64_t* ppl = (int64_t*)((char*)C.stage.p + st_cnt);
+    EsimRec* prec_ = (EsimRec*)((char*)C.stage.p + st_cnt + st_pl);
+    int32_t* ppe = (int32_t*)((char*)C.stage.p + st_cnt + st_pl + st_rec);
+    cudaMemcpyAsync(pc, base + cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, C.st);
+    if ((e = cudaStreamSynchronize(C.st)) != cudaSuccess) return cuda_fail(e, "esim_run_host");
+    std::vector<char> redo(groups.size(), 0);
+    bool any = false;
+    for (size_t g = 0; g < groups.size(); g++)
+        for (int i = groups[g].first; i < groups[g].second; i++)
+            if (pc[i].status == -5) { redo[g] = 1; any = true; }
+    if (any) {   // a channel outgrew the default ring: those groups again with the exact bound
+        if ((rc = replay_groups(-1, redo))) return rc;
+        cudaMemcpyAsync(pc, base + cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, C.st);
     }
+    cudaMemcpyAsync(ppl, base + pl_off, sizeof(int64_t) * n * pls, cudaMemcpyDeviceToHost, C.st);
+    if (recs) {
+        cudaMemcpyAsync(prec_, base + rec_off, sizeof(EsimRec) * n * rec_cap, cudaMemcpyDeviceToHost, C.st);
+        cudaMemcpyAsync(ppe, base + pe_off, sizeof(int32_t) * n * pe_cap, cudaMemcpyDeviceToHost, C.st);
+    }
+    if ((e = cudaStreamSynchronize(C.st)) != cudaSuccess) return cuda_fail(e, "esim_run_host");
+    if (prof) fprintf(stderr, "[esim_run_host] d2h done %.2f ms\n", now_ms() - t_start);
+    for (int i = 0; i < n; i++) {           // back to the caller's order
+        const int j = order[i];
+        counters[j] = pc[i];
+        std::memcpy(per_layer + (size_t)j * pls, ppl + (size_t)i * pls, pls * sizeof(int64_t));
+        if (recs) {
+            std::memcpy(recs + (size_t)j * rec_cap, prec_ + (size_t)i * rec_cap, rec_cap * sizeof(EsimRec));
+            std::memcpy(pred_experts + (size_t)j * pe_cap, ppe + (size_t)i * pe_cap, pe_cap * sizeof(int32_t));
+        }
+    }
+    if (prof) fprintf(stderr, "[esim_run_host] total %.2f ms\n", now_ms() - t_start);
     for (int i = 0; i < n; i++)
         if (counters[i].status) {
-            int s = (int)counters[i].status;
-            return fail(s, s == -4 ? "record buffer too small" : s == -1 ? "config error during replay"
-                                                                          : "runtime invariant broken during replay");
+            const int st = (int)counters[i].status;
+            return fail(st, st == -4 ? "record buffer too small"
+                            : st == -1 ? "config error during replay (an expert exceeds the cache capacity)"
+                                       : "runtime invariant broken during replay");
         }
     return 0;
 }

@@ -51,11 +51,44 @@ __device__ __forceinline__ int warp_argmax(const float* s, int E, int lane, uint
     return bi;
 }
 
+__device__ __forceinline__ void route_event_cta(const RouterArgs& a, int64_t ev, unsigned char* smem);
+
 __global__ void __launch_bounds__(kRouterWarps * 32)
 router_kernel(RouterArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    route_event_cta(a, blockIdx.x, smem);
+}
+
+// one launch over many traces: block b -> (trace t, event b - prefix[t])
+struct RouterBatchArgs {
+    const EsimTraceDesc* traces;
+    const EsimRouterOut* outs;
+    const int32_t* params;        // [n][4]: pred_mode, pred_count, pred_clamped, pct_rank
+    const int64_t* prefix;        // [n+1] event prefix sums
+    int n;
+};
+
+__global__ void __launch_bounds__(kRouterWarps * 32)
+router_batch_kernel(RouterBatchArgs b) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int64_t g = blockIdx.x;
+    int lo = 0, hi = b.n - 1;
+    while (lo < hi) {                       // last t with prefix[t] <= g
+        const int mid = (lo + hi + 1) >> 1;
+        if (b.prefix[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    RouterArgs a;
+    a.tr = b.traces[lo];
+    a.out = b.outs[lo];
+    a.pred_mode = b.params[lo * 4 + 0];
+    a.pred_count = b.params[lo * 4 + 1];
+    a.pred_clamped = b.params[lo * 4 + 2];
+    a.pct_rank = b.params[lo * 4 + 3];
+    route_event_cta(a, g - b.prefix[lo], smem);
+}
+
+__device__ __forceinline__ void route_event_cta(const RouterArgs& a, int64_t ev, unsigned char* smem) {
     const int E = a.tr.experts, K = a.tr.top_k;
-    const int64_t ev = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* rowbuf = reinterpret_cast<float*>(smem) + warp * E;             // [warps][E]
     unsigned* best = reinterpret_cast<unsigned*>(smem) + kRouterWarps * E;  // [E] prediction union
@@ -200,6 +233,16 @@ router_kernel(RouterArgs a) {
 }
 
 }  // namespace esim
+
+extern "C" int esim_router_launch_batch(const EsimTraceDesc* d_traces, const EsimRouterOut* d_outs,
+                                        const int32_t* d_params, const int64_t* d_prefix, int32_t n_traces,
+                                        int64_t total_events, int32_t max_experts, void* stream) {
+    if (total_events <= 0) return 0;
+    esim::RouterBatchArgs b{d_traces, d_outs, d_params, d_prefix, n_traces};
+    const size_t smem = (size_t)(esim::kRouterWarps * max_experts + max_experts) * 4 + 16;
+    esim::router_batch_kernel<<<(unsigned)total_events, esim::kRouterWarps * 32, smem, (cudaStream_t)stream>>>(b);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
 
 // host launcher (declared in capi.cu)
 cudaError_t esim_router_launch_impl(const EsimTraceDesc& tr, const EsimRouterOut& out, int pred_mode,

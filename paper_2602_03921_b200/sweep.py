@@ -74,6 +74,33 @@ def _lib():
     return lib()
 
 
+def pin_traces(traces) -> None:
+    """Page-lock the packed arrays of each trace (idempotent) so run_grid_host's
+    host->device copies are DMA from pinned memory."""
+    seen = set()
+    for tr in traces:
+        if id(tr) in seen:
+            continue
+        seen.add(id(tr))
+        pk = tr.packed()
+        for a in (pk.logits, pk.row_offset, pk.pass_tokens, pk.pass_kind):
+            if a.nbytes:
+                rc = _lib().esim_host_register(a.ctypes.data, a.nbytes)
+                if rc:
+                    raise RuntimeError(_lib().esim_last_error().decode())
+
+
+_CCFG_CACHE: dict = {}
+
+
+def _c_config(cfg, trace_id: int):
+    key = (cfg, trace_id)
+    c = _CCFG_CACHE.get(key)
+    if c is None:
+        c = _CCFG_CACHE[key] = bytes(cfg.to_c(trace_id, False))
+    return c
+
+
 def run_grid_host(cfgs, traces, pl_stride: int | None = None):
     """One end-to-end C-ABI call (esim_run_host): host buffers in and out.
 
@@ -92,10 +119,10 @@ def run_grid_host(cfgs, traces, pl_stride: int | None = None):
             d, k = _abi.trace_desc_host(tr.packed())
             descs.append(d)
             keep.append(k)
-        ccfg.append(cfg.to_c(ids[key], False))
+        ccfg.append(_c_config(cfg, ids[key]))
     n = len(ccfg)
-    L = pl_stride or max(c.num_layers for c in ccfg)
-    carr = (_abi.EsimConfig * n)(*ccfg)
+    L = pl_stride or max(c.model.num_layers for c in cfgs)
+    carr = (_abi.EsimConfig * n).from_buffer_copy(b"".join(ccfg))
     darr = (_abi.EsimTraceDesc * len(descs))(*descs)
     counters = (_abi.EsimCounters * n)()
     per_layer = np.zeros((n, L, _abi.ESIM_PL_FIELDS), np.int64)
@@ -129,14 +156,32 @@ class DeviceSweep:
         self.cfgs, self.traces = list(cfgs), list(traces)
         self.batch = ReplayBatch(self.cfgs, self.traces, full_log=False, digest=digest)
 
-    def route(self, stream=None) -> None:
-        from ._device import PREFETCH_CODE, _check, lib
+    def _router_tables(self):
+        import torch
+        from ._device import PREFETCH_CODE, lib
+        params, prefix = [], [0]
         for _, dt, ro, (mode, over, pct), noised in self.batch.sets:
             if noised:
                 raise ConfigError("DeviceSweep.route: noised prediction streams are host-prepared")
-            rc = lib().esim_router_launch(C.addressof(dt.desc), C.addressof(ro.desc), PREFETCH_CODE[mode],
-                                          float(over), float(pct), stream)
-            _check(rc, "router")
+            out4 = (C.c_int32 * 4)()
+            lib().esim_predictor_params(dt.pk.top_k, dt.pk.experts, PREFETCH_CODE[mode], float(over), float(pct), out4)
+            params += list(out4)
+            prefix.append(prefix[-1] + dt.pk.n_events)
+        self._rparams = torch.tensor(params, dtype=torch.int32, device="cuda")
+        self._rprefix = torch.tensor(prefix, dtype=torch.int64, device="cuda")
+        self._total_events = prefix[-1]
+        self._max_e = max(dt.pk.experts for _, dt, *_ in self.batch.sets)
+
+    def route(self, stream=None) -> None:
+        """Fused router over every trace of the sweep in one launch."""
+        from ._device import _check, _stream, lib
+        if not hasattr(self, "_rparams"):
+            self._router_tables()
+        rc = lib().esim_router_launch_batch(self.batch.d_traces.data_ptr(), self.batch.d_routers.data_ptr(),
+                                            self._rparams.data_ptr(), self._rprefix.data_ptr(),
+                                            len(self.batch.sets), self._total_events, self._max_e,
+                                            stream or _stream())
+        _check(rc, "router batch")
 
     def replay(self, stream=None) -> None:
         self.batch.launch(stream)
@@ -147,7 +192,7 @@ class DeviceSweep:
 
     @property
     def n_router_launches(self) -> int:
-        return len(self.batch.sets)
+        return 1
 
     @property
     def n_replay_launches(self) -> int:

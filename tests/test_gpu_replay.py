@@ -82,3 +82,40 @@ def test_softmax_and_topk_plugins_bit_exact():
             k = min(8, E)
             want = [int(i) for i in np.argsort(-ref[r], kind="stable")[:k]]
             assert routing.topk_indices(ref[r], k) == want
+
+
+def test_device_sweep_batched_router_matches_oracle(oracle_lib):
+    """C5 grid over two seeds through DeviceSweep (one batched router launch +
+    concurrent per-model replay launches) == the oracle, point by point."""
+    from paper_2602_03921_b200.models import builtin_spec
+    from paper_2602_03921_b200.sweep import C5_MODELS, DeviceSweep, c5_points
+    from paper_2602_03921_b200.trace import generate_synthetic
+    trs = {m: [generate_synthetic(builtin_spec(m), seed=s, prefill_tokens=64, decode_tokens=16)
+               for s in (3, 4)] for m in C5_MODELS}
+    cfgs, tl = c5_points(trs)
+    ds = DeviceSweep(cfgs, tl)
+    ds.step()
+    ds.step()
+    res = ds.results()
+    for cfg, tr, r in zip(cfgs, tl, res):
+        o = oracle_lib.run(cfg, tr, full_log=False)
+        assert o.counters.digest == r.counters.digest, (cfg.model.name, cfg.eviction)
+        assert json.dumps(o.report) == json.dumps(r.report)
+
+
+def test_c_abi_host_path_matches_oracle(oracle_lib):
+    """esim_run_host (host buffers in/out, grouped concurrent replays) == oracle."""
+    from paper_2602_03921_b200.models import builtin_spec
+    from paper_2602_03921_b200.sweep import C5_MODELS, c5_points, reports, run_grid_host
+    from paper_2602_03921_b200.trace import generate_synthetic
+    trs = {m: [generate_synthetic(builtin_spec(m), seed=5, prefill_tokens=32, decode_tokens=24)] for m in C5_MODELS}
+    cfgs, tl = c5_points(trs)
+    # interleave models so the C side has to regroup and restore the order
+    perm = sorted(range(len(cfgs)), key=lambda i: (i % 27, i // 27))
+    cfgs, tl = [cfgs[i] for i in perm], [tl[i] for i in perm]
+    cs, pl = run_grid_host(cfgs, tl)
+    reps = reports(cfgs, cs, pl)
+    for cfg, tr, c, rep in zip(cfgs, tl, cs, reps):
+        o = oracle_lib.run(cfg, tr, full_log=False)
+        assert o.counters.digest == c.digest, (cfg.model.name, cfg.eviction)
+        assert json.dumps(o.report) == json.dumps(rep)
