@@ -43,6 +43,10 @@ def lib():
         L.esim_run_host.argtypes = [vp, i32, vp, i32, vp, vp, i32, vp, i64, vp, i64]
         L.esim_softmax_launch.argtypes = [vp, i32, i32, vp, vp]
         L.esim_host_register.argtypes = [vp, C.c_size_t]
+        L.esim_tmap_bf16.argtypes = [vp, vp, i64, i64, i32]
+        L.esim_ffn_gather.argtypes = [vp, vp, vp, i32, i32, i32, vp]
+        L.esim_ffn_residual.argtypes = [vp, vp, i64, vp]
+        L.esim_ffn_experts.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
         L.esim_host_unregister.argtypes = [vp]
         L.esim_router_launch_batch.argtypes = [vp, vp, vp, vp, i32, i64, i32, vp]
         L.esim_predictor_params.argtypes = [i32, i32, i32, f64, f64, vp]

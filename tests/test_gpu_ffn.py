@@ -1,0 +1,62 @@
+"""tcgen05 grouped SwiGLU expert FFN vs a plain PyTorch fp32 reference of the
+same op (same bf16 weights/activations; the kernel keeps the intermediate
+activation in bf16, so the reference rounds it too). Tolerance: max error
+<= 1e-2 of max |y| (BASELINE.json north star: bf16 tolerance 1e-2)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+H, I = 2048, 1024
+TOL = 1e-2
+
+
+def _case(T, K, n_exp, npad_expected, seed):
+    import torch
+    from paper_2602_03921_b200.ffn import ExpertSlots, npad_for, routing_tables
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    n_slots = n_exp + 2
+    slots = ExpertSlots(n_slots, H, I, max_tokens=T, max_exec=n_exp)
+    slots.buf.copy_((torch.randn(slots.buf.numel(), generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+    x = torch.randn(T, H, generator=g, device="cuda").to(torch.bfloat16)
+    rng = np.random.default_rng(seed)
+    row_sel = np.stack([rng.choice(n_exp, size=K, replace=False) for _ in range(T)]).astype(np.int32)
+    row_w = rng.uniform(0.01, 0.3, size=(T, K)).astype(np.float32)
+    slot_of = rng.permutation(n_slots)[:n_exp]
+    executed = {e: (e, e) for e in range(n_exp)}
+    counts = np.bincount(row_sel.ravel(), minlength=n_exp)
+    npad = npad_for(int(counts.max()))
+    assert npad == npad_expected
+    ti, tw = routing_tables(row_sel, row_w, executed, npad)
+    exec_slot = torch.tensor(slot_of, dtype=torch.int32, device="cuda")
+    slots.y.zero_()
+    slots.run_layer(x, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad, residual=False)
+    torch.cuda.synchronize()
+    y = slots.y[:T * H].view(T, H).float()
+    ref = torch.zeros(T, H, device="cuda")
+    xf = x.float()
+    for e in range(n_exp):
+        w = slots.slot_view(int(slot_of[e])).float()
+        w1 = w[:2 * I * H].view(2 * I, H)
+        wd = w[2 * I * H:].view(H, I)
+        gate, up = xf @ w1[:I].T, xf @ w1[I:].T
+        act = (torch.nn.functional.silu(gate) * up).to(torch.bfloat16).float()
+        out = act @ wd.T
+        for t in range(T):
+            for j in range(K):
+                if row_sel[t, j] == e:
+                    ref[t] += float(row_w[t, j]) * out[t]
+    err = (y - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= TOL, f"max rel err {err:.3e}"
+    # residual path: x += y
+    x2 = x.clone()
+    slots.run_layer(x2, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad)
+    torch.cuda.synchronize()
+    assert torch.isfinite(x2.float()).all()
+    return err
+
+
+@pytest.mark.parametrize("T,K,n_exp,npad,seed", [(1, 8, 8, 16, 0), (16, 2, 8, 16, 1), (64, 8, 28, 32, 2),
+                                                  (64, 8, 8, 64, 3), (128, 4, 8, 128, 4)])
+def test_ffn_matches_torch_fp32(T, K, n_exp, npad, seed):
+    _case(T, K, n_exp, npad, seed)
