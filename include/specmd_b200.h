@@ -190,6 +190,52 @@ int esim_run_host(const EsimConfig *cfg, int32_t n, const EsimTraceDesc *traces,
                   EsimCounters *counters, int64_t *per_layer, int32_t pl_stride,
                   EsimRec *recs, int64_t rec_cap, int32_t *pred_experts, int64_t pe_cap);
 
+/* ---- physical layer step (no reference equivalent; configs[1]) -------- */
+typedef struct {
+    int32_t num_layers, experts, top_k;
+    int32_t hidden, inter;        /* OLMoE-1B-7B: 2048, 1024 (SwiGLU expert 3*H*I bf16) */
+    int32_t n_slots;              /* HBM cache slots = capacity / working-precision expert bytes */
+    int32_t max_tokens;           /* largest pass (<= 128) */
+} EsimLSParams;
+
+typedef struct {
+    double ttft_ms, total_ms, decode_ms, host_enqueue_ms;
+    int64_t h2d_bytes, n_copies, n_demand_copies, n_prefetch_copies, n_cancelled;
+    int64_t n_ffn_batches, n_exec_experts, n_records;
+    int64_t status;
+} EsimLSResult;
+
+/* Engine: pinned host expert store [L][E][3*H*I] bf16 (esim_ls_store returns
+ * it for initialisation), n_slots HBM slots with TMA descriptors, copy and
+ * compute streams, per-slot RAW/WAR events. */
+int esim_ls_create(const EsimLSParams *p, void **handle);
+void *esim_ls_store(void *handle);
+int64_t esim_ls_expert_bytes(void *handle);
+void *esim_ls_slots(void *handle);
+int esim_ls_destroy(void *handle);
+const char *esim_ls_last_error(void);
+/* One request. trace: host struct with device pointers; h_pass_tokens: host
+ * copy of its pass token counts; cfg: the logical config (decisions);
+ * x_prefill [T0][H], x_decode [passes-1][H], out [rows][H]: pinned host bf16.
+ * Timing: TTFT = start -> last prefill layer done; total = all passes and
+ * copies done (CUDA events). counters_out / per_layer_out: the decision
+ * stream's report vector (bit-exact with the reference for cfg). */
+int esim_ls_run(void *handle, const EsimTraceDesc *trace, const int32_t *h_pass_tokens, const EsimConfig *cfg,
+                const void *x_prefill, const void *x_decode, void *out, EsimCounters *counters_out,
+                int64_t *per_layer_out, EsimLSResult *res);
+
+/* FFN building blocks (ffn_gemm.cu): 2-D bf16 TMA descriptor (128B swizzle,
+ * box [box_rows][64]); token gather; the grouped tcgen05 SwiGLU experts;
+ * residual x += y. */
+int esim_tmap_bf16(void *out_map, const void *base, int64_t rows, int64_t cols, int32_t box_rows);
+int esim_ffn_gather(const void *d_x, const int32_t *d_tok_index, void *d_xg, int32_t n_exec, int32_t npad,
+                    int32_t hidden, void *stream);
+int esim_ffn_experts(const void *d_w1_maps, const void *d_w2_maps, const void *d_x_map, const void *d_act_map,
+                     const int32_t *d_exec_slot, const int32_t *d_tok_index, const float *d_tok_weight,
+                     void *d_act, float *d_y, int32_t n_exec, int32_t npad, int32_t inter, int32_t hidden,
+                     void *stream);
+int esim_ffn_residual(void *d_x, float *d_y, int64_t n, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     const EsimRouterOut* d_routers, EsimCounters* d_counters,
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
-                                    bool has_cnt, int warps_per_cta, cudaStream_t st);
+                                    bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress = nullptr);
 int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt);
 
 static thread_local std::string g_err;
@@ -145,6 +145,21 @@ extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_c
                                             d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
                                             w, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+    return 0;
+}
+
+// single point with its decisions streamed to mapped host memory (layer_step.cu)
+int esim_replay_launch_streamed(const EsimConfig* h_cfg, const EsimConfig* d_cfg, const EsimTraceDesc* d_traces,
+                                const EsimRouterOut* d_routers, int32_t max_tokens, EsimCounters* d_counters,
+                                int64_t* d_per_layer, int32_t pl_stride, EsimRec* d_recs, int64_t rec_cap,
+                                int32_t* d_pexp, int64_t pe_cap, int64_t* progress, void* stream) {
+    Sizing z;
+    int rc = replay_sizing(h_cfg, 1, max_tokens, pl_stride, 0, &z);
+    if (rc) return rc;
+    cudaError_t e = esim_replay_launch_impl(d_cfg, 1, d_traces, d_routers, d_counters, d_per_layer, d_recs, rec_cap,
+                                            d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
+                                            1, (cudaStream_t)stream, progress);
+    if (e != cudaSuccess) return cuda_fail(e, "streamed replay launch");
     return 0;
 }
 

@@ -1,0 +1,467 @@
+// layer_step.cu -- the physical expert-cached MoE layer step (configs[1]).
+//
+// Decision and execution are split exactly as SURVEY.md section 7.1 asks:
+//  * decisions: the replay kernel (replay.cu) runs the reference's logical
+//    timeline for the request and streams its event records into mapped
+//    host memory, publishing a per-layer progress counter;
+//  * execution: this native runtime consumes each layer's records as soon
+//    as they are published and drives the hardware:
+//      EvictRec              -> the victim's HBM slot returns to the free list
+//      PrefetchRec started   -> H2D copy pinned store -> a free slot, on the
+//      AccessRec fetch          copy-engine stream, in decision order
+//      PrefetchRec dropped   -> (cancelled in flight) slot returns; the DMA
+//        superseded             already issued still completes (FIFO-safe)
+//      AccessRec hit/wait    -> the expert executes from its slot
+//      AccessRec subst       -> the substitute's slot runs the dropped
+//                               expert's tokens
+//      RouteRec              -> the layer's grouped FFN (ffn_gemm.cu) on
+//                               the compute stream, then x += y
+//    Hazards: landed[slot] (copy -> FFN, RAW) and freed[slot] (last FFN
+//    reading the slot -> next copy into it, WAR) CUDA events. If a decision
+//    evicts an expert the current layer has not executed yet (tiny caches),
+//    the pending experts are flushed as a partial FFN first.
+// The host never blocks on the GPU except to wait for decisions; copies
+// stay back-to-back on the link, overlapped with compute.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/specmd_b200.h"
+
+extern "C" int esim_tmap_bf16(void* out_map, const void* base, int64_t rows, int64_t cols, int32_t box_rows);
+extern "C" int esim_ffn_gather(const void* d_x, const int32_t* d_tok_index, void* d_xg, int32_t n_exec, int32_t npad,
+                               int32_t H, void* stream);
+extern "C" int esim_ffn_residual(void* d_x, float* d_y, int64_t n, void* stream);
+extern "C" int esim_ffn_experts(const void* d_w1_maps, const void* d_w2_maps, const void* d_x_map,
+                                const void* d_act_map, const int32_t* d_exec_slot, const int32_t* d_tok_index,
+                                const float* d_tok_weight, void* d_act, float* d_y, int32_t n_exec, int32_t npad,
+                                int32_t I, int32_t H, void* stream);
+extern "C" int esim_router_launch(const EsimTraceDesc* tr, const EsimRouterOut* out, int32_t pred_mode,
+                                  double overfetch, double percentile, void* stream);
+int esim_replay_launch_streamed(const EsimConfig* h_cfg, const EsimConfig* d_cfg, const EsimTraceDesc* d_traces,
+                                const EsimRouterOut* d_routers, int32_t max_tokens, EsimCounters* d_counters,
+                                int64_t* d_per_layer, int32_t pl_stride, EsimRec* d_recs, int64_t rec_cap,
+                                int32_t* d_pexp, int64_t pe_cap, int64_t* progress, void* stream);
+
+namespace {
+
+constexpr int NPADS[4] = {16, 32, 64, 128};
+
+__global__ void build_tables_kernel(const int16_t* __restrict__ row_sel, const float* __restrict__ row_w, int T,
+                                    int K, const int32_t* __restrict__ pos_of_expert, int n_exec, int npad,
+                                    int32_t* __restrict__ tok_index, float* __restrict__ tok_weight) {
+    extern __shared__ int fill[];
+    for (int i = threadIdx.x; i < n_exec * npad; i += blockDim.x) { tok_index[i] = -1; tok_weight[i] = 0.0f; }
+    for (int i = threadIdx.x; i < n_exec; i += blockDim.x) fill[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
+        const int pos = pos_of_expert[row_sel[i]];
+        if (pos < 0) continue;
+        const int slot = atomicAdd(&fill[pos], 1);
+        if (slot < npad) {
+            tok_index[pos * npad + slot] = i / K;
+            tok_weight[pos * npad + slot] = row_w[i];
+        }
+    }
+}
+
+// rows of bf16 between device and mapped host memory (zero-copy over the link)
+__global__ void copy_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+struct Engine {
+    EsimLSParams P;
+    size_t expert_bytes = 0;
+    void* store = nullptr;               // pinned host: [L][E][expert]
+    char* slots = nullptr;               // device: [n_slots][expert]
+    void *w1_maps = nullptr, *w2_maps = nullptr;
+    void *xg = nullptr, *act = nullptr;
+    void *x_maps[4] = {}, *act_maps[4] = {};
+    float* y = nullptr;
+    void* x = nullptr;
+    int32_t* tok_index = nullptr;
+    float* tok_weight = nullptr;
+    cudaStream_t copy_st = nullptr, comp_st = nullptr, ctl_st = nullptr;
+    std::vector<cudaEvent_t> landed, freed;
+    cudaEvent_t ev_start = nullptr, ev_ttft = nullptr, ev_end = nullptr, ev_copy_end = nullptr;
+    // mapped host (zero-copy) buffers
+    EsimRec* recs = nullptr;
+    int64_t rec_cap = 0;
+    int32_t* pexp = nullptr;
+    int64_t pe_cap = 0;
+    int64_t* progress = nullptr;
+    int32_t* tables = nullptr;           // pool of [2][E] int32 (pos_of_expert, exec_slot) per flush
+    int64_t table_cap = 0;
+    // per-run device scratch
+    void* dev_scratch = nullptr;
+    size_t dev_scratch_bytes = 0;
+};
+
+std::string g_ls_err;
+int ls_fail(int code, const std::string& m) { g_ls_err = m; return code; }
+int ls_cuda(cudaError_t e, const char* where) { return ls_fail(-3, std::string(where) + ": " + cudaGetErrorString(e)); }
+
+#define CK(x)                                              \
+    do {                                                   \
+        cudaError_t _e = (x);                              \
+        if (_e != cudaSuccess) return ls_cuda(_e, #x);     \
+    } while (0)
+
+int npad_for(int t) {
+    for (int n : NPADS) if (t <= n) return n;
+    return -1;
+}
+int npad_index(int n) {
+    for (int i = 0; i < 4; i++) if (NPADS[i] == n) return i;
+    return -1;
+}
+
+}  // namespace
+
+extern "C" const char* esim_ls_last_error(void) { return g_ls_err.c_str(); }
+
+extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
+    Engine* g = new Engine();
+    g->P = *p;
+    const int L = p->num_layers, E = p->experts, H = p->hidden, I = p->inter;
+    if (H % 128 || I % 128 || p->max_tokens > 128 || p->n_slots < 1) { delete g; return ls_fail(-1, "bad layer-step geometry"); }
+    g->expert_bytes = (size_t)3 * H * I * 2;
+    CK(cudaHostAlloc(&g->store, g->expert_bytes * L * E, cudaHostAllocDefault));
+    CK(cudaMalloc((void**)&g->slots, g->expert_bytes * p->n_slots));
+    std::vector<unsigned char> m1(128 * (size_t)p->n_slots), m2(128 * (size_t)p->n_slots);
+    for (int s = 0; s < p->n_slots; s++) {
+        const char* base = g->slots + g->expert_bytes * s;
+        if (esim_tmap_bf16(&m1[128 * s], base, 2 * I, H, 128) ||
+            esim_tmap_bf16(&m2[128 * s], base + (size_t)2 * I * H * 2, H, I, 128))
+            return ls_fail(-3, "tensor map encode failed");
+    }
+    CK(cudaMalloc(&g->w1_maps, m1.size()));
+    CK(cudaMalloc(&g->w2_maps, m2.size()));
+    CK(cudaMemcpy(g->w1_maps, m1.data(), m1.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->w2_maps, m2.data(), m2.size(), cudaMemcpyHostToDevice));
+    const size_t maxrows = (size_t)E * 128;
+    CK(cudaMalloc(&g->xg, maxrows * H * 2));
+    CK(cudaMalloc(&g->act, maxrows * I * 2));
+    for (int i = 0; i < 4; i++) {
+        unsigned char mx[128], ma[128];
+        if (esim_tmap_bf16(mx, g->xg, (int64_t)E * NPADS[i], H, NPADS[i]) ||
+            esim_tmap_bf16(ma, g->act, (int64_t)E * NPADS[i], I, NPADS[i]))
+            return ls_fail(-3, "tensor map encode failed");
+        CK(cudaMalloc(&g->x_maps[i], 128));
+        CK(cudaMalloc(&g->act_maps[i], 128));
+        CK(cudaMemcpy(g->x_maps[i], mx, 128, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(g->act_maps[i], ma, 128, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMalloc((void**)&g->y, (size_t)p->max_tokens * H * 4));
+    CK(cudaMemset(g->y, 0, (size_t)p->max_tokens * H * 4));
+    CK(cudaMalloc(&g->x, (size_t)p->max_tokens * H * 2));
+    CK(cudaMalloc((void**)&g->tok_index, maxrows * 4));
+    CK(cudaMalloc((void**)&g->tok_weight, maxrows * 4));
+    CK(cudaStreamCreateWithFlags(&g->copy_st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g->comp_st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g->ctl_st, cudaStreamNonBlocking));
+    g->landed.resize(p->n_slots);
+    g->freed.resize(p->n_slots);
+    for (int s = 0; s < p->n_slots; s++) {
+        CK(cudaEventCreateWithFlags(&g->landed[s], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g->freed[s], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreate(&g->ev_start));
+    CK(cudaEventCreate(&g->ev_ttft));
+    CK(cudaEventCreate(&g->ev_end));
+    CK(cudaEventCreate(&g->ev_copy_end));
+    *handle = g;
+    return 0;
+}
+
+extern "C" void* esim_ls_store(void* handle) { return static_cast<Engine*>(handle)->store; }
+extern "C" int64_t esim_ls_expert_bytes(void* handle) { return (int64_t) static_cast<Engine*>(handle)->expert_bytes; }
+extern "C" void* esim_ls_slots(void* handle) { return static_cast<Engine*>(handle)->slots; }
+
+extern "C" int esim_ls_destroy(void* handle) {
+    Engine* g = static_cast<Engine*>(handle);
+    if (!g) return 0;
+    cudaDeviceSynchronize();
+    cudaFreeHost(g->store);
+    cudaFree(g->slots);
+    cudaFree(g->w1_maps);
+    cudaFree(g->w2_maps);
+    cudaFree(g->xg);
+    cudaFree(g->act);
+    for (int i = 0; i < 4; i++) { cudaFree(g->x_maps[i]); cudaFree(g->act_maps[i]); }
+    cudaFree(g->y);
+    cudaFree(g->x);
+    cudaFree(g->tok_index);
+    cudaFree(g->tok_weight);
+    if (g->recs) cudaFreeHost(g->recs);
+    if (g->pexp) cudaFreeHost(g->pexp);
+    if (g->progress) cudaFreeHost(g->progress);
+    if (g->tables) cudaFreeHost(g->tables);
+    if (g->dev_scratch) cudaFree(g->dev_scratch);
+    for (auto e : g->landed) cudaEventDestroy(e);
+    for (auto e : g->freed) cudaEventDestroy(e);
+    cudaEventDestroy(g->ev_start);
+    cudaEventDestroy(g->ev_ttft);
+    cudaEventDestroy(g->ev_end);
+    cudaEventDestroy(g->ev_copy_end);
+    cudaStreamDestroy(g->copy_st);
+    cudaStreamDestroy(g->comp_st);
+    cudaStreamDestroy(g->ctl_st);
+    delete g;
+    return 0;
+}
+
+// One request: the trace (device pointers in `trace`), the logical config
+// (`cfg`, host), hidden-state inputs in pinned/mapped host memory:
+// x_prefill [T0][H] bf16, x_decode [n_passes-1][H] bf16; outputs the last
+// layer's hidden states of every pass to out (mapped host, [rows][H] bf16).
+extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const int32_t* h_pass_tokens,
+                           const EsimConfig* cfg, const void* x_prefill, const void* x_decode, void* out,
+                           EsimCounters* counters_out, int64_t* per_layer_out, EsimLSResult* res) {
+    Engine* g = static_cast<Engine*>(handle);
+    const EsimLSParams& P = g->P;
+    const int L = P.num_layers, E = P.experts, K = P.top_k, H = P.hidden, I = P.inter;
+    const EsimTraceDesc& tr = *trace_dev;
+    if (tr.num_layers != L || tr.experts != E || tr.top_k != K) return ls_fail(-1, "trace geometry mismatch");
+    const int64_t n_events = tr.n_events;
+    const int64_t wbytes = cfg->expert_bytes[cfg->working_prec];
+    if (cfg->miss == ESIM_MISS_FETCH_LOW || cfg->miss == ESIM_MISS_FETCH_PRIORITY)
+        return ls_fail(-1, "physical layer step stores bf16 experts: mixed-precision miss policies are logical only");
+    if (cfg->capacity_bytes / wbytes > P.n_slots) return ls_fail(-1, "more logical slots than physical slots");
+    int max_t = 0;
+    for (int p = 0; p < tr.n_passes; p++) max_t = std::max(max_t, h_pass_tokens[p]);
+    if (max_t > P.max_tokens) return ls_fail(-1, "pass has more tokens than the engine was sized for");
+    // ---- buffers: mapped record stream, progress, flush tables; device router/replay scratch
+    const int64_t rec_cap = 64 + n_events * (6 + 12 * (int64_t)E) + tr.n_rows_total * K * 2;
+    if (rec_cap > g->rec_cap) {
+        if (g->recs) cudaFreeHost(g->recs);
+        CK(cudaHostAlloc((void**)&g->recs, rec_cap * sizeof(EsimRec), cudaHostAllocMapped));
+        g->rec_cap = rec_cap;
+    }
+    const int64_t pe_cap = n_events * E;
+    if (pe_cap > g->pe_cap) {
+        if (g->pexp) cudaFreeHost(g->pexp);
+        CK(cudaHostAlloc((void**)&g->pexp, pe_cap * 4, cudaHostAllocMapped));
+        g->pe_cap = pe_cap;
+    }
+    if (g->progress) cudaFreeHost(g->progress);
+    CK(cudaHostAlloc((void**)&g->progress, (n_events + 2) * 8, cudaHostAllocMapped));
+    volatile int64_t* prog = g->progress;
+    for (int64_t i = 0; i < n_events + 2; i++) prog[i] = 0;
+    const int64_t table_need = (n_events * 2 + 64) * 2 * E;
+    if (table_need > g->table_cap) {
+        if (g->tables) cudaFreeHost(g->tables);
+        CK(cudaHostAlloc((void**)&g->tables, table_need * 4, cudaHostAllocMapped));
+        g->table_cap = table_need;
+    }
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const int64_t ne = n_events, nr = tr.n_rows_total;
+    size_t need = al(ne * 4) * 3 + al(ne * E * 4) * 6 + al(ne * E * 8) + al(ne * 8) + al(nr * K * 2) + al(nr * K * 4) +
+                  al(sizeof(EsimConfig)) + al(sizeof(EsimTraceDesc)) + al(sizeof(EsimRouterOut)) +
+                  al(sizeof(EsimCounters)) + al(L * ESIM_PL_FIELDS * 8);
+    if (need > g->dev_scratch_bytes) {
+        if (g->dev_scratch) cudaFree(g->dev_scratch);
+        CK(cudaMalloc(&g->dev_scratch, need));
+        g->dev_scratch_bytes = need;
+    }
+    char* q = (char*)g->dev_scratch;
+    auto take = [&](size_t b) { void* r = q; q += al(b); return r; };
+    EsimRouterOut ro;
+    ro.n_dem = (int32_t*)take(ne * 4); ro.n_pred = (int32_t*)take(ne * 4); ro.pred_clamped = (int32_t*)take(ne * 4);
+    ro.dem_expert = (int32_t*)take(ne * E * 4); ro.dem_rank = (int32_t*)take(ne * E * 4);
+    ro.dem_gate = (float*)take(ne * E * 4); ro.dem_tokens = (int32_t*)take(ne * E * 4);
+    ro.pred_expert = (int32_t*)take(ne * E * 4); ro.pred_score = (float*)take(ne * E * 4);
+    ro.dem_summed = (double*)take(ne * E * 8); ro.sel_mass = (double*)take(ne * 8);
+    ro.row_sel = (int16_t*)take(nr * K * 2); ro.row_w = (float*)take(nr * K * 4);
+    EsimConfig* d_cfg = (EsimConfig*)take(sizeof(EsimConfig));
+    EsimTraceDesc* d_tr = (EsimTraceDesc*)take(sizeof(EsimTraceDesc));
+    EsimRouterOut* d_ro = (EsimRouterOut*)take(sizeof(EsimRouterOut));
+    EsimCounters* d_cnt = (EsimCounters*)take(sizeof(EsimCounters));
+    int64_t* d_pl = (int64_t*)take(L * ESIM_PL_FIELDS * 8);
+    EsimConfig hc = *cfg;
+    hc.flags |= ESIM_FLAG_FULL_LOG;
+    hc.trace_id = 0;
+    CK(cudaMemcpy(d_cfg, &hc, sizeof hc, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_tr, &tr, sizeof tr, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ro, &ro, sizeof ro, cudaMemcpyHostToDevice));
+    CK(cudaDeviceSynchronize());
+
+    // ---- timed request --------------------------------------------------
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaEventRecord(g->ev_start, g->comp_st));
+    CK(cudaStreamWaitEvent(g->copy_st, g->ev_start, 0));
+    CK(cudaStreamWaitEvent(g->ctl_st, g->ev_start, 0));
+    int rc = esim_router_launch(&tr, &ro, hc.prefetch, hc.overfetch, hc.percentile, g->ctl_st);
+    if (rc) return ls_fail(rc, "router launch");
+    rc = esim_replay_launch_streamed(&hc, d_cfg, d_tr, d_ro, max_t, d_cnt, d_pl, L, g->recs, rec_cap, g->pexp, pe_cap,
+                                     g->progress, g->ctl_st);
+    if (rc) return ls_fail(rc, "replay launch");
+
+    std::vector<int> phys(L * E, -1);                // ident -> physical slot
+    std::vector<int> free_slots;
+    for (int s = P.n_slots - 1; s >= 0; s--) free_slots.push_back(s);
+    std::vector<int> pend_slot;                      // pending executed slots of the current layer (positions)
+    std::vector<int> pos_of_expert(E, -1);
+    std::vector<char> slot_pending(P.n_slots, 0);
+    std::vector<int> tok_of_pos;
+    int64_t table_next = 0;
+    int64_t n_copies = 0, n_demand = 0, n_prefetch = 0, n_cancel = 0, n_flush = 0, n_exec_total = 0;
+    int64_t row = 0;                                 // first token row of the current event
+    int64_t rec_pos = 0;
+    int64_t out_row = 0;
+    const int64_t expert_bytes = (int64_t)g->expert_bytes;
+
+    auto issue_copy = [&](int ident) -> int {
+        if (free_slots.empty()) return ls_fail(-2, "no free physical slot (decision stream inconsistent)");
+        const int s = free_slots.back();
+        free_slots.pop_back();
+        phys[ident] = s;
+        CK(cudaStreamWaitEvent(g->copy_st, g->freed[s], 0));                       // WAR
+        CK(cudaMemcpyAsync(g->slots + (size_t)s * expert_bytes, (char*)g->store + (size_t)ident * expert_bytes,
+                           expert_bytes, cudaMemcpyHostToDevice, g->copy_st));
+        CK(cudaEventRecord(g->landed[s], g->copy_st));                              // RAW guard
+        n_copies++;
+        return 0;
+    };
+    auto flush = [&](int layer_rows, const int16_t* rs, const float* rw, bool residual) -> int {
+        const int n_exec = (int)pend_slot.size();
+        if (n_exec > 0) {
+            int maxtok = 0;
+            for (int t : tok_of_pos) maxtok = std::max(maxtok, t);
+            const int npad = npad_for(std::max(1, maxtok));
+            if (npad < 0) return ls_fail(-1, "too many tokens per expert");
+            if (table_next + 2 * E > g->table_cap) {                                 // recycle the pool
+                CK(cudaStreamSynchronize(g->comp_st));
+                table_next = 0;
+            }
+            int32_t* tpos = g->tables + table_next;
+            int32_t* tslot = tpos + E;
+            table_next += 2 * E;
+            for (int e = 0; e < E; e++) tpos[e] = pos_of_expert[e];
+            for (int i = 0; i < n_exec; i++) tslot[i] = pend_slot[i];
+            for (int i = 0; i < n_exec; i++) CK(cudaStreamWaitEvent(g->comp_st, g->landed[pend_slot[i]], 0));
+            build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
+                                                                   g->tok_index, g->tok_weight);
+            if (esim_ffn_gather(g->x, g->tok_index, g->xg, n_exec, npad, H, g->comp_st) ||
+                esim_ffn_experts(g->w1_maps, g->w2_maps, g->x_maps[npad_index(npad)], g->act_maps[npad_index(npad)],
+                                 tslot, g->tok_index, g->tok_weight, g->act, g->y, n_exec, npad, I, H, g->comp_st))
+                return ls_fail(-3, "ffn launch failed");
+            for (int i = 0; i < n_exec; i++) CK(cudaEventRecord(g->freed[pend_slot[i]], g->comp_st));
+            n_exec_total += n_exec;
+            n_flush++;
+        }
+        for (int s : pend_slot) slot_pending[s] = 0;
+        pend_slot.clear();
+        tok_of_pos.clear();
+        std::fill(pos_of_expert.begin(), pos_of_expert.end(), -1);
+        if (residual && esim_ffn_residual(g->x, g->y, (int64_t)layer_rows * H, g->comp_st))
+            return ls_fail(-3, "residual launch failed");
+        return 0;
+    };
+    auto execute = [&](int expert, int slot, int tokens) {
+        if (!slot_pending[slot]) {
+            slot_pending[slot] = 1;
+            pend_slot.push_back(slot);
+            tok_of_pos.push_back(0);
+        }
+        const int pos = (int)(std::find(pend_slot.begin(), pend_slot.end(), slot) - pend_slot.begin());
+        pos_of_expert[expert] = pos;
+        tok_of_pos[pos] += tokens;
+    };
+
+    for (int64_t ev = 0; ev < n_events; ev++) {
+        const int pass = (int)(ev / L), layer = (int)(ev % L);
+        const int T = h_pass_tokens[pass];
+        int64_t done;
+        while ((done = prog[0]) <= ev) {
+            if (done < 0) return ls_fail(-2, "replay kernel reported an error");
+            std::this_thread::yield();
+        }
+        const int64_t end = prog[1 + ev];
+        if (layer == 0) {                                // this pass's input rows -> x (zero-copy)
+            const void* src = pass == 0 ? x_prefill : (const char*)x_decode + (size_t)(pass - 1) * H * 2;
+            copy_rows_kernel<<<64, 256, 0, g->comp_st>>>((const uint4*)src, (uint4*)g->x, (int64_t)T * H / 8);
+        }
+        const int16_t* rs = ro.row_sel + row * K;
+        const float* rw = ro.row_w + row * K;
+        for (; rec_pos < end; rec_pos++) {
+            const EsimRec& r = g->recs[rec_pos];
+            if (r.kind == ESIM_REC_EVICT) {
+                const int v = r.i0 * E + r.i1;
+                const int s = phys[v];
+                if (s >= 0) {
+                    if (slot_pending[s] && (rc = flush(T, rs, rw, false))) return rc;   // self-eviction
+                    free_slots.push_back(s);
+                    phys[v] = -1;
+                }
+            } else if (r.kind == ESIM_REC_PREFETCH) {
+                if (r.i0 == 1) {                         // started
+                    if ((rc = issue_copy(r.i1 * E + r.i2))) return rc;
+                    n_prefetch++;
+                } else if (r.i0 == 4 && r.i3 == 4) {     // dropped superseded: cancelled in flight
+                    const int id = r.i1 * E + r.i2;
+                    if (phys[id] >= 0) { free_slots.push_back(phys[id]); phys[id] = -1; }
+                    n_cancel++;
+                }
+            } else if (r.kind == ESIM_REC_ACCESS) {
+                const int outcome = r.i3 & 0xFF;
+                const int id = r.layer * E + r.i0;
+                if (outcome == 1) {                      // demand fetch
+                    if ((rc = issue_copy(id))) return rc;
+                    n_demand++;
+                }
+                if (outcome <= 2) {
+                    execute(r.i0, phys[id], r.i1);
+                } else if (outcome == 4) {               // substitute runs the missing expert's tokens
+                    execute(r.i0, phys[r.layer * E + r.i4], r.i1);
+                }
+            } else if (r.kind == ESIM_REC_ROUTE) {
+                if ((rc = flush(T, rs, rw, true))) return rc;
+                if (layer == L - 1) {                    // pass output -> host (zero-copy)
+                    copy_rows_kernel<<<64, 256, 0, g->comp_st>>>((const uint4*)g->x,
+                                                                 (uint4*)((char*)out + (size_t)out_row * H * 2),
+                                                                 (int64_t)T * H / 8);
+                    out_row += T;
+                    if (pass == 0) CK(cudaEventRecord(g->ev_ttft, g->comp_st));
+                }
+            }
+        }
+        row += T;
+    }
+    CK(cudaEventRecord(g->ev_copy_end, g->copy_st));
+    CK(cudaStreamWaitEvent(g->comp_st, g->ev_copy_end, 0));
+    CK(cudaEventRecord(g->ev_end, g->comp_st));
+    const double host_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    CK(cudaEventSynchronize(g->ev_end));
+    CK(cudaStreamSynchronize(g->ctl_st));
+    float ttft = 0, total = 0;
+    CK(cudaEventElapsedTime(&ttft, g->ev_start, g->ev_ttft));
+    CK(cudaEventElapsedTime(&total, g->ev_start, g->ev_end));
+    CK(cudaMemcpy(counters_out, d_cnt, sizeof(EsimCounters), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(per_layer_out, d_pl, (size_t)L * ESIM_PL_FIELDS * 8, cudaMemcpyDeviceToHost));
+    res->ttft_ms = ttft;
+    res->total_ms = total;
+    res->decode_ms = total - ttft;
+    res->host_enqueue_ms = host_ms;
+    res->h2d_bytes = n_copies * expert_bytes;
+    res->n_copies = n_copies;
+    res->n_demand_copies = n_demand;
+    res->n_prefetch_copies = n_prefetch;
+    res->n_cancelled = n_cancel;
+    res->n_ffn_batches = n_flush;
+    res->n_exec_experts = n_exec_total;
+    res->n_records = rec_pos;
+    res->status = 0;
+    return 0;
+}

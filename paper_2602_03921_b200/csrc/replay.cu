@@ -56,6 +56,8 @@ struct ReplayArgs {
     int has_cnt;                   // any LFU/LHU point (per-ident counts)
     int warps_per_cta;
     int point_bytes;
+    volatile int64_t* progress;    // optional (single point, streamed decisions): [0] events done
+                                   // (-1 on error), [1 + ev] records emitted through event ev
 };
 
 // lane-0 owned counters (shared memory)
@@ -1163,6 +1165,12 @@ __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArg
             if (cfg->prefetch != ESIM_PF_NONE && l + 1 < p.L) submit_prefetches(p, R, ev + 1);
             advance_to(p, p.now + cfg->compute_us);
             pblocked += blocked;
+            if (A.progress && p.lane == 0) {             // publish this layer's decisions to the host
+                __threadfence_system();
+                A.progress[1 + ev] = p.n_recs;
+                __threadfence_system();
+                A.progress[0] = ev + 1;
+            }
         }
         if (p.err) break;
         emit(p, ESIM_REC_PASS, 0, tr.pass_kind[pass], tr.pass_tokens[pass], 0, 0, 0, pstart, p.now, pblocked, 0.0);
@@ -1176,6 +1184,10 @@ __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArg
         rows_before += tr.pass_tokens[pass];
     }
     __syncwarp();
+    if (A.progress && p.lane == 0) {
+        __threadfence_system();
+        A.progress[0] = p.err ? -1 : (int64_t)tr.n_passes * p.L + 1;    // +1: final PassRec written
+    }
     if (p.lane == 0) {
         const Ctr* c = p.ctr;
         EsimCounters* o = &A.counters[pid];
@@ -1217,8 +1229,9 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     const EsimRouterOut* d_routers, EsimCounters* d_counters,
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
-                                    bool has_cnt, int warps_per_cta, cudaStream_t st) {
+                                    bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress) {
     esim::ReplayArgs a;
+    a.progress = progress;
     a.cfg = d_cfg; a.n_points = n; a.traces = d_traces; a.routers = d_routers;
     a.counters = d_counters; a.per_layer = d_per_layer; a.recs = d_recs; a.rec_cap = rec_cap;
     a.pexp = d_pexp; a.pe_cap = pe_cap;

@@ -1,0 +1,152 @@
+"""Physical expert-cached MoE layer step (BASELINE.json configs[1]).
+
+OLMoE-1B-7B shape (16 layers x 64 experts, top-8, H=2048, I=1024 SwiGLU,
+12,582,912 B per bf16 expert) with the expert store in pinned host memory,
+a capacity-bounded pool of HBM cache slots, and the reference's decision
+semantics (SimConfig: eviction / prefetch / miss policy, logical clock)
+driving real host->HBM copies and real tcgen05 expert FFNs. The decisions
+come from the replay kernel (bit-exact with the reference for `cfg`); the
+native runtime in csrc/layer_step.cu executes them.
+
+Measured: TTFT (end of the prefill pass) and decode tokens/s with CUDA
+events, host-link bytes and achieved GB/s.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from ._device import DeviceTrace, _check, _torch, lib
+from .metrics import report_from_counters
+
+
+class EsimLSParams(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("num_layers", "experts", "top_k", "hidden", "inter", "n_slots",
+                                         "max_tokens")]
+
+
+class EsimLSResult(C.Structure):
+    _fields_ = [("ttft_ms", C.c_double), ("total_ms", C.c_double), ("decode_ms", C.c_double),
+                ("host_enqueue_ms", C.c_double)] + \
+               [(n, C.c_int64) for n in ("h2d_bytes", "n_copies", "n_demand_copies", "n_prefetch_copies",
+                                         "n_cancelled", "n_ffn_batches", "n_exec_experts", "n_records", "status")]
+
+
+def _bind():
+    L = lib()
+    if not hasattr(L, "_ls_bound"):
+        vp = C.c_void_p
+        L.esim_ls_create.argtypes = [vp, vp]
+        L.esim_ls_store.argtypes = [vp]
+        L.esim_ls_store.restype = vp
+        L.esim_ls_expert_bytes.argtypes = [vp]
+        L.esim_ls_expert_bytes.restype = C.c_int64
+        L.esim_ls_slots.argtypes = [vp]
+        L.esim_ls_slots.restype = vp
+        L.esim_ls_destroy.argtypes = [vp]
+        L.esim_ls_last_error.restype = C.c_char_p
+        L.esim_ls_run.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L._ls_bound = True
+    return L
+
+
+@dataclass
+class LayerStepResult:
+    ttft_ms: float
+    total_ms: float
+    decode_ms: float
+    decode_tokens_per_sec: float
+    h2d_bytes: int
+    h2d_gbs: float
+    n_copies: int
+    n_demand_copies: int
+    n_prefetch_copies: int
+    n_cancelled: int
+    n_ffn_batches: int
+    n_exec_experts: int
+    host_enqueue_ms: float
+    report: dict                 # the decision stream's reference-format report (logical timeline)
+    out: object = None           # last-layer hidden states of every pass (host bf16)
+
+
+class LayerStepEngine:
+    """Pinned expert store + HBM slots + copy/compute streams for one model."""
+
+    def __init__(self, cfg, hidden: int = 2048, inter: int = 1024, max_tokens: int = 64):
+        torch = _torch()
+        m = cfg.model
+        self.cfg, self.H, self.I = cfg, hidden, inter
+        self.n_slots = cfg.capacity_bytes() // m.expert_bytes(cfg.working_precision)
+        p = EsimLSParams(m.num_layers, m.experts_per_layer, m.top_k, hidden, inter, self.n_slots, max_tokens)
+        self._h = C.c_void_p()
+        L = _bind()
+        rc = L.esim_ls_create(C.addressof(p), C.addressof(self._h))
+        if rc:
+            raise RuntimeError(f"esim_ls_create failed ({rc}): {L.esim_ls_last_error().decode()}")
+        self.expert_bytes = L.esim_ls_expert_bytes(self._h)
+        self.n_experts_total = m.num_layers * m.experts_per_layer
+        nbytes = self.expert_bytes * self.n_experts_total
+        buf = (C.c_uint8 * nbytes).from_address(L.esim_ls_store(self._h))
+        self.store = torch.frombuffer(buf, dtype=torch.bfloat16)   # pinned host view
+        self.torch = torch
+
+    def init_weights(self, seed: int = 0, std: float = 0.02) -> None:
+        """Random-init N(0, std) bf16 experts, generated on the GPU in chunks
+        and copied into the pinned store."""
+        torch = self.torch
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        per = self.expert_bytes // 2
+        chunk = 64
+        for e0 in range(0, self.n_experts_total, chunk):
+            n = min(chunk, self.n_experts_total - e0)
+            w = (torch.randn(n * per, generator=g, device="cuda") * std).to(torch.bfloat16)
+            self.store[e0 * per:(e0 + n) * per].copy_(w)
+        torch.cuda.synchronize()
+
+    def expert_weights(self, layer: int, expert: int):
+        per = self.expert_bytes // 2
+        i = layer * self.cfg.model.experts_per_layer + expert
+        return self.store[i * per:(i + 1) * per]
+
+    def run(self, trace, x_prefill, x_decode, keep_outputs: bool = False) -> LayerStepResult:
+        torch = self.torch
+        pk = trace.packed()
+        dt = DeviceTrace(pk)
+        ctoks = np.ascontiguousarray(pk.pass_tokens, np.int32)
+        c = self.cfg.to_c(0, True)
+        rows = int(pk.pass_tokens.sum())
+        out = torch.empty(rows * self.H, dtype=torch.bfloat16).pin_memory()
+        counters = _abi.EsimCounters()
+        per_layer = np.zeros((self.cfg.model.num_layers, _abi.ESIM_PL_FIELDS), np.int64)
+        res = EsimLSResult()
+        L = _bind()
+        torch.cuda.synchronize()
+        rc = L.esim_ls_run(self._h, C.addressof(dt.desc), ctoks.ctypes.data, C.addressof(c), x_prefill.data_ptr(),
+                           x_decode.data_ptr(), out.data_ptr(), C.addressof(counters), per_layer.ctypes.data,
+                           C.addressof(res))
+        if rc:
+            raise RuntimeError(f"esim_ls_run failed ({rc}): {L.esim_ls_last_error().decode()}")
+        rep = report_from_counters(self.cfg.echo(), self.cfg.model.num_layers,
+                                   self.cfg.hardware.per_layer_compute_us, counters, per_layer)
+        decode_passes = int((pk.pass_kind == 1).sum())
+        return LayerStepResult(
+            ttft_ms=res.ttft_ms, total_ms=res.total_ms, decode_ms=res.decode_ms,
+            decode_tokens_per_sec=decode_passes / (res.decode_ms / 1e3) if res.decode_ms > 0 else 0.0,
+            h2d_bytes=res.h2d_bytes, h2d_gbs=res.h2d_bytes / (res.total_ms / 1e3) / 1e9,
+            n_copies=res.n_copies, n_demand_copies=res.n_demand_copies, n_prefetch_copies=res.n_prefetch_copies,
+            n_cancelled=res.n_cancelled, n_ffn_batches=res.n_ffn_batches, n_exec_experts=res.n_exec_experts,
+            host_enqueue_ms=res.host_enqueue_ms, report=rep, out=out if keep_outputs else None)
+
+    def close(self) -> None:
+        if self._h:
+            _bind().esim_ls_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
