@@ -1,0 +1,34 @@
+"""FFN kernel microbenchmark: prefill-64 layer (~28 experts x ~18 tokens) and decode (8 experts x 1 token).
+Reports per-layer time and achieved HBM GB/s (12,582,912 B weights per expert + activations)."""
+import sys, json
+sys.path.insert(0, ".")
+import numpy as np, torch
+from paper_2602_03921_b200.ffn import ExpertSlots, npad_for, routing_tables
+H, I = 2048, 1024
+out = {}
+slots = ExpertSlots(64, H, I, max_tokens=64, max_exec=64)
+slots.buf.copy_((torch.randn(slots.buf.numel(), device="cuda") * 0.02).to(torch.bfloat16))
+flush = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")
+for name, T, K, n_exp in (("prefill64", 64, 8, 28), ("decode", 1, 8, 8), ("prefill64_all64", 64, 8, 64)):
+    rng = np.random.default_rng(0)
+    x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
+    row_sel = np.stack([rng.choice(n_exp, size=K, replace=False) for _ in range(T)]).astype(np.int32)
+    row_w = rng.uniform(0.01, 0.3, size=(T, K)).astype(np.float32)
+    npad = npad_for(int(np.bincount(row_sel.ravel()).max()))
+    ti, tw = routing_tables(row_sel, row_w, {e: (e, e) for e in range(n_exp)}, npad)
+    ti, tw = torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda()
+    es = torch.arange(n_exp, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        slots.run_layer(x, es, ti, tw, npad, residual=False)
+    ts = []
+    for _ in range(20):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); slots.run_layer(x, es, ti, tw, npad, residual=False); e1.record()
+        torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    byt = n_exp * 3 * H * I * 2
+    flops = 2 * 3 * H * I * int(row_sel.size)
+    out[name] = {"ms": ms, "npad": npad, "weight_gbs": byt / ms / 1e6, "tflops": flops / ms / 1e9}
+    print(name, out[name], flush=True)
+json.dump(out, open("gpurun_out/bench_ffn.json", "w"), indent=1)
