@@ -82,6 +82,44 @@ class Tally:
         return t
 
 
+def prefetch_precision_recall(predictions: list, demanded: dict) -> dict:
+    """Micro/macro prediction quality over predicted (pass, layer) pairs
+    (metrics.py:150-187). `demanded` maps (pass_id, layer) -> expert set."""
+    t = Tally(0)
+    precs, recs = [], []
+    for r in predictions:
+        dem = demanded.get((r.pass_id, r.target_layer), set())
+        hit = len(dem.intersection(r.experts))
+        t.pf_tp += hit
+        t.pf_pred_total += len(r.experts)
+        t.pf_dem_total += len(dem)
+        t.pf_records += 1
+        if r.experts:
+            precs.append(hit / len(r.experts))
+        else:
+            t.pf_empty += 1
+        if dem:
+            recs.append(hit / len(dem))
+    t.pf_prec_sum, t.pf_rec_sum = sum(precs), sum(recs)
+    t.pf_prec_parts, t.pf_rec_parts = len(precs), len(recs)
+    return _prefetch_section(t)
+
+
+def _prefetch_section(t: "Tally") -> dict:
+    zero_den = t.pf_pred_total == 0
+    return {
+        "precision_micro": 1.0 if zero_den else t.pf_tp / t.pf_pred_total,
+        "recall_micro": 1.0 if t.pf_dem_total == 0 else _ratio(t.pf_tp, t.pf_dem_total),
+        "precision_macro": _ratio(t.pf_prec_sum, t.pf_prec_parts) if t.pf_prec_parts else 1.0,
+        "recall_macro": _ratio(t.pf_rec_sum, t.pf_rec_parts) if t.pf_rec_parts else 1.0,
+        "predicted_layers": t.pf_records,
+        "predicted_total": t.pf_pred_total,
+        "predicted_hit_total": t.pf_tp,
+        "empty_predictions": t.pf_empty,
+        "zero_denominator": zero_den,
+    }
+
+
 def _count_log(num_layers: int, log: list) -> Tally:
     t = Tally(num_layers)
     demanded: dict = {}
@@ -186,18 +224,7 @@ def _format_report(config_echo: dict, num_layers: int, per_layer_compute_us: int
         "per_layer_compute_us": per_layer_compute_us,
         "decode_tokens_per_sec": t.decode_passes * 1_000_000 / t.decode_us if t.decode_us > 0 else 0.0,
     }
-    zero_den = t.pf_pred_total == 0
-    prefetch = {
-        "precision_micro": 1.0 if zero_den else t.pf_tp / t.pf_pred_total,
-        "recall_micro": 1.0 if t.pf_dem_total == 0 else _ratio(t.pf_tp, t.pf_dem_total),
-        "precision_macro": _ratio(t.pf_prec_sum, t.pf_prec_parts) if t.pf_prec_parts else 1.0,
-        "recall_macro": _ratio(t.pf_rec_sum, t.pf_rec_parts) if t.pf_rec_parts else 1.0,
-        "predicted_layers": t.pf_records,
-        "predicted_total": t.pf_pred_total,
-        "predicted_hit_total": t.pf_tp,
-        "empty_predictions": t.pf_empty,
-        "zero_denominator": zero_den,
-    }
+    prefetch = _prefetch_section(t)
     report = {"config": config_echo, "totals": tot, "rates": rates, "timing": timing,
               "fidelity": fidelity, "prefetch": prefetch, "per_layer": per_layer}
     check_identities(report)

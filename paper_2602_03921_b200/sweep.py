@@ -203,3 +203,44 @@ class DeviceSweep:
 
     def results(self) -> list:
         return self.batch.results()
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU sharding: contiguous cost-balanced blocks
+# of the grid per rank, fixed-size counter records all-gathered to every rank
+# ---------------------------------------------------------------------------
+RECORD_BYTES = C.sizeof(_abi.EsimCounters)
+
+
+def point_costs(cfgs, traces) -> list:
+    """Relative replay cost per point: demanded token-expert selections of its trace."""
+    cache: dict = {}
+    out = []
+    for cfg, tr in zip(cfgs, traces):
+        if id(tr) not in cache:
+            pk = tr.packed()
+            cache[id(tr)] = int(pk.row_offset[-1]) * pk.top_k
+        out.append(cache[id(tr)])
+    return out
+
+
+def gather_counter_records(local: bytes, bounds: list, group=None, device=None) -> bytes:
+    """All-gather each rank's packed EsimCounters records (rank r holds points
+    bounds[r][0]:bounds[r][1]) and return all records in global point order.
+    One all_gather_into_tensor of equal-size (padded) buffers: NCCL on GPU
+    ranks, gloo on CPU."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lens = [(hi - lo) * RECORD_BYTES for lo, hi in bounds]
+    assert len(local) == lens[rank], (len(local), lens[rank])
+    width = max(lens) if lens else 0
+    dev = device if device is not None else torch.device("cpu")
+    buf = torch.zeros(width, dtype=torch.uint8, device=dev)
+    if local:
+        buf[:len(local)] = torch.frombuffer(bytearray(local), dtype=torch.uint8).to(dev)
+    out = torch.empty(world * width, dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    host = out.cpu().numpy().tobytes()
+    return b"".join(host[r * width:r * width + lens[r]] for r in range(world))
