@@ -236,7 +236,13 @@ class ReplayBatch:
         groups: dict = {}
         for i, c in enumerate(self.ccfg):
             groups.setdefault((c.num_layers, c.experts), []).append(i)
-        self.groups = list(groups.values())
+        # costliest points first so the long replays start in the first wave:
+        # cost ~ capacity in experts (victim-scan length) x link slowness
+        def cost(i):
+            c = self.ccfg[i]
+            slots = c.capacity_bytes // max(1, c.expert_bytes[c.working_prec])
+            return (-slots, c.bandwidth if c.bandwidth else 1 << 62, i)
+        self.groups = [sorted(g, key=cost) for g in groups.values()]
         self.order = [i for g in self.groups for i in g]
         harr = (_abi.EsimConfig * n)(*[self.ccfg[i] for i in self.order])
         self.h_cfg = harr

@@ -100,6 +100,8 @@ static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stri
         for (int p = 0; p < 4; p++)
             if (c.expert_bytes[p] > 0) minb = std::min(minb, c.expert_bytes[p]);
         if (minb == INT64_MAX) return fail(-1, "no precision available");
+        // only fetch_low / fetch_priority can admit below the working precision
+        if (c.miss != ESIM_MISS_FETCH_LOW && c.miss != ESIM_MISS_FETCH_PRIORITY) minb = c.expert_bytes[c.working_prec];
         int64_t slots = std::min<int64_t>(c.capacity_bytes / minb, N);
         s.N = std::max(s.N, N);
         s.S = std::max<int>(s.S, (int)std::max<int64_t>(slots, 1));

@@ -977,6 +977,9 @@ __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArg
     }
     p.eb0 = ebs[0]; p.eb1 = ebs[1]; p.eb2 = ebs[2]; p.eb3 = ebs[3];
     p.dur0 = durs[0]; p.dur1 = durs[1]; p.dur2 = durs[2]; p.dur3 = durs[3];
+    // residents + queued transfers <= capacity / (smallest expert this point can admit):
+    // only fetch_low / fetch_priority ever admit below the working precision
+    if (cfg->miss != ESIM_MISS_FETCH_LOW && cfg->miss != ESIM_MISS_FETCH_PRIORITY) minb = peb(p, cfg->working_prec);
     int64_t slots = p.cap / minb;
     if (slots > N) slots = N;
     if (slots > A.S) slots = A.S;
