@@ -162,6 +162,40 @@ int esim_predictor_params(int32_t top_k, int32_t experts, int32_t pred_mode, dou
 int esim_softmax_launch(const float *d_x, int32_t rows, int32_t experts, float *d_out, void *stream);
 int esim_topk_launch(const float *d_scores, int32_t rows, int32_t experts, int32_t k, int32_t *d_idx, void *stream);
 
+/* routing.route_event(policy=CACHE_AWARE) for one event (routing.py:143-161):
+ * cached_mask bit e = expert e resident at the layer; delta[2] = (sum, count)
+ * of the layer's DeltaAvgState, updated in place. Outputs per row: selected
+ * and original top-k (int16 [rows][k]) with their original-softmax weights,
+ * and the modified flag. Device pointers, one warp. */
+int esim_route_cache_aware_launch(const float *d_x, int32_t rows, int32_t experts, int32_t top_k,
+                                  const uint32_t *d_cached_mask, double lam, double *d_delta, int16_t *d_sel,
+                                  float *d_w, int16_t *d_orig, float *d_ow, int32_t *d_modified, void *stream);
+
+/* Eviction-policy plug-in objects (eviction.py:29-294) on the device.
+ * op: 0 begin_pass, 1 note_access, 2 note_admit, 3 note_prefetch_hit,
+ * 4 select_victim (result appended to d_results: key index or -1).
+ * gate NaN = None; prec = precision code or -1. */
+typedef struct {
+    int32_t op, key, layer, prec;
+    int32_t forced, pad;
+    double gate;
+} EsimPolicyOp;                    /* 32 bytes */
+
+typedef struct {
+    int32_t policy, num_layers, highest_prec, n_keys;
+    double decay;
+    int64_t *seq;                  /* device [1] */
+    int64_t *counters;             /* device [2]: forced_current_evictions, refusals (LS) */
+    uint8_t *flags;                /* device [n_keys] */
+    int64_t *key;                  /* stamp / generation / touch */
+    int32_t *count;                /* LFU / LHU */
+    double *signal;                /* SB */
+    int32_t *layer, *expert;
+} EsimPolicyState;
+
+int esim_policy_apply(const EsimPolicyState *state, const EsimPolicyOp *d_ops, int32_t n_ops, int32_t *d_results,
+                      void *stream);
+
 /* Shared memory one replayed grid point needs (for the host's grouping). */
 int esim_replay_smem_per_point(const EsimConfig *h_cfg, int32_t n, int32_t max_tokens, int32_t pl_stride,
                                int32_t queue_cap);

@@ -70,3 +70,17 @@ def trace_desc_host(pk) -> tuple[EsimTraceDesc, list]:
                       int(pk.row_offset[-1]), keep[0].ctypes.data, keep[1].ctypes.data,
                       keep[2].ctypes.data, keep[3].ctypes.data)
     return d, keep
+
+
+class EsimPolicyOp(C.Structure):
+    _fields_ = [("op", C.c_int32), ("key", C.c_int32), ("layer", C.c_int32), ("prec", C.c_int32),
+                ("forced", C.c_int32), ("pad", C.c_int32), ("gate", C.c_double)]
+
+
+class EsimPolicyState(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("num_layers", C.c_int32), ("highest_prec", C.c_int32),
+                ("n_keys", C.c_int32), ("decay", C.c_double)] + \
+               [(n, C.c_void_p) for n in ("seq", "counters", "flags", "key", "count", "signal", "layer", "expert")]
+
+
+assert C.sizeof(EsimPolicyOp) == 32

@@ -43,6 +43,7 @@ def lib():
         L.esim_run_host.argtypes = [vp, i32, vp, i32, vp, vp, i32, vp, i64, vp, i64]
         L.esim_softmax_launch.argtypes = [vp, i32, i32, vp, vp]
         L.esim_host_register.argtypes = [vp, C.c_size_t]
+        L.esim_route_cache_aware_launch.argtypes = [vp, i32, i32, i32, vp, f64, vp, vp, vp, vp, vp, vp, vp]
         L.esim_tmap_bf16.argtypes = [vp, vp, i64, i64, i32]
         L.esim_ffn_gather.argtypes = [vp, vp, vp, i32, i32, i32, vp]
         L.esim_ffn_residual.argtypes = [vp, vp, i64, vp]
@@ -378,8 +379,8 @@ def _single_event_trace(logits: np.ndarray, k: int):
 
 
 def route_event(logits, k, policy, lam, cached, delta, layer) -> list:
-    if policy != "standard":
-        raise NotImplementedError("standalone cache-aware route_event: use Simulation (replay kernel routes it)")
+    if policy == "cache_aware":
+        return _route_cache_aware(logits, k, lam, cached, delta, layer)
     tr = _single_event_trace(logits, k)
     dt = DeviceTrace(tr.packed())
     ro = route_trace(dt, "none", 1.0, 80.0)
@@ -392,6 +393,38 @@ def route_event(logits, k, policy, lam, cached, delta, layer) -> list:
         ws = [float(v) for v in w[r]]
         out.append(RoutingDecision(idx, ws, list(idx), list(ws), False))
     return out
+
+
+def _route_cache_aware(logits, k, lam, cached, delta, layer) -> list:
+    from .routing import validate_lambda
+    torch = _torch()
+    validate_lambda(lam)
+    x = np.ascontiguousarray(logits, np.float32)
+    if x.ndim == 1:
+        x = x[None, :]
+    T, E = x.shape
+    mask = np.zeros((E + 31) // 32, np.uint32)
+    for e in cached:
+        mask[e >> 5] |= np.uint32(1 << (e & 31))
+    d = torch.tensor([delta.sums.get(layer, 0.0), float(delta.counts.get(layer, 0))], dtype=torch.float64,
+                     device="cuda")
+    dx = torch.from_numpy(x).cuda()
+    dm = torch.from_numpy(mask).cuda()
+    sel = torch.empty(T * k, dtype=torch.int16, device="cuda")
+    orig = torch.empty_like(sel)
+    w = torch.empty(T * k, dtype=torch.float32, device="cuda")
+    ow = torch.empty_like(w)
+    mod = torch.empty(T, dtype=torch.int32, device="cuda")
+    _check(lib().esim_route_cache_aware_launch(dx.data_ptr(), T, E, k, dm.data_ptr(), float(lam), d.data_ptr(),
+                                               sel.data_ptr(), w.data_ptr(), orig.data_ptr(), ow.data_ptr(),
+                                               mod.data_ptr(), _stream()), "cache-aware route")
+    dh = d.cpu().numpy()
+    delta.sums[layer] = float(dh[0])
+    delta.counts[layer] = int(dh[1])
+    sel, orig = sel.cpu().numpy().reshape(T, k), orig.cpu().numpy().reshape(T, k)
+    w, ow, mod = w.cpu().numpy().reshape(T, k), ow.cpu().numpy().reshape(T, k), mod.cpu().numpy()
+    return [RoutingDecision([int(i) for i in sel[r]], [float(v) for v in w[r]], [int(i) for i in orig[r]],
+                            [float(v) for v in ow[r]], bool(mod[r])) for r in range(T)]
 
 
 def predict_event(next_logits, k, mode, overfetch, percentile):

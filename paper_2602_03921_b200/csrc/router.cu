@@ -323,3 +323,72 @@ extern "C" int esim_topk_launch(const float* d_s, int32_t rows, int32_t E, int32
     esim::topk_rows_kernel<<<blocks, wpb * 32, wpb * E * 4, (cudaStream_t)stream>>>(d_s, rows, E, k, d_idx);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
+
+// ---------------------------------------------------------------------------
+// routing.route_event(policy=CACHE_AWARE) for one event (routing.py:143-161):
+// rows in order (the running mean a row's bias uses includes every earlier
+// row), one warp. cached: bit e of cached_mask set when expert e is resident
+// at this layer. delta[0] = sums[layer], delta[1] = counts[layer] (in/out).
+// ---------------------------------------------------------------------------
+#include "warp_route.cuh"
+namespace esim {
+__global__ void route_cache_aware_kernel(const float* __restrict__ x, int T, int E, int K,
+                                         const uint32_t* __restrict__ cached_mask, double lam, double* delta,
+                                         int16_t* sel, float* w, int16_t* orig, float* ow, int32_t* modified) {
+    extern __shared__ float rbuf[];
+    float* buf = rbuf;          // [E]
+    float* sc = rbuf + E;       // [E] original scores
+    const int lane = threadIdx.x & 31;
+    bool any_cached = false;
+    for (int e = lane; e < E; e += 32) any_cached |= (cached_mask[e >> 5] >> (e & 31)) & 1;
+    any_cached = __any_sync(0xffffffffu, any_cached);
+    double sum = delta[0];
+    double cnt = delta[1];
+    for (int r = 0; r < T; r++) {
+        const float* xr = x + (int64_t)r * E;
+        for (int i = lane; i < E; i += 32) buf[i] = xr[i];
+        __syncwarp();
+        warp_softmax(buf, E, lane);
+        for (int i = lane; i < E; i += 32) sc[i] = buf[i];
+        __syncwarp();
+        warp_topk(sc, E, K, lane, orig + r * K);
+        const double mean = cnt != 0.0 ? __ddiv_rn(sum, cnt) : 0.0;
+        const bool on = lam != 0.0 && mean != 0.0 && any_cached;
+        const float bias = __double2float_rn(__dmul_rn(lam, mean));
+        for (int i = lane; i < E; i += 32) {
+            float v = xr[i];
+            if (on && ((cached_mask[i >> 5] >> (i & 31)) & 1)) v = __fadd_rn(v, bias);
+            buf[i] = v;
+        }
+        __syncwarp();
+        warp_softmax(buf, E, lane);
+        warp_topk(buf, E, K, lane, sel + r * K);
+        for (int i = lane; i < E; i += 32) buf[i] = xr[i];
+        __syncwarp();
+        sum = __dadd_rn(sum, __dadd_rn(0.0, warp_pw_sum_f64(buf, E, lane)));
+        cnt = __dadd_rn(cnt, (double)E);
+        if (lane == 0) {
+            bool same = true;
+            for (int a = 0; a < K; a++) {
+                bool f = false;
+                for (int b = 0; b < K; b++) f |= sel[r * K + a] == orig[r * K + b];
+                same &= f;
+            }
+            modified[r] = same ? 0 : 1;
+            for (int a = 0; a < K; a++) { w[r * K + a] = sc[sel[r * K + a]]; ow[r * K + a] = sc[orig[r * K + a]]; }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) { delta[0] = sum; delta[1] = cnt; }
+}
+}  // namespace esim
+
+extern "C" int esim_route_cache_aware_launch(const float* d_x, int32_t rows, int32_t experts, int32_t top_k,
+                                             const uint32_t* d_cached_mask, double lam, double* d_delta,
+                                             int16_t* d_sel, float* d_w, int16_t* d_orig, float* d_ow,
+                                             int32_t* d_modified, void* stream) {
+    if (experts < 1 || experts > ESIM_MAX_E || top_k < 1 || top_k > ESIM_MAX_K || top_k > experts) return -1;
+    esim::route_cache_aware_kernel<<<1, 32, 2 * experts * 4, (cudaStream_t)stream>>>(
+        d_x, rows, experts, top_k, d_cached_mask, lam, d_delta, d_sel, d_w, d_orig, d_ow, d_modified);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}

@@ -119,3 +119,39 @@ def test_c_abi_host_path_matches_oracle(oracle_lib):
         o = oracle_lib.run(cfg, tr, full_log=False)
         assert o.counters.digest == c.digest, (cfg.model.name, cfg.eviction)
         assert json.dumps(o.report) == json.dumps(rep)
+
+
+def test_standalone_route_event_cache_aware_matches_reference():
+    import os
+    import numpy as np
+    from paper_2602_03921_b200.routing import DeltaAvgState, route_event
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "router_cache_aware.json")))
+    for case in gold:
+        delta = DeltaAvgState()
+        for ev in case["events"]:
+            x = np.array([[float.fromhex(v) for v in r] for r in ev["logits"]], np.float32)
+            dec = route_event(x, case["k"], "cache_aware", case["lam"], set(ev["cached"]), delta, ev["layer"])
+            assert [d.selected for d in dec] == ev["selected"]
+            assert [d.original_selected for d in dec] == ev["original"]
+            assert [[float(w).hex() for w in d.weights] for d in dec] == ev["weights"]
+            assert [d.modified for d in dec] == ev["modified"]
+            assert [float(delta.sums[ev["layer"]]).hex(), delta.counts[ev["layer"]]] == ev["delta"]
+
+
+def test_standalone_router_kats_match_reference():
+    import gzip
+    import os
+    import numpy as np
+    from paper_2602_03921_b200.prefetch import predict_event
+    from paper_2602_03921_b200.routing import DeltaAvgState, route_event, softmax_rows
+    gold = json.load(gzip.open(os.path.join(os.path.dirname(__file__), "golden", "router.json.gz"), "rt"))
+    for c in gold["cases"]:
+        x = np.array([[float.fromhex(v) for v in r] for r in c["logits"]], np.float32)
+        sm = softmax_rows(x)
+        assert [[float(v).hex() for v in r] for r in sm] == c["softmax"]
+        dec = route_event(x, c["k"], "standard", 0.3, set(), DeltaAvgState(), 0)
+        assert [d.selected for d in dec] == c["selected"]
+        for mode, kw in (("topk", {"overfetch": 1.5}), ("score", {"percentile": 80.0}), ("oracle", {}),
+                         ("score0", {"percentile": 0.0})):
+            p, cl = predict_event(x, c["k"], "score" if mode == "score0" else mode, **kw)
+            assert [[int(a), float(b).hex()] for a, b in p] + [bool(cl)] == c["predict"][mode], mode
