@@ -252,8 +252,18 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
     // geometry groups (stable), each replayed on its own stream with its own shared-memory sizing
     std::vector<int> order(n);
     for (int i = 0; i < n; i++) order[i] = i;
+    // group by geometry; inside a group the costliest points first (largest cache in
+    // experts = longest victim scans, then slowest link) so long replays start in wave 1
+    auto slots_of = [&](int a) {
+        const int64_t wb = cfg[a].expert_bytes[cfg[a].working_prec];
+        return wb > 0 ? cfg[a].capacity_bytes / wb : 0;
+    };
+    auto bw_of = [&](int a) { return cfg[a].bandwidth ? cfg[a].bandwidth : INT64_MAX; };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        return std::make_pair(cfg[a].num_layers, cfg[a].experts) < std::make_pair(cfg[b].num_layers, cfg[b].experts);
+        if (cfg[a].num_layers != cfg[b].num_layers) return cfg[a].num_layers < cfg[b].num_layers;
+        if (cfg[a].experts != cfg[b].experts) return cfg[a].experts < cfg[b].experts;
+        if (slots_of(a) != slots_of(b)) return slots_of(a) > slots_of(b);
+        return bw_of(a) < bw_of(b);
     });
     std::vector<std::pair<int, int>> groups;   // [begin, end) in `order`
     for (int i = 0; i < n; i++) {

@@ -4,7 +4,7 @@ set -e
 cd $GRAFT_REPO_ROOT
 for MINB in 1 2 3 4; do
   D=/tmp/v$MINB; mkdir -p $D
-  for f in capi router replay; do
+  for f in capi router replay ffn_gemm layer_step policy; do
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -DESIM_REPLAY_MINB=$MINB -c paper_2602_03921_b200/csrc/$f.cu -o $D/$f.o 2>&1 | grep -E "error" || true
   done
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $D/lib.so $D/*.o -lcudart
