@@ -235,8 +235,9 @@ class ReplayBatch:
         n = len(self.ccfg)
         self.Lmax = max(c.num_layers for c in self.ccfg)
         groups: dict = {}
-        for i, c in enumerate(self.ccfg):
-            groups.setdefault((c.num_layers, c.experts), []).append(i)
+        for i, c in enumerate(self.ccfg):   # one launch per (geometry, policy, general): specialised kernels
+            general = c.miss != 0 or c.routing != 0
+            groups.setdefault((c.num_layers, c.experts, c.eviction, general), []).append(i)
         # costliest points first so the long replays start in the first wave:
         # cost ~ capacity in experts (victim-scan length) x link slowness
         def cost(i):

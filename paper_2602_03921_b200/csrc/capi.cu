@@ -23,7 +23,8 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     const EsimRouterOut* d_routers, EsimCounters* d_counters,
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
-                                    bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress = nullptr);
+                                    bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
+                                    int policy, bool general);
 int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt);
 
 static thread_local std::string g_err;
@@ -83,14 +84,14 @@ extern "C" int esim_router_launch(const EsimTraceDesc* tr, const EsimRouterOut* 
     return 0;
 }
 
-struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca, has_cnt; };
+struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca, has_cnt; int policy; bool general; };
 
 // queue_cap <= 0: the exact bound (resident slots + 1 entries: every queued
 // transfer holds a reservation of >= the smallest expert, so the channel can
 // never outgrow it). A positive cap trades shared memory for the risk of
 // status -5, which the caller resolves by re-launching with the bound.
 static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stride, int queue_cap, Sizing* z) {
-    Sizing s{0, 1, 2, 0, 0, 0, 0, false, false};
+    Sizing s{0, 1, 2, 0, 0, 0, 0, false, false, n > 0 ? h[0].eviction : 0, false};
     for (int i = 0; i < n; i++) {
         const EsimConfig& c = h[i];
         if (c.experts > ESIM_MAX_E || c.top_k > ESIM_MAX_K) return fail(-1, "geometry exceeds device limits");
@@ -110,6 +111,8 @@ static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stri
         s.Kmax = std::max(s.Kmax, c.top_k);
         if (c.routing == ESIM_ROUTE_CACHE_AWARE) s.ca = true;
         if (c.eviction == ESIM_EV_LFU || c.eviction == ESIM_EV_LHU) s.has_cnt = true;
+        if (c.eviction != s.policy) return fail(-1, "one replay launch replays one eviction policy (group the points)");
+        if (c.miss != ESIM_MISS_FETCH || c.routing != ESIM_ROUTE_STANDARD) s.general = true;
     }
     if (s.S > 4095) return fail(-1, "more than 4095 resident experts per cache is not supported by the device directory");
     s.Q = queue_cap > 0 ? std::min(queue_cap, s.S + 1) : s.S + 1;
@@ -145,7 +148,7 @@ extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_c
                                               std::to_string(per) + " B)");
     cudaError_t e = esim_replay_launch_impl(d_cfg, n, d_traces, d_routers, d_counters, d_per_layer, d_recs, rec_cap,
                                             d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
-                                            w, (cudaStream_t)stream);
+                                            w, (cudaStream_t)stream, nullptr, z.policy, z.general);
     if (e != cudaSuccess) return cuda_fail(e, "replay launch");
     return 0;
 }
@@ -160,7 +163,7 @@ int esim_replay_launch_streamed(const EsimConfig* h_cfg, const EsimConfig* d_cfg
     if (rc) return rc;
     cudaError_t e = esim_replay_launch_impl(d_cfg, 1, d_traces, d_routers, d_counters, d_per_layer, d_recs, rec_cap,
                                             d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
-                                            1, (cudaStream_t)stream, progress);
+                                            1, (cudaStream_t)stream, progress, z.policy, z.general);
     if (e != cudaSuccess) return cuda_fail(e, "streamed replay launch");
     return 0;
 }
@@ -259,16 +262,20 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
         return wb > 0 ? cfg[a].capacity_bytes / wb : 0;
     };
     auto bw_of = [&](int a) { return cfg[a].bandwidth ? cfg[a].bandwidth : INT64_MAX; };
+    auto gen_of = [&](int a) { return cfg[a].miss != ESIM_MISS_FETCH || cfg[a].routing != ESIM_ROUTE_STANDARD; };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
         if (cfg[a].num_layers != cfg[b].num_layers) return cfg[a].num_layers < cfg[b].num_layers;
         if (cfg[a].experts != cfg[b].experts) return cfg[a].experts < cfg[b].experts;
+        if (cfg[a].eviction != cfg[b].eviction) return cfg[a].eviction < cfg[b].eviction;
+        if (gen_of(a) != gen_of(b)) return gen_of(a) < gen_of(b);
         if (slots_of(a) != slots_of(b)) return slots_of(a) > slots_of(b);
         return bw_of(a) < bw_of(b);
     });
     std::vector<std::pair<int, int>> groups;   // [begin, end) in `order`
     for (int i = 0; i < n; i++) {
         if (i == 0 || cfg[order[i]].num_layers != cfg[order[i - 1]].num_layers ||
-            cfg[order[i]].experts != cfg[order[i - 1]].experts)
+            cfg[order[i]].experts != cfg[order[i - 1]].experts ||
+            cfg[order[i]].eviction != cfg[order[i - 1]].eviction || gen_of(order[i]) != gen_of(order[i - 1]))
             groups.push_back({i, i + 1});
         else
             groups.back().second = i + 1;

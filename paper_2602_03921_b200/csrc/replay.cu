@@ -128,6 +128,7 @@ struct Pt {
     const EsimConfig* c;
     int L, E, K, S, Q;
     int pol, lane;
+    int miss;                       // ESIM_MISS_* (constant-folded in the simple specialisation)
     int64_t cap;
     int64_t dur0, dur1, dur2, dur3, eb0, eb1, eb2, eb3;   // by precision code (registers, not an array)
     // shared memory
@@ -653,12 +654,12 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
         access_rec(p, expert, tokens, rank, 2, mclass, blocked, 0.0, prec, -1);
         return 2;
     }
-    if (cfg->miss == ESIM_MISS_DROP && rank > cfg->drop_rank_threshold) {
+    if (p.miss == ESIM_MISS_DROP && rank > cfg->drop_rank_threshold) {
         wd = -summed;
         access_rec(p, expert, tokens, rank, 3, -1, 0, wd, -1, -1);
         return 3;
     }
-    if (cfg->miss == ESIM_MISS_SUBST) {                                   // find_substitute (miss.py:66-79)
+    if (p.miss == ESIM_MISS_SUBST) {                                     // find_substitute (miss.py:66-79)
         double bd = 0.0;
         int be = -1;
         for (int e0 = 0; e0 < p.E; e0 += 32) {
@@ -695,10 +696,10 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
     }
     int prec = cfg->working_prec;
     int64_t b = -1;
-    if (cfg->miss == ESIM_MISS_FETCH_LOW) {
+    if (p.miss == ESIM_MISS_FETCH_LOW) {
         prec = cfg->precisions[cfg->n_precisions - 1];
         b = do_fetch(p, ident, gate, prec, true);
-    } else if (cfg->miss == ESIM_MISS_FETCH_PRIORITY) {
+    } else if (p.miss == ESIM_MISS_FETCH_PRIORITY) {
         int start = 0;
         if (cfg->n_precisions > 1 && nd > 0) {
             long rk = (long)ceil(cfg->degrade_percentile / 100.0 * (double)nd);
@@ -883,6 +884,10 @@ DFI int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int
 #ifndef ESIM_REPLAY_MINB
 #define ESIM_REPLAY_MINB 1
 #endif
+// POL: eviction policy; GEN: 0 = the common case (miss=fetch, standard routing) with every
+// other miss/routing path compiled out, 1 = all paths. Every helper is force-inlined, so the
+// compile-time policy/miss constants delete the other policies' code from the kernel.
+template <int POL, int GEN>
 __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int wid = threadIdx.x >> 5;
@@ -892,7 +897,7 @@ __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArg
     const EsimTraceDesc tr = A.traces[cfg->trace_id];
     const EsimRouterOut R = A.routers[cfg->trace_id];
     unsigned char* base = smem_raw + (size_t)wid * A.point_bytes;
-    const bool ca = cfg->routing == ESIM_ROUTE_CACHE_AWARE;
+    const bool ca = GEN && cfg->routing == ESIM_ROUTE_CACHE_AWARE;
     const Layout lay = make_layout(A.N, A.S, A.Q, A.Lmax, A.Emax, A.Tmax, A.Kmax, A.Tmax > 0, A.has_cnt != 0);
 
     Pt p;
@@ -900,7 +905,12 @@ __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArg
     p.L = cfg->num_layers; p.E = cfg->experts; p.K = cfg->top_k;
     const int N = p.L * p.E;
     p.lane = threadIdx.x & 31;
-    p.pol = cfg->eviction;
+    p.pol = POL;
+    p.miss = GEN ? cfg->miss : ESIM_MISS_FETCH;
+    if (cfg->eviction != POL || (!GEN && (cfg->miss != ESIM_MISS_FETCH || cfg->routing != ESIM_ROUTE_STANDARD))) {
+        if ((threadIdx.x & 31) == 0) A.counters[pid].status = -1;      // dispatch error
+        return;
+    }
     p.cap = cfg->capacity_bytes;
     const int64_t bw = cfg->bandwidth;
     int64_t minb = INT64_MAX;
@@ -916,7 +926,7 @@ __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArg
     p.dur0 = durs[0]; p.dur1 = durs[1]; p.dur2 = durs[2]; p.dur3 = durs[3];
     // residents + queued transfers <= capacity / (smallest expert this point can admit):
     // only fetch_low / fetch_priority ever admit below the working precision
-    if (cfg->miss != ESIM_MISS_FETCH_LOW && cfg->miss != ESIM_MISS_FETCH_PRIORITY) minb = peb(p, cfg->working_prec);
+    if (p.miss != ESIM_MISS_FETCH_LOW && p.miss != ESIM_MISS_FETCH_PRIORITY) minb = peb(p, cfg->working_prec);
     int64_t slots = p.cap / minb;
     if (slots > N) slots = N;
     if (slots > A.S) slots = A.S;
@@ -1012,7 +1022,7 @@ __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArg
                 d_exp = R.dem_expert + ev * p.E; d_rank = R.dem_rank + ev * p.E; d_gate = R.dem_gate + ev * p.E;
                 d_sum = R.dem_summed + ev * p.E; d_tok = R.dem_tokens + ev * p.E;
             }
-            if (cfg->miss == ESIM_MISS_FETCH_PRIORITY) {                  // layer scores in demand order
+            if (p.miss == ESIM_MISS_FETCH_PRIORITY) {                    // layer scores in demand order
                 for (int i = p.lane; i < nd; i += 32) p.lsc[i] = ca ? d_gate[d_exp[i]] : d_gate[i];
                 __syncwarp();
             }
@@ -1041,7 +1051,7 @@ __global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArg
             int64_t blocked = 0;
             double wdelta = 0.0;
             bool any_aff = false;
-            if (cfg->miss == ESIM_MISS_DROP || cfg->miss == ESIM_MISS_SUBST) {
+            if (p.miss == ESIM_MISS_DROP || p.miss == ESIM_MISS_SUBST) {
                 for (int i = p.lane; i < (p.E + 31) / 32; i += 32) p.demmask[i] = 0;
                 __syncwarp();
             }
@@ -1169,7 +1179,8 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     const EsimRouterOut* d_routers, EsimCounters* d_counters,
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
-                                    bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress) {
+                                    bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
+                                    int policy, bool general) {
     esim::ReplayArgs a;
     a.progress = progress;
     a.cfg = d_cfg; a.n_points = n; a.traces = d_traces; a.routers = d_routers;
@@ -1180,10 +1191,18 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
     a.warps_per_cta = warps_per_cta;
     a.point_bytes = esim::make_layout(N, S, Q, Lmax, Emax, Tmax, Kmax, Tmax > 0, has_cnt).total;
     const size_t smem = (size_t)a.point_bytes * warps_per_cta;
-    cudaError_t e = cudaFuncSetAttribute(esim::replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
     const int blocks = (n + warps_per_cta - 1) / warps_per_cta;
-    esim::replay_kernel<<<blocks, 32 * warps_per_cta, smem, st>>>(a);
+    void (*k)(esim::ReplayArgs) = nullptr;
+#define ESIM_PICK(P)                                                                   \
+    case P: k = general ? esim::replay_kernel<P, 1> : esim::replay_kernel<P, 0>; break;
+    switch (policy) {
+        ESIM_PICK(ESIM_EV_LRU) ESIM_PICK(ESIM_EV_LFU) ESIM_PICK(ESIM_EV_LHU)
+        ESIM_PICK(ESIM_EV_FLD) ESIM_PICK(ESIM_EV_SB) ESIM_PICK(ESIM_EV_LS)
+        default: return cudaErrorInvalidValue;
+    }
+#undef ESIM_PICK
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<blocks, 32 * warps_per_cta, smem, st>>>(a);
     return cudaGetLastError();
 }
