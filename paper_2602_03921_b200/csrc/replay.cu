@@ -884,11 +884,14 @@ DFI int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int
 #ifndef ESIM_REPLAY_MINB
 #define ESIM_REPLAY_MINB 1
 #endif
+#ifndef ESIM_SIMPLE_MINB
+#define ESIM_SIMPLE_MINB 1          // blocks/SM hint for the common-path instances
+#endif
 // POL: eviction policy; GEN: 0 = the common case (miss=fetch, standard routing) with every
 // other miss/routing path compiled out, 1 = all paths. Every helper is force-inlined, so the
 // compile-time policy/miss constants delete the other policies' code from the kernel.
 template <int POL, int GEN>
-__global__ void __launch_bounds__(128, ESIM_REPLAY_MINB) replay_kernel(ReplayArgs A) {
+__global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB) replay_kernel(ReplayArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int wid = threadIdx.x >> 5;
     const int pid = blockIdx.x * A.warps_per_cta + wid;
