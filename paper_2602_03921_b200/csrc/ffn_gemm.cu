@@ -33,7 +33,14 @@ namespace ffn {
 
 constexpr int BM = 128;          // weight rows per tile (UMMA M)
 constexpr int BK = 64;           // 64 bf16 = 128 B = one swizzle-128B atom row
-constexpr int STAGES = 4;
+
+// Pipeline depth from the shared-memory budget: with tiny token tiles the
+// stage is almost all weight tile, and a deep ring keeps enough bytes in
+// flight per SM (Little's law) for one CTA to stream at a high rate.
+__host__ __device__ constexpr int stages_for(int npad, int na) {
+    return (200 * 1024) / ((na * BM * BK + npad * BK) * 2) > 12 ? 12
+                                                                 : (200 * 1024) / ((na * BM * BK + npad * BK) * 2);
+}
 
 // ---- PTX wrappers ----------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -140,6 +147,7 @@ __host__ __device__ inline uint32_t tmem_cols(uint32_t n) {
 // ---- shared layout ----------------------------------------------------------
 template <int NPAD, int NA>   // NA = number of A tiles per stage (2 for gemm1: gate + up)
 struct Smem {
+    static constexpr int STAGES = stages_for(NPAD, NA);
     alignas(1024) __nv_bfloat16 a[STAGES][NA][BM * BK];
     alignas(1024) __nv_bfloat16 b[STAGES][NPAD * BK];
     uint64_t full[STAGES], empty[STAGES], done;
@@ -157,7 +165,9 @@ struct Gemm1Args {
 template <int NPAD>
 __global__ void __launch_bounds__(128, 1) gemm1_kernel(const __grid_constant__ Gemm1Args g) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    auto& s = *reinterpret_cast<Smem<NPAD, 2>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using S = Smem<NPAD, 2>;
+    constexpr int STAGES = S::STAGES;
+    auto& s = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int e = blockIdx.x / g.n_mtiles, mt = blockIdx.x % g.n_mtiles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const CUtensorMap* wmap = g.w1_maps + g.exec_slot[e];
@@ -238,7 +248,9 @@ struct Gemm2Args {
 template <int NPAD>
 __global__ void __launch_bounds__(128, 1) gemm2_kernel(const __grid_constant__ Gemm2Args g) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    auto& s = *reinterpret_cast<Smem<NPAD, 1>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using S = Smem<NPAD, 1>;
+    constexpr int STAGES = S::STAGES;
+    auto& s = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int e = blockIdx.x / g.n_mtiles, mt = blockIdx.x % g.n_mtiles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const CUtensorMap* wmap = g.w2_maps + g.exec_slot[e];

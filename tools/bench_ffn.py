@@ -1,5 +1,6 @@
-"""FFN kernel microbenchmark: prefill-64 layer (~28 experts x ~18 tokens) and decode (8 experts x 1 token).
-Reports per-layer time and achieved HBM GB/s (12,582,912 B weights per expert + activations)."""
+"""FFN kernel microbenchmark (enqueue-ahead, per-iteration CUDA events, L2 flushed between
+iterations): a prefill-64 layer (28 experts, ~18 tokens each), decode (8 experts x 1 token),
+all 64 experts. Algorithmic bytes = 12,582,912 B weights per executed expert."""
 import sys, json
 sys.path.insert(0, ".")
 import numpy as np, torch
@@ -9,6 +10,7 @@ out = {}
 slots = ExpertSlots(64, H, I, max_tokens=64, max_exec=64)
 slots.buf.copy_((torch.randn(slots.buf.numel(), device="cuda") * 0.02).to(torch.bfloat16))
 flush = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")
+peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if __import__("os").path.exists("MEASURED_PEAKS.json") else 6650.0
 for name, T, K, n_exp in (("prefill64", 64, 8, 28), ("decode", 1, 8, 8), ("prefill64_all64", 64, 8, 64)):
     rng = np.random.default_rng(0)
     x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
@@ -20,15 +22,19 @@ for name, T, K, n_exp in (("prefill64", 64, 8, 28), ("decode", 1, 8, 8), ("prefi
     es = torch.arange(n_exp, dtype=torch.int32, device="cuda")
     for _ in range(3):
         slots.run_layer(x, es, ti, tw, npad, residual=False)
-    ts = []
-    for _ in range(20):
+    torch.cuda.synchronize()
+    n = 30
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    for i in range(n):
         flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(); slots.run_layer(x, es, ti, tw, npad, residual=False); e1.record()
-        torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
-    ms = float(np.median(ts))
+        ev[i][0].record()
+        slots.run_layer(x, es, ti, tw, npad, residual=False)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
     byt = n_exp * 3 * H * I * 2
     flops = 2 * 3 * H * I * int(row_sel.size)
-    out[name] = {"ms": ms, "npad": npad, "weight_gbs": byt / ms / 1e6, "tflops": flops / ms / 1e9}
+    out[name] = {"ms": ms, "npad": npad, "n_exec": n_exp, "weight_gbs": byt / ms / 1e6,
+                 "frac_of_hbm_peak": byt / ms / 1e6 / peak, "tflops": flops / ms / 1e9}
     print(name, out[name], flush=True)
 json.dump(out, open("gpurun_out/bench_ffn.json", "w"), indent=1)
