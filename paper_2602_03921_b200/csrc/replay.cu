@@ -131,6 +131,8 @@ struct Pt {
     int miss;                       // ESIM_MISS_* (constant-folded in the simple specialisation)
     int64_t cap;
     int64_t dur0, dur1, dur2, dur3, eb0, eb1, eb2, eb3;   // by precision code (registers, not an array)
+    int64_t dur_w, eb_w;            // working precision
+    bool uniform;                   // all transfers at the working precision (common path)
     // shared memory
     uint64_t* key;
     int64_t *q_submit, *q_comp;
@@ -177,8 +179,16 @@ struct Pt {
     bool full;
 };
 
-DFI int64_t pdur(const Pt& p, int c) { return c == 0 ? p.dur0 : c == 1 ? p.dur1 : c == 2 ? p.dur2 : p.dur3; }
-DFI int64_t peb(const Pt& p, int c) { return c == 0 ? p.eb0 : c == 1 ? p.eb1 : c == 2 ? p.eb2 : p.eb3; }
+// per-precision sizes; on the common path (miss=fetch) every transfer is at the working
+// precision, which `uniform` (a template constant after inlining) exploits
+DFI int64_t pdur(const Pt& p, int c) {
+    if (p.uniform) return p.dur_w;
+    return c == 0 ? p.dur0 : c == 1 ? p.dur1 : c == 2 ? p.dur2 : p.dur3;
+}
+DFI int64_t peb(const Pt& p, int c) {
+    if (p.uniform) return p.eb_w;
+    return c == 0 ? p.eb0 : c == 1 ? p.eb1 : c == 2 ? p.eb2 : p.eb3;
+}
 
 DFI int qphys(const Pt& p, int i) {
     int x = p.qh + i;
@@ -206,28 +216,26 @@ DFI void ps_add(Pt& p, int which, double x) {
 
 // ---------------------------------------------------------------------------
 // record output + digest
-// digest: mix = sum_i w_i * K_i over the record's 8 words (t0 skipped for
-// predictions), h = ((h ^ mix) * P) ^ (>> 29); prediction experts chained.
+// digest: mix = sum_i w_i * K_i (mod 2^32) over the record's sixteen 32-bit
+// words (t0 skipped for predictions), h = ((h ^ mix) * P) ^ (h >> 29);
+// prediction experts chained. Zero/constant words fold at compile time.
 // ---------------------------------------------------------------------------
-#define KMIX0 0x9E3779B97F4A7C15ULL
-#define KMIX1 0xBF58476D1CE4E5B9ULL
-#define KMIX2 0x94D049BB133111EBULL
-#define KMIX3 0xD6E8FEB86659FD93ULL
-#define KMIX4 0xA0761D6478BD642FULL
-#define KMIX5 0xE7037ED1A0B428DBULL
-#define KMIX6 0x8EBC6AF09C88C6E3ULL
-#define KMIX7 0x589965CC75374CC3ULL
-
-DFI uint64_t w2(int32_t a, int32_t b) { return (uint64_t)(uint32_t)a | ((uint64_t)(uint32_t)b << 32); }
+#define KM(i) (i == 0 ? 0x9E3779B1u : i == 1 ? 0x85EBCA77u : i == 2 ? 0xC2B2AE3Du : i == 3 ? 0x27D4EB2Fu : \
+               i == 4 ? 0x165667B1u : i == 5 ? 0xD3A2646Bu : i == 6 ? 0xFD7046C5u : i == 7 ? 0xB55A4F09u : \
+               i == 8 ? 0x68E31DA5u : i == 9 ? 0x2C1B3C6Du : i == 10 ? 0x297A2D39u : i == 11 ? 0x95E4A8F1u : \
+               i == 12 ? 0x7FEB352Du : i == 13 ? 0x846CA68Bu : i == 14 ? 0x2545F491u : 0x9E6C63D1u)
 
 DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0, int64_t t1,
               int64_t t2, double x0, const int32_t* pe = nullptr, int npe = 0) {
     if (p.digest_on) {
-    uint64_t mix = w2(kind, p.pass_id) * KMIX0 + w2(layer, i0) * KMIX1 + w2(i1, i2) * KMIX2 +
-                   w2(i3, i4) * KMIX3 + (uint64_t)t1 * KMIX5 + (uint64_t)t2 * KMIX6 +
-                   (uint64_t)__double_as_longlong(x0) * KMIX7;
-    if (kind != ESIM_REC_PREDICTION) mix += (uint64_t)t0 * KMIX4;
-    uint64_t h = (p.digest ^ mix) * FNV_PRIME;
+    const uint64_t x0b = (uint64_t)__double_as_longlong(x0);
+    uint32_t mix = (uint32_t)kind * KM(0) + (uint32_t)p.pass_id * KM(1) + (uint32_t)layer * KM(2) +
+                   (uint32_t)i0 * KM(3) + (uint32_t)i1 * KM(4) + (uint32_t)i2 * KM(5) + (uint32_t)i3 * KM(6) +
+                   (uint32_t)i4 * KM(7) + (uint32_t)t1 * KM(10) + (uint32_t)((uint64_t)t1 >> 32) * KM(11) +
+                   (uint32_t)t2 * KM(12) + (uint32_t)((uint64_t)t2 >> 32) * KM(13) + (uint32_t)x0b * KM(14) +
+                   (uint32_t)(x0b >> 32) * KM(15);
+    if (kind != ESIM_REC_PREDICTION) mix += (uint32_t)t0 * KM(8) + (uint32_t)((uint64_t)t0 >> 32) * KM(9);
+    uint64_t h = (p.digest ^ (uint64_t)mix) * FNV_PRIME;
     h ^= h >> 29;
     for (int j = 0; j < npe; j++) h = (h ^ (uint64_t)(uint32_t)pe[j]) * FNV_PRIME;
     p.digest = h;
@@ -317,13 +325,11 @@ DFI void note_access(Pt& p, int ident, int slot, bool has_gate, double gate, int
 //   LFU / LHU  count:20 | touch:32 | slot:12      touches are unique
 //   FLD        (L-1-dist):8 | expert:16 | layer:16 | slot:12
 //   SB         two stages: min signal, then min ident among equal signals
-DFI uint64_t warp_min_u64(uint64_t v) {
-    #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t w = __shfl_xor_sync(FULL, v, o);
-        v = w < v ? w : v;
-    }
-    return v;
+DFI uint64_t warp_min_u64(uint64_t v) {         // two redux.sync (hi word, then lo among ties)
+    const uint32_t hi = (uint32_t)(v >> 32);
+    const uint32_t mhi = __reduce_min_sync(FULL, hi);
+    const uint32_t mlo = __reduce_min_sync(FULL, hi == mhi ? (uint32_t)v : 0xFFFFFFFFu);
+    return ((uint64_t)mhi << 32) | mlo;
 }
 
 DFI int select_victim(Pt& p, bool forced) {
@@ -927,6 +933,9 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     }
     p.eb0 = ebs[0]; p.eb1 = ebs[1]; p.eb2 = ebs[2]; p.eb3 = ebs[3];
     p.dur0 = durs[0]; p.dur1 = durs[1]; p.dur2 = durs[2]; p.dur3 = durs[3];
+    p.uniform = !GEN;
+    p.eb_w = ebs[cfg->working_prec & 3];
+    p.dur_w = durs[cfg->working_prec & 3];
     // residents + queued transfers <= capacity / (smallest expert this point can admit):
     // only fetch_low / fetch_priority ever admit below the working precision
     if (p.miss != ESIM_MISS_FETCH_LOW && p.miss != ESIM_MISS_FETCH_PRIORITY) minb = peb(p, cfg->working_prec);
