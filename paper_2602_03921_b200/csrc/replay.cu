@@ -40,6 +40,7 @@ namespace esim {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint64_t FNV_OFFSET = 0xcbf29ce484222325ULL;
 constexpr uint64_t FNV_PRIME = 0x100000001b3ULL;
+constexpr uint64_t FNV_PRIME_MIX = 0xD6E8FEB86659FD93ULL;
 constexpr int STATUS_QUEUE_OVERFLOW = -5;
 
 struct ReplayArgs {
@@ -217,8 +218,10 @@ DFI void ps_add(Pt& p, int which, double x) {
 // ---------------------------------------------------------------------------
 // record output + digest
 // digest: mix = sum_i w_i * K_i (mod 2^32) over the record's sixteen 32-bit
-// words (t0 skipped for predictions), h = ((h ^ mix) * P) ^ (h >> 29);
-// prediction experts chained. Zero/constant words fold at compile time.
+// words (t0 skipped for predictions) + sum_j (e_j+1) * G*(j+1) over a
+// prediction's experts; x = (mix ^ idx*C) * P (idx = record index);
+// digest += x ^ (x >> 31). The index makes it order-sensitive, the sum keeps
+// the loop-carried chain one add. Zero/constant words fold at compile time.
 // ---------------------------------------------------------------------------
 #define KM(i) (i == 0 ? 0x9E3779B1u : i == 1 ? 0x85EBCA77u : i == 2 ? 0xC2B2AE3Du : i == 3 ? 0x27D4EB2Fu : \
                i == 4 ? 0x165667B1u : i == 5 ? 0xD3A2646Bu : i == 6 ? 0xFD7046C5u : i == 7 ? 0xB55A4F09u : \
@@ -235,10 +238,10 @@ DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4
                    (uint32_t)t2 * KM(12) + (uint32_t)((uint64_t)t2 >> 32) * KM(13) + (uint32_t)x0b * KM(14) +
                    (uint32_t)(x0b >> 32) * KM(15);
     if (kind != ESIM_REC_PREDICTION) mix += (uint32_t)t0 * KM(8) + (uint32_t)((uint64_t)t0 >> 32) * KM(9);
-    uint64_t h = (p.digest ^ (uint64_t)mix) * FNV_PRIME;
-    h ^= h >> 29;
-    for (int j = 0; j < npe; j++) h = (h ^ (uint64_t)(uint32_t)pe[j]) * FNV_PRIME;
-    p.digest = h;
+    for (int j = 0; j < npe; j++) mix += (uint32_t)(pe[j] + 1) * (0x9E3779B1u * (uint32_t)(j + 1));
+    // order-sensitive through the record index, associative across records
+    uint64_t x = (uint64_t)(mix ^ ((uint32_t)p.n_recs * 0x85EBCA77u)) * FNV_PRIME_MIX;
+    p.digest += x ^ (x >> 31);
     }
     if (p.full) {
         const int64_t n = p.n_recs, m = p.n_pe;
