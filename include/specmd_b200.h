@@ -130,7 +130,23 @@ typedef struct {
     int32_t *pred_expert;         /* [n_events][E] */
     float   *pred_score;          /* [n_events][E] */
     int32_t *pred_clamped;        /* [n_events] */
+    /* Policy-independent summary (filled by the router launchers, or by
+     * esim_route_summary_launch after predictions are replaced): work every
+     * grid point sharing this router output would otherwise repeat. */
+    uint32_t *route_mix;          /* [n_events] RouteRec digest word (standard routing, no drop/subst) */
+    uint32_t *pred_mix;           /* [n_events] digest word of the PredictionRec targeting the event */
+    int64_t  *layer_pred;         /* [2*num_layers] per target layer: sum n_pred, prediction events */
+    struct EsimRouteSummary *summary;  /* [1] */
 } EsimRouterOut;
+
+/* Router-only totals of a trace (metrics.py:150-187 P/R accounting under
+ * standard routing; engine.py:625-643 RouteRec masses). Neumaier (f, c)
+ * pairs in event order, exactly as the replay accumulates them. */
+typedef struct EsimRouteSummary {
+    int64_t pf_tp, pf_pred, pf_dem, pf_records, pf_prec_parts, pf_empty, pf_rec_parts;
+    int64_t rows_total;
+    double  orig_f, orig_c, prec_f, prec_c, rec_f, rec_c;
+} EsimRouteSummary;                /* 112 bytes */
 
 const char *esim_last_error(void);
 /* Page-lock / release a caller-owned host buffer (trace arrays) so that
@@ -154,6 +170,12 @@ int esim_router_launch_batch(const EsimTraceDesc *d_traces, const EsimRouterOut 
                              int64_t total_events, int32_t max_experts, void *stream);
 /* Host helper: the predictor constants the router uses, computed in double
  * exactly as the reference does (prefetch.py:35, 48). out[4] as above. */
+/* Recompute the router summary (route_mix, pred_mix, layer_pred, summary)
+ * of one router output after its predictions were replaced (noised
+ * prediction streams, prefetch.py:110-160). `trace` / `out` are host structs
+ * holding device pointers; pred_mode as for esim_router_launch. */
+int esim_route_summary_launch(const EsimTraceDesc *trace, const EsimRouterOut *out, int32_t pred_mode,
+                              void *stream);
 int esim_predictor_params(int32_t top_k, int32_t experts, int32_t pred_mode, double overfetch,
                           double percentile, int32_t *out4);
 

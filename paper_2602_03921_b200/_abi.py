@@ -50,11 +50,19 @@ class EsimTraceDesc(C.Structure):
 class EsimRouterOut(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in (
         "n_dem", "dem_expert", "dem_rank", "dem_gate", "dem_summed", "dem_tokens", "sel_mass",
-        "row_sel", "row_w", "n_pred", "pred_expert", "pred_score", "pred_clamped")]
+        "row_sel", "row_w", "n_pred", "pred_expert", "pred_score", "pred_clamped",
+        "route_mix", "pred_mix", "layer_pred", "summary")]
+
+
+class EsimRouteSummary(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("pf_tp", "pf_pred", "pf_dem", "pf_records", "pf_prec_parts", "pf_empty",
+                                        "pf_rec_parts", "rows_total")] + \
+               [(n, C.c_double) for n in ("orig_f", "orig_c", "prec_f", "prec_c", "rec_f", "rec_c")]
 
 
 assert C.sizeof(EsimConfig) == 168, C.sizeof(EsimConfig)
 assert C.sizeof(EsimCounters) == 360, C.sizeof(EsimCounters)
+assert C.sizeof(EsimRouteSummary) == 112, C.sizeof(EsimRouteSummary)
 COUNTERS_DTYPE = np.dtype((np.void, C.sizeof(EsimCounters)))
 
 

@@ -52,6 +52,7 @@ def lib():
         L.esim_router_launch_batch.argtypes = [vp, vp, vp, vp, i32, i64, i32, vp]
         L.esim_predictor_params.argtypes = [i32, i32, i32, f64, f64, vp]
         L.esim_topk_launch.argtypes = [vp, i32, i32, i32, vp, vp]
+        L.esim_route_summary_launch.argtypes = [vp, vp, i32, vp]
         _lib = L
     return _lib
 
@@ -113,7 +114,8 @@ class RouterOut:
     """Router output buffers for one DeviceTrace (EsimRouterOut)."""
 
     FIELDS = ("n_dem", "dem_expert", "dem_rank", "dem_gate", "dem_summed", "dem_tokens", "sel_mass",
-              "row_sel", "row_w", "n_pred", "pred_expert", "pred_score", "pred_clamped")
+              "row_sel", "row_w", "n_pred", "pred_expert", "pred_score", "pred_clamped",
+              "route_mix", "pred_mix", "layer_pred", "summary")
 
     def __init__(self, dt: DeviceTrace):
         torch = _torch()
@@ -127,22 +129,31 @@ class RouterOut:
             "row_sel": z(rows * K, torch.int16), "row_w": z(rows * K, torch.float32),
             "n_pred": z(ne, torch.int32), "pred_expert": z(ne * E, torch.int32),
             "pred_score": z(ne * E, torch.float32), "pred_clamped": z(ne, torch.int32),
+            "route_mix": z(ne, torch.int32), "pred_mix": z(ne, torch.int32),
+            "layer_pred": z(2 * pk.num_layers, torch.int64),
+            "summary": z(C.sizeof(_abi.EsimRouteSummary), torch.uint8),
         }
         self.refresh()
 
     def refresh(self) -> None:
         self.desc = _abi.EsimRouterOut(*[self.t[f].data_ptr() for f in self.FIELDS])
 
-    def with_predictions(self, n_pred, pred_expert, pred_score, pred_clamped) -> "RouterOut":
-        """A copy sharing the demand stream but with host-supplied predictions."""
+    def with_predictions(self, dt: "DeviceTrace", pred_mode: int, n_pred, pred_expert, pred_score,
+                         pred_clamped) -> "RouterOut":
+        """A copy sharing the demand stream but with host-supplied predictions
+        (its router summary recomputed on the device)."""
         torch = _torch()
         other = object.__new__(RouterOut)
         other.t = dict(self.t)
+        for f in ("route_mix", "pred_mix", "layer_pred", "summary"):
+            other.t[f] = torch.empty_like(self.t[f])
         other.t["n_pred"] = torch.from_numpy(np.ascontiguousarray(n_pred, np.int32)).cuda()
         other.t["pred_expert"] = torch.from_numpy(np.ascontiguousarray(pred_expert, np.int32)).cuda()
         other.t["pred_score"] = torch.from_numpy(np.ascontiguousarray(pred_score, np.float32)).cuda()
         other.t["pred_clamped"] = torch.from_numpy(np.ascontiguousarray(pred_clamped, np.int32)).cuda()
         other.refresh()
+        _check(lib().esim_route_summary_launch(C.addressof(dt.desc), C.addressof(other.desc), pred_mode, _stream()),
+               "route summary")
         return other
 
 
@@ -175,7 +186,7 @@ def _noised(dt: DeviceTrace, ro: RouterOut, cfg) -> RouterOut:
     for i in range(pk.n_events):
         pe2[i, :npred[i]] = ne_[noff[i]:noff[i + 1]]
         ps2[i, :npred[i]] = ns_[noff[i]:noff[i + 1]]
-    return ro.with_predictions(npred, pe2.ravel(), ps2.ravel(), ncl)
+    return ro.with_predictions(dt, PREFETCH_CODE[cfg.prefetch], npred, pe2.ravel(), ps2.ravel(), ncl)
 
 
 # ---------------------------------------------------------------------------

@@ -294,7 +294,8 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
         total += al256(d.n_passes * 4) * 2 + al256((ne + 1) * 8) + al256(nr * E * 4);
         roff[t] = total;
         total += al256(ne * 4) * 3 + al256(ne * E * 4) * 6 + al256(ne * E * 8) + al256(ne * 8) +
-                 al256(nr * K * 2) + al256(nr * K * 4);
+                 al256(nr * K * 2) + al256(nr * K * 4) + al256(ne * 4) * 2 + al256(d.num_layers * 16) +
+                 al256(sizeof(EsimRouteSummary));
         prefix[t + 1] = prefix[t] + ne;
         max_e = std::max(max_e, (int)E);
         for (int p = 0; p < d.n_passes; p++) max_tokens = std::max(max_tokens, d.pass_tokens[p]);
@@ -344,6 +345,10 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
         o.sel_mass = (double*)take(ne * 8);
         o.row_sel = (int16_t*)take(nr * K * 2);
         o.row_w = (float*)take(nr * K * 4);
+        o.route_mix = (uint32_t*)take(ne * 4);
+        o.pred_mix = (uint32_t*)take(ne * 4);
+        o.layer_pred = (int64_t*)take(h.num_layers * 16);
+        o.summary = (EsimRouteSummary*)take(sizeof(EsimRouteSummary));
         dro[t] = o;
     }
     cudaMemcpyAsync(base + cfg_off, pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice, C.st);

@@ -268,7 +268,8 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     const int64_t ne = n_events, nr = tr.n_rows_total;
     size_t need = al(ne * 4) * 3 + al(ne * E * 4) * 6 + al(ne * E * 8) + al(ne * 8) + al(nr * K * 2) + al(nr * K * 4) +
                   al(sizeof(EsimConfig)) + al(sizeof(EsimTraceDesc)) + al(sizeof(EsimRouterOut)) +
-                  al(sizeof(EsimCounters)) + al(L * ESIM_PL_FIELDS * 8);
+                  al(sizeof(EsimCounters)) + al(L * ESIM_PL_FIELDS * 8) + al(ne * 4) * 2 + al(L * 16) +
+                  al(sizeof(EsimRouteSummary));
     if (need > g->dev_scratch_bytes) {
         if (g->dev_scratch) cudaFree(g->dev_scratch);
         CK(cudaMalloc(&g->dev_scratch, need));
@@ -283,6 +284,8 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     ro.pred_expert = (int32_t*)take(ne * E * 4); ro.pred_score = (float*)take(ne * E * 4);
     ro.dem_summed = (double*)take(ne * E * 8); ro.sel_mass = (double*)take(ne * 8);
     ro.row_sel = (int16_t*)take(nr * K * 2); ro.row_w = (float*)take(nr * K * 4);
+    ro.route_mix = (uint32_t*)take(ne * 4); ro.pred_mix = (uint32_t*)take(ne * 4);
+    ro.layer_pred = (int64_t*)take(L * 16); ro.summary = (EsimRouteSummary*)take(sizeof(EsimRouteSummary));
     EsimConfig* d_cfg = (EsimConfig*)take(sizeof(EsimConfig));
     EsimTraceDesc* d_tr = (EsimTraceDesc*)take(sizeof(EsimTraceDesc));
     EsimRouterOut* d_ro = (EsimRouterOut*)take(sizeof(EsimRouterOut));

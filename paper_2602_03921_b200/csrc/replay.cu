@@ -32,6 +32,7 @@
 #include "../../include/specmd_b200.h"
 #include "numpy_f32.cuh"
 #include "warp_route.cuh"
+#include "digest.cuh"
 
 #define DFI __device__ __forceinline__
 
@@ -223,25 +224,13 @@ DFI void ps_add(Pt& p, int which, double x) {
 // digest += x ^ (x >> 31). The index makes it order-sensitive, the sum keeps
 // the loop-carried chain one add. Zero/constant words fold at compile time.
 // ---------------------------------------------------------------------------
-#define KM(i) (i == 0 ? 0x9E3779B1u : i == 1 ? 0x85EBCA77u : i == 2 ? 0xC2B2AE3Du : i == 3 ? 0x27D4EB2Fu : \
-               i == 4 ? 0x165667B1u : i == 5 ? 0xD3A2646Bu : i == 6 ? 0xFD7046C5u : i == 7 ? 0xB55A4F09u : \
-               i == 8 ? 0x68E31DA5u : i == 9 ? 0x2C1B3C6Du : i == 10 ? 0x297A2D39u : i == 11 ? 0x95E4A8F1u : \
-               i == 12 ? 0x7FEB352Du : i == 13 ? 0x846CA68Bu : i == 14 ? 0x2545F491u : 0x9E6C63D1u)
-
-DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0, int64_t t1,
-              int64_t t2, double x0, const int32_t* pe = nullptr, int npe = 0) {
+// record with its digest word already mixed (premixed: from the router summary)
+DFI void emit_mixed(Pt& p, uint32_t mix, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0,
+                    int64_t t1, int64_t t2, double x0, const int32_t* pe = nullptr, int npe = 0) {
     if (p.digest_on) {
-    const uint64_t x0b = (uint64_t)__double_as_longlong(x0);
-    uint32_t mix = (uint32_t)kind * KM(0) + (uint32_t)p.pass_id * KM(1) + (uint32_t)layer * KM(2) +
-                   (uint32_t)i0 * KM(3) + (uint32_t)i1 * KM(4) + (uint32_t)i2 * KM(5) + (uint32_t)i3 * KM(6) +
-                   (uint32_t)i4 * KM(7) + (uint32_t)t1 * KM(10) + (uint32_t)((uint64_t)t1 >> 32) * KM(11) +
-                   (uint32_t)t2 * KM(12) + (uint32_t)((uint64_t)t2 >> 32) * KM(13) + (uint32_t)x0b * KM(14) +
-                   (uint32_t)(x0b >> 32) * KM(15);
-    if (kind != ESIM_REC_PREDICTION) mix += (uint32_t)t0 * KM(8) + (uint32_t)((uint64_t)t0 >> 32) * KM(9);
-    for (int j = 0; j < npe; j++) mix += (uint32_t)(pe[j] + 1) * (0x9E3779B1u * (uint32_t)(j + 1));
-    // order-sensitive through the record index, associative across records
-    uint64_t x = (uint64_t)(mix ^ ((uint32_t)p.n_recs * 0x85EBCA77u)) * FNV_PRIME_MIX;
-    p.digest += x ^ (x >> 31);
+        // order-sensitive through the record index, associative across records
+        uint64_t x = (uint64_t)(mix ^ ((uint32_t)p.n_recs * 0x85EBCA77u)) * FNV_PRIME_MIX;
+        p.digest += x ^ (x >> 31);
     }
     if (p.full) {
         const int64_t n = p.n_recs, m = p.n_pe;
@@ -260,6 +249,13 @@ DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4
     }
     p.n_recs++;
     p.n_pe += npe;
+}
+
+// record mixed here (digest.cuh; zero/constant words fold at compile time)
+DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0, int64_t t1,
+              int64_t t2, double x0) {
+    const uint32_t mix = p.digest_on ? rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0) : 0u;
+    emit_mixed(p, mix, kind, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0);
 }
 
 DFI void rec_prefetch(Pt& p, int ev, int target, int expert, int64_t t, float score, int reason) {
@@ -741,9 +737,10 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
     const int n = R.n_pred[tev];
     const int32_t* pe = R.pred_expert + tev * p.E;
     const float* ps = R.pred_score + tev * p.E;
-    emit(p, ESIM_REC_PREDICTION, p.layer, target, n, R.pred_clamped[tev], 0, 0, 0, 0, 0, 0.0, pe, n);
-    pl_add(p, target * ESIM_PL_FIELDS + 8, n);
-    pl_add(p, target * ESIM_PL_FIELDS + 9, 1);
+    // PredictionRec: fixed by the router output (digest word from the summary;
+    // the per-layer predicted-set sizes are added from it at the end)
+    emit_mixed(p, p.digest_on ? R.pred_mix[tev] : 0u, ESIM_REC_PREDICTION, p.layer, target, n,
+               p.full ? R.pred_clamped[tev] : 0, 0, 0, 0, 0, 0, 0.0, pe, n);
     for (int j = 0; j < n; j++) rec_prefetch(p, 0, target, pe[j], p.now, ps[j], 0);
     const int wp = p.c->working_prec;
     const int64_t nb = peb(p, wp);
@@ -912,6 +909,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     const bool ca = GEN && cfg->routing == ESIM_ROUTE_CACHE_AWARE;
     const Layout lay = make_layout(A.N, A.S, A.Q, A.Lmax, A.Emax, A.Tmax, A.Kmax, A.Tmax > 0, A.has_cnt != 0);
 
+    const long long t_begin = clock64();
     Pt p;
     p.c = cfg;
     p.L = cfg->num_layers; p.E = cfg->experts; p.K = cfg->top_k;
@@ -1041,7 +1039,10 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
                 for (int i = p.lane; i < nd; i += 32) p.lsc[i] = ca ? d_gate[d_exp[i]] : d_gate[i];
                 __syncwarp();
             }
-            if (cfg->prefetch != ESIM_PF_NONE && l >= 1) {                // prefetch P/R (metrics.py:150-187)
+            // prefetch P/R (metrics.py:150-187): router-only under standard routing
+            // (taken from the router summary at the end); per point only when
+            // cache-aware routing changes the demand sets
+            if (ca && cfg->prefetch != ESIM_PF_NONE && l >= 1) {
                 for (int i = p.lane; i < (p.E + 31) / 32; i += 32) p.demmask[i] = 0;
                 __syncwarp();
                 for (int i = p.lane; i < nd; i += 32) atomicOr(&p.demmask[d_exp[i] >> 5], 1u << (d_exp[i] & 31));
@@ -1086,6 +1087,13 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
             }
             if (p.err) break;
             int faithful = T, nmod = 0;                                   // RouteRec (engine.py:625-643)
+            if (!GEN) {
+                // standard routing, every demand served: the record is the router's
+                // (digest word and mass sums from the summary)
+                const double origm = R.sel_mass[ev];
+                emit_mixed(p, p.digest_on ? R.route_mix[ev] : 0u, ESIM_REC_ROUTE, l, T, T, 0, 0, 0, 0,
+                           __double_as_longlong(origm), __double_as_longlong(__dadd_rn(origm, 0.0)), origm);
+            } else {
             if (ca || any_aff) {
                 const int16_t* rsel = ca ? p.ca_sel : R.row_sel + tr.row_offset[ev] * p.K;
                 int bad = 0;
@@ -1122,11 +1130,9 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
             const double exm = __dadd_rn(selm, wdelta);
             emit(p, ESIM_REC_ROUTE, l, T, faithful, nmod, 0, 0, 0, __double_as_longlong(origm),
                  __double_as_longlong(exm), selm);
-            if (p.lane == 0) {
-                p.ctr->rows_total += T; p.ctr->faithful += faithful; p.ctr->modified += nmod;
+            if (p.lane == 0) { p.ctr->faithful += faithful; p.ctr->modified += nmod; }
+            ps_add(p, 1, exm);                   // rows and the original mass: router summary
             }
-            ps_add(p, 0, origm);
-            ps_add(p, 1, exm);
             if (cfg->prefetch != ESIM_PF_NONE && l + 1 < p.L) submit_prefetches(p, R, ev + 1);
             advance_to(p, p.now + cfg->compute_us);
             pblocked += blocked;
@@ -1166,22 +1172,46 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
         for (int i = 0; i < 5; i++) o->totals[10 + i] = p.pf_ev[i];
         o->ttft_us = c->ttft; o->total_us = c->total; o->decode_us = c->decode_us;
         o->sync_overhead_us = c->sync_overhead; o->passes = c->passes; o->decode_passes = c->decode_passes;
-        o->rows_total = c->rows_total; o->faithful_rows = c->faithful; o->modified_rows = c->modified;
-        o->pf_tp = c->pf_tp; o->pf_pred_total = c->pf_pred; o->pf_dem_total = c->pf_dem;
-        o->pf_records = c->pf_records; o->pf_empty = c->pf_empty; o->pf_prec_parts = c->pf_prec_parts;
-        o->pf_rec_parts = c->pf_rec_parts;
+        // router-only parts from the summary (router.cu route_totals_kernel)
+        const EsimRouteSummary& S = *R.summary;
+        o->rows_total = S.rows_total;
+        o->faithful_rows = GEN ? (int64_t)c->faithful : S.rows_total;
+        o->modified_rows = GEN ? (int64_t)c->modified : 0;
+        double fc[8] = {S.orig_f, S.orig_c, S.orig_f, S.orig_c, S.prec_f, S.prec_c, S.rec_f, S.rec_c};
+        if (GEN) { fc[2] = c->ps[2]; fc[3] = c->ps[3]; }
+        if (ca) {
+            o->pf_tp = c->pf_tp; o->pf_pred_total = c->pf_pred; o->pf_dem_total = c->pf_dem;
+            o->pf_records = c->pf_records; o->pf_empty = c->pf_empty; o->pf_prec_parts = c->pf_prec_parts;
+            o->pf_rec_parts = c->pf_rec_parts;
+            for (int i = 4; i < 8; i++) fc[i] = c->ps[i];
+        } else {
+            o->pf_tp = S.pf_tp; o->pf_pred_total = S.pf_pred; o->pf_dem_total = S.pf_dem;
+            o->pf_records = S.pf_records; o->pf_empty = S.pf_empty; o->pf_prec_parts = S.pf_prec_parts;
+            o->pf_rec_parts = S.pf_rec_parts;
+        }
         o->ls_forced = c->ls_forced; o->ls_unforced = 0; o->ls_refusals = c->ls_refusals;
         o->n_recs = p.n_recs; o->n_pred_experts = p.n_pe; o->digest = p.digest;
         double* vo = &o->original_mass;
         for (int i = 0; i < 4; i++) {
-            const double f = c->ps[2 * i], cc = c->ps[2 * i + 1];
+            const double f = fc[2 * i], cc = fc[2 * i + 1];
             vo[i] = (cc != 0.0 && isfinite(cc)) ? __dadd_rn(f, cc) : f;
         }
         o->status = p.err;
-        o->pad[0] = o->pad[1] = o->pad[2] = 0;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        o->pad[0] = t_begin;                 // scheduling diagnostics: SM clock at start / end, SM id
+        o->pad[1] = clock64();
+        o->pad[2] = smid;
     }
     int64_t* plo = A.per_layer + (int64_t)pid * A.Lmax * ESIM_PL_FIELDS;
-    for (int i = p.lane; i < A.Lmax * ESIM_PL_FIELDS; i += 32) plo[i] = i < p.L * ESIM_PL_FIELDS ? p.pl[i] : 0;
+    for (int i = p.lane; i < A.Lmax * ESIM_PL_FIELDS; i += 32) {
+        int64_t v = 0;
+        if (i < p.L * ESIM_PL_FIELDS) {
+            const int l = i / ESIM_PL_FIELDS, f = i - l * ESIM_PL_FIELDS;
+            v = f < 8 ? (int64_t)p.pl[i] : R.layer_pred[2 * l + (f - 8)];   // 8, 9: predicted-set sizes (router)
+        }
+        plo[i] = v;
+    }
 }
 
 }  // namespace esim

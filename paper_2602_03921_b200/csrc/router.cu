@@ -17,6 +17,7 @@
 
 #include "../../include/specmd_b200.h"
 #include "numpy_f32.cuh"
+#include "digest.cuh"
 
 namespace esim {
 
@@ -232,6 +233,150 @@ __device__ __forceinline__ void route_event_cta(const RouterArgs& a, int64_t ev,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Router summary: the part of every replay that depends on the router output
+// alone, computed once per trace instead of once per grid point.
+//   * per event: the RouteRec digest word under standard routing with no
+//     drop/substitution (faithful = T, modified = 0, executed = original
+//     mass), the PredictionRec digest word of the predictions targeting the
+//     event (emitted at layer l-1, engine.py:651-660);
+//   * per trace: the prefetch precision/recall accounting
+//     (metrics.py:150-187: |pred & dem| / |pred|, / |dem| for every event
+//     with layer >= 1, Neumaier-summed in event order), the RouteRec
+//     original-mass sum, rows, and per target layer the predicted-set sizes.
+// ---------------------------------------------------------------------------
+struct SumArgs {
+    const EsimTraceDesc* traces;   // batch: device arrays; nullptr: the single trace below
+    const EsimRouterOut* outs;
+    const int32_t* params;         // [n][4], params[4t] = pred_mode
+    const int64_t* prefix;         // [n+1]
+    int n;
+    EsimTraceDesc tr1;
+    EsimRouterOut out1;
+    int mode1;
+};
+
+__device__ __forceinline__ int sum_trace_of(const SumArgs& a, int64_t g) {
+    int lo = 0, hi = a.n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.prefix[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// one warp per event
+__global__ void __launch_bounds__(256) route_events_kernel(SumArgs a, int64_t total) {
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= total) return;
+    int t = 0;
+    int64_t ev = g;
+    if (a.traces) { t = sum_trace_of(a, g); ev = g - a.prefix[t]; }
+    const EsimTraceDesc& tr = a.traces ? a.traces[t] : a.tr1;
+    const EsimRouterOut& o = a.traces ? a.outs[t] : a.out1;
+    const int E = tr.experts, L = tr.num_layers;
+    const int pass = (int)(ev / L), l = (int)(ev % L);
+    const int np = o.n_pred[ev];
+    uint32_t pm = 0;
+    for (int j = lane; j < np; j += 32) pm += pe_mix_term(j, o.pred_expert[ev * E + j]);
+    #pragma unroll
+    for (int s = 16; s > 0; s >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, s);
+    if (lane == 0) {
+        const int T = (int)(tr.row_offset[ev + 1] - tr.row_offset[ev]);
+        const double origm = o.sel_mass[ev];
+        const double exm = __dadd_rn(origm, 0.0);
+        o.route_mix[ev] = rec_mix(ESIM_REC_ROUTE, pass, l, T, T, 0, 0, 0, 0, __double_as_longlong(origm),
+                                  __double_as_longlong(exm), origm);
+        o.pred_mix[ev] = l >= 1 ? rec_mix(ESIM_REC_PREDICTION, pass, l - 1, l, np, o.pred_clamped[ev], 0, 0, 0, 0, 0,
+                                          0.0) + pm
+                                : 0u;
+    }
+}
+
+__device__ __forceinline__ void nsum_add(double& f, double& c, double x) {   // PySum step (ps_add)
+    const double t = __dadd_rn(f, x);
+    if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+    else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+    f = t;
+}
+
+// one warp per trace: events in chunks of 32 (lane i evaluates event base+i),
+// folded in event order with warp-uniform Neumaier sums
+__global__ void __launch_bounds__(32) route_totals_kernel(SumArgs a) {
+    const int t = blockIdx.x, lane = threadIdx.x;
+    const EsimTraceDesc& tr = a.traces ? a.traces[t] : a.tr1;
+    const EsimRouterOut& o = a.traces ? a.outs[t] : a.out1;
+    const int mode = a.traces ? a.params[4 * t] : a.mode1;
+    const int E = tr.experts, L = tr.num_layers;
+    const int64_t ne = tr.n_events;
+    const bool pf = mode != ESIM_PF_NONE;
+    EsimRouteSummary s;
+    s.pf_tp = s.pf_pred = s.pf_dem = s.pf_records = s.pf_prec_parts = s.pf_empty = s.pf_rec_parts = 0;
+    s.rows_total = 0;
+    s.orig_f = s.orig_c = s.prec_f = s.prec_c = s.rec_f = s.rec_c = 0.0;
+    for (int64_t base = 0; base < ne; base += 32) {
+        const int64_t ev = base + lane;
+        int T = 0, inter = 0, np = 0, nd = 0, has = 0;
+        double origm = 0.0, pr = 0.0, rc = 0.0;
+        if (ev < ne) {
+            T = (int)(tr.row_offset[ev + 1] - tr.row_offset[ev]);
+            origm = o.sel_mass[ev];
+            if (pf && ev % L >= 1) {
+                has = 1;
+                np = o.n_pred[ev];
+                nd = o.n_dem[ev];
+                const int32_t* de = o.dem_expert + ev * E;
+                const int32_t* pe = o.pred_expert + ev * E;
+                for (int j = 0; j < np; j++) {
+                    const int e = pe[j];
+                    for (int i = 0; i < nd; i++) inter += de[i] == e;
+                }
+                if (np) pr = __ddiv_rn((double)inter, (double)np);
+                rc = __ddiv_rn((double)inter, (double)nd);
+            }
+        }
+        const int cnt = ne - base < 32 ? (int)(ne - base) : 32;
+        for (int k = 0; k < cnt; k++) {
+            const int Tk = __shfl_sync(0xffffffffu, T, k);
+            const double ok = __shfl_sync(0xffffffffu, origm, k);
+            const int hk = __shfl_sync(0xffffffffu, has, k);
+            s.rows_total += Tk;
+            nsum_add(s.orig_f, s.orig_c, ok);
+            if (hk) {
+                const int ik = __shfl_sync(0xffffffffu, inter, k);
+                const int npk = __shfl_sync(0xffffffffu, np, k);
+                const int ndk = __shfl_sync(0xffffffffu, nd, k);
+                const double prk = __shfl_sync(0xffffffffu, pr, k);
+                const double rck = __shfl_sync(0xffffffffu, rc, k);
+                s.pf_tp += ik; s.pf_pred += npk; s.pf_dem += ndk; s.pf_records++;
+                if (npk) { s.pf_prec_parts++; nsum_add(s.prec_f, s.prec_c, prk); }
+                else s.pf_empty++;
+                s.pf_rec_parts++;
+                nsum_add(s.rec_f, s.rec_c, rck);
+            }
+        }
+    }
+    if (lane == 0) *o.summary = s;
+    // per target layer (>= 1): predicted-set sizes and prediction events
+    const int passes = tr.n_passes;
+    for (int l = lane; l < L; l += 32) {
+        int64_t n = 0, c = 0;
+        if (pf && l >= 1)
+            for (int p = 0; p < passes; p++) { n += o.n_pred[(int64_t)p * L + l]; c++; }
+        o.layer_pred[2 * l] = n;
+        o.layer_pred[2 * l + 1] = c;
+    }
+}
+
+cudaError_t route_summary(const SumArgs& a, int n_traces, int64_t total_events, cudaStream_t st) {
+    if (total_events <= 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((total_events * 32 + 255) / 256);
+    route_events_kernel<<<blocks, 256, 0, st>>>(a, total_events);
+    route_totals_kernel<<<n_traces, 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 }  // namespace esim
 
 extern "C" int esim_router_launch_batch(const EsimTraceDesc* d_traces, const EsimRouterOut* d_outs,
@@ -241,7 +386,17 @@ extern "C" int esim_router_launch_batch(const EsimTraceDesc* d_traces, const Esi
     esim::RouterBatchArgs b{d_traces, d_outs, d_params, d_prefix, n_traces};
     const size_t smem = (size_t)(esim::kRouterWarps * max_experts + max_experts) * 4 + 16;
     esim::router_batch_kernel<<<(unsigned)total_events, esim::kRouterWarps * 32, smem, (cudaStream_t)stream>>>(b);
+    esim::SumArgs s{};
+    s.traces = d_traces; s.outs = d_outs; s.params = d_params; s.prefix = d_prefix; s.n = n_traces;
+    if (esim::route_summary(s, n_traces, total_events, (cudaStream_t)stream) != cudaSuccess) return -3;
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+extern "C" int esim_route_summary_launch(const EsimTraceDesc* tr, const EsimRouterOut* out, int32_t pred_mode,
+                                         void* stream) {
+    esim::SumArgs s{};
+    s.n = 1; s.tr1 = *tr; s.out1 = *out; s.mode1 = pred_mode;
+    return esim::route_summary(s, 1, tr->n_events, (cudaStream_t)stream) == cudaSuccess ? 0 : -3;
 }
 
 // host launcher (declared in capi.cu)
@@ -251,7 +406,9 @@ cudaError_t esim_router_launch_impl(const EsimTraceDesc& tr, const EsimRouterOut
     size_t smem = (size_t)(esim::kRouterWarps * tr.experts + tr.experts) * 4 + 16;
     if (tr.n_events == 0) return cudaSuccess;
     esim::router_kernel<<<(unsigned)tr.n_events, esim::kRouterWarps * 32, smem, st>>>(a);
-    return cudaGetLastError();
+    esim::SumArgs s{};
+    s.n = 1; s.tr1 = tr; s.out1 = out; s.mode1 = pred_mode;
+    return esim::route_summary(s, 1, tr.n_events, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -50,7 +50,7 @@ def c5_points(traces_by_model: dict) -> tuple[list, list]:
     """The 108-point C5 grid (x len(traces) per model): parallel lists of configs and traces."""
     cfgs, trs = [], []
     for m in C5_MODELS:
-        for tr in traces_by_model[m]:
+        for tr in traces_by_model.get(m, ()):
             g = grid(m)
             cfgs += g
             trs += [tr] * len(g)

@@ -33,5 +33,5 @@ def test_struct_sizes_match_the_header():
     assert ctypes.sizeof(_abi.EsimConfig) == 168
     assert ctypes.sizeof(_abi.EsimCounters) == 360
     assert ctypes.sizeof(_abi.EsimTraceDesc) == 64
-    assert ctypes.sizeof(_abi.EsimRouterOut) == 13 * 8
+    assert ctypes.sizeof(_abi.EsimRouterOut) == 17 * 8
     assert REC_DTYPE.itemsize == 64
