@@ -258,6 +258,40 @@ DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4
     emit_mixed(p, mix, kind, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0);
 }
 
+// up to 32 records emitted at once, one per active lane (lane-varying fields),
+// in `rank` order after the records already emitted; cnt = number active
+DFI void emit_lanes(Pt& p, bool act, int rank, int cnt, int kind, int layer, int i0, int i1, int i2, int i3,
+                    int i4, int64_t t0, int64_t t1, int64_t t2, double x0) {
+    if (cnt == 0) return;
+    if (p.digest_on) {
+        uint64_t v = 0;
+        if (act) {
+            const uint32_t mix = rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0);
+            const uint64_t x = (uint64_t)(mix ^ ((uint32_t)(p.n_recs + rank) * 0x85EBCA77u)) * FNV_PRIME_MIX;
+            v = x ^ (x >> 31);
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        p.digest += v;
+    }
+    if (p.full) {
+        if (p.n_recs + cnt <= p.rec_cap) {
+            if (act) {
+                EsimRec r;
+                r.kind = kind; r.pass_id = p.pass_id; r.layer = layer;
+                r.i0 = i0; r.i1 = i1; r.i2 = i2; r.i3 = i3; r.i4 = i4;
+                r.t0 = t0; r.t1 = t1; r.t2 = t2; r.x0 = x0;
+                p.recs[p.n_recs + rank] = r;
+            }
+        } else if (!p.err) {
+            p.err = -4;
+        }
+    }
+    p.n_recs += cnt;
+}
+
+DFI unsigned lanes_below(int lane) { return (1u << lane) - 1u; }
+
 DFI void rec_prefetch(Pt& p, int ev, int target, int expert, int64_t t, float score, int reason) {
     emit(p, ESIM_REC_PREFETCH, p.layer, ev, target, expert, reason, 0, t, 0, 0, (double)score);
     p.pf_ev[ev]++;                  // ev is a compile-time constant at every call site
@@ -741,23 +775,46 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
     // the per-layer predicted-set sizes are added from it at the end)
     emit_mixed(p, p.digest_on ? R.pred_mix[tev] : 0u, ESIM_REC_PREDICTION, p.layer, target, n,
                p.full ? R.pred_clamped[tev] : 0, 0, 0, 0, 0, 0, 0.0, pe, n);
-    for (int j = 0; j < n; j++) rec_prefetch(p, 0, target, pe[j], p.now, ps[j], 0);
     const int wp = p.c->working_prec;
     const int64_t nb = peb(p, wp);
+    const unsigned below = lanes_below(p.lane);
+    // "predicted" records, one per prediction in order (lane j: prediction j)
+    for (int b = 0; b < n; b += 32) {
+        const int j = b + p.lane;
+        const bool act = j < n;
+        const int e = act ? pe[j] : 0;
+        const float sc = act ? ps[j] : 0.0f;
+        emit_lanes(p, act, p.lane, n - b < 32 ? n - b : 32, ESIM_REC_PREFETCH, p.layer, 0, target, e, 0, 0, p.now,
+                   0, 0, (double)sc);
+    }
+    p.pf_ev[0] += n;
+    // sweep 1, lane-parallel: resident -> (LS: first touch of the pass stamps the
+    // key, in prediction order) "skip resident"; in flight -> "skip in flight";
+    // otherwise compacted, in order, into the fetch list
     int nt = 0;
-    for (int j = 0; j < n; j++) {                                         // sweep 1
-        const int e = pe[j];
-        const int ident = target * p.E + e;
-        const uint16_t w = p.rs[ident];
-        if (rs_res(w)) {
-            if (p.pol == ESIM_EV_LS) ls_touch(p, rs_slot(w));
-            rec_prefetch(p, 3, target, e, p.now, ps[j], 1);
-        } else if (w & RS_INF) {
-            rec_prefetch(p, 3, target, e, p.now, ps[j], 2);
-        } else {
-            if (p.lane == 0) p.tofetch[nt] = (uint8_t)j;
-            nt++;
+    for (int b = 0; b < n; b += 32) {
+        const int j = b + p.lane;
+        const bool act = j < n;
+        int e = 0;
+        float sc = 0.0f;
+        uint16_t w = 0;
+        if (act) { e = pe[j]; sc = ps[j]; w = p.rs[target * p.E + e]; }
+        const bool res = act && rs_res(w);
+        const bool inf = act && !res && (w & RS_INF);
+        const bool fetch = act && !res && !inf;
+        if (p.pol == ESIM_EV_LS) {
+            const bool touch = res && !(p.key[rs_slot(w)] & LS_CURRENT);
+            const unsigned tm = __ballot_sync(FULL, touch);
+            if (touch) p.key[rs_slot(w)] = LS_CURRENT | (p.seq + __popc(tm & below));
+            p.seq += __popc(tm);
         }
+        const unsigned hm = __ballot_sync(FULL, res || inf);
+        emit_lanes(p, res || inf, __popc(hm & below), __popc(hm), ESIM_REC_PREFETCH, p.layer, 3, target, e,
+                   res ? 1 : 2, 0, p.now, 0, 0, (double)sc);
+        p.pf_ev[3] += __popc(hm);
+        const unsigned fm = __ballot_sync(FULL, fetch);
+        if (fetch) p.tofetch[nt + __popc(fm & below)] = (uint8_t)j;
+        nt += __popc(fm);
     }
     __syncwarp();
     for (int t = 0; t < nt && !p.err; t++) {                              // sweep 2
