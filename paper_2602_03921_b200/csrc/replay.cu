@@ -137,7 +137,8 @@ struct Pt {
     bool uniform;                   // all transfers at the working precision (common path)
     // shared memory
     uint64_t* key;
-    int64_t *q_submit, *q_comp;
+    int64_t *q_submit, *q_comp;     // non-uniform instances only
+    int64_t qc0;                    // uniform instances: completion time of the head entry
     double* dsum;
     Ctr* ctr;
     double* dem_summed_s;
@@ -451,17 +452,27 @@ DFI void evict(Pt& p, int slot, int cause, bool forced) {                 // eng
 // ---------------------------------------------------------------------------
 struct QEntry { int16_t ident; uint8_t flags; float score; int64_t submit, comp; };
 
+// The queue is settled whenever it is touched (every entry has comp > now >=
+// its submit time: settle() lands comp <= now from the head after every time
+// step), so comp_i = max(comp_{i-1}, submit_i) + dur_i (engine.py:283-288)
+// never idles for i >= 1. With one transfer size (the uniform instances) that
+// is comp_i = comp_0 + i * dur: only the head's completion time is stored.
+DFI int64_t qcomp(const Pt& p, int i) {
+    if (p.uniform) return p.qc0 + (int64_t)i * p.dur_w;
+    return p.q_comp[qphys(p, i)];
+}
+
 DFI QEntry q_load(const Pt& p, int i) {
     const int x = qphys(p, i);
     QEntry e;
     e.ident = p.q_ident[x]; e.flags = p.q_flags[x]; e.score = p.q_score[x];
-    e.submit = p.q_submit[x]; e.comp = p.q_comp[x];
+    if (!p.uniform) { e.submit = p.q_submit[x]; e.comp = p.q_comp[x]; }
     return e;
 }
 DFI void q_store(Pt& p, int i, const QEntry& e) {
     const int x = qphys(p, i);
     p.q_ident[x] = e.ident; p.q_flags[x] = e.flags; p.q_score[x] = e.score;
-    p.q_submit[x] = e.submit; p.q_comp[x] = e.comp;
+    if (!p.uniform) { p.q_submit[x] = e.submit; p.q_comp[x] = e.comp; }
 }
 
 // open a hole at logical index `at` (shift [at, qn) right by one); false on overflow
@@ -497,6 +508,7 @@ DFI void q_close(Pt& p, int at) {
 // comp_i = max(comp_{i-1}, submit_i) + dur_i for i >= from >= 1 (engine.py:283-288):
 // a warp inclusive scan composing x -> max(x + a, b)
 DFI void retime(Pt& p, int from) {
+    if (p.uniform) return;                       // implied by qcomp()
     if (from < 1) from = 1;
     if (from >= p.qn) return;
     int64_t carry = p.q_comp[qphys(p, from - 1)];
@@ -539,7 +551,7 @@ DFI int q_find(const Pt& p, int ident) {
 DFI void settle(Pt& p) {                                                   // engine.py:422-442
     while (p.qn > 0) {
         const int h = p.qh;
-        const int64_t comp = p.q_comp[h];
+        const int64_t comp = qcomp(p, 0);
         if (comp > p.now) break;
         const int ident = p.q_ident[h];
         const uint8_t fl = p.q_flags[h];
@@ -552,6 +564,7 @@ DFI void settle(Pt& p) {                                                   // en
         p.fs_top--;
         p.qh = (p.qh + 1 == p.Q) ? 0 : p.qh + 1;
         p.qn--;
+        if (p.uniform) p.qc0 = comp + p.dur_w;       // the next entry's completion
         if (p.nA > 0) p.nA--;
         p.reserved_bytes -= nb;
         p.resident_bytes += nb;
@@ -596,7 +609,7 @@ DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
             continue;
         }
         if (p.qn == 0) { p.err = -2; return 0; }
-        const int64_t nd = p.q_comp[p.qh];
+        const int64_t nd = qcomp(p, 0);
         advance_to(p, nd > p.now ? nd : p.now);
     }
     if (p.err) return 0;
@@ -608,9 +621,10 @@ DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
     e.submit = p.now; e.comp = p.now + pdur(p, prec);
     if (p.lane == 0) { q_store(p, at, e); p.rs[ident] = RS_INF; }
     __syncwarp();
+    if (at == 0 && p.uniform) p.qc0 = e.comp;
     if (at > 0) p.nA++;
     retime(p, at);
-    const int64_t comp = p.q_comp[qphys(p, at)];
+    const int64_t comp = qcomp(p, at);
     const int64_t blocked = comp - p.now;
     advance_to(p, comp);
     return blocked;
@@ -683,7 +697,7 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
             retime(p, min(idx, at));
         }
         const int prec = (e.flags >> 2) & 3;
-        const int64_t comp = p.q_comp[qphys(p, at)];
+        const int64_t comp = qcomp(p, at);
         blocked = comp - p.now;
         advance_to(p, comp);
         const int slot = rs_slot(p.rs[ident]);
@@ -834,8 +848,9 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
         QEntry q;
         q.ident = (int16_t)ident; q.flags = (uint8_t)(1 | (wp << 2)); q.score = sc; q.submit = p.now;
         int64_t start = p.now;
-        if (p.qn) { const int64_t tail = p.q_comp[qphys(p, p.qn - 1)]; start = p.now > tail ? p.now : tail; }
+        if (p.qn) { const int64_t tail = qcomp(p, p.qn - 1); start = p.now > tail ? p.now : tail; }
         q.comp = start + pdur(p, wp);
+        if (p.qn == 0 && p.uniform) p.qc0 = q.comp;
         const int at = p.qn;
         __syncwarp();
         if (p.lane == 0) { q_store(p, at, q); p.rs[ident] = RS_INF; }
@@ -1045,7 +1060,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     }
     __syncwarp();
     p.now = 0; p.resident_bytes = 0; p.reserved_bytes = 0;
-    p.qh = 0; p.qn = 0; p.nA = 0; p.fs_top = p.S; p.seq = 0;
+    p.qh = 0; p.qn = 0; p.nA = 0; p.fs_top = p.S; p.seq = 0; p.qc0 = 0;
     p.digest = FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
     p.n_evict = 0; p.n_forced = 0;
     #pragma unroll

@@ -11,4 +11,4 @@ cfgs, traces = c5_points({model: trs[model]})
 keep = [i for i, c in enumerate(cfgs) if c.eviction == pol]
 ds = DeviceSweep([cfgs[i] for i in keep], [traces[i] for i in keep])
 ds.step(); torch.cuda.synchronize()
-print("points", len(keep), "groups", len(ds.groups))
+print("points", len(keep))
