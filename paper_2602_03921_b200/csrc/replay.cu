@@ -139,6 +139,7 @@ struct Pt {
     uint64_t* key;
     int64_t *q_submit, *q_comp;     // non-uniform instances only
     int64_t qc0;                    // uniform instances: completion time of the head entry
+    uint64_t einv;                  // ceil(2^32 / E): ident / E as a multiply-high
     double* dsum;
     Ctr* ctr;
     double* dem_summed_s;
@@ -193,6 +194,10 @@ DFI int64_t peb(const Pt& p, int c) {
     return c == 0 ? p.eb0 : c == 1 ? p.eb1 : c == 2 ? p.eb2 : p.eb3;
 }
 
+DFI int ediv(const Pt& p, int ident) {             // ident / E, exact for ident < 2^24
+    return (int)(((uint64_t)(uint32_t)ident * p.einv) >> 32);
+}
+
 DFI int qphys(const Pt& p, int i) {
     int x = p.qh + i;
     return x >= p.Q ? x - p.Q : x;
@@ -225,13 +230,17 @@ DFI void ps_add(Pt& p, int which, double x) {
 // digest += x ^ (x >> 31). The index makes it order-sensitive, the sum keeps
 // the loop-carried chain one add. Zero/constant words fold at compile time.
 // ---------------------------------------------------------------------------
+DFI uint64_t fold(uint32_t mix, int64_t idx) {
+    const uint64_t x = (uint64_t)(mix ^ ((uint32_t)idx * 0x85EBCA77u)) * FNV_PRIME_MIX;
+    return x ^ (x >> 31);
+}
+
 // record with its digest word already mixed (premixed: from the router summary)
 DFI void emit_mixed(Pt& p, uint32_t mix, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0,
                     int64_t t1, int64_t t2, double x0, const int32_t* pe = nullptr, int npe = 0) {
     if (p.digest_on) {
         // order-sensitive through the record index, associative across records
-        uint64_t x = (uint64_t)(mix ^ ((uint32_t)p.n_recs * 0x85EBCA77u)) * FNV_PRIME_MIX;
-        p.digest += x ^ (x >> 31);
+        p.digest += fold(mix, p.n_recs);
     }
     if (p.full) {
         const int64_t n = p.n_recs, m = p.n_pe;
@@ -267,9 +276,7 @@ DFI void emit_lanes(Pt& p, bool act, int rank, int cnt, int kind, int layer, int
     if (p.digest_on) {
         uint64_t v = 0;
         if (act) {
-            const uint32_t mix = rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0);
-            const uint64_t x = (uint64_t)(mix ^ ((uint32_t)(p.n_recs + rank) * 0x85EBCA77u)) * FNV_PRIME_MIX;
-            v = x ^ (x >> 31);
+            v = fold(rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0), p.n_recs + rank);
         }
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -409,7 +416,7 @@ DFI int select_victim(Pt& p, bool forced) {
         if (p.pol == ESIM_EV_LFU || p.pol == ESIM_EV_LHU) {
             k = ((uint64_t)(uint32_t)p.cnt[id] << 44) | ((uint64_t)(uint32_t)p.key[s] << 12) | (uint64_t)s;
         } else {                                                          // FLD
-            const int l = id / p.E, e = id - l * p.E;
+            const int l = ediv(p, id), e = id - l * p.E;
             int d = l - c;
             d = d < 0 ? d + p.L : d;
             k = ((uint64_t)(p.L - 1 - d) << 44) | ((uint64_t)e << 28) | ((uint64_t)l << 12) | (uint64_t)s;
@@ -442,7 +449,8 @@ DFI void evict(Pt& p, int slot, int cause, bool forced) {                 // eng
     }
     __syncwarp();
     p.fs_top++;
-    emit(p, ESIM_REC_EVICT, p.layer, ident / p.E, ident % p.E, prec, cause, forced ? 1 : 0, 0, 0, 0, 0.0);
+    const int il = ediv(p, ident);
+    emit(p, ESIM_REC_EVICT, p.layer, il, ident - il * p.E, prec, cause, forced ? 1 : 0, 0, 0, 0, 0.0);
     p.n_evict++;
     p.n_forced += forced ? 1 : 0;
 }
@@ -577,7 +585,10 @@ DFI void settle(Pt& p) {                                                   // en
         __syncwarp();
         if (p.resident_bytes + p.reserved_bytes > p.cap && !p.err) p.err = -2;
         note_admit(p, slot);
-        if (fl & 1) rec_prefetch(p, 2, ident / p.E, ident % p.E, comp, score, 0);
+        if (fl & 1) {
+            const int il = ediv(p, ident);
+            rec_prefetch(p, 2, il, ident - il * p.E, comp, score, 0);
+        }
     }
 }
 
@@ -605,7 +616,8 @@ DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
             p.reserved_bytes -= peb(p, (e.flags >> 2) & 3);
             if (p.lane == 0) p.rs[e.ident] = 0;
             __syncwarp();
-            rec_prefetch(p, 4, e.ident / p.E, e.ident % p.E, p.now, e.score, 4);
+            const int il = ediv(p, e.ident);
+            rec_prefetch(p, 4, il, e.ident - il * p.E, p.now, e.score, 4);
             continue;
         }
         if (p.qn == 0) { p.err = -2; return 0; }
@@ -1061,6 +1073,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     __syncwarp();
     p.now = 0; p.resident_bytes = 0; p.reserved_bytes = 0;
     p.qh = 0; p.qn = 0; p.nA = 0; p.fs_top = p.S; p.seq = 0; p.qc0 = 0;
+    p.einv = ((1ull << 32) + (uint64_t)p.E - 1) / (uint64_t)p.E;
     p.digest = FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
     p.n_evict = 0; p.n_forced = 0;
     #pragma unroll
