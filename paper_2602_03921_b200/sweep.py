@@ -101,39 +101,54 @@ def _c_config(cfg, trace_id: int):
     return c
 
 
+class HostGrid:
+    """A sweep grid packed once for the C-ABI end-to-end call (esim_run_host):
+    the EsimConfig array and the trace descriptors (pointers into the
+    callers' host trace arrays) are built here; every `run()` is one
+    esim_run_host call -- trace H2D, router, replays, results D2H.
+
+    Configs that share a trace object must share the predictor; prediction
+    noise is not supported on this path (use engine.Simulation)."""
+
+    def __init__(self, cfgs, traces, pl_stride: int | None = None):
+        if any(c.prefetch != "none" and c.prefetch_noise > 0 for c in cfgs):
+            raise ConfigError("run_grid_host: prediction noise needs the Simulation path")
+        ids, descs, self._keep = {}, [], []
+        ccfg = []
+        for cfg, tr in zip(cfgs, traces):
+            check_geometry(cfg, tr)
+            key = (id(tr), cfg.prefetch, cfg.overfetch, cfg.percentile)
+            if key not in ids:
+                ids[key] = len(descs)
+                d, k = _abi.trace_desc_host(tr.packed())
+                descs.append(d)
+                self._keep.append(k)
+            ccfg.append(_c_config(cfg, ids[key]))
+        self.n = n = len(ccfg)
+        self.L = pl_stride or max(c.model.num_layers for c in cfgs)
+        self.carr = (_abi.EsimConfig * n).from_buffer_copy(b"".join(ccfg))
+        self.darr = (_abi.EsimTraceDesc * len(descs))(*descs)
+        self.n_traces = len(descs)
+        self.counters = (_abi.EsimCounters * n)()
+        self.per_layer = np.zeros((n, self.L, _abi.ESIM_PL_FIELDS), np.int64)
+
+    def run(self):
+        """Returns (counters list, per_layer array [n][pl_stride][ESIM_PL_FIELDS])."""
+        rc = _lib().esim_run_host(C.addressof(self.carr), self.n, C.addressof(self.darr), self.n_traces,
+                                  C.addressof(self.counters), self.per_layer.ctypes.data, self.L, None, 0, None, 0)
+        if rc != 0:
+            msg = _lib().esim_last_error().decode()
+            if rc == -1:
+                raise ConfigError(msg)
+            raise RuntimeError(f"esim_run_host failed ({rc}): {msg}")
+        return list(self.counters), self.per_layer.copy()
+
+
 def run_grid_host(cfgs, traces, pl_stride: int | None = None):
     """One end-to-end C-ABI call (esim_run_host): host buffers in and out.
 
-    Returns (counters list, per_layer array [n][pl_stride][ESIM_PL_FIELDS]).
-    Configs that share a trace object must share the predictor; prediction
-    noise is not supported on this path (use engine.Simulation)."""
-    if any(c.prefetch != "none" and c.prefetch_noise > 0 for c in cfgs):
-        raise ConfigError("run_grid_host: prediction noise needs the Simulation path")
-    ids, descs, keep = {}, [], []
-    ccfg = []
-    for cfg, tr in zip(cfgs, traces):
-        check_geometry(cfg, tr)
-        key = (id(tr), cfg.prefetch, cfg.overfetch, cfg.percentile)
-        if key not in ids:
-            ids[key] = len(descs)
-            d, k = _abi.trace_desc_host(tr.packed())
-            descs.append(d)
-            keep.append(k)
-        ccfg.append(_c_config(cfg, ids[key]))
-    n = len(ccfg)
-    L = pl_stride or max(c.model.num_layers for c in cfgs)
-    carr = (_abi.EsimConfig * n).from_buffer_copy(b"".join(ccfg))
-    darr = (_abi.EsimTraceDesc * len(descs))(*descs)
-    counters = (_abi.EsimCounters * n)()
-    per_layer = np.zeros((n, L, _abi.ESIM_PL_FIELDS), np.int64)
-    rc = _lib().esim_run_host(C.addressof(carr), n, C.addressof(darr), len(descs), C.addressof(counters),
-                              per_layer.ctypes.data, L, None, 0, None, 0)
-    if rc != 0:
-        msg = _lib().esim_last_error().decode()
-        if rc == -1:
-            raise ConfigError(msg)
-        raise RuntimeError(f"esim_run_host failed ({rc}): {msg}")
-    return list(counters), per_layer
+    Returns (counters list, per_layer array [n][pl_stride][ESIM_PL_FIELDS])."""
+    return HostGrid(cfgs, traces, pl_stride).run()
 
 
 def reports(cfgs, counters, per_layer) -> list:

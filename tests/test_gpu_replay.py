@@ -155,3 +155,26 @@ def test_standalone_router_kats_match_reference():
                          ("score0", {"percentile": 0.0})):
             p, cl = predict_event(x, c["k"], "score" if mode == "score0" else mode, **kw)
             assert [[int(a), float(b).hex()] for a, b in p] + [bool(cl)] == c["predict"][mode], mode
+
+
+@pytest.mark.parametrize("experts,top_k", [(5, 2), (33, 3), (60, 4), (64, 8), (96, 6), (200, 16)])
+def test_router_paths_by_width_match_oracle(oracle_lib, experts, top_k):
+    """Every router path (single-row warp path for E <= 32 / <= 64, multi-row
+    CTA path, generic E > 64 path) under every predictor mode == the oracle."""
+    from paper_2602_03921_b200 import HardwareSpec, ModelSpec, SimConfig
+    from paper_2602_03921_b200 import _device
+    from paper_2602_03921_b200.trace import generate_synthetic
+    spec = ModelSpec(f"w{experts}", num_layers=4, experts_per_layer=experts, top_k=top_k,
+                     expert_bytes_fp16=1_000_000)
+    tr = generate_synthetic(spec, seed=experts, prefill_tokens=70, decode_tokens=6)
+    cfgs = []
+    for pf, kw in (("topk", {"overfetch": 1.5}), ("score", {"percentile": 80.0}), ("score", {"percentile": 35.0}),
+                   ("oracle", {}), ("none", {})):
+        cfgs.append(SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=3 * experts * 250_000),
+                              working_precision="int4", eviction="ls", prefetch=pf, **kw))
+    b = _device.ReplayBatch(cfgs, [tr] * len(cfgs), full_log=True)
+    b.launch()
+    for cfg, r in zip(cfgs, b.results()):
+        o = oracle_lib.run(cfg, tr, full_log=True)
+        assert [canon_reference_record(x) for x in r.log] == [canon_reference_record(x) for x in o.log], cfg.prefetch
+        assert json.dumps(r.report) == json.dumps(o.report)
