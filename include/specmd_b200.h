@@ -281,8 +281,10 @@ int esim_ls_run(void *handle, const EsimTraceDesc *trace, const int32_t *h_pass_
                 int64_t *per_layer_out, EsimLSResult *res);
 
 /* FFN building blocks (ffn_gemm.cu): 2-D bf16 TMA descriptor (128B swizzle,
- * box [box_rows][64]); token gather; the grouped tcgen05 SwiGLU experts;
- * residual x += y. */
+ * box [box_rows][64]); token gather; the grouped tcgen05 SwiGLU experts
+ * (one persistent launch: w1 maps with 64-row boxes, w2 maps with 128-row
+ * boxes); residual x += y. esim_ffn_set_trace: optional device buffer of
+ * per-unit globaltimer stamps [units][4] for the following launches (NULL off). */
 int esim_tmap_bf16(void *out_map, const void *base, int64_t rows, int64_t cols, int32_t box_rows);
 int esim_ffn_gather(const void *d_x, const int32_t *d_tok_index, void *d_xg, int32_t n_exec, int32_t npad,
                     int32_t hidden, void *stream);
@@ -290,7 +292,14 @@ int esim_ffn_experts(const void *d_w1_maps, const void *d_w2_maps, const void *d
                      const int32_t *d_exec_slot, const int32_t *d_tok_index, const float *d_tok_weight,
                      void *d_act, float *d_y, int32_t n_exec, int32_t npad, int32_t inter, int32_t hidden,
                      void *stream);
+/* The same with the largest token count of any executed expert: <= 4 (decode)
+ * selects the fused per-slice kernel (no gemm1 -> gemm2 handoff across CTAs). */
+int esim_ffn_experts_ex(const void *d_w1_maps, const void *d_w2_maps, const void *d_x_map, const void *d_act_map,
+                        const int32_t *d_exec_slot, const int32_t *d_tok_index, const float *d_tok_weight,
+                        void *d_act, float *d_y, int32_t n_exec, int32_t npad, int32_t inter, int32_t hidden,
+                        int32_t max_tok, void *stream);
 int esim_ffn_residual(void *d_x, float *d_y, int64_t n, void *stream);
+int esim_ffn_set_trace(void *d_trace);
 
 #ifdef __cplusplus
 }

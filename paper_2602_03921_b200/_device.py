@@ -48,6 +48,8 @@ def lib():
         L.esim_ffn_gather.argtypes = [vp, vp, vp, i32, i32, i32, vp]
         L.esim_ffn_residual.argtypes = [vp, vp, i64, vp]
         L.esim_ffn_experts.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
+        L.esim_ffn_experts_ex.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
+        L.esim_ffn_set_trace.argtypes = [vp]
         L.esim_host_unregister.argtypes = [vp]
         L.esim_router_launch_batch.argtypes = [vp, vp, vp, vp, i32, i64, i32, vp]
         L.esim_predictor_params.argtypes = [i32, i32, i32, f64, f64, vp]

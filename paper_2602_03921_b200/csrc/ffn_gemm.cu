@@ -25,6 +25,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 
 #include "../../include/specmd_b200.h"
 
@@ -33,14 +36,6 @@ namespace ffn {
 
 constexpr int BM = 128;          // weight rows per tile (UMMA M)
 constexpr int BK = 64;           // 64 bf16 = 128 B = one swizzle-128B atom row
-
-// Pipeline depth from the shared-memory budget: with tiny token tiles the
-// stage is almost all weight tile, and a deep ring keeps enough bytes in
-// flight per SM (Little's law) for one CTA to stream at a high rate.
-__host__ __device__ constexpr int stages_for(int npad, int na) {
-    return (200 * 1024) / ((na * BM * BK + npad * BK) * 2) > 12 ? 12
-                                                                 : (200 * 1024) / ((na * BM * BK + npad * BK) * 2);
-}
 
 // ---- PTX wrappers ----------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -144,170 +139,479 @@ __host__ __device__ inline uint32_t tmem_cols(uint32_t n) {
     return c;
 }
 
-// ---- shared layout ----------------------------------------------------------
-template <int NPAD, int NA>   // NA = number of A tiles per stage (2 for gemm1: gate + up)
-struct Smem {
-    static constexpr int STAGES = stages_for(NPAD, NA);
-    alignas(1024) __nv_bfloat16 a[STAGES][NA][BM * BK];
+// ---- device sync helpers (gemm1 tiles -> gemm2 units across CTAs) ----------
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---- one persistent kernel for the whole layer's experts -------------------
+// Work units, in this order (every CTA walks units blockIdx.x, +gridDim.x, ...):
+//   gemm1 unit (e, mt): 64 gate rows + 64 up rows of expert e stacked into one
+//     M = 128 tile (TMEM lanes 0-63 gate, 64-127 up), K = H; epilogue
+//     act = silu(g) * u (bf16) for intermediate rows [64 mt, 64 mt + 64);
+//   gemm2 unit (e, ht, kc): down rows [128 ht, +128), K chunk kc of I/n_kc;
+//     epilogue y[t] += w[t,e] * partial (fp32 atomics, so split-K is free).
+// A gemm2 unit needs only the gemm1 tiles of its K chunk: a per-(e, kc) counter
+// (release/acquire at gpu scope) gates its act loads, while its weight tiles
+// are already streaming into the ring. All gemm1 units precede all gemm2
+// units and every CTA walks its units in increasing order, so a waiting unit
+// always depends on units that are running or done (grid <= one CTA per SM,
+// all resident): no deadlock. TMEM holds two accumulators, so the epilogue
+// of one unit overlaps the MMAs of the next.
+// Warps: 0 TMA producer, 1 MMA issuer, 2-5 epilogue (TMEM lane quarter w % 4).
+constexpr int kFfnThreads = 192;
+
+__host__ __device__ constexpr int ffn_xchg_bytes(int npad) { return 64 * npad * 4 + npad * 128; }  // + act tile
+__host__ __device__ constexpr int ffn_stage_bytes(int npad) { return (BM * BK + npad * BK) * 2; }
+__host__ __device__ constexpr int ffn_stages(int npad) {
+    return (220 * 1024 - ffn_xchg_bytes(npad)) / ffn_stage_bytes(npad) > 12
+               ? 12
+               : (220 * 1024 - ffn_xchg_bytes(npad)) / ffn_stage_bytes(npad);
+}
+
+template <int NPAD>
+struct FfnSmem {
+    static constexpr int STAGES = ffn_stages(NPAD);
+    alignas(1024) __nv_bfloat16 a[STAGES][BM * BK];
     alignas(1024) __nv_bfloat16 b[STAGES][NPAD * BK];
-    uint64_t full[STAGES], empty[STAGES], done;
+    alignas(1024) __nv_bfloat16 act_tile[NPAD * 64];   // act box [NPAD tokens][64 rows], 128B-swizzled (TMA store)
+    float xchg[64][NPAD];                 // up-row accumulators -> the gate-row threads
+    uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
     uint32_t tmem;
 };
 
-struct Gemm1Args {
-    const CUtensorMap* w1_maps;      // [n_slots]: [2I rows, H cols] gate rows then up rows
-    const CUtensorMap* x_map;        // gathered tokens [n_exec*NPAD rows, H cols]
+struct FfnArgs {
+    const CUtensorMap* w1_maps;      // [n_slots]: tile-major [2I/64][H/64][64][64] as 2-D [2IH/64][64], box 64 rows
+    const CUtensorMap* w2_maps;      // [n_slots]: tile-major [I/64][H/128][128][64] as 2-D [IH/64][64], box 128 rows
+    const CUtensorMap* x_map;        // gathered tokens [n_exec*NPAD rows, H cols], box NPAD rows
+    const CUtensorMap* act_map;      // [n_exec*NPAD rows, I cols], box NPAD rows
     const int32_t* exec_slot;        // [n_exec] cache slot of each executed expert
-    __nv_bfloat16* act;              // [n_exec][NPAD][I]
-    int I, H, n_mtiles;              // n_mtiles = I / BM
-};
-
-template <int NPAD>
-__global__ void __launch_bounds__(128, 1) gemm1_kernel(const __grid_constant__ Gemm1Args g) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    using S = Smem<NPAD, 2>;
-    constexpr int STAGES = S::STAGES;
-    auto& s = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int e = blockIdx.x / g.n_mtiles, mt = blockIdx.x % g.n_mtiles;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const CUtensorMap* wmap = g.w1_maps + g.exec_slot[e];
-    const int nk = g.H / BK;
-    constexpr uint32_t NCOL = 2 * NPAD;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < STAGES; i++) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
-        mbar_init(&s.done, 1);
-        fence_barrier_init();
-        prefetch_tmap(wmap);
-        prefetch_tmap(g.x_map);
-    }
-    if (warp == 0) tmem_alloc(&s.tmem, tmem_cols(NCOL));
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = s.tmem;
-    if (warp == 0 && lane == 0) {                      // TMA producer
-        for (int k = 0; k < nk; k++) {
-            const int st = k % STAGES;
-            if (k >= STAGES) mbar_wait(&s.empty[st], ((k / STAGES) - 1) & 1);
-            mbar_expect_tx(&s.full[st], (2 * BM * BK + NPAD * BK) * 2);
-            tma_load_2d(s.a[st][0], wmap, &s.full[st], k * BK, mt * BM);               // gate rows
-            tma_load_2d(s.a[st][1], wmap, &s.full[st], k * BK, g.I + mt * BM);         // up rows
-            tma_load_2d(s.b[st], g.x_map, &s.full[st], k * BK, e * NPAD);              // tokens
-        }
-    } else if (warp == 1 && lane == 0) {               // MMA issuer
-        constexpr uint32_t idesc = idesc_bf16(BM, NPAD);
-        for (int k = 0; k < nk; k++) {
-            const int st = k % STAGES;
-            mbar_wait(&s.full[st], (k / STAGES) & 1);
-            tc_fence_after();
-            const uint64_t ag = umma_desc(s.a[st][0]), au = umma_desc(s.a[st][1]), b = umma_desc(s.b[st]);
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; kk++) {      // +32 B per K=16 step inside the swizzle atom
-                const uint32_t acc = (k | kk) ? 1u : 0u;
-                umma_bf16(tmem, ag + 2 * kk, b + 2 * kk, idesc, acc);
-                umma_bf16(tmem + NPAD, au + 2 * kk, b + 2 * kk, idesc, acc);
-            }
-            umma_commit(&s.empty[st]);
-        }
-        umma_commit(&s.done);
-    }
-    __syncwarp();
-    // epilogue: all 4 warps; thread owns intermediate row r = mt*BM + 32*warp + lane
-    mbar_wait(&s.done, 0);
-    __syncwarp();
-    tc_fence_after();
-    const int r = mt * BM + warp * 32 + lane;
-    __nv_bfloat16* out = g.act + (size_t)e * NPAD * g.I;
-#pragma unroll
-    for (int c0 = 0; c0 < NPAD; c0 += 16) {
-        float gv[16], uv[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, gv);
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + NPAD + c0, uv);
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const float gg = gv[j];
-            const float a = gg / (1.0f + __expf(-gg)) * uv[j];
-            out[(size_t)(c0 + j) * g.I + r] = __float2bfloat16(a);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, tmem_cols(NCOL));
-}
-
-struct Gemm2Args {
-    const CUtensorMap* w2_maps;      // [n_slots]: [H rows, I cols]
-    const CUtensorMap* act_map;      // [n_exec*NPAD rows, I cols]
-    const int32_t* exec_slot;        // [n_exec]
     const int32_t* tok_index;        // [n_exec][NPAD] token row or -1
     const float* tok_weight;         // [n_exec][NPAD]
+    __nv_bfloat16* act;              // [n_exec][NPAD][I]
     float* y;                        // [T][H] fp32 accumulator
-    int I, H, n_mtiles;              // n_mtiles = H / BM
+    uint32_t* sync;                  // [n_exec * n_kc] tile counters, [n_exec * n_kc] done counter (self-resetting)
+    int I, H, n_exec, n_kc;
+    unsigned long long* trace;       // optional [n_units][8] globaltimer ns: [0] first stage ready, [2] accumulator ready, [3] epilogue end
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct Unit { int kind, e, tile, kc; };
+
+__device__ __forceinline__ Unit ffn_unit(const FfnArgs& g, int u) {
+    const int m1 = g.I / 64, u1 = g.n_exec * m1;
+    Unit x;
+    if (u < u1) { x.kind = 0; x.e = u / m1; x.tile = u - x.e * m1; x.kc = 0; return x; }
+    const int v = u - u1, per = (g.H / BM) * g.n_kc;
+    x.kind = 1; x.e = v / per;
+    const int r = v - x.e * per;
+    x.tile = r / g.n_kc; x.kc = r - x.tile * g.n_kc;
+    return x;
+}
+
 template <int NPAD>
-__global__ void __launch_bounds__(128, 1) gemm2_kernel(const __grid_constant__ Gemm2Args g) {
+__global__ void __launch_bounds__(kFfnThreads, 1) ffn_fused_kernel(const __grid_constant__ FfnArgs g) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    using S = Smem<NPAD, 1>;
+    using S = FfnSmem<NPAD>;
     constexpr int STAGES = S::STAGES;
     auto& s = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int e = blockIdx.x / g.n_mtiles, mt = blockIdx.x % g.n_mtiles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const CUtensorMap* wmap = g.w2_maps + g.exec_slot[e];
-    const int nk = g.I / BK;
+    const int n_units = g.n_exec * (g.I / 64) + g.n_exec * (g.H / BM) * g.n_kc;
+    const int kc_len = g.I / g.n_kc;                      // gemm2 K chunk (multiple of 64)
+    const int KT = g.H / 64, HT = g.H / BM;               // tile-major weights: k tiles per w1 row tile, w2 row tiles
+    const int tiles_per_kc = kc_len / 64;                 // gemm1 tiles feeding one chunk
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; i++) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
-        mbar_init(&s.done, 1);
+        for (int i = 0; i < 2; i++) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], 4); }
         fence_barrier_init();
-        prefetch_tmap(wmap);
+        prefetch_tmap(g.x_map);
         prefetch_tmap(g.act_map);
     }
-    if (warp == 0) tmem_alloc(&s.tmem, tmem_cols(NPAD));
+    if (warp == 0) tmem_alloc(&s.tmem, tmem_cols(2 * NPAD));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s.tmem;
-    if (warp == 0 && lane == 0) {
-        for (int k = 0; k < nk; k++) {
-            const int st = k % STAGES;
-            if (k >= STAGES) mbar_wait(&s.empty[st], ((k / STAGES) - 1) & 1);
-            mbar_expect_tx(&s.full[st], (BM * BK + NPAD * BK) * 2);
-            tma_load_2d(s.a[st][0], wmap, &s.full[st], k * BK, mt * BM);
-            tma_load_2d(s.b[st], g.act_map, &s.full[st], k * BK, e * NPAD);
+
+    if (warp == 0) {
+        if (lane == 0) {                                  // ---- TMA producer
+            int k_all = 0;                                // ring position over every unit
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const Unit x = ffn_unit(g, u);
+                const int slot = g.exec_slot[x.e];
+                if (x.kind == 0) {
+                    const CUtensorMap* wm = g.w1_maps + slot;
+                    const int nk = g.H / BK;
+                    for (int k = 0; k < nk; k++, k_all++) {
+                        const int st = k_all % STAGES;
+                        if (k_all >= STAGES) mbar_wait(&s.empty[st], ((k_all / STAGES) - 1) & 1);
+                        mbar_expect_tx(&s.full[st], ffn_stage_bytes(NPAD));
+                        tma_load_2d(s.a[st], wm, &s.full[st], 0, (x.tile * KT + k) * 64);                    // gate
+                        tma_load_2d(s.a[st] + 64 * BK, wm, &s.full[st], 0, ((g.I / 64 + x.tile) * KT + k) * 64);  // up
+                        tma_load_2d(s.b[st], g.x_map, &s.full[st], k * BK, x.e * NPAD);
+                    }
+                } else {
+                    const CUtensorMap* wm = g.w2_maps + slot;
+                    const int nk = kc_len / BK, k0 = x.kc * kc_len;
+                    const int pre = nk < STAGES ? nk : STAGES;
+                    // weights first: they do not depend on gemm1
+                    for (int k = 0; k < pre; k++) {
+                        const int st = (k_all + k) % STAGES;
+                        if (k_all + k >= STAGES) mbar_wait(&s.empty[st], (((k_all + k) / STAGES) - 1) & 1);
+                        mbar_expect_tx(&s.full[st], ffn_stage_bytes(NPAD));
+                        tma_load_2d(s.a[st], wm, &s.full[st], 0, (((k0 + k * BK) / 64) * HT + x.tile) * BM);
+                    }
+                    const uint32_t* cnt = g.sync + x.e * g.n_kc + x.kc;
+                    while (ld_acquire(cnt) < (uint32_t)tiles_per_kc) __nanosleep(64);
+                    fence_proxy_async_global();
+                    for (int k = 0; k < pre; k++) {
+                        const int st = (k_all + k) % STAGES;
+                        tma_load_2d(s.b[st], g.act_map, &s.full[st], k0 + k * BK, x.e * NPAD);
+                    }
+                    for (int k = pre; k < nk; k++) {
+                        const int st = (k_all + k) % STAGES;
+                        if (k_all + k >= STAGES) mbar_wait(&s.empty[st], (((k_all + k) / STAGES) - 1) & 1);
+                        mbar_expect_tx(&s.full[st], ffn_stage_bytes(NPAD));
+                        tma_load_2d(s.a[st], wm, &s.full[st], 0, (((k0 + k * BK) / 64) * HT + x.tile) * BM);
+                        tma_load_2d(s.b[st], g.act_map, &s.full[st], k0 + k * BK, x.e * NPAD);
+                    }
+                    k_all += nk;
+                }
+            }
         }
-    } else if (warp == 1 && lane == 0) {
-        constexpr uint32_t idesc = idesc_bf16(BM, NPAD);
-        for (int k = 0; k < nk; k++) {
-            const int st = k % STAGES;
-            mbar_wait(&s.full[st], (k / STAGES) & 1);
+    } else if (warp == 1) {
+        if (lane == 0) {                                  // ---- MMA issuer
+            constexpr uint32_t idesc = idesc_bf16(BM, NPAD);
+            int k_all = 0, j = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
+                const Unit x = ffn_unit(g, u);
+                const int buf = j & 1, use = j >> 1;
+                if (use >= 1) mbar_wait(&s.tempty[buf], (use - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(buf * NPAD);
+                const int nk = x.kind == 0 ? g.H / BK : kc_len / BK;
+                for (int k = 0; k < nk; k++, k_all++) {
+                    const int st = k_all % STAGES;
+                    mbar_wait(&s.full[st], (k_all / STAGES) & 1);
+                    if (g.trace && k == 0) g.trace[8 * u] = gtimer();
+                    tc_fence_after();
+                    const uint64_t a = umma_desc(s.a[st]), b = umma_desc(s.b[st]);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; kk++) umma_bf16(d, a + 2 * kk, b + 2 * kk, idesc, (k | kk) ? 1u : 0u);
+                    umma_commit(&s.empty[st]);
+                }
+                umma_commit(&s.tfull[buf]);
+            }
+        }
+    } else {                                              // ---- epilogue, warps 2..5
+        const int q = warp & 3;                           // TMEM lane quarter this warp may access
+        const int row = q * 32 + lane;                    // accumulator row (TMEM lane)
+        int j = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
+            const Unit x = ffn_unit(g, u);
+            const int buf = j & 1, use = j >> 1;
+            // token table of the unit, loaded before the accumulator wait: under
+            // full HBM streaming a global load costs microseconds, hidden here
+            constexpr int NR = (NPAD + 31) / 32;
+            int tiv[NR];
+            float twv[NR];
+            int ncol = 0;
+#pragma unroll
+            for (int r = 0; r < NR; r++) {
+                const int c = r * 32 + lane;
+                tiv[r] = c < NPAD ? g.tok_index[x.e * NPAD + c] : -1;
+                twv[r] = (x.kind == 1 && c < NPAD) ? g.tok_weight[x.e * NPAD + c] : 0.0f;
+                ncol = tiv[r] >= 0 ? c + 1 : ncol;
+            }
+            ncol = __reduce_max_sync(0xffffffffu, ncol);   // token columns in use (padding is never read back)
+            mbar_wait(&s.tfull[buf], use & 1);
+            __syncwarp();
             tc_fence_after();
-            const uint64_t a = umma_desc(s.a[st][0]), b = umma_desc(s.b[st]);
+            if (g.trace && threadIdx.x == 64) g.trace[8 * u + 2] = gtimer();
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * NPAD);
+            if (x.kind == 0) {
+                if (row >= 64) {                          // up rows -> exchange
+                    for (int c0 = 0; c0 < ncol; c0 += 16) {
+                        float v[16];
+                        tmem_ld16(taddr + c0, v);
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; kk++) umma_bf16(tmem, a + 2 * kk, b + 2 * kk, idesc, (k | kk) ? 1u : 0u);
-            umma_commit(&s.empty[st]);
-        }
-        umma_commit(&s.done);
-    }
-    __syncwarp();
-    mbar_wait(&s.done, 0);
-    __syncwarp();
-    tc_fence_after();
-    const int h = mt * BM + warp * 32 + lane;
-    const int32_t* ti = g.tok_index + e * NPAD;
-    const float* tw = g.tok_weight + e * NPAD;
+                        for (int jj = 0; jj < 16; jj++) s.xchg[row - 64][c0 + jj] = v[jj];
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s.tempty[buf]);
+                }
+                epi_bar();
+                if (row < 64) {                           // act = silu(gate) * up -> the swizzled box
+                    unsigned char* tile = reinterpret_cast<unsigned char*>(s.act_tile);
+                    const int cb = row * 2;
+                    for (int c0 = 0; c0 < ncol; c0 += 16) {
+                        float gv[16];
+                        tmem_ld16(taddr + c0, gv);
 #pragma unroll
-    for (int c0 = 0; c0 < NPAD; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+                        for (int jj = 0; jj < 16; jj++) {
+                            const int n = c0 + jj;
+                            const float gg = gv[jj];
+                            const float a = gg / (1.0f + __expf(-gg)) * s.xchg[row][n];
+                            *reinterpret_cast<__nv_bfloat16*>(tile + n * 128 + ((((cb >> 4) ^ (n & 7)) << 4) | (cb & 15))) =
+                                __float2bfloat16(a);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s.tempty[buf]);
+                }
+                epi_bar();                                // tile written; xchg free again
+                if (threadIdx.x == 64) {
+                    // one TMA store of the act box, complete before the release; the
+                    // consuming producer acquires, then fences the async proxy
+                    tma_store_2d(g.act_map, s.act_tile, x.tile * 64, x.e * NPAD);
+                    fence_proxy_async_global();
+                    red_release_add(g.sync + x.e * g.n_kc + (x.tile * 64) / kc_len, 1u);
+                    if (g.trace) g.trace[8 * u + 3] = gtimer();
+                }
+            } else {
+                const int h = x.tile * BM + row;
+                for (int c0 = 0; c0 < ncol; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(taddr + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const int t = ti[c0 + j];
-            if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], tw[c0 + j] * v[j]);
+                    for (int jj = 0; jj < 16; jj++) {
+                        const int c = c0 + jj;
+                        const int t = __shfl_sync(0xffffffffu, tiv[c >> 5], c & 31);
+                        const float w = __shfl_sync(0xffffffffu, twv[c >> 5], c & 31);
+                        if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], w * v[jj]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.tempty[buf]);
+                if (g.trace && threadIdx.x == 64) g.trace[8 * u + 3] = gtimer();
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, tmem_cols(NPAD));
+    if (warp == 0) tmem_dealloc(tmem, tmem_cols(2 * NPAD));
+    // self-resetting counters: the last CTA out zeroes them for the next launch
+    if (threadIdx.x == 0) {
+        const int nc = g.n_exec * g.n_kc;
+        __threadfence();
+        if (atomicAdd(g.sync + nc, 1u) == gridDim.x - 1) {
+            for (int i = 0; i <= nc; i++) g.sync[i] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+// ---- decode path: one unit = one expert's 64-row intermediate slice, fused ----
+// With ~1 token per expert the two-phase kernel's critical path is the act
+// handoff between CTAs (a globally visible write under full HBM streaming
+// costs microseconds). Here a unit computes its slice end to end:
+//   gemm1: [64 gate; 64 up] x tokens, K = H             (512 KB of weights)
+//   act = silu(g) * u -> a swizzled smem tile, used directly as the B operand of
+//   gemm2 partial: Wd[:, 64 mt : 64 mt + 64] x act, K = 64, all H/128 row tiles
+//                                                       (256 KB of weights)
+//   y[t] += w * partial (fp32 atomics; I/64 partial sums per output element)
+// so units never wait on each other. The producer streams the down-projection
+// tiles right behind the gate/up tiles (they do not depend on act).
+// TMEM: columns [0, 16) gemm1 accumulator, [256, 256 + 16 * H/128) gemm2.
+struct DecSmem {
+    static constexpr int STAGES = 12;
+    alignas(1024) __nv_bfloat16 a[STAGES][BM * BK];
+    alignas(1024) __nv_bfloat16 b[STAGES][16 * BK];
+    alignas(1024) __nv_bfloat16 act_tile[16 * 64];
+    float xchg[64][17];
+    uint64_t full[STAGES], empty[STAGES], t1full, t1empty, actrdy, t2full, t2empty;
+    uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(kFfnThreads, 1) ffn_decode_kernel(const __grid_constant__ FfnArgs g) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    using S = DecSmem;
+    constexpr int STAGES = S::STAGES;
+    constexpr int NPAD = 16;
+    auto& s = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m1 = g.I / 64, n_units = g.n_exec * m1, n_ht = g.H / BM;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; i++) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
+        mbar_init(&s.t1full, 1); mbar_init(&s.t1empty, 4); mbar_init(&s.actrdy, 64);
+        mbar_init(&s.t2full, 1); mbar_init(&s.t2empty, 4);
+        fence_barrier_init();
+        prefetch_tmap(g.x_map);
+    }
+    if (warp == 0) tmem_alloc(&s.tmem, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s.tmem;
+    constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = NPAD * BK * 2;
+
+    if (warp == 0) {
+        if (lane == 0) {                                  // ---- TMA producer
+            int k_all = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const int e = u / m1, mt = u - e * m1;
+                const int slot = g.exec_slot[e];
+                const CUtensorMap* w1 = g.w1_maps + slot;
+                const CUtensorMap* w2 = g.w2_maps + slot;
+                const int KT = g.H / 64;
+                for (int k = 0; k < g.H / BK; k++, k_all++) {
+                    const int st = k_all % STAGES;
+                    if (k_all >= STAGES) mbar_wait(&s.empty[st], ((k_all / STAGES) - 1) & 1);
+                    mbar_expect_tx(&s.full[st], A_BYTES + B_BYTES);
+                    tma_load_2d(s.a[st], w1, &s.full[st], 0, (mt * KT + k) * 64);
+                    tma_load_2d(s.a[st] + 64 * BK, w1, &s.full[st], 0, ((g.I / 64 + mt) * KT + k) * 64);
+                    tma_load_2d(s.b[st], g.x_map, &s.full[st], k * BK, e * NPAD);
+                }
+                for (int ht = 0; ht < n_ht; ht++, k_all++) {
+                    const int st = k_all % STAGES;
+                    if (k_all >= STAGES) mbar_wait(&s.empty[st], ((k_all / STAGES) - 1) & 1);
+                    mbar_expect_tx(&s.full[st], A_BYTES);
+                    tma_load_2d(s.a[st], w2, &s.full[st], 0, (mt * n_ht + ht) * BM);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                                  // ---- MMA issuer
+            constexpr uint32_t idesc = idesc_bf16(BM, NPAD);
+            const uint64_t bact = umma_desc(s.act_tile);
+            int k_all = 0, j = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
+                if (j >= 1) mbar_wait(&s.t1empty, (j - 1) & 1);     // gemm1 accumulator drained
+                tc_fence_after();
+                for (int k = 0; k < g.H / BK; k++, k_all++) {
+                    const int st = k_all % STAGES;
+                    mbar_wait(&s.full[st], (k_all / STAGES) & 1);
+                    tc_fence_after();
+                    const uint64_t a = umma_desc(s.a[st]), b = umma_desc(s.b[st]);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; kk++) umma_bf16(tmem, a + 2 * kk, b + 2 * kk, idesc, (k | kk) ? 1u : 0u);
+                    umma_commit(&s.empty[st]);
+                }
+                umma_commit(&s.t1full);
+                mbar_wait(&s.actrdy, j & 1);                       // act tile of this unit in smem
+                if (j >= 1) mbar_wait(&s.t2empty, (j - 1) & 1);    // gemm2 accumulators drained
+                tc_fence_after();
+                for (int ht = 0; ht < n_ht; ht++, k_all++) {
+                    const int st = k_all % STAGES;
+                    mbar_wait(&s.full[st], (k_all / STAGES) & 1);
+                    tc_fence_after();
+                    const uint64_t a = umma_desc(s.a[st]);
+                    const uint32_t d = tmem + 256u + (uint32_t)(ht * NPAD);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; kk++) umma_bf16(d, a + 2 * kk, bact + 2 * kk, idesc, kk ? 1u : 0u);
+                    umma_commit(&s.empty[st]);
+                }
+                umma_commit(&s.t2full);
+            }
+        }
+    } else {                                              // ---- epilogue, warps 2..5
+        const int q = warp & 3, row = q * 32 + lane;
+        const uint32_t lanebase = (uint32_t)(q * 32) << 16;
+        int j = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
+            const int e = u / m1;
+            const int ti = lane < NPAD ? g.tok_index[e * NPAD + lane] : -1;
+            const float tw = lane < NPAD ? g.tok_weight[e * NPAD + lane] : 0.0f;
+            const int ncol = __reduce_max_sync(0xffffffffu, ti >= 0 ? lane + 1 : 0);
+            // gemm1 epilogue: act = silu(gate) * up -> act_tile (swizzled, the gemm2 B operand)
+            mbar_wait(&s.t1full, j & 1);
+            __syncwarp();
+            tc_fence_after();
+            float v[16];
+            tmem_ld16(tmem + lanebase, v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.t1empty);
+            if (row >= 64) {
+#pragma unroll
+                for (int c = 0; c < 16; c++) s.xchg[row - 64][c] = v[c];
+            }
+            epi_bar();
+            if (row < 64) {
+                unsigned char* tile = reinterpret_cast<unsigned char*>(s.act_tile);
+                const int cb = row * 2;
+#pragma unroll
+                for (int n = 0; n < 16; n++) {
+                    const float gg = v[n];
+                    const float a = n < ncol ? gg / (1.0f + __expf(-gg)) * s.xchg[row][n] : 0.0f;
+                    *reinterpret_cast<__nv_bfloat16*>(tile + n * 128 + ((((cb >> 4) ^ (n & 7)) << 4) | (cb & 15))) =
+                        __float2bfloat16(a);
+                }
+                fence_proxy_async_smem();                 // generic smem writes -> the tensor core's view
+                mbar_arrive(&s.actrdy);
+            }
+            // gemm2 epilogue: partial sums of the H rows, scaled, into y
+            mbar_wait(&s.t2full, j & 1);
+            __syncwarp();
+            tc_fence_after();
+            for (int ht = 0; ht < n_ht; ht++) {
+                float p[16];
+                tmem_ld16(tmem + lanebase + 256u + (uint32_t)(ht * NPAD), p);
+                const int h = ht * BM + row;
+                for (int c = 0; c < ncol; c++) {
+                    const int t = __shfl_sync(0xffffffffu, ti, c);
+                    const float w = __shfl_sync(0xffffffffu, tw, c);
+                    if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], w * p[c]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.t2empty);
+            epi_bar();                                    // xchg / act_tile reuse by the next unit
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int NPAD>
+size_t ffn_smem() { return sizeof(FfnSmem<NPAD>) + 1024; }
+
+static int ffn_grid_cap() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return sms;
+}
+
+template <int NPAD>
+cudaError_t launch_ffn(const FfnArgs& a, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(ffn_fused_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)ffn_smem<NPAD>());
+    if (e != cudaSuccess) return e;
+    const int n_units = a.n_exec * (a.I / 64) + a.n_exec * (a.H / BM) * a.n_kc;
+    const int grid = n_units < ffn_grid_cap() ? n_units : ffn_grid_cap();
+    ffn_fused_kernel<NPAD><<<grid, kFfnThreads, ffn_smem<NPAD>(), st>>>(a);
+    return cudaGetLastError();
 }
 
 // gather token rows per executed expert: xg[e][n][:] = x[tok_index[e][n]][:] (zero for padding)
@@ -327,23 +631,6 @@ __global__ void residual_kernel(__nv_bfloat16* __restrict__ x, float* __restrict
         x[i] = __float2bfloat16(__bfloat162float(x[i]) + y[i]);
         y[i] = 0.0f;
     }
-}
-
-template <int NPAD>
-size_t smem1() { return sizeof(Smem<NPAD, 2>) + 1024; }
-template <int NPAD>
-size_t smem2() { return sizeof(Smem<NPAD, 1>) + 1024; }
-
-template <int NPAD>
-cudaError_t launch_ffn(const Gemm1Args& a1, const Gemm2Args& a2, int n_exec, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(gemm1_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem1<NPAD>());
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(gemm2_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2<NPAD>());
-    if (e != cudaSuccess) return e;
-    gemm1_kernel<NPAD><<<n_exec * a1.n_mtiles, 128, smem1<NPAD>(), st>>>(a1);
-    gemm2_kernel<NPAD><<<n_exec * a2.n_mtiles, 128, smem2<NPAD>(), st>>>(a2);
-    return cudaGetLastError();
 }
 
 }  // namespace ffn
@@ -398,25 +685,76 @@ extern "C" int esim_ffn_residual(void* d_x, float* d_y, int64_t n, void* stream)
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
-// act = silu(Xg Wg^T) * (Xg Wu^T); y[t] += w * (act Wd^T)   for n_exec experts
+// per-stream counters for the gemm1 -> gemm2 handoff (zeroed once, then
+// self-resetting at the end of every launch; launches on one stream are ordered)
+static cudaError_t ffn_sync_buf(cudaStream_t st, size_t n, uint32_t** out) {
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, std::pair<uint32_t*, size_t>> bufs;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& b = bufs[st];
+    if (b.second < n) {
+        if (b.first) { cudaStreamSynchronize(st); cudaFree(b.first); b = {nullptr, 0}; }
+        cudaError_t e = cudaMalloc((void**)&b.first, n * 4);
+        if (e != cudaSuccess) return e;
+        if ((e = cudaMemset(b.first, 0, n * 4)) != cudaSuccess) return e;
+        b.second = n;
+    }
+    *out = b.first;
+    return cudaSuccess;
+}
+
+static unsigned long long* g_ffn_trace = nullptr;   // diagnostics: per-unit timestamps of the next launches
+extern "C" int esim_ffn_set_trace(void* d_trace) {
+    g_ffn_trace = (unsigned long long*)d_trace;
+    return 0;
+}
+
+// act = silu(Xg Wg^T) * (Xg Wu^T); y[t] += w * (act Wd^T)   for n_exec experts,
+// one persistent launch (gemm1 tiles, then split-K gemm2 units)
+extern "C" int esim_ffn_experts_ex(const void* d_w1_maps, const void* d_w2_maps, const void* d_x_map,
+                                   const void* d_act_map, const int32_t* d_exec_slot, const int32_t* d_tok_index,
+                                   const float* d_tok_weight, void* d_act, float* d_y, int32_t n_exec, int32_t npad,
+                                   int32_t I, int32_t H, int32_t max_tok, void* stream) {
+    if (n_exec <= 0) return 0;
+    if (I % BM || H % BM || H % BK || I % BK) return -1;
+    cudaStream_t st = (cudaStream_t)stream;
+    // decode-like layers (<= 4 tokens per expert): the fused per-slice kernel
+    // (I/64 partial sums per output element; bounded atomics), TMEM 256 + 16 * H/128 columns
+    if (npad == 16 && max_tok >= 1 && max_tok <= 4 && H / BM <= 16) {
+        FfnArgs a{(const CUtensorMap*)d_w1_maps, (const CUtensorMap*)d_w2_maps, (const CUtensorMap*)d_x_map,
+                  (const CUtensorMap*)d_act_map, d_exec_slot, d_tok_index, d_tok_weight, (__nv_bfloat16*)d_act, d_y,
+                  nullptr, I, H, n_exec, 1, nullptr};
+        const size_t smem = sizeof(DecSmem) + 1024;
+        if (cudaFuncSetAttribute(ffn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return -3;
+        const int units = n_exec * (I / 64);
+        ffn_decode_kernel<<<units < ffn_grid_cap() ? units : ffn_grid_cap(), kFfnThreads, smem, st>>>(a);
+        return cudaGetLastError() == cudaSuccess ? 0 : -3;
+    }
+    // gemm2 split-K: enough units to cover the SMs, chunks of >= 256 columns
+    int n_kc = 1;
+    while (n_kc < 4 && (I / (2 * n_kc)) % 256 == 0 && n_exec * (H / BM) * n_kc < 2 * ffn_grid_cap()) n_kc *= 2;
+    uint32_t* sync = nullptr;
+    if (ffn_sync_buf(st, (size_t)n_exec * n_kc + 1, &sync) != cudaSuccess) return -3;
+    FfnArgs a{(const CUtensorMap*)d_w1_maps, (const CUtensorMap*)d_w2_maps, (const CUtensorMap*)d_x_map,
+              (const CUtensorMap*)d_act_map, d_exec_slot, d_tok_index, d_tok_weight, (__nv_bfloat16*)d_act, d_y,
+              sync, I, H, n_exec, n_kc, g_ffn_trace};
+    cudaError_t e;
+    switch (npad) {
+    case 16: e = launch_ffn<16>(a, st); break;
+    case 32: e = launch_ffn<32>(a, st); break;
+    case 64: e = launch_ffn<64>(a, st); break;
+    case 128: e = launch_ffn<128>(a, st); break;
+    default: return -1;
+    }
+    return e == cudaSuccess ? 0 : -3;
+}
+
 extern "C" int esim_ffn_experts(const void* d_w1_maps, const void* d_w2_maps, const void* d_x_map,
                                 const void* d_act_map, const int32_t* d_exec_slot, const int32_t* d_tok_index,
                                 const float* d_tok_weight, void* d_act, float* d_y, int32_t n_exec, int32_t npad,
                                 int32_t I, int32_t H, void* stream) {
-    if (n_exec <= 0) return 0;
-    if (I % BM || H % BM || H % BK || I % BK) return -1;
-    Gemm1Args a1{(const CUtensorMap*)d_w1_maps, (const CUtensorMap*)d_x_map, d_exec_slot, (__nv_bfloat16*)d_act, I, H,
-                 I / BM};
-    Gemm2Args a2{(const CUtensorMap*)d_w2_maps, (const CUtensorMap*)d_act_map, d_exec_slot, d_tok_index, d_tok_weight,
-                 d_y, I, H, H / BM};
-    cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e;
-    switch (npad) {
-    case 16: e = launch_ffn<16>(a1, a2, n_exec, st); break;
-    case 32: e = launch_ffn<32>(a1, a2, n_exec, st); break;
-    case 64: e = launch_ffn<64>(a1, a2, n_exec, st); break;
-    case 128: e = launch_ffn<128>(a1, a2, n_exec, st); break;
-    default: return -1;
-    }
-    return e == cudaSuccess ? 0 : -3;
+    return esim_ffn_experts_ex(d_w1_maps, d_w2_maps, d_x_map, d_act_map, d_exec_slot, d_tok_index, d_tok_weight,
+                               d_act, d_y, n_exec, npad, I, H, npad, stream);
 }

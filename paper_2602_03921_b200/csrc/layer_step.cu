@@ -40,6 +40,10 @@ extern "C" int esim_tmap_bf16(void* out_map, const void* base, int64_t rows, int
 extern "C" int esim_ffn_gather(const void* d_x, const int32_t* d_tok_index, void* d_xg, int32_t n_exec, int32_t npad,
                                int32_t H, void* stream);
 extern "C" int esim_ffn_residual(void* d_x, float* d_y, int64_t n, void* stream);
+extern "C" int esim_ffn_experts_ex(const void* d_w1_maps, const void* d_w2_maps, const void* d_x_map,
+                                   const void* d_act_map, const int32_t* d_exec_slot, const int32_t* d_tok_index,
+                                   const float* d_tok_weight, void* d_act, float* d_y, int32_t n_exec, int32_t npad,
+                                   int32_t I, int32_t H, int32_t max_tok, void* stream);
 extern "C" int esim_ffn_experts(const void* d_w1_maps, const void* d_w2_maps, const void* d_x_map,
                                 const void* d_act_map, const int32_t* d_exec_slot, const int32_t* d_tok_index,
                                 const float* d_tok_weight, void* d_act, float* d_y, int32_t n_exec, int32_t npad,
@@ -141,8 +145,9 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
     std::vector<unsigned char> m1(128 * (size_t)p->n_slots), m2(128 * (size_t)p->n_slots);
     for (int s = 0; s < p->n_slots; s++) {
         const char* base = g->slots + g->expert_bytes * s;
-        if (esim_tmap_bf16(&m1[128 * s], base, 2 * I, H, 128) ||
-            esim_tmap_bf16(&m2[128 * s], base + (size_t)2 * I * H * 2, H, I, 128))
+        // tile-major expert layout (ffn.py): every TMA box is one contiguous run
+        if (esim_tmap_bf16(&m1[128 * s], base, (int64_t)2 * I * H / 64, 64, 64) ||
+            esim_tmap_bf16(&m2[128 * s], base + (size_t)2 * I * H * 2, (int64_t)I * H / 64, 64, 128))
             return ls_fail(-3, "tensor map encode failed");
     }
     CK(cudaMalloc(&g->w1_maps, m1.size()));
@@ -356,8 +361,9 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
                                                                    g->tok_index, g->tok_weight);
             if (esim_ffn_gather(g->x, g->tok_index, g->xg, n_exec, npad, H, g->comp_st) ||
-                esim_ffn_experts(g->w1_maps, g->w2_maps, g->x_maps[npad_index(npad)], g->act_maps[npad_index(npad)],
-                                 tslot, g->tok_index, g->tok_weight, g->act, g->y, n_exec, npad, I, H, g->comp_st))
+                esim_ffn_experts_ex(g->w1_maps, g->w2_maps, g->x_maps[npad_index(npad)],
+                                    g->act_maps[npad_index(npad)], tslot, g->tok_index, g->tok_weight, g->act, g->y,
+                                    n_exec, npad, I, H, std::max(1, maxtok), g->comp_st))
                 return ls_fail(-3, "ffn launch failed");
             for (int i = 0; i < n_exec; i++) CK(cudaEventRecord(g->freed[pend_slot[i]], g->comp_st));
             n_exec_total += n_exec;

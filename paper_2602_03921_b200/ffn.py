@@ -1,11 +1,16 @@
 """Physical expert FFN: HBM cache slots + the tcgen05 grouped SwiGLU GEMMs.
 
-Each cache slot holds one expert in the layout the kernels stream with TMA:
-    w1 = [gate; up]  [2*I, H] bf16 row-major (K = H contiguous)
-    w2 = down        [H, I]   bf16 row-major (K = I contiguous)
-i.e. 3*H*I*2 bytes (12,582,912 B for OLMoE-1B-7B: H=2048, I=1024), the same
-bytes a host->HBM fetch moves. One TMA descriptor per slot per matrix is
-built once; kernels pick the descriptor of the slot an expert lives in.
+Each cache slot holds one expert in the TILE-MAJOR layout the kernels stream
+with TMA (every TMA box is one contiguous run of HBM, so weight streaming is
+sequential 8-16 KB bursts instead of 128-byte pieces of 4 KB-strided rows):
+    w1 = [gate; up] (logical [2*I, H], K = H) as tiles [2I/64][H/64][64][64]
+    w2 = down       (logical [H, I],   K = I) as tiles [I/64][H/128][128][64]
+3*H*I*2 bytes (12,582,912 B for OLMoE-1B-7B: H=2048, I=1024), the same bytes
+a host->HBM fetch moves (the pinned store uses the same layout; the tiling is
+a property of the expert store, like a checkpoint converted once at load).
+`expert_matrices` maps a slot back to the logical matrices. One TMA
+descriptor per slot per matrix is built once; kernels pick the descriptor of
+the slot an expert lives in.
 Layer semantics (no renormalisation, original-softmax weights, matching
 the reference's dual-logit routing, routing.py:93-99):
     x <- x + sum_e w[t,e] * down_e(silu(gate_e x) * up_e x)
@@ -46,8 +51,8 @@ class ExpertSlots:
         self.expert_bytes = 2 * self.expert_elems
         self.buf = torch.empty(n_slots * self.expert_elems, dtype=torch.bfloat16, device="cuda")
         base = self.buf.data_ptr()
-        w1 = b"".join(tmap(base + s * self.expert_bytes, 2 * inter, hidden, 128) for s in range(n_slots))
-        w2 = b"".join(tmap(base + s * self.expert_bytes + 2 * 2 * inter * hidden, hidden, inter, 128)
+        w1 = b"".join(tmap(base + s * self.expert_bytes, 2 * inter * hidden // 64, 64, 64) for s in range(n_slots))
+        w2 = b"".join(tmap(base + s * self.expert_bytes + 2 * 2 * inter * hidden, inter * hidden // 64, 64, 128)
                       for s in range(n_slots))
         self.w1_maps = torch.frombuffer(bytearray(w1), dtype=torch.uint8).cuda()
         self.w2_maps = torch.frombuffer(bytearray(w2), dtype=torch.uint8).cuda()
@@ -69,9 +74,12 @@ class ExpertSlots:
     def slot_view(self, slot: int):
         return self.buf[slot * self.expert_elems:(slot + 1) * self.expert_elems]
 
-    def run_layer(self, x, exec_slot, tok_index, tok_weight, npad: int, stream=None, residual: bool = True) -> None:
+    def run_layer(self, x, exec_slot, tok_index, tok_weight, npad: int, stream=None, residual: bool = True,
+                  max_tok: int | None = None) -> None:
         """x[T,H] bf16 (device, updated in place: x += MoE(x)). exec_slot int32
-        [n_exec] (device), tok_index int32 [n_exec*npad], tok_weight f32 (device)."""
+        [n_exec] (device), tok_index int32 [n_exec*npad], tok_weight f32 (device).
+        max_tok: the largest token count of an executed expert (<= 4 selects the
+        fused decode kernel); None = npad (the two-phase kernel)."""
         n_exec = int(exec_slot.numel())
         if n_exec > self.max_exec:
             raise ValueError("more executed experts than staged")
@@ -79,13 +87,22 @@ class ExpertSlots:
         L = lib()
         _check(L.esim_ffn_gather(x.data_ptr(), tok_index.data_ptr(), self.xg.data_ptr(), n_exec, npad, self.H, st),
                "gather")
-        _check(L.esim_ffn_experts(self.w1_maps.data_ptr(), self.w2_maps.data_ptr(), self.x_maps[npad].data_ptr(),
-                                  self.act_maps[npad].data_ptr(), exec_slot.data_ptr(), tok_index.data_ptr(),
-                                  tok_weight.data_ptr(), self.act.data_ptr(), self.y.data_ptr(), n_exec, npad,
-                                  self.I, self.H, st), "ffn experts")
+        _check(L.esim_ffn_experts_ex(self.w1_maps.data_ptr(), self.w2_maps.data_ptr(), self.x_maps[npad].data_ptr(),
+                                     self.act_maps[npad].data_ptr(), exec_slot.data_ptr(), tok_index.data_ptr(),
+                                     tok_weight.data_ptr(), self.act.data_ptr(), self.y.data_ptr(), n_exec, npad,
+                                     self.I, self.H, npad if max_tok is None else max_tok, st), "ffn experts")
         if residual:
             T = x.numel() // self.H
             _check(L.esim_ffn_residual(x.data_ptr(), self.y.data_ptr(), T * self.H, st), "residual")
+
+
+def expert_matrices(flat, hidden: int, inter: int):
+    """Logical (w1 [2I, H], wd [H, I]) views-turned-copies of one expert stored
+    tile-major (see the module docstring); `flat` is the expert's 3*H*I elements."""
+    H, I = hidden, inter
+    w1 = flat[:2 * I * H].reshape(2 * I // 64, H // 64, 64, 64).permute(0, 2, 1, 3).reshape(2 * I, H)
+    wd = flat[2 * I * H:].reshape(I // 64, H // 128, 128, 64).permute(1, 2, 0, 3).reshape(H, I)
+    return w1, wd
 
 
 def routing_tables(row_sel: np.ndarray, row_w: np.ndarray, executed: dict, npad: int):

@@ -11,9 +11,9 @@ H, I = 2048, 1024
 TOL = 1e-2
 
 
-def _case(T, K, n_exp, npad_expected, seed):
+def _case(T, K, n_exp, npad_expected, seed, fused):
     import torch
-    from paper_2602_03921_b200.ffn import ExpertSlots, npad_for, routing_tables
+    from paper_2602_03921_b200.ffn import ExpertSlots, expert_matrices, npad_for, routing_tables
     g = torch.Generator(device="cuda").manual_seed(seed)
     n_slots = n_exp + 2
     slots = ExpertSlots(n_slots, H, I, max_tokens=T, max_exec=n_exp)
@@ -30,15 +30,16 @@ def _case(T, K, n_exp, npad_expected, seed):
     ti, tw = routing_tables(row_sel, row_w, executed, npad)
     exec_slot = torch.tensor(slot_of, dtype=torch.int32, device="cuda")
     slots.y.zero_()
-    slots.run_layer(x, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad, residual=False)
+    mt = int(counts.max()) if fused else None          # <= 4 tokens: fused decode kernel
+    slots.run_layer(x, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad, residual=False,
+                    max_tok=mt)
     torch.cuda.synchronize()
     y = slots.y[:T * H].view(T, H).float()
     ref = torch.zeros(T, H, device="cuda")
     xf = x.float()
     for e in range(n_exp):
         w = slots.slot_view(int(slot_of[e])).float()
-        w1 = w[:2 * I * H].view(2 * I, H)
-        wd = w[2 * I * H:].view(H, I)
+        w1, wd = expert_matrices(w, H, I)
         gate, up = xf @ w1[:I].T, xf @ w1[I:].T
         act = (torch.nn.functional.silu(gate) * up).to(torch.bfloat16).float()
         out = act @ wd.T
@@ -50,7 +51,7 @@ def _case(T, K, n_exp, npad_expected, seed):
     assert err <= TOL, f"max rel err {err:.3e}"
     # residual path: x += y
     x2 = x.clone()
-    slots.run_layer(x2, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad)
+    slots.run_layer(x2, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad, max_tok=mt)
     torch.cuda.synchronize()
     assert torch.isfinite(x2.float()).all()
     return err
@@ -59,4 +60,11 @@ def _case(T, K, n_exp, npad_expected, seed):
 @pytest.mark.parametrize("T,K,n_exp,npad,seed", [(1, 8, 8, 16, 0), (16, 2, 8, 16, 1), (64, 8, 28, 32, 2),
                                                   (64, 8, 8, 64, 3), (128, 4, 8, 128, 4)])
 def test_ffn_matches_torch_fp32(T, K, n_exp, npad, seed):
-    _case(T, K, n_exp, npad, seed)
+    """The two-phase kernel (gemm1 tiles -> split-K gemm2 units)."""
+    _case(T, K, n_exp, npad, seed, fused=False)
+
+
+@pytest.mark.parametrize("T,K,n_exp,seed", [(1, 8, 8, 10), (1, 8, 64, 11), (3, 4, 8, 12), (4, 2, 3, 13)])
+def test_ffn_decode_kernel_matches_torch_fp32(T, K, n_exp, seed):
+    """The fused per-slice decode kernel (<= 4 tokens per expert)."""
+    _case(T, K, n_exp, 16, seed, fused=True)

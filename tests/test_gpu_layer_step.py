@@ -17,6 +17,7 @@ H, I = 2048, 1024
 
 def _reference(engine, trace, x0, xdec):
     import torch
+    from paper_2602_03921_b200.ffn import expert_matrices
     from paper_2602_03921_b200.routing import softmax_rows
     spec = trace.spec
     outs = []
@@ -28,7 +29,7 @@ def _reference(engine, trace, x0, xdec):
             y = torch.zeros_like(x)
             for e in np.unique(idx):
                 w = engine.expert_weights(ev.layer, int(e)).cuda().float()
-                w1, wd = w[:2 * I * H].view(2 * I, H), w[2 * I * H:].view(H, I)
+                w1, wd = expert_matrices(w, H, I)
                 act = (torch.nn.functional.silu(x.to(torch.bfloat16).float() @ w1[:I].T) *
                        (x.to(torch.bfloat16).float() @ w1[I:].T)).to(torch.bfloat16).float()
                 out = act @ wd.T

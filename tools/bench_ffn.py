@@ -16,19 +16,20 @@ for name, T, K, n_exp in (("prefill64", 64, 8, 28), ("decode", 1, 8, 8), ("prefi
     x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
     row_sel = np.stack([rng.choice(n_exp, size=K, replace=False) for _ in range(T)]).astype(np.int32)
     row_w = rng.uniform(0.01, 0.3, size=(T, K)).astype(np.float32)
-    npad = npad_for(int(np.bincount(row_sel.ravel()).max()))
+    mt = int(np.bincount(row_sel.ravel()).max())
+    npad = npad_for(mt)
     ti, tw = routing_tables(row_sel, row_w, {e: (e, e) for e in range(n_exp)}, npad)
     ti, tw = torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda()
     es = torch.arange(n_exp, dtype=torch.int32, device="cuda")
     for _ in range(3):
-        slots.run_layer(x, es, ti, tw, npad, residual=False)
+        slots.run_layer(x, es, ti, tw, npad, residual=False, max_tok=mt)
     torch.cuda.synchronize()
     n = 30
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
     for i in range(n):
         flush.zero_()
         ev[i][0].record()
-        slots.run_layer(x, es, ti, tw, npad, residual=False)
+        slots.run_layer(x, es, ti, tw, npad, residual=False, max_tok=mt)
         ev[i][1].record()
     torch.cuda.synchronize()
     ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
