@@ -12,7 +12,7 @@ res = ds.results()
 st = np.array([r.counters.pad[0] for r in res], np.int64)
 en = np.array([r.counters.pad[1] for r in res], np.int64)
 sm = np.array([r.counters.pad[2] for r in res])
-dur = (en - st) / 1.965e6   # ms at 1965 MHz
+dur = (en - st) / 1e6       # globaltimer ns -> ms
 ms = e0.elapsed_time(e1)
 print(f"replay {ms:.1f} ms, points {len(res)}, mean point {dur.mean():.1f} ms, max {dur.max():.1f} ms")
 print("point-ms sum / (148 SM * 8 warps * kernel ms) =", dur.sum() / (148 * 8 * ms))
@@ -25,6 +25,13 @@ for ev in ("lru", "lfu", "ls"):
 for cap in (0.01, 0.05, 0.25):
     idx = [i for i, c in enumerate(cfgs) if c.hardware.capacity_fraction == cap]
     print(cap, f"mean {dur[idx].mean():.1f} ms")
+# concurrency timeline: running points per 1 ms bin
+t0 = st.min()
+T = int((en.max() - t0) / 1e6) + 1
+run = np.zeros(T)
+for a, b in zip((st - t0) / 1e6, (en - t0) / 1e6):
+    run[int(a):int(b) + 1] += 1
+print("running points per ms:", " ".join(str(int(x)) for x in run))
 # per-SM busy: sum of durations per SM
 busy = np.bincount(sm, weights=dur, minlength=148)
 print("per-SM busy ms: min %.1f mean %.1f max %.1f" % (busy.min(), busy.mean(), busy.max()))
@@ -48,3 +55,15 @@ for i, c in enumerate(cfgs):
 import os
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(rows, open("gpurun_out/sched_points.json", "w"))
+# per-group start times (launch order) and host enqueue time of one replay()
+import time
+torch.cuda.synchronize()
+h0 = time.perf_counter(); ds.replay(); h1 = time.perf_counter(); torch.cuda.synchronize()
+print(f"host enqueue of replay(): {(h1 - h0) * 1e3:.2f} ms for {len(ds.batch.groups)} groups")
+res = ds.results()
+st = np.array([r.counters.pad[0] for r in res], np.int64)
+t0 = st.min()
+for gi, g in enumerate(ds.batch.groups):
+    idx = list(g)
+    c = cfgs[idx[0]]
+    print(f"group {gi}: {c.model.name:10s} {c.eviction:4s} n={len(g)} first start {(st[idx].min() - t0) / 1e6:.2f} ms, median start {(np.median(st[idx]) - t0) / 1e6:.2f} ms")
