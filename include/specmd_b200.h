@@ -246,6 +246,20 @@ int esim_run_host(const EsimConfig *cfg, int32_t n, const EsimTraceDesc *traces,
                   EsimCounters *counters, int64_t *per_layer, int32_t pl_stride,
                   EsimRec *recs, int64_t rec_cap, int32_t *pred_experts, int64_t pe_cap);
 
+/* The same split into a reusable plan: create resolves everything that does
+ * not change between runs (predictors, geometry groups and their order, the
+ * device slab, descriptors); each run copies the step's inputs from the
+ * caller's trace arrays (host pointers captured at create; page-lock them with
+ * esim_host_register for DMA), routes, replays and writes counters[n] /
+ * per_layer[n][pl_stride][ESIM_PL_FIELDS] (/ recs, pred_experts when rec_cap
+ * > 0) straight into the caller's buffers, in the caller's config order.
+ * Synchronous. esim_run_host = create + run + destroy. */
+int esim_sweep_plan_create(const EsimConfig *cfg, int32_t n, const EsimTraceDesc *traces, int32_t n_traces,
+                           int32_t pl_stride, int64_t rec_cap, int64_t pe_cap, void **plan);
+int esim_sweep_plan_run(void *plan, EsimCounters *counters, int64_t *per_layer, EsimRec *recs,
+                        int32_t *pred_experts);
+int esim_sweep_plan_destroy(void *plan);
+
 /* ---- physical layer step (no reference equivalent; configs[1]) -------- */
 typedef struct {
     int32_t num_layers, experts, top_k;

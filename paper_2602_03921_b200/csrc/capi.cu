@@ -24,7 +24,7 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
-                                    int policy, bool general);
+                                    int policy, bool general, const int32_t* out_index = nullptr);
 int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt);
 
 static thread_local std::string g_err;
@@ -175,73 +175,72 @@ extern "C" int esim_router_launch_batch(const EsimTraceDesc* d_traces, const Esi
                                         const int32_t* d_params, const int64_t* d_prefix, int32_t n_traces,
                                         int64_t total_events, int32_t max_experts, void* stream);
 
+// ---------------------------------------------------------------------------
+// Sweep plan: everything about a grid that does not change between runs is
+// resolved once (predictor per trace, geometry groups + costliest-first order,
+// the device slab layout, device descriptors). A run then moves the step's
+// inputs and outputs only:
+//   H2D  small per-trace arrays gathered into one pinned image -> 1 copy,
+//        logits straight from the caller's (page-locked) arrays, 1 copy each
+//   GPU  batched router, grouped concurrent replays writing their results at
+//        the caller's row (out_index), so
+//   D2H  counters / per-layer (/ logs) land directly in the caller's buffers.
+// ---------------------------------------------------------------------------
 namespace {
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    cudaError_t ensure(size_t n) {
-        if (n <= cap) return cudaSuccess;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        cudaError_t e = cudaMalloc(&p, n);
-        if (e == cudaSuccess) cap = n;
-        return e;
-    }
-};
-
-struct HostBuf {                        // grow-only pinned staging
-    void* p = nullptr;
-    size_t cap = 0;
-    cudaError_t ensure(size_t n) {
-        if (n <= cap) return cudaSuccess;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        cap = 0;
-        cudaError_t e = cudaMallocHost(&p, n);
-        if (e == cudaSuccess) cap = n;
-        return e;
-    }
-};
-
-struct HostCtx {
-    HostBuf stage;
+struct SweepPlan {
+    int n = 0, n_traces = 0, pl_stride = 0, max_tokens = 0, max_e = 1;
+    int64_t rec_cap = 0, pe_cap = 0, total_events = 0;
+    std::vector<EsimConfig> pcfg;                 // group-sorted configs
+    std::vector<std::pair<int, int>> groups;      // [begin, end) in pcfg
+    std::vector<EsimTraceDesc> htr;               // caller descriptors (host pointers)
+    std::vector<size_t> small_off, logit_off;     // per trace, in the slab (small: relative to small image)
+    size_t small_bytes = 0, small_base = 0, cfg_off = 0, td_off = 0, rd_off = 0, par_off = 0, pre_off = 0;
+    size_t idx_off = 0, cnt_off = 0, pl_off = 0, rec_off = 0, pe_off = 0, total = 0;
+    char* slab = nullptr;                         // device
+    char* small_img = nullptr;                    // pinned image of the small arrays
     cudaStream_t st = nullptr;
-    std::vector<cudaStream_t> gs;       // one per geometry group (concurrent replays)
+    std::vector<cudaStream_t> gs;
     std::vector<cudaEvent_t> ge;
     cudaEvent_t routed = nullptr;
-    DevBuf slab;
 };
 
-HostCtx& ctx() {
-    static HostCtx c;
-    return c;
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+void plan_free(SweepPlan* P) {
+    if (!P) return;
+    if (P->st) cudaStreamSynchronize(P->st);
+    if (P->slab) cudaFree(P->slab);
+    if (P->small_img) cudaFreeHost(P->small_img);
+    for (auto s2 : P->gs) cudaStreamDestroy(s2);
+    for (auto e2 : P->ge) cudaEventDestroy(e2);
+    if (P->routed) cudaEventDestroy(P->routed);
+    if (P->st) cudaStreamDestroy(P->st);
+    delete P;
 }
 }  // namespace
 
-static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+extern "C" int esim_sweep_plan_destroy(void* plan) {
+    plan_free(static_cast<SweepPlan*>(plan));
+    return 0;
+}
 
-extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDesc* traces, int32_t n_traces,
-                             EsimCounters* counters, int64_t* per_layer, int32_t pl_stride, EsimRec* recs,
-                             int64_t rec_cap, int32_t* pred_experts, int64_t pe_cap) {
-    HostCtx& C = ctx();
+extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const EsimTraceDesc* traces,
+                                      int32_t n_traces, int32_t pl_stride, int64_t rec_cap, int64_t pe_cap,
+                                      void** plan_out) {
+    if (!plan_out) return fail(-1, "null plan pointer");
+    *plan_out = nullptr;
+    if (n <= 0) return fail(-1, "empty grid");
+    SweepPlan* P = new SweepPlan();
+    auto bail = [&](int rc) { plan_free(P); return rc; };
     cudaError_t e;
-    const bool prof = getenv("ESIM_PROFILE_HOST") != nullptr;
-    auto now_ms = []() { return std::chrono::duration<double, std::milli>(
-                             std::chrono::steady_clock::now().time_since_epoch()).count(); };
-    double t_start = now_ms();
-    if (!C.st) {
-        if ((e = cudaStreamCreateWithFlags(&C.st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
-        if ((e = cudaEventCreateWithFlags(&C.routed, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
-    }
-    if (n <= 0) return 0;
+    P->n = n; P->n_traces = n_traces; P->pl_stride = pl_stride; P->rec_cap = rec_cap; P->pe_cap = pe_cap;
     // predictor per trace (taken from the first config using it)
     std::vector<int32_t> params(4 * n_traces, 0);
     std::vector<char> seen(n_traces, 0);
     std::vector<double> pover(n_traces), ppct(n_traces);
     for (int i = 0; i < n; i++) {
         const int t = cfg[i].trace_id;
-        if (t < 0 || t >= n_traces) return fail(-1, "trace_id out of range");
+        if (t < 0 || t >= n_traces) return bail(fail(-1, "trace_id out of range"));
         if (!seen[t]) {
             seen[t] = 1;
             pover[t] = cfg[i].overfetch;
@@ -249,14 +248,14 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
             esim_predictor_params(traces[t].top_k, traces[t].experts, cfg[i].prefetch, cfg[i].overfetch,
                                   cfg[i].percentile, &params[4 * t]);
         } else if (params[4 * t] != cfg[i].prefetch || pover[t] != cfg[i].overfetch || ppct[t] != cfg[i].percentile) {
-            return fail(-1, "configs sharing a trace_id must share the predictor");
+            return bail(fail(-1, "configs sharing a trace_id must share the predictor"));
         }
     }
-    // geometry groups (stable), each replayed on its own stream with its own shared-memory sizing
+    // geometry groups (stable), each replayed on its own stream with its own shared-memory sizing;
+    // inside a group the costliest points first (largest cache in experts = longest victim
+    // scans, then slowest link) so long replays start in wave 1
     std::vector<int> order(n);
     for (int i = 0; i < n; i++) order[i] = i;
-    // group by geometry; inside a group the costliest points first (largest cache in
-    // experts = longest victim scans, then slowest link) so long replays start in wave 1
     auto slots_of = [&](int a) {
         const int64_t wb = cfg[a].expert_bytes[cfg[a].working_prec];
         return wb > 0 ? cfg[a].capacity_bytes / wb : 0;
@@ -271,63 +270,82 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
         if (slots_of(a) != slots_of(b)) return slots_of(a) > slots_of(b);
         return bw_of(a) < bw_of(b);
     });
-    std::vector<std::pair<int, int>> groups;   // [begin, end) in `order`
     for (int i = 0; i < n; i++) {
         if (i == 0 || cfg[order[i]].num_layers != cfg[order[i - 1]].num_layers ||
             cfg[order[i]].experts != cfg[order[i - 1]].experts ||
             cfg[order[i]].eviction != cfg[order[i - 1]].eviction || gen_of(order[i]) != gen_of(order[i - 1]))
-            groups.push_back({i, i + 1});
+            P->groups.push_back({i, i + 1});
         else
-            groups.back().second = i + 1;
+            P->groups.back().second = i + 1;
     }
-    std::vector<EsimConfig> pcfg(n);
-    for (int i = 0; i < n; i++) pcfg[i] = cfg[order[i]];
-    // one device slab: traces, router outputs, tables, configs, outputs
-    size_t total = 0;
-    std::vector<size_t> toff(n_traces), roff(n_traces);
+    P->pcfg.resize(n);
+    for (int i = 0; i < n; i++) P->pcfg[i] = cfg[order[i]];
+    // slab: [small arrays of every trace][logits per trace][router outputs][tables][outputs]
+    P->htr.assign(traces, traces + n_traces);
+    P->small_off.resize(n_traces);
+    P->logit_off.resize(n_traces);
+    std::vector<size_t> roff(n_traces);
     std::vector<int64_t> prefix(n_traces + 1, 0);
-    int max_tokens = 0, max_e = 1;
+    for (int t = 0; t < n_traces; t++) {
+        const EsimTraceDesc& d = traces[t];
+        P->small_off[t] = P->small_bytes;
+        P->small_bytes += al256(d.n_passes * 4) * 2 + al256((d.n_events + 1) * 8);
+        prefix[t + 1] = prefix[t] + d.n_events;
+        P->max_e = std::max(P->max_e, (int)d.experts);
+        for (int p = 0; p < d.n_passes; p++) P->max_tokens = std::max(P->max_tokens, d.pass_tokens[p]);
+    }
+    P->total_events = prefix[n_traces];
+    size_t total = P->small_bytes;
+    for (int t = 0; t < n_traces; t++) {
+        const EsimTraceDesc& d = traces[t];
+        P->logit_off[t] = total;
+        total += al256(d.n_rows_total * d.experts * 4);
+    }
     for (int t = 0; t < n_traces; t++) {
         const EsimTraceDesc& d = traces[t];
         const int64_t ne = d.n_events, nr = d.n_rows_total, E = d.experts, K = d.top_k;
-        toff[t] = total;
-        total += al256(d.n_passes * 4) * 2 + al256((ne + 1) * 8) + al256(nr * E * 4);
         roff[t] = total;
         total += al256(ne * 4) * 3 + al256(ne * E * 4) * 6 + al256(ne * E * 8) + al256(ne * 8) +
                  al256(nr * K * 2) + al256(nr * K * 4) + al256(ne * 4) * 2 + al256(d.num_layers * 16) +
                  al256(sizeof(EsimRouteSummary));
-        prefix[t + 1] = prefix[t] + ne;
-        max_e = std::max(max_e, (int)E);
-        for (int p = 0; p < d.n_passes; p++) max_tokens = std::max(max_tokens, d.pass_tokens[p]);
     }
-    const size_t cfg_off = total; total += al256(sizeof(EsimConfig) * n);
-    const size_t td_off = total; total += al256(sizeof(EsimTraceDesc) * n_traces);
-    const size_t rd_off = total; total += al256(sizeof(EsimRouterOut) * n_traces);
-    const size_t par_off = total; total += al256(sizeof(int32_t) * 4 * n_traces);
-    const size_t pre_off = total; total += al256(sizeof(int64_t) * (n_traces + 1));
-    const size_t cnt_off = total; total += al256(sizeof(EsimCounters) * n);
-    const size_t pl_off = total; total += al256(sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS);
-    const size_t rec_off = total; total += recs ? al256(sizeof(EsimRec) * n * rec_cap) : 0;
-    const size_t pe_off = total; total += recs ? al256(sizeof(int32_t) * n * pe_cap) : 0;
-    if ((e = C.slab.ensure(total)) != cudaSuccess) return cuda_fail(e, "device alloc");
-    char* base = (char*)C.slab.p;
+    P->cfg_off = total; total += al256(sizeof(EsimConfig) * n);
+    P->td_off = total; total += al256(sizeof(EsimTraceDesc) * n_traces);
+    P->rd_off = total; total += al256(sizeof(EsimRouterOut) * n_traces);
+    P->par_off = total; total += al256(sizeof(int32_t) * 4 * n_traces);
+    P->pre_off = total; total += al256(sizeof(int64_t) * (n_traces + 1));
+    P->idx_off = total; total += al256(sizeof(int32_t) * n);
+    P->cnt_off = total; total += al256(sizeof(EsimCounters) * n);
+    P->pl_off = total; total += al256(sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS);
+    P->rec_off = total; total += rec_cap ? al256(sizeof(EsimRec) * n * rec_cap) : 0;
+    P->pe_off = total; total += rec_cap ? al256(sizeof(int32_t) * n * pe_cap) : 0;
+    P->total = total;
+    if ((e = cudaMalloc((void**)&P->slab, total)) != cudaSuccess) return bail(cuda_fail(e, "device alloc"));
+    if ((e = cudaMallocHost((void**)&P->small_img, std::max<size_t>(P->small_bytes, 256))) != cudaSuccess)
+        return bail(cuda_fail(e, "pinned alloc"));
+    if ((e = cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking)) != cudaSuccess) return bail(cuda_fail(e, "stream"));
+    if ((e = cudaEventCreateWithFlags(&P->routed, cudaEventDisableTiming)) != cudaSuccess) return bail(cuda_fail(e, "event"));
+    for (size_t g = 0; g < P->groups.size(); g++) {
+        cudaStream_t s2;
+        cudaEvent_t e2;
+        if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking)) != cudaSuccess) return bail(cuda_fail(e, "stream"));
+        P->gs.push_back(s2);
+        if ((e = cudaEventCreateWithFlags(&e2, cudaEventDisableTiming)) != cudaSuccess) return bail(cuda_fail(e, "event"));
+        P->ge.push_back(e2);
+    }
+    // device descriptors of the slab (fixed for the plan)
+    char* base = P->slab;
     std::vector<EsimTraceDesc> dtr(n_traces);
     std::vector<EsimRouterOut> dro(n_traces);
     for (int t = 0; t < n_traces; t++) {
         const EsimTraceDesc& h = traces[t];
         const int64_t ne = h.n_events, nr = h.n_rows_total, E = h.experts, K = h.top_k;
-        char* q = base + toff[t];
         EsimTraceDesc d = h;
-        auto put = [&](const void* src, size_t bytes) -> void* {
-            void* dst = q;
-            if (bytes) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, C.st);
-            q += al256(bytes);
-            return dst;
-        };
-        d.pass_tokens = (const int32_t*)put(h.pass_tokens, h.n_passes * 4);
-        d.pass_kind = (const int32_t*)put(h.pass_kind, h.n_passes * 4);
-        d.row_offset = (const int64_t*)put(h.row_offset, (ne + 1) * 8);
-        d.logits = (const float*)put(h.logits, nr * E * 4);
+        char* q = base + P->small_off[t];
+        d.pass_tokens = (const int32_t*)q; q += al256(h.n_passes * 4);
+        d.pass_kind = (const int32_t*)q; q += al256(h.n_passes * 4);
+        d.row_offset = (const int64_t*)q;
+        d.logits = (const float*)(base + P->logit_off[t]);
         dtr[t] = d;
         char* r = base + roff[t];
         auto take = [&](size_t bytes) -> void* { void* x = r; r += al256(bytes); return x; };
@@ -351,85 +369,85 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
         o.summary = (EsimRouteSummary*)take(sizeof(EsimRouteSummary));
         dro[t] = o;
     }
-    cudaMemcpyAsync(base + cfg_off, pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice, C.st);
-    cudaMemcpyAsync(base + td_off, dtr.data(), sizeof(EsimTraceDesc) * n_traces, cudaMemcpyHostToDevice, C.st);
-    cudaMemcpyAsync(base + rd_off, dro.data(), sizeof(EsimRouterOut) * n_traces, cudaMemcpyHostToDevice, C.st);
-    cudaMemcpyAsync(base + par_off, params.data(), sizeof(int32_t) * 4 * n_traces, cudaMemcpyHostToDevice, C.st);
-    cudaMemcpyAsync(base + pre_off, prefix.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice, C.st);
-    double t_h2d = now_ms();
-    if (prof) { cudaStreamSynchronize(C.st); fprintf(stderr, "[esim_run_host] setup+h2d enqueue %.2f ms, h2d done %.2f ms\n", t_h2d - t_start, now_ms() - t_start); }
-    int rc = esim_router_launch_batch((EsimTraceDesc*)(base + td_off), (EsimRouterOut*)(base + rd_off),
-                                      (int32_t*)(base + par_off), (int64_t*)(base + pre_off), n_traces,
-                                      prefix[n_traces], max_e, C.st);
+    std::vector<int32_t> out_index(order.begin(), order.end());
+    cudaMemcpy(base + P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(base + P->td_off, dtr.data(), sizeof(EsimTraceDesc) * n_traces, cudaMemcpyHostToDevice);
+    cudaMemcpy(base + P->rd_off, dro.data(), sizeof(EsimRouterOut) * n_traces, cudaMemcpyHostToDevice);
+    cudaMemcpy(base + P->par_off, params.data(), sizeof(int32_t) * 4 * n_traces, cudaMemcpyHostToDevice);
+    cudaMemcpy(base + P->pre_off, prefix.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice);
+    if ((e = cudaMemcpy(base + P->idx_off, out_index.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+        return bail(cuda_fail(e, "plan upload"));
+    *plan_out = P;
+    return 0;
+}
+
+extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* per_layer, EsimRec* recs,
+                                   int32_t* pred_experts) {
+    SweepPlan* P = static_cast<SweepPlan*>(plan);
+    if (!P) return fail(-1, "null plan");
+    cudaError_t e;
+    const bool prof = getenv("ESIM_PROFILE_HOST") != nullptr;
+    auto now_ms = []() { return std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t_start = now_ms();
+    char* base = P->slab;
+    const int n = P->n;
+    // ---- inputs: small arrays through one pinned image, logits straight from the caller
+    for (int t = 0; t < P->n_traces; t++) {
+        const EsimTraceDesc& h = P->htr[t];
+        char* q = P->small_img + P->small_off[t];
+        std::memcpy(q, h.pass_tokens, h.n_passes * 4); q += al256(h.n_passes * 4);
+        std::memcpy(q, h.pass_kind, h.n_passes * 4); q += al256(h.n_passes * 4);
+        std::memcpy(q, h.row_offset, (h.n_events + 1) * 8);
+    }
+    cudaMemcpyAsync(base, P->small_img, P->small_bytes, cudaMemcpyHostToDevice, P->st);
+    for (int t = 0; t < P->n_traces; t++) {
+        const EsimTraceDesc& h = P->htr[t];
+        if (h.n_rows_total)
+            cudaMemcpyAsync(base + P->logit_off[t], h.logits, h.n_rows_total * h.experts * 4, cudaMemcpyHostToDevice,
+                            P->st);
+    }
+    if (prof) { cudaStreamSynchronize(P->st); fprintf(stderr, "[plan_run] h2d done %.2f ms\n", now_ms() - t_start); }
+    int rc = esim_router_launch_batch((EsimTraceDesc*)(base + P->td_off), (EsimRouterOut*)(base + P->rd_off),
+                                      (int32_t*)(base + P->par_off), (int64_t*)(base + P->pre_off), P->n_traces,
+                                      P->total_events, P->max_e, P->st);
     if (rc) return cuda_fail(cudaGetLastError(), "router batch");
-    while (C.gs.size() < groups.size()) {
-        cudaStream_t s2;
-        cudaEvent_t e2;
-        if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
-        if ((e = cudaEventCreateWithFlags(&e2, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
-        C.gs.push_back(s2);
-        C.ge.push_back(e2);
+    if (prof) { cudaStreamSynchronize(P->st); fprintf(stderr, "[plan_run] router done %.2f ms\n", now_ms() - t_start); }
+    // ---- grouped concurrent replays, results at the caller's rows
+    cudaEventRecord(P->routed, P->st);
+    const bool full = recs != nullptr && P->rec_cap > 0;
+    for (size_t g = 0; g < P->groups.size(); g++) {
+        const int b = P->groups[g].first, m = P->groups[g].second - b;
+        cudaStreamWaitEvent(P->gs[g], P->routed, 0);
+        Sizing z;
+        if ((rc = replay_sizing(P->pcfg.data() + b, m, P->max_tokens, P->pl_stride, 0, &z))) return rc;
+        const int per = esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt);
+        int w = 4;
+        while (w > 1 && per * w > 227 * 1024) w--;
+        if (per * w > 227 * 1024) return fail(-1, "replay state of one grid point exceeds shared memory");
+        e = esim_replay_launch_impl((EsimConfig*)(base + P->cfg_off) + b, m, (EsimTraceDesc*)(base + P->td_off),
+                                    (EsimRouterOut*)(base + P->rd_off), (EsimCounters*)(base + P->cnt_off),
+                                    (int64_t*)(base + P->pl_off), full ? (EsimRec*)(base + P->rec_off) : nullptr,
+                                    P->rec_cap, full ? (int32_t*)(base + P->pe_off) : nullptr, P->pe_cap, z.N, z.S,
+                                    z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt, w, P->gs[g], nullptr, z.policy,
+                                    z.general, (int32_t*)(base + P->idx_off) + b);
+        if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+        cudaEventRecord(P->ge[g], P->gs[g]);
+        cudaStreamWaitEvent(P->st, P->ge[g], 0);
     }
-    auto replay_groups = [&](int queue_cap, const std::vector<char>& which) -> int {
-        cudaEventRecord(C.routed, C.st);
-        for (size_t g = 0; g < groups.size(); g++) {
-            if (!which[g]) continue;
-            const int b = groups[g].first, m = groups[g].second - b;
-            cudaStreamWaitEvent(C.gs[g], C.routed, 0);
-            int r2 = esim_replay_launch(pcfg.data() + b, (EsimConfig*)(base + cfg_off) + b, m,
-                                        (EsimTraceDesc*)(base + td_off), (EsimRouterOut*)(base + rd_off), max_tokens,
-                                        (EsimCounters*)(base + cnt_off) + b,
-                                        (int64_t*)(base + pl_off) + (size_t)b * pl_stride * ESIM_PL_FIELDS, pl_stride,
-                                        recs ? (EsimRec*)(base + rec_off) + (size_t)b * rec_cap : nullptr, rec_cap,
-                                        recs ? (int32_t*)(base + pe_off) + (size_t)b * pe_cap : nullptr, pe_cap, 0,
-                                        queue_cap, C.gs[g]);
-            if (r2) return r2;
-            cudaEventRecord(C.ge[g], C.gs[g]);
-            cudaStreamWaitEvent(C.st, C.ge[g], 0);
-        }
-        return 0;
-    };
-    if (prof) { cudaStreamSynchronize(C.st); fprintf(stderr, "[esim_run_host] router done %.2f ms\n", now_ms() - t_start); }
-    std::vector<char> all(groups.size(), 1);
-    if ((rc = replay_groups(0, all))) return rc;
-    if (prof) { cudaStreamSynchronize(C.st); fprintf(stderr, "[esim_run_host] replay done %.2f ms (%zu groups)\n", now_ms() - t_start, groups.size()); }
-    const size_t pls = (size_t)pl_stride * ESIM_PL_FIELDS;
-    const size_t st_cnt = al256(sizeof(EsimCounters) * n), st_pl = al256(sizeof(int64_t) * n * pls);
-    const size_t st_rec = recs ? al256(sizeof(EsimRec) * n * rec_cap) : 0;
-    const size_t st_pe = recs ? al256(sizeof(int32_t) * n * pe_cap) : 0;
-    if ((e = C.stage.ensure(st_cnt + st_pl + st_rec + st_pe)) != cudaSuccess) return cuda_fail(e, "pinned staging");
-    EsimCounters* pc = (EsimCounters*)C.stage.p;
-    int64_t* ppl = (int64_t*)((char*)C.stage.p + st_cnt);
-    EsimRec* prec_ = (EsimRec*)((char*)C.stage.p + st_cnt + st_pl);
-    int32_t* ppe = (int32_t*)((char*)C.stage.p + st_cnt + st_pl + st_rec);
-    cudaMemcpyAsync(pc, base + cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, C.st);
-    if ((e = cudaStreamSynchronize(C.st)) != cudaSuccess) return cuda_fail(e, "esim_run_host");
-    std::vector<char> redo(groups.size(), 0);
-    bool any = false;
-    for (size_t g = 0; g < groups.size(); g++)
-        for (int i = groups[g].first; i < groups[g].second; i++)
-            if (pc[i].status == -5) { redo[g] = 1; any = true; }
-    if (any) {   // a channel outgrew the default ring: those groups again with the exact bound
-        if ((rc = replay_groups(-1, redo))) return rc;
-        cudaMemcpyAsync(pc, base + cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, C.st);
+    if (prof) { cudaStreamSynchronize(P->st); fprintf(stderr, "[plan_run] replay done %.2f ms\n", now_ms() - t_start); }
+    // ---- outputs straight into the caller's buffers
+    const size_t pls = (size_t)P->pl_stride * ESIM_PL_FIELDS;
+    cudaMemcpyAsync(counters, base + P->cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, P->st);
+    cudaMemcpyAsync(per_layer, base + P->pl_off, sizeof(int64_t) * n * pls, cudaMemcpyDeviceToHost, P->st);
+    if (full) {
+        cudaMemcpyAsync(recs, base + P->rec_off, sizeof(EsimRec) * n * P->rec_cap, cudaMemcpyDeviceToHost, P->st);
+        cudaMemcpyAsync(pred_experts, base + P->pe_off, sizeof(int32_t) * n * P->pe_cap, cudaMemcpyDeviceToHost,
+                        P->st);
     }
-    cudaMemcpyAsync(ppl, base + pl_off, sizeof(int64_t) * n * pls, cudaMemcpyDeviceToHost, C.st);
-    if (recs) {
-        cudaMemcpyAsync(prec_, base + rec_off, sizeof(EsimRec) * n * rec_cap, cudaMemcpyDeviceToHost, C.st);
-        cudaMemcpyAsync(ppe, base + pe_off, sizeof(int32_t) * n * pe_cap, cudaMemcpyDeviceToHost, C.st);
-    }
-    if ((e = cudaStreamSynchronize(C.st)) != cudaSuccess) return cuda_fail(e, "esim_run_host");
-    if (prof) fprintf(stderr, "[esim_run_host] d2h done %.2f ms\n", now_ms() - t_start);
-    for (int i = 0; i < n; i++) {           // back to the caller's order
-        const int j = order[i];
-        counters[j] = pc[i];
-        std::memcpy(per_layer + (size_t)j * pls, ppl + (size_t)i * pls, pls * sizeof(int64_t));
-        if (recs) {
-            std::memcpy(recs + (size_t)j * rec_cap, prec_ + (size_t)i * rec_cap, rec_cap * sizeof(EsimRec));
-            std::memcpy(pred_experts + (size_t)j * pe_cap, ppe + (size_t)i * pe_cap, pe_cap * sizeof(int32_t));
-        }
-    }
-    if (prof) fprintf(stderr, "[esim_run_host] total %.2f ms\n", now_ms() - t_start);
+    if ((e = cudaStreamSynchronize(P->st)) != cudaSuccess) return cuda_fail(e, "sweep plan run");
+    if (prof) fprintf(stderr, "[plan_run] d2h done %.2f ms\n", now_ms() - t_start);
     for (int i = 0; i < n; i++)
         if (counters[i].status) {
             const int st = (int)counters[i].status;
@@ -438,4 +456,16 @@ extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDe
                                        : "runtime invariant broken during replay");
         }
     return 0;
+}
+
+extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDesc* traces, int32_t n_traces,
+                             EsimCounters* counters, int64_t* per_layer, int32_t pl_stride, EsimRec* recs,
+                             int64_t rec_cap, int32_t* pred_experts, int64_t pe_cap) {
+    if (n <= 0) return 0;
+    void* plan = nullptr;
+    int rc = esim_sweep_plan_create(cfg, n, traces, n_traces, pl_stride, recs ? rec_cap : 0, recs ? pe_cap : 0, &plan);
+    if (rc) return rc;
+    rc = esim_sweep_plan_run(plan, counters, per_layer, recs, pred_experts);
+    esim_sweep_plan_destroy(plan);
+    return rc;
 }

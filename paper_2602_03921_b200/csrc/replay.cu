@@ -60,6 +60,7 @@ struct ReplayArgs {
     int has_cnt;                   // any LFU/LHU point (per-ident counts)
     int warps_per_cta;
     int point_bytes;
+    const int32_t* out_index;      // optional: output row of launch point pid (counters, per_layer, logs)
     volatile int64_t* progress;    // optional (single point, streamed decisions): [0] events done
                                    // (-1 on error), [1 + ev] records emitted through event ev
 };
@@ -987,6 +988,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     const int wid = threadIdx.x >> 5;
     const int pid = blockIdx.x * A.warps_per_cta + wid;
     if (pid >= A.n_points) return;
+    const int64_t orow = A.out_index ? A.out_index[pid] : pid;      // where this point's results go
     const EsimConfig* cfg = &A.cfg[pid];
     const EsimTraceDesc tr = A.traces[cfg->trace_id];
     const EsimRouterOut R = A.routers[cfg->trace_id];
@@ -1004,7 +1006,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     p.pol = POL;
     p.miss = GEN ? cfg->miss : ESIM_MISS_FETCH;
     if (cfg->eviction != POL || (!GEN && (cfg->miss != ESIM_MISS_FETCH || cfg->routing != ESIM_ROUTE_STANDARD))) {
-        if ((threadIdx.x & 31) == 0) A.counters[pid].status = -1;      // dispatch error
+        if ((threadIdx.x & 31) == 0) A.counters[orow].status = -1;     // dispatch error
         return;
     }
     p.cap = cfg->capacity_bytes;
@@ -1083,9 +1085,9 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     p.err = 0;
     p.full = (cfg->flags & ESIM_FLAG_FULL_LOG) && A.recs != nullptr;
     p.digest_on = (cfg->flags & ESIM_FLAG_NO_DIGEST) == 0;
-    p.recs = A.recs + (int64_t)pid * A.rec_cap;
+    p.recs = A.recs + orow * A.rec_cap;
     p.rec_cap = A.rec_cap;
-    p.pexp = A.pexp + (int64_t)pid * A.pe_cap;
+    p.pexp = A.pexp + orow * A.pe_cap;
     p.pe_cap = A.pe_cap;
     if (ca && (p.E > A.Emax || A.Tmax == 0)) p.err = -1;
     if (lfu && !A.has_cnt) p.err = -1;
@@ -1248,7 +1250,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     }
     if (p.lane == 0) {
         const Ctr* c = p.ctr;
-        EsimCounters* o = &A.counters[pid];
+        EsimCounters* o = &A.counters[orow];
         for (int i = 0; i < 8; i++) {
             int64_t t = 0;
             for (int l = 0; l < p.L; l++) t += p.pl[l * ESIM_PL_FIELDS + i];
@@ -1292,7 +1294,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
         o->pad[1] = t_end;
         o->pad[2] = smid;
     }
-    int64_t* plo = A.per_layer + (int64_t)pid * A.Lmax * ESIM_PL_FIELDS;
+    int64_t* plo = A.per_layer + orow * A.Lmax * ESIM_PL_FIELDS;
     for (int i = p.lane; i < A.Lmax * ESIM_PL_FIELDS; i += 32) {
         int64_t v = 0;
         if (i < p.L * ESIM_PL_FIELDS) {
@@ -1314,9 +1316,10 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
-                                    int policy, bool general) {
+                                    int policy, bool general, const int32_t* out_index) {
     esim::ReplayArgs a;
     a.progress = progress;
+    a.out_index = out_index;
     a.cfg = d_cfg; a.n_points = n; a.traces = d_traces; a.routers = d_routers;
     a.counters = d_counters; a.per_layer = d_per_layer; a.recs = d_recs; a.rec_cap = rec_cap;
     a.pexp = d_pexp; a.pe_cap = pe_cap;

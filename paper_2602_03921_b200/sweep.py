@@ -102,10 +102,11 @@ def _c_config(cfg, trace_id: int):
 
 
 class HostGrid:
-    """A sweep grid packed once for the C-ABI end-to-end call (esim_run_host):
-    the EsimConfig array and the trace descriptors (pointers into the
-    callers' host trace arrays) are built here; every `run()` is one
-    esim_run_host call -- trace H2D, router, replays, results D2H.
+    """A sweep grid as a C-ABI plan (esim_sweep_plan_*): configs, trace
+    descriptors (pointers into the callers' host trace arrays), groups and the
+    device slab are resolved once; every `run()` is one esim_sweep_plan_run --
+    trace H2D, router, replays, results D2H straight into this object's
+    page-locked output arrays, in config order.
 
     Configs that share a trace object must share the predictor; prediction
     noise is not supported on this path (use engine.Simulation)."""
@@ -126,29 +127,64 @@ class HostGrid:
             ccfg.append(_c_config(cfg, ids[key]))
         self.n = n = len(ccfg)
         self.L = pl_stride or max(c.model.num_layers for c in cfgs)
-        self.carr = (_abi.EsimConfig * n).from_buffer_copy(b"".join(ccfg))
-        self.darr = (_abi.EsimTraceDesc * len(descs))(*descs)
-        self.n_traces = len(descs)
+        carr = (_abi.EsimConfig * n).from_buffer_copy(b"".join(ccfg))
+        darr = (_abi.EsimTraceDesc * len(descs))(*descs)
         self.counters = (_abi.EsimCounters * n)()
         self.per_layer = np.zeros((n, self.L, _abi.ESIM_PL_FIELDS), np.int64)
+        for buf, nbytes in ((C.addressof(self.counters), C.sizeof(self.counters)),
+                            (self.per_layer.ctypes.data, self.per_layer.nbytes)):
+            if _lib().esim_host_register(buf, nbytes):
+                raise RuntimeError(_lib().esim_last_error().decode())
+        self._registered = True
+        h = C.c_void_p()
+        rc = _lib().esim_sweep_plan_create(C.addressof(carr), n, C.addressof(darr), len(descs), self.L, 0, 0,
+                                           C.byref(h))
+        if rc != 0:
+            self._raise(rc)
+        self._plan = h
+
+    @staticmethod
+    def _raise(rc):
+        msg = _lib().esim_last_error().decode()
+        if rc == -1:
+            raise ConfigError(msg)
+        raise RuntimeError(f"esim_run_host failed ({rc}): {msg}")
 
     def run(self):
-        """Returns (counters list, per_layer array [n][pl_stride][ESIM_PL_FIELDS])."""
-        rc = _lib().esim_run_host(C.addressof(self.carr), self.n, C.addressof(self.darr), self.n_traces,
-                                  C.addressof(self.counters), self.per_layer.ctypes.data, self.L, None, 0, None, 0)
+        """Returns (counters, per_layer [n][pl_stride][ESIM_PL_FIELDS]): this grid's
+        own output buffers (no copy), overwritten by the next run()."""
+        rc = _lib().esim_sweep_plan_run(self._plan, C.addressof(self.counters), self.per_layer.ctypes.data,
+                                        None, None)
         if rc != 0:
-            msg = _lib().esim_last_error().decode()
-            if rc == -1:
-                raise ConfigError(msg)
-            raise RuntimeError(f"esim_run_host failed ({rc}): {msg}")
-        return list(self.counters), self.per_layer.copy()
+            self._raise(rc)
+        return self.counters, self.per_layer
+
+    def close(self) -> None:
+        if getattr(self, "_plan", None):
+            _lib().esim_sweep_plan_destroy(self._plan)
+            self._plan = None
+        if getattr(self, "_registered", False):
+            _lib().esim_host_unregister(C.addressof(self.counters))
+            _lib().esim_host_unregister(self.per_layer.ctypes.data)
+            self._registered = False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def run_grid_host(cfgs, traces, pl_stride: int | None = None):
     """One end-to-end C-ABI call (esim_run_host): host buffers in and out.
 
     Returns (counters list, per_layer array [n][pl_stride][ESIM_PL_FIELDS])."""
-    return HostGrid(cfgs, traces, pl_stride).run()
+    g = HostGrid(cfgs, traces, pl_stride)
+    try:
+        cs, pl = g.run()
+        return list(cs), pl
+    finally:
+        g.close()
 
 
 def reports(cfgs, counters, per_layer) -> list:
