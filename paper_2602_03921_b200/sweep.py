@@ -243,7 +243,7 @@ class DeviceSweep:
 
     @property
     def n_router_launches(self) -> int:
-        return 1
+        return 3        # classify_kernel, router_persistent_kernel, route_totals_kernel
 
     @property
     def n_replay_launches(self) -> int:
