@@ -377,15 +377,14 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             return ls_fail(-3, "residual launch failed");
         return 0;
     };
+    // one FFN entry per executed expert; a substitute serving several missing
+    // experts appears once per expert (same slot, separate token lists), so
+    // no entry ever holds more than one expert's tokens
     auto execute = [&](int expert, int slot, int tokens) {
-        if (!slot_pending[slot]) {
-            slot_pending[slot] = 1;
-            pend_slot.push_back(slot);
-            tok_of_pos.push_back(0);
-        }
-        const int pos = (int)(std::find(pend_slot.begin(), pend_slot.end(), slot) - pend_slot.begin());
-        pos_of_expert[expert] = pos;
-        tok_of_pos[pos] += tokens;
+        slot_pending[slot] = 1;
+        pos_of_expert[expert] = (int)pend_slot.size();
+        pend_slot.push_back(slot);
+        tok_of_pos.push_back(tokens);
     };
 
     for (int64_t ev = 0; ev < n_events; ev++) {

@@ -15,7 +15,9 @@ pytestmark = pytest.mark.gpu
 H, I = 2048, 1024
 
 
-def _reference(engine, trace, x0, xdec):
+def _reference(engine, trace, x0, xdec, served=None, I=1024):
+    """No-cache fp32 forward; served[(pass, layer)][e] = the expert whose
+    weights serve e's tokens (a substitute), or None when e was dropped."""
     import torch
     from paper_2602_03921_b200.ffn import expert_matrices
     from paper_2602_03921_b200.routing import softmax_rows
@@ -28,7 +30,10 @@ def _reference(engine, trace, x0, xdec):
             idx = np.argsort(-sc, axis=1, kind="stable")[:, :spec.top_k]
             y = torch.zeros_like(x)
             for e in np.unique(idx):
-                w = engine.expert_weights(ev.layer, int(e)).cuda().float()
+                we = (served or {}).get((p, ev.layer), {}).get(int(e), int(e))
+                if we is None:
+                    continue
+                w = engine.expert_weights(ev.layer, we).cuda().float()
                 w1, wd = expert_matrices(w, H, I)
                 act = (torch.nn.functional.silu(x.to(torch.bfloat16).float() @ w1[:I].T) *
                        (x.to(torch.bfloat16).float() @ w1[I:].T)).to(torch.bfloat16).float()
@@ -42,15 +47,21 @@ def _reference(engine, trace, x0, xdec):
     return torch.cat(outs)
 
 
-@pytest.mark.parametrize("eviction,cap_experts", [("ls", 12), ("lru", 6), ("ls", 3)])
-def test_layer_step_matches_nocache_reference(eviction, cap_experts, oracle_lib):
+@pytest.mark.parametrize("eviction,cap_experts,miss,inter", [("ls", 12, "fetch", 1024), ("lru", 6, "fetch", 1024),
+                                                             ("ls", 3, "fetch", 1024), ("ls", 5, "fetch", 1408),
+                                                             ("ls", 5, "subst", 1408), ("lru", 4, "drop", 1024)])
+def test_layer_step_matches_nocache_reference(eviction, cap_experts, miss, inter, oracle_lib):
+    """I = 1408 is the Qwen1.5-MoE expert width (not a power of two); subst /
+    drop follow the decision stream (substitute weights / no contribution)."""
     import torch
     from paper_2602_03921_b200 import HardwareSpec, ModelSpec, SimConfig, generate_synthetic
     from paper_2602_03921_b200.layer_step import LayerStepEngine
+    I = inter
     eb = 3 * H * I * 2
-    spec = ModelSpec("mini_olmoe", num_layers=4, experts_per_layer=16, top_k=4, expert_bytes_fp16=eb)
+    spec = ModelSpec("mini_moe", num_layers=4, experts_per_layer=16, top_k=4, expert_bytes_fp16=eb)
     cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=cap_experts * eb), working_precision="fp16",
-                    eviction=eviction, prefetch="score", percentile=80.0, miss="fetch")
+                    eviction=eviction, prefetch="score", percentile=80.0, miss=miss, subst_tolerance=0.2,
+                    drop_rank_threshold=2)
     tr = generate_synthetic(spec, seed=7, prefill_tokens=8, decode_tokens=3)
     eng = LayerStepEngine(cfg, H, I, max_tokens=8)
     eng.init_weights(seed=3)
@@ -58,11 +69,17 @@ def test_layer_step_matches_nocache_reference(eviction, cap_experts, oracle_lib)
     x0 = torch.randn(8, H, generator=g).to(torch.bfloat16).pin_memory()
     xd = torch.randn(3, H, generator=g).to(torch.bfloat16).pin_memory()
     res = eng.run(tr, x0, xd, keep_outputs=True)
+    o = oracle_lib.run(cfg, tr, full_log=True)
+    assert json.dumps(o.report) == json.dumps(res.report)
+    served = {}
+    for r in o.log:
+        if type(r).__name__ == "AccessRec" and r.outcome in ("drop", "subst"):
+            served.setdefault((r.pass_id, r.layer), {})[r.expert] = r.substitute if r.outcome == "subst" else None
+    if miss != "fetch":
+        assert served, "the case must exercise its miss policy"
     got = res.out.view(-1, H).float()
-    ref = _reference(eng, tr, x0, xd).cpu()
+    ref = _reference(eng, tr, x0, xd, served, I).cpu()
     err = (got - ref).abs().max().item() / ref.abs().max().item()
     assert err <= 1e-2, f"max rel err {err:.3e}"
-    o = oracle_lib.run(cfg, tr, full_log=False)
-    assert json.dumps(o.report) == json.dumps(res.report)
     assert res.n_copies >= res.report["totals"]["misses"] - res.report["totals"]["prefetch_started"]
     eng.close()

@@ -178,3 +178,51 @@ def test_router_paths_by_width_match_oracle(oracle_lib, experts, top_k):
         o = oracle_lib.run(cfg, tr, full_log=True)
         assert [canon_reference_record(x) for x in r.log] == [canon_reference_record(x) for x in o.log], cfg.prefetch
         assert json.dumps(r.report) == json.dumps(o.report)
+
+
+def test_sweep_plan_full_logs_match_reference():
+    """esim_sweep_plan_* with record buffers (results at the caller's rows,
+    reused across runs): full event logs == the reference goldens."""
+    import ctypes as C
+    import numpy as np
+    from paper_2602_03921_b200 import _abi
+    from paper_2602_03921_b200._device import lib, rec_capacity
+    from paper_2602_03921_b200.records import REC_DTYPE, decode_records
+    from paper_2602_03921_b200.metrics import report_from_counters
+    cs = [c for c in SMALL if not c["config"].get("prefetch_noise")][::11][:40]   # noise: Simulation path only
+    cfgs = [config_from(c) for c in cs]
+    trs = [trace_from(c["trace"]) for c in cs]
+    descs, keep, ccfg = [], [], []
+    for cfg, tr in zip(cfgs, trs):
+        d, k = _abi.trace_desc_host(tr.packed())
+        descs.append(d)
+        keep.append(k)
+        ccfg.append(cfg.to_c(len(descs) - 1, True))
+    n = len(ccfg)
+    L = max(c.model.num_layers for c in cfgs)
+    rec_cap = max(rec_capacity(t.packed())[0] for t in trs)
+    pe_cap = max(rec_capacity(t.packed())[1] for t in trs)
+    carr = (_abi.EsimConfig * n)(*ccfg)
+    darr = (_abi.EsimTraceDesc * n)(*descs)
+    plan = C.c_void_p()
+    assert lib().esim_sweep_plan_create(C.addressof(carr), n, C.addressof(darr), n, L, rec_cap, pe_cap,
+                                        C.byref(plan)) == 0, lib().esim_last_error()
+    try:
+        for _ in range(2):                                  # the plan is reusable
+            counters = (_abi.EsimCounters * n)()
+            per_layer = np.zeros((n, L, _abi.ESIM_PL_FIELDS), np.int64)
+            recs = np.zeros(n * rec_cap, REC_DTYPE)
+            pexp = np.zeros(n * pe_cap, np.int32)
+            rc = lib().esim_sweep_plan_run(plan, C.addressof(counters), per_layer.ctypes.data, recs.ctypes.data,
+                                           pexp.ctypes.data)
+            assert rc == 0, lib().esim_last_error()
+            for i, (c, cfg) in enumerate(zip(cs, cfgs)):
+                ctr = counters[i]
+                log = decode_records(recs[i * rec_cap:i * rec_cap + ctr.n_recs], pexp[i * pe_cap:(i + 1) * pe_cap])
+                canon = [canon_reference_record(x) for x in log]
+                assert digest_records(canon) == c["log_sha256"], c["name"]
+                rep = report_from_counters(cfg.echo(), cfg.model.num_layers, cfg.hardware.per_layer_compute_us, ctr,
+                                           per_layer[i][:cfg.model.num_layers])
+                assert json.dumps(rep) == json.dumps(c["report"]), c["name"]
+    finally:
+        lib().esim_sweep_plan_destroy(plan)
