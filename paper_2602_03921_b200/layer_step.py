@@ -99,7 +99,7 @@ class LayerStepEngine:
         torch = self.torch
         g = torch.Generator(device="cuda").manual_seed(seed)
         per = self.expert_bytes // 2
-        chunk = 64
+        chunk = max(1, min(64, (2 << 30) // self.expert_bytes))     # <= ~2 GiB of bf16 per generated chunk
         for e0 in range(0, self.n_experts_total, chunk):
             n = min(chunk, self.n_experts_total - e0)
             w = (torch.randn(n * per, generator=g, device="cuda") * std).to(torch.bfloat16)

@@ -4,7 +4,8 @@ Qwen1.5-MoE-A2.7B shape (24 x 60, top-4, H=2048, I=1408 -> 17,301,504 B/expert)
 at 5 % capacity with expert substitution. Decisions are checked against the C
 oracle (test infrastructure) for the same config; TTFT / decode tok/s / host
 link measured with CUDA events.
-usage: python tools/layer_step_models.py [qwen15moe] [miss] [capacity_fraction]"""
+usage: python tools/layer_step_models.py [model] [miss] [capacity_fraction,...] [policies] [decode_tokens]
+Mixtral (configs[2]): 32 x 8 top-2, H=4096, I=14336, 352,321,536 B/expert -> a 90 GB pinned store."""
 import json, sys, time
 sys.path.insert(0, ".")
 import torch
@@ -14,37 +15,45 @@ from oracle import oracle
 
 model = sys.argv[1] if len(sys.argv) > 1 else "qwen15moe"
 miss = sys.argv[2] if len(sys.argv) > 2 else "subst"
-frac = float(sys.argv[3]) if len(sys.argv) > 3 else 0.05
-H, I = {"qwen15moe": (2048, 1408), "olmoe": (2048, 1024)}[model]
+fracs = [float(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "0.05").split(",")]
+pols = (sys.argv[4] if len(sys.argv) > 4 else "ls,lru").split(",")
+n_dec = int(sys.argv[5]) if len(sys.argv) > 5 else 64
+H, I = {"qwen15moe": (2048, 1408), "olmoe": (2048, 1024), "mixtral": (4096, 14336)}[model]
 spec = builtin_spec(model)
-tr = generate_synthetic(spec, seed=1, prefill_tokens=64, decode_tokens=64)
+tr = generate_synthetic(spec, seed=1, prefill_tokens=64, decode_tokens=n_dec)
 g = torch.Generator().manual_seed(0)
 x0 = torch.randn(64, H, generator=g).to(torch.bfloat16).pin_memory()
-xd = torch.randn(64, H, generator=g).to(torch.bfloat16).pin_memory()
-out = {"model": model, "H": H, "I": I, "expert_bytes_bf16": 3 * H * I * 2, "miss": miss, "capacity_fraction": frac}
+xd = torch.randn(n_dec, H, generator=g).to(torch.bfloat16).pin_memory()
+out = {"model": model, "H": H, "I": I, "expert_bytes_bf16": 3 * H * I * 2, "miss": miss,
+       "trace": f"64 prefill + {n_dec} decode tokens, seed 1"}
 eng = None
 t0 = time.time()
-for ev in ("ls", "lru"):
+runs = 2 if model != "mixtral" else 1
+for frac in fracs:
+  for ev in pols:
     cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_fraction=frac), working_precision="fp16",
                     eviction=ev, prefetch="score", percentile=80.0, miss=miss, subst_tolerance=0.05)
     if eng is None:
-        eng = LayerStepEngine(cfg, H, I, max_tokens=64)
+        # slots for the largest capacity; smaller ones use a prefix (the decisions bound the live slots)
+        big = SimConfig(model=spec, hardware=HardwareSpec(capacity_fraction=max(fracs)), working_precision="fp16",
+                        eviction=ev, prefetch="score", percentile=80.0, miss=miss)
+        eng = LayerStepEngine(big, H, I, max_tokens=64)
         eng.init_weights(seed=0)
-        out["n_slots"] = eng.n_slots
+        out["n_slots_allocated"] = eng.n_slots
         out["store_gb"] = eng.expert_bytes * eng.n_experts_total / 1e9
         out["init_s"] = time.time() - t0
     eng.cfg = cfg
     best = None
-    for _ in range(2):
+    for _ in range(runs):
         r = eng.run(tr, x0, xd)
         best = r if best is None or r.total_ms < best.total_ms else best
     ref = oracle.run(cfg, tr, full_log=False).report
-    out[ev] = {"ttft_ms": best.ttft_ms, "decode_tok_s": best.decode_tokens_per_sec, "total_ms": best.total_ms,
+    out[f"{ev}@{frac}"] = {"n_slots": cfg.capacity_bytes() // spec.expert_bytes("fp16"), "ttft_ms": best.ttft_ms, "decode_tok_s": best.decode_tokens_per_sec, "total_ms": best.total_ms,
                "host_link_gbs": best.h2d_gbs, "copies": best.n_copies, "ffn_batches": best.n_ffn_batches,
                "logical_hit_rate": best.report["rates"]["hit_rate"],
                "substituted": best.report["totals"].get("substituted"),
                "decisions_match_oracle": json.dumps(ref) == json.dumps(best.report)}
-    print(ev, out[ev], flush=True)
+    print(ev, frac, out[f"{ev}@{frac}"], flush=True)
 eng.close()
 json.dump(out, open(f"gpurun_out/layer_step_{model}_{miss}.json", "w"), indent=1)
 print(json.dumps(out))
