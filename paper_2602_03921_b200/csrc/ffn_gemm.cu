@@ -197,7 +197,7 @@ struct FfnSmem {
 };
 
 struct FfnArgs {
-    const CUtensorMap* w1_maps;      // [n_slots]: tile-major [2I/64][H/64][64][64] as 2-D [2IH/64][64], box 64 rows
+    const CUtensorMap* w1_maps;      // [n_slots]: tile-major [I/64][H/64][64 gate + 64 up][64] as 2-D [2IH/64][64], box 128 rows
     const CUtensorMap* w2_maps;      // [n_slots]: tile-major [I/64][H/128][128][64] as 2-D [IH/64][64], box 128 rows
     const CUtensorMap* x_map;        // gathered tokens [n_exec*NPAD rows, H cols], box NPAD rows
     const CUtensorMap* act_map;      // [n_exec*NPAD rows, I cols], box NPAD rows
@@ -267,8 +267,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_fused_kernel(const __grid_
                         const int st = k_all % STAGES;
                         if (k_all >= STAGES) mbar_wait(&s.empty[st], ((k_all / STAGES) - 1) & 1);
                         mbar_expect_tx(&s.full[st], ffn_stage_bytes(NPAD));
-                        tma_load_2d(s.a[st], wm, &s.full[st], 0, (x.tile * KT + k) * 64);                    // gate
-                        tma_load_2d(s.a[st] + 64 * BK, wm, &s.full[st], 0, ((g.I / 64 + x.tile) * KT + k) * 64);  // up
+                        tma_load_2d(s.a[st], wm, &s.full[st], 0, (x.tile * KT + k) * BM);    // [64 gate; 64 up] rows
                         tma_load_2d(s.b[st], g.x_map, &s.full[st], k * BK, x.e * NPAD);
                     }
                 } else {
@@ -483,8 +482,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_decode_kernel(const __grid
                     const int st = k_all % STAGES;
                     if (k_all >= STAGES) mbar_wait(&s.empty[st], ((k_all / STAGES) - 1) & 1);
                     mbar_expect_tx(&s.full[st], A_BYTES + B_BYTES);
-                    tma_load_2d(s.a[st], w1, &s.full[st], 0, (mt * KT + k) * 64);
-                    tma_load_2d(s.a[st] + 64 * BK, w1, &s.full[st], 0, ((g.I / 64 + mt) * KT + k) * 64);
+                    tma_load_2d(s.a[st], w1, &s.full[st], 0, (mt * KT + k) * BM);          // [64 gate; 64 up] rows
                     tma_load_2d(s.b[st], g.x_map, &s.full[st], k * BK, e * NPAD);
                 }
                 for (int ht = 0; ht < n_ht; ht++, k_all++) {

@@ -146,7 +146,7 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
     for (int s = 0; s < p->n_slots; s++) {
         const char* base = g->slots + g->expert_bytes * s;
         // tile-major expert layout (ffn.py): every TMA box is one contiguous run
-        if (esim_tmap_bf16(&m1[128 * s], base, (int64_t)2 * I * H / 64, 64, 64) ||
+        if (esim_tmap_bf16(&m1[128 * s], base, (int64_t)2 * I * H / 64, 64, 128) ||
             esim_tmap_bf16(&m2[128 * s], base + (size_t)2 * I * H * 2, (int64_t)I * H / 64, 64, 128))
             return ls_fail(-3, "tensor map encode failed");
     }

@@ -2,8 +2,9 @@
 
 Each cache slot holds one expert in the TILE-MAJOR layout the kernels stream
 with TMA (every TMA box is one contiguous run of HBM, so weight streaming is
-sequential 8-16 KB bursts instead of 128-byte pieces of 4 KB-strided rows):
-    w1 = [gate; up] (logical [2*I, H], K = H) as tiles [2I/64][H/64][64][64]
+sequential 16 KB bursts instead of 128-byte pieces of 4 KB-strided rows):
+    w1 = [gate; up] (logical [2*I, H], K = H) as tiles [I/64][H/64][128][64]:
+         tile (m, k) = gate rows 64m..64m+63 then up rows 64m..64m+63, K cols 64k..
     w2 = down       (logical [H, I],   K = I) as tiles [I/64][H/128][128][64]
 3*H*I*2 bytes (12,582,912 B for OLMoE-1B-7B: H=2048, I=1024), the same bytes
 a host->HBM fetch moves (the pinned store uses the same layout; the tiling is
@@ -51,7 +52,7 @@ class ExpertSlots:
         self.expert_bytes = 2 * self.expert_elems
         self.buf = torch.empty(n_slots * self.expert_elems, dtype=torch.bfloat16, device="cuda")
         base = self.buf.data_ptr()
-        w1 = b"".join(tmap(base + s * self.expert_bytes, 2 * inter * hidden // 64, 64, 64) for s in range(n_slots))
+        w1 = b"".join(tmap(base + s * self.expert_bytes, 2 * inter * hidden // 64, 64, 128) for s in range(n_slots))
         w2 = b"".join(tmap(base + s * self.expert_bytes + 2 * 2 * inter * hidden, inter * hidden // 64, 64, 128)
                       for s in range(n_slots))
         self.w1_maps = torch.frombuffer(bytearray(w1), dtype=torch.uint8).cuda()
@@ -100,7 +101,8 @@ def expert_matrices(flat, hidden: int, inter: int):
     """Logical (w1 [2I, H], wd [H, I]) views-turned-copies of one expert stored
     tile-major (see the module docstring); `flat` is the expert's 3*H*I elements."""
     H, I = hidden, inter
-    w1 = flat[:2 * I * H].reshape(2 * I // 64, H // 64, 64, 64).permute(0, 2, 1, 3).reshape(2 * I, H)
+    t = flat[:2 * I * H].reshape(I // 64, H // 64, 2, 64, 64)          # [m][k][gate/up][row][col]
+    w1 = t.permute(2, 0, 3, 1, 4).reshape(2 * I, H)
     wd = flat[2 * I * H:].reshape(I // 64, H // 128, 128, 64).permute(1, 2, 0, 3).reshape(H, I)
     return w1, wd
 
