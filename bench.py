@@ -44,6 +44,14 @@ def env_int(name, default):
     return int(os.environ.get(name, default))
 
 
+def bench_config(seeds: int, points: int) -> dict:
+    """The workload both arms measure (BASELINE.json configs[4])."""
+    return {"workload": "c5_policy_sweep_replay", "trace_shapes": list(MODELS),
+            "grid": "eviction{lru,lfu,ls} x capacity{0.01,0.05,0.25} x bandwidth{1,5,25}GB/s",
+            "policy": "score:80 + fetch + int4", "traces": "64 prefill + 64 decode, affinity 0.6 skew 1.0",
+            "seeds_per_rank": seeds, "points_per_rank": points}
+
+
 def make_traces(seeds):
     from paper_2602_03921_b200.models import builtin_spec
     from paper_2602_03921_b200.trace import generate_synthetic
@@ -198,8 +206,7 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": value, "unit": "accesses/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64+f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "c5_policy_sweep_replay", "models": list(MODELS), "grid": "3x3x3 per model",
-                       "seeds": args.seeds, "points": 108 * args.seeds},
+            "config": dict(bench_config(args.seeds, 108 * args.seeds), parallelism=f"{threads} host threads"),
             "cpu_baseline": {"value": value, "unit": "accesses/s", "cores": threads, "kind": "port",
                              "sample": f"C5 grid x {args.seeds} seeds ({acc} demanded accesses) per step"},
             "e2e": {"value": value, "unit": "accesses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -326,11 +333,8 @@ def main():
         "metric": METRIC, "value": value, "unit": "accesses/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64+f32", "data": "synthetic",
-        "config": {"workload": "c5_policy_sweep_replay", "models": list(MODELS),
-                   "grid": "eviction{lru,lfu,ls} x capacity{0.01,0.05,0.25} x bandwidth{1,5,25}GB/s",
-                   "policy": "score:80 + fetch + int4", "traces": "64 prefill + 64 decode, affinity 0.6 skew 1.0",
-                   "seeds_per_rank": args.seeds, "points_per_rank": n_pts, "parallelism": f"grid-shard x{world}",
-                   "l2": "flushed between steps (256 MiB memset, untimed)"},
+        "config": dict(bench_config(args.seeds, n_pts), parallelism=f"grid-shard x{world}",
+                       l2="flushed between steps (256 MiB memset, untimed)"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "kernel": "replay_kernel", "algorithmic_bytes_per_access": REPLAY_BYTES_PER_ACCESS,
