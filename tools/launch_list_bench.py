@@ -9,11 +9,9 @@ ki, vi, ui, ii, gi = (h.index(x) for x in ("Kernel Name", "Metric Value", "Metri
 sc = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 launches = [(r[ki].split("(")[0], r[gi], float(r[vi].replace(",", "")) * sc[r[ui]]) for r in rows[hi + 1:]
             if len(r) > vi and "at::" not in r[ki]]
-per_step = [l for l in launches if "replay_kernel" in l[0] or "classify" in l[0] or
-            ("router_persistent" in l[0] and l[1] != launches[0][1]) or "route_totals" in l[0]]
-# the timed steps are the tail: 3 router kernels + the replay groups, per step
-n_replay = sum(1 for l in launches[-40:] if "replay_kernel" in l[0]) // max(1, min(steps, 2))
-tail = launches[-steps * (3 + n_replay):]
+# the timed steps are the tail: each step starts with classify_kernel (the batched router)
+starts = [i for i, l in enumerate(launches) if "classify" in l[0]]
+tail = launches[starts[-steps]:]
 agg = collections.defaultdict(lambda: [0, 0.0])
 for k, g, t in tail:
     agg[k][0] += 1
