@@ -323,10 +323,12 @@ def main():
     peaks, peak_kind = measured_peaks()
     rms = sum(replay_ms) / len(replay_ms)
     achieved = REPLAY_BYTES_PER_ACCESS * acc_local / (rms / 1e3) / 1e9
-    traffic = None
+    traffic, winst = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "replay_traffic.json")) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_step")
+            prof = json.load(fh)
+        if args.seeds == 48:                       # the profiled workload
+            traffic, winst = prof.get("dram_bytes_per_step"), prof.get("warp_instructions_per_step")
     except OSError:
         pass
     line = {
@@ -339,6 +341,13 @@ def main():
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "kernel": "replay_kernel", "algorithmic_bytes_per_access": REPLAY_BYTES_PER_ACCESS,
                      "peak_source": peak_kind},
+        # the replay is a serial state machine per grid point: its real ceiling is
+        # instruction issue (148 SMs x 4 schedulers x 1 warp-instruction / clock)
+        "roofline_issue": None if winst is None else {
+            "bound": "issue", "achieved": winst / (rms / 1e3),
+            "peak": 148 * 4 * peaks.get("sm_max_mhz", 1965.0) * 1e6, "unit": "warp-instructions/s",
+            "frac": winst / (rms / 1e3) / (148 * 4 * peaks.get("sm_max_mhz", 1965.0) * 1e6),
+            "instructions_per_access": winst / acc_local, "source": "profiles/replay_traffic.json (ncu)"},
         "gpu_launches": args.steps * (ds.n_router_launches + ds.n_replay_launches),
         "kernel_ms": {"router": sum(route_ms) / len(route_ms), "replay": rms},
         "wall_s_timed_region": t_wall,
