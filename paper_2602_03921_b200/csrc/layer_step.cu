@@ -69,10 +69,11 @@ __global__ void build_tables_kernel(const int16_t* __restrict__ row_sel, const f
     for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
         const int pos = pos_of_expert[row_sel[i]];
         if (pos < 0) continue;
-        const int slot = atomicAdd(&fill[pos], 1);
-        if (slot < npad) {
-            tok_index[pos * npad + slot] = i / K;
-            tok_weight[pos * npad + slot] = row_w[i];
+        const int f = atomicAdd(&fill[pos], 1);        // the expert's f-th token -> entry pos + f / npad
+        const int e = pos + f / npad, c = f % npad;     // (npad == 128 whenever an expert is split)
+        if (e < n_exec) {
+            tok_index[e * npad + c] = i / K;
+            tok_weight[e * npad + c] = row_w[i];
         }
     }
 }
@@ -106,6 +107,7 @@ struct Engine {
     int64_t* progress = nullptr;
     int32_t* tables = nullptr;           // pool of [2][E] int32 (pos_of_expert, exec_slot) per flush
     int64_t table_cap = 0;
+    int max_entries = 0;                 // FFN entries per flush: experts + token-count splits at 128
     // per-run device scratch
     void* dev_scratch = nullptr;
     size_t dev_scratch_bytes = 0;
@@ -138,7 +140,12 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
     Engine* g = new Engine();
     g->P = *p;
     const int L = p->num_layers, E = p->experts, H = p->hidden, I = p->inter;
-    if (H % 128 || I % 128 || p->max_tokens > 128 || p->n_slots < 1) { delete g; return ls_fail(-1, "bad layer-step geometry"); }
+    if (H % 128 || I % 128 || p->max_tokens < 1 || p->max_tokens > 16384 || p->n_slots < 1) {
+        delete g;
+        return ls_fail(-1, "bad layer-step geometry");
+    }
+    // an expert with more than 128 tokens in a pass runs as several FFN entries of <= 128
+    g->max_entries = E + (int)(((int64_t)p->max_tokens * p->top_k + 127) / 128);
     g->expert_bytes = (size_t)3 * H * I * 2;
     CK(cudaHostAlloc(&g->store, g->expert_bytes * L * E, cudaHostAllocDefault));
     CK(cudaMalloc((void**)&g->slots, g->expert_bytes * p->n_slots));
@@ -154,13 +161,13 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
     CK(cudaMalloc(&g->w2_maps, m2.size()));
     CK(cudaMemcpy(g->w1_maps, m1.data(), m1.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->w2_maps, m2.data(), m2.size(), cudaMemcpyHostToDevice));
-    const size_t maxrows = (size_t)E * 128;
+    const size_t maxrows = (size_t)g->max_entries * 128;
     CK(cudaMalloc(&g->xg, maxrows * H * 2));
     CK(cudaMalloc(&g->act, maxrows * I * 2));
     for (int i = 0; i < 4; i++) {
         unsigned char mx[128], ma[128];
-        if (esim_tmap_bf16(mx, g->xg, (int64_t)E * NPADS[i], H, NPADS[i]) ||
-            esim_tmap_bf16(ma, g->act, (int64_t)E * NPADS[i], I, NPADS[i]))
+        if (esim_tmap_bf16(mx, g->xg, (int64_t)g->max_entries * NPADS[i], H, NPADS[i]) ||
+            esim_tmap_bf16(ma, g->act, (int64_t)g->max_entries * NPADS[i], I, NPADS[i]))
             return ls_fail(-3, "tensor map encode failed");
         CK(cudaMalloc(&g->x_maps[i], 128));
         CK(cudaMalloc(&g->act_maps[i], 128));
@@ -263,7 +270,7 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     CK(cudaHostAlloc((void**)&g->progress, (n_events + 2) * 8, cudaHostAllocMapped));
     volatile int64_t* prog = g->progress;
     for (int64_t i = 0; i < n_events + 2; i++) prog[i] = 0;
-    const int64_t table_need = (n_events * 2 + 64) * 2 * E;
+    const int64_t table_need = (n_events * 2 + 64) * (E + g->max_entries);
     if (table_need > g->table_cap) {
         if (g->tables) cudaFreeHost(g->tables);
         CK(cudaHostAlloc((void**)&g->tables, table_need * 4, cudaHostAllocMapped));
@@ -348,13 +355,13 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             for (int t : tok_of_pos) maxtok = std::max(maxtok, t);
             const int npad = npad_for(std::max(1, maxtok));
             if (npad < 0) return ls_fail(-1, "too many tokens per expert");
-            if (table_next + 2 * E > g->table_cap) {                                 // recycle the pool
+            if (table_next + E + g->max_entries > g->table_cap) {                 // recycle the pool
                 CK(cudaStreamSynchronize(g->comp_st));
                 table_next = 0;
             }
             int32_t* tpos = g->tables + table_next;
             int32_t* tslot = tpos + E;
-            table_next += 2 * E;
+            table_next += E + g->max_entries;
             for (int e = 0; e < E; e++) tpos[e] = pos_of_expert[e];
             for (int i = 0; i < n_exec; i++) tslot[i] = pend_slot[i];
             for (int i = 0; i < n_exec; i++) CK(cudaStreamWaitEvent(g->comp_st, g->landed[pend_slot[i]], 0));
@@ -380,11 +387,15 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     // one FFN entry per executed expert; a substitute serving several missing
     // experts appears once per expert (same slot, separate token lists), so
     // no entry ever holds more than one expert's tokens
+    // (more than 128 tokens: consecutive entries of 128 on the same slot)
     auto execute = [&](int expert, int slot, int tokens) {
         slot_pending[slot] = 1;
         pos_of_expert[expert] = (int)pend_slot.size();
-        pend_slot.push_back(slot);
-        tok_of_pos.push_back(tokens);
+        do {
+            pend_slot.push_back(slot);
+            tok_of_pos.push_back(std::min(tokens, 128));
+            tokens -= 128;
+        } while (tokens > 0);
     };
 
     for (int64_t ev = 0; ev < n_events; ev++) {

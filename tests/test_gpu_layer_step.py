@@ -38,10 +38,9 @@ def _reference(engine, trace, x0, xdec, served=None, I=1024):
                 act = (torch.nn.functional.silu(x.to(torch.bfloat16).float() @ w1[:I].T) *
                        (x.to(torch.bfloat16).float() @ w1[I:].T)).to(torch.bfloat16).float()
                 out = act @ wd.T
-                for t in range(x.shape[0]):
-                    for j in range(spec.top_k):
-                        if idx[t, j] == e:
-                            y[t] += float(sc[t, e]) * out[t]
+                wt = torch.tensor(np.where((idx == e).any(axis=1), sc[:, e], 0.0), dtype=torch.float32,
+                                  device=out.device)
+                y += wt[:, None] * out
             x = (x.to(torch.bfloat16).float() + y).to(torch.bfloat16).float()
         outs.append(x)
     return torch.cat(outs)
@@ -51,6 +50,16 @@ def _reference(engine, trace, x0, xdec, served=None, I=1024):
                                                              ("ls", 3, "fetch", 1024), ("ls", 5, "fetch", 1408),
                                                              ("ls", 5, "subst", 1408), ("lru", 4, "drop", 1024)])
 def test_layer_step_matches_nocache_reference(eviction, cap_experts, miss, inter, oracle_lib):
+    _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts=16, top_k=4, prefill=8, decode=3)
+
+
+def test_layer_step_long_prefill_splits_experts(oracle_lib):
+    """A 300-token prefill over 8 experts (top-4: ~150 tokens per expert): an
+    expert with more than 128 tokens runs as several FFN entries."""
+    _run_case("ls", 4, "fetch", 1024, oracle_lib, experts=8, top_k=4, prefill=300, decode=2)
+
+
+def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, prefill, decode):
     """I = 1408 is the Qwen1.5-MoE expert width (not a power of two); subst /
     drop follow the decision stream (substitute weights / no contribution)."""
     import torch
@@ -58,16 +67,16 @@ def test_layer_step_matches_nocache_reference(eviction, cap_experts, miss, inter
     from paper_2602_03921_b200.layer_step import LayerStepEngine
     I = inter
     eb = 3 * H * I * 2
-    spec = ModelSpec("mini_moe", num_layers=4, experts_per_layer=16, top_k=4, expert_bytes_fp16=eb)
+    spec = ModelSpec("mini_moe", num_layers=4, experts_per_layer=experts, top_k=top_k, expert_bytes_fp16=eb)
     cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=cap_experts * eb), working_precision="fp16",
                     eviction=eviction, prefetch="score", percentile=80.0, miss=miss, subst_tolerance=0.2,
                     drop_rank_threshold=2)
-    tr = generate_synthetic(spec, seed=7, prefill_tokens=8, decode_tokens=3)
-    eng = LayerStepEngine(cfg, H, I, max_tokens=8)
+    tr = generate_synthetic(spec, seed=7, prefill_tokens=prefill, decode_tokens=decode)
+    eng = LayerStepEngine(cfg, H, I, max_tokens=prefill)
     eng.init_weights(seed=3)
     g = torch.Generator().manual_seed(1)
-    x0 = torch.randn(8, H, generator=g).to(torch.bfloat16).pin_memory()
-    xd = torch.randn(3, H, generator=g).to(torch.bfloat16).pin_memory()
+    x0 = torch.randn(prefill, H, generator=g).to(torch.bfloat16).pin_memory()
+    xd = torch.randn(decode, H, generator=g).to(torch.bfloat16).pin_memory()
     res = eng.run(tr, x0, xd, keep_outputs=True)
     o = oracle_lib.run(cfg, tr, full_log=True)
     assert json.dumps(o.report) == json.dumps(res.report)

@@ -7,14 +7,18 @@ import numpy as np, torch
 from paper_2602_03921_b200.ffn import ExpertSlots, npad_for, routing_tables
 H, I = 2048, 1024
 out = {}
-slots = ExpertSlots(64, H, I, max_tokens=64, max_exec=64)
+slots = ExpertSlots(64, H, I, max_tokens=1024, max_exec=64)
 slots.buf.copy_((torch.randn(slots.buf.numel(), device="cuda") * 0.02).to(torch.bfloat16))
 flush = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if __import__("os").path.exists("MEASURED_PEAKS.json") else 6650.0
-for name, T, K, n_exp in (("prefill64", 64, 8, 28), ("decode", 1, 8, 8), ("prefill64_all64", 64, 8, 64)):
+for name, T, K, n_exp in (("prefill64", 64, 8, 28), ("decode", 1, 8, 8), ("prefill64_all64", 64, 8, 64),
+                          ("prefill1024_128tok_all64", 1024, 8, 64)):
     rng = np.random.default_rng(0)
     x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
-    row_sel = np.stack([rng.choice(n_exp, size=K, replace=False) for _ in range(T)]).astype(np.int32)
+    if T * K == 128 * n_exp:       # every expert exactly 128 tokens (the largest tile, N = 128)
+        row_sel = (np.arange(T * K) % n_exp).reshape(T, K).astype(np.int32)
+    else:
+        row_sel = np.stack([rng.choice(n_exp, size=K, replace=False) for _ in range(T)]).astype(np.int32)
     row_w = rng.uniform(0.01, 0.3, size=(T, K)).astype(np.float32)
     mt = int(np.bincount(row_sel.ravel()).max())
     npad = npad_for(mt)
