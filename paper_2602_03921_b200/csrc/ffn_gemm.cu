@@ -177,7 +177,9 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 // Warps: 0 TMA producer, 1 MMA issuer, 2-5 epilogue (TMEM lane quarter w % 4).
 constexpr int kFfnThreads = 192;
 
-__host__ __device__ constexpr int ffn_xchg_bytes(int npad) { return 64 * npad * 4 + npad * 128; }  // + act tile
+__host__ __device__ constexpr int ffn_xchg_bytes(int npad) {   // xchg + act tile + scatter staging
+    return 64 * npad * 4 + npad * 128 + 4 * 16 * 36 * 4;
+}
 __host__ __device__ constexpr int ffn_stage_bytes(int npad) { return (BM * BK + npad * BK) * 2; }
 __host__ __device__ constexpr int ffn_stages(int npad) {
     return (220 * 1024 - ffn_xchg_bytes(npad)) / ffn_stage_bytes(npad) > 12
@@ -192,6 +194,7 @@ struct FfnSmem {
     alignas(1024) __nv_bfloat16 b[STAGES][NPAD * BK];
     alignas(1024) __nv_bfloat16 act_tile[NPAD * 64];   // act box [NPAD tokens][64 rows], 128B-swizzled (TMA store)
     float xchg[64][NPAD];                 // up-row accumulators -> the gate-row threads
+    alignas(16) float red[4][16][36];     // per epilogue warp: 16 tokens x 32 rows, transposed for v4 reductions
     uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
     uint32_t tmem;
 };
@@ -392,17 +395,35 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_fused_kernel(const __grid_
                     if (g.trace) g.trace[8 * u + 3] = gtimer();
                 }
             } else {
-                const int h = x.tile * BM + row;
+                // y[t][h] += w * v: the warp's 32 rows x 16 token columns are transposed
+                // through smem so each lane issues 4-wide vector reductions
+                // (red.global.add.v4.f32) over 4 consecutive rows of one token
+                float (*rb)[36] = s.red[warp - 2];
+                const int hbase = x.tile * BM + q * 32;
                 for (int c0 = 0; c0 < ncol; c0 += 16) {
                     float v[16];
                     tmem_ld16(taddr + c0, v);
 #pragma unroll
                     for (int jj = 0; jj < 16; jj++) {
                         const int c = c0 + jj;
-                        const int t = __shfl_sync(0xffffffffu, tiv[c >> 5], c & 31);
                         const float w = __shfl_sync(0xffffffffu, twv[c >> 5], c & 31);
-                        if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], w * v[jj]);
+                        rb[jj][lane] = w * v[jj];
                     }
+                    __syncwarp();
+#pragma unroll
+                    for (int r = 0; r < 4; r++) {
+                        const int pr = lane + 32 * r, jj = pr >> 3, h4 = (pr & 7) * 4;
+                        const int c = c0 + jj;
+                        const int t = __shfl_sync(0xffffffffu, tiv[c >> 5], c & 31);
+                        if (t >= 0) {
+                            const float4 a = *reinterpret_cast<const float4*>(&rb[jj][h4]);
+                            float* dst = g.y + (size_t)t * g.H + hbase + h4;
+                            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a.x),
+                                         "f"(a.y), "f"(a.z), "f"(a.w)
+                                         : "memory");
+                        }
+                    }
+                    __syncwarp();
                 }
                 tc_fence_before();
                 __syncwarp();
