@@ -237,6 +237,10 @@ class DeviceSweep:
     def replay(self, stream=None) -> None:
         self.batch.launch(stream)
 
+    def tune_order(self) -> None:
+        """Longest-measured replays first in every launch group (see ReplayBatch.tune_order)."""
+        self.batch.tune_order()
+
     def step(self, stream=None) -> None:
         self.route(stream)
         self.replay(stream)
