@@ -8,6 +8,7 @@ S = int(sys.argv[1]) if len(sys.argv) > 1 else 48
 cfgs, trs = c5_points(make_traces(list(range(1, S + 1))))
 ds = DeviceSweep(cfgs, trs)
 ds.step(); torch.cuda.synchronize()
+ds.tune_order(); ds.step(); torch.cuda.synchronize()
 for name, fn in (("route", ds.route), ("replay", ds.replay)):
     ts = []
     for _ in range(5):

@@ -6,6 +6,7 @@ from paper_2602_03921_b200.sweep import DeviceSweep, c5_points
 cfgs, trs = c5_points(make_traces(list(range(1, 49))))
 ds = DeviceSweep(cfgs, trs)
 ds.step(); torch.cuda.synchronize()
+ds.tune_order(); ds.step(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); ds.replay(); e1.record(); torch.cuda.synchronize()
 res = ds.results()
