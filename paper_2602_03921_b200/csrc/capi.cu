@@ -24,7 +24,8 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
-                                    int policy, bool general, const int32_t* out_index = nullptr);
+                                    int policy, bool general, const int32_t* out_index = nullptr,
+                                    bool log_rt = true);
 int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt);
 
 static thread_local std::string g_err;
@@ -84,14 +85,14 @@ extern "C" int esim_router_launch(const EsimTraceDesc* tr, const EsimRouterOut* 
     return 0;
 }
 
-struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca, has_cnt; int policy; bool general; };
+struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca, has_cnt; int policy; bool general; bool log_rt; };
 
 // queue_cap <= 0: the exact bound (resident slots + 1 entries: every queued
 // transfer holds a reservation of >= the smallest expert, so the channel can
 // never outgrow it). A positive cap trades shared memory for the risk of
 // status -5, which the caller resolves by re-launching with the bound.
 static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stride, int queue_cap, Sizing* z) {
-    Sizing s{0, 1, 2, 0, 0, 0, 0, false, false, n > 0 ? h[0].eviction : 0, false};
+    Sizing s{0, 1, 2, 0, 0, 0, 0, false, false, n > 0 ? h[0].eviction : 0, false, false};
     for (int i = 0; i < n; i++) {
         const EsimConfig& c = h[i];
         if (c.experts > ESIM_MAX_E || c.top_k > ESIM_MAX_K) return fail(-1, "geometry exceeds device limits");
@@ -113,6 +114,7 @@ static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stri
         if (c.eviction == ESIM_EV_LFU || c.eviction == ESIM_EV_LHU) s.has_cnt = true;
         if (c.eviction != s.policy) return fail(-1, "one replay launch replays one eviction policy (group the points)");
         if (c.miss != ESIM_MISS_FETCH || c.routing != ESIM_ROUTE_STANDARD) s.general = true;
+        if (c.flags & (ESIM_FLAG_FULL_LOG | ESIM_FLAG_NO_DIGEST)) s.log_rt = true;   // else: digest-only kernel
     }
     if (s.S > 4095) return fail(-1, "more than 4095 resident experts per cache is not supported by the device directory");
     s.Q = queue_cap > 0 ? std::min(queue_cap, s.S + 1) : s.S + 1;
@@ -148,7 +150,8 @@ extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_c
                                               std::to_string(per) + " B)");
     cudaError_t e = esim_replay_launch_impl(d_cfg, n, d_traces, d_routers, d_counters, d_per_layer, d_recs, rec_cap,
                                             d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
-                                            w, (cudaStream_t)stream, nullptr, z.policy, z.general);
+                                            w, (cudaStream_t)stream, nullptr, z.policy, z.general, nullptr,
+                                            z.log_rt);
     if (e != cudaSuccess) return cuda_fail(e, "replay launch");
     return 0;
 }
@@ -163,7 +166,8 @@ int esim_replay_launch_streamed(const EsimConfig* h_cfg, const EsimConfig* d_cfg
     if (rc) return rc;
     cudaError_t e = esim_replay_launch_impl(d_cfg, 1, d_traces, d_routers, d_counters, d_per_layer, d_recs, rec_cap,
                                             d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
-                                            1, (cudaStream_t)stream, progress, z.policy, z.general);
+                                            1, (cudaStream_t)stream, progress, z.policy, z.general, nullptr,
+                                            z.log_rt);
     if (e != cudaSuccess) return cuda_fail(e, "streamed replay launch");
     return 0;
 }
@@ -427,7 +431,7 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
                                     (int64_t*)(base + P->pl_off), full ? (EsimRec*)(base + P->rec_off) : nullptr,
                                     P->rec_cap, full ? (int32_t*)(base + P->pe_off) : nullptr, P->pe_cap, z.N, z.S,
                                     z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt, w, P->gs[g], nullptr, z.policy,
-                                    z.general, (int32_t*)(base + P->idx_off) + b);
+                                    z.general, (int32_t*)(base + P->idx_off) + b, z.log_rt);
         if (e != cudaSuccess) return cuda_fail(e, "replay launch");
         cudaEventRecord(P->ge[g], P->gs[g]);
         cudaStreamWaitEvent(P->st, P->ge[g], 0);

@@ -982,7 +982,9 @@ DFI int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int
 // POL: eviction policy; GEN: 0 = the common case (miss=fetch, standard routing) with every
 // other miss/routing path compiled out, 1 = all paths. Every helper is force-inlined, so the
 // compile-time policy/miss constants delete the other policies' code from the kernel.
-template <int POL, int GEN>
+// LOG: 0 = digest only, no record log (compile-time: the log-writing code is gone
+// from the kernel), 1 = per-point runtime flags (full log and/or digest)
+template <int POL, int GEN, int LOG>
 __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB) replay_kernel(ReplayArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int wid = threadIdx.x >> 5;
@@ -1083,8 +1085,8 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     #pragma unroll
     for (int i = 0; i < 5; i++) p.pf_ev[i] = 0;
     p.err = 0;
-    p.full = (cfg->flags & ESIM_FLAG_FULL_LOG) && A.recs != nullptr;
-    p.digest_on = (cfg->flags & ESIM_FLAG_NO_DIGEST) == 0;
+    p.full = LOG ? ((cfg->flags & ESIM_FLAG_FULL_LOG) && A.recs != nullptr) : false;
+    p.digest_on = LOG ? (cfg->flags & ESIM_FLAG_NO_DIGEST) == 0 : true;
     p.recs = A.recs + orow * A.rec_cap;
     p.rec_cap = A.rec_cap;
     p.pexp = A.pexp + orow * A.pe_cap;
@@ -1316,7 +1318,7 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
-                                    int policy, bool general, const int32_t* out_index) {
+                                    int policy, bool general, const int32_t* out_index, bool log_rt) {
     esim::ReplayArgs a;
     a.progress = progress;
     a.out_index = out_index;
@@ -1331,7 +1333,8 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
     const int blocks = (n + warps_per_cta - 1) / warps_per_cta;
     void (*k)(esim::ReplayArgs) = nullptr;
 #define ESIM_PICK(P)                                                                   \
-    case P: k = general ? esim::replay_kernel<P, 1> : esim::replay_kernel<P, 0>; break;
+    case P: k = general ? esim::replay_kernel<P, 1, 1>                                 \
+                        : (log_rt ? esim::replay_kernel<P, 0, 1> : esim::replay_kernel<P, 0, 0>); break;
     switch (policy) {
         ESIM_PICK(ESIM_EV_LRU) ESIM_PICK(ESIM_EV_LFU) ESIM_PICK(ESIM_EV_LHU)
         ESIM_PICK(ESIM_EV_FLD) ESIM_PICK(ESIM_EV_SB) ESIM_PICK(ESIM_EV_LS)
