@@ -26,7 +26,7 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
                                     int policy, bool general, const int32_t* out_index = nullptr,
                                     bool log_rt = true);
-int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt);
+int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt, bool gen);
 
 static thread_local std::string g_err;
 
@@ -130,7 +130,7 @@ extern "C" int esim_replay_smem_per_point(const EsimConfig* h_cfg, int32_t n, in
     Sizing z;
     int rc = replay_sizing(h_cfg, n, max_tokens, pl_stride, queue_cap, &z);
     if (rc) return rc;
-    return esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt);
+    return esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt, z.general);
 }
 
 extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_cfg, int32_t n,
@@ -142,7 +142,7 @@ extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_c
     Sizing z;
     int rc = replay_sizing(h_cfg, n, max_tokens, pl_stride, queue_cap, &z);
     if (rc) return rc;
-    int per = esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt);
+    int per = esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt, z.general);
     const int budget = 227 * 1024;
     int w = warps_per_cta > 0 ? warps_per_cta : 4;
     while (w > 1 && per * w > budget) w--;
@@ -422,7 +422,7 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
         cudaStreamWaitEvent(P->gs[g], P->routed, 0);
         Sizing z;
         if ((rc = replay_sizing(P->pcfg.data() + b, m, P->max_tokens, P->pl_stride, 0, &z))) return rc;
-        const int per = esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt);
+        const int per = esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt, z.general);
         int w = 4;
         while (w > 1 && per * w > 227 * 1024) w--;
         if (per * w > 227 * 1024) return fail(-1, "replay state of one grid point exceeds shared memory");

@@ -86,18 +86,21 @@ struct Layout {
 
 __host__ __device__ inline int al8(int x) { return (x + 7) & ~7; }
 
+// gen = false (common-path kernels: uniform transfers, no substitution): the
+// per-entry submit/completion times and the recorded scores are never touched
+// and take no space
 __host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E, int T, int K, bool ca,
-                                              bool has_cnt) {
+                                              bool has_cnt, bool gen) {
     Layout l;
     int o = 0;
     l.key = o; o += al8(S * 8);
-    l.q_submit = o; o += al8(Q * 8);
-    l.q_comp = o; o += al8(Q * 8);
+    l.q_submit = o; o += al8(gen ? Q * 8 : 0);
+    l.q_comp = o; o += al8(gen ? Q * 8 : 0);
     l.dsum = o; o += al8(ca ? L * 8 : 0);
     l.ctr = o; o += al8((int)sizeof(Ctr));
     l.dem_summed = o; o += al8(ca ? E * 8 : 0);
     l.cnt = o; o += al8(has_cnt ? N * 4 : 0);
-    l.rscore = o; o += al8(S * 4);
+    l.rscore = o; o += al8(gen ? S * 4 : 0);
     l.q_score = o; o += al8(Q * 4);
     l.pl = o; o += al8(L * ESIM_PL_FIELDS * 4);
     l.demmask = o; o += al8(((E + 31) / 32) * 4);
@@ -581,7 +584,7 @@ DFI void settle(Pt& p) {                                                   // en
         if (p.lane == 0) {
             p.rs[ident] = rs_make(prec, slot);
             p.res_ident[slot] = (int16_t)ident;
-            p.rscore[slot] = score;
+            if (p.miss == ESIM_MISS_SUBST) p.rscore[slot] = score;   // recorded_score: read by subst only
             if (p.hist[ident] == -2) p.hist[ident] = -1;
         }
         __syncwarp();
@@ -683,7 +686,7 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
     if (rs_res(w)) {
         const int prec = rs_prec(w), slot = rs_slot(w);
         note_access(p, ident, slot, true, (double)gate, prec);
-        if (p.lane == 0) p.rscore[slot] = gate;
+        if (p.lane == 0 && p.miss == ESIM_MISS_SUBST) p.rscore[slot] = gate;
         __syncwarp();
         access_rec(p, expert, tokens, rank, 0, -1, 0, 0.0, prec, -1);
         return 0;
@@ -716,7 +719,7 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
         advance_to(p, comp);
         const int slot = rs_slot(p.rs[ident]);
         note_access(p, ident, slot, true, (double)gate, prec);
-        if (p.lane == 0) p.rscore[slot] = gate;
+        if (p.lane == 0 && p.miss == ESIM_MISS_SUBST) p.rscore[slot] = gate;
         __syncwarp();
         access_rec(p, expert, tokens, rank, 2, mclass, blocked, 0.0, prec, -1);
         return 2;
@@ -786,7 +789,7 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
     if (p.err) return -1;
     const int slot = rs_slot(p.rs[ident]);
     note_access(p, ident, slot, true, (double)gate, prec);
-    if (p.lane == 0) p.rscore[slot] = gate;
+    if (p.lane == 0 && p.miss == ESIM_MISS_SUBST) p.rscore[slot] = gate;
     __syncwarp();
     blocked = b;
     access_rec(p, expert, tokens, rank, 1, mclass, b, 0.0, prec, -1);
@@ -996,7 +999,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     const EsimRouterOut R = A.routers[cfg->trace_id];
     unsigned char* base = smem_raw + (size_t)wid * A.point_bytes;
     const bool ca = GEN && cfg->routing == ESIM_ROUTE_CACHE_AWARE;
-    const Layout lay = make_layout(A.N, A.S, A.Q, A.Lmax, A.Emax, A.Tmax, A.Kmax, A.Tmax > 0, A.has_cnt != 0);
+    const Layout lay = make_layout(A.N, A.S, A.Q, A.Lmax, A.Emax, A.Tmax, A.Kmax, A.Tmax > 0, A.has_cnt != 0, GEN != 0);
 
     long long t_begin;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
@@ -1309,8 +1312,8 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
 
 }  // namespace esim
 
-int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt) {
-    return esim::make_layout(N, S, Q, L, E, T, K, ca, has_cnt).total;
+int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt, bool gen) {
+    return esim::make_layout(N, S, Q, L, E, T, K, ca, has_cnt, gen).total;
 }
 
 cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTraceDesc* d_traces,
@@ -1328,7 +1331,7 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
     a.N = N; a.S = S; a.Q = Q; a.Lmax = Lmax; a.Emax = Emax; a.Tmax = Tmax; a.Kmax = Kmax;
     a.has_cnt = has_cnt ? 1 : 0;
     a.warps_per_cta = warps_per_cta;
-    a.point_bytes = esim::make_layout(N, S, Q, Lmax, Emax, Tmax, Kmax, Tmax > 0, has_cnt).total;
+    a.point_bytes = esim::make_layout(N, S, Q, Lmax, Emax, Tmax, Kmax, Tmax > 0, has_cnt, general).total;
     const size_t smem = (size_t)a.point_bytes * warps_per_cta;
     const int blocks = (n + warps_per_cta - 1) / warps_per_cta;
     void (*k)(esim::ReplayArgs) = nullptr;
