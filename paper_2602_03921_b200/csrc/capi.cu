@@ -474,6 +474,7 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
             const int st = (int)counters[i].status;
             return fail(st, st == -4 ? "record buffer too small"
                             : st == -1 ? "config error during replay (an expert exceeds the cache capacity)"
+                            : st == -7 ? "an LFU/LHU access count exceeded the device's 16-bit counters"
                                        : "runtime invariant broken during replay");
         }
     return 0;

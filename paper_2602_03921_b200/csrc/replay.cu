@@ -44,6 +44,7 @@ constexpr uint64_t FNV_OFFSET = 0xcbf29ce484222325ULL;
 constexpr uint64_t FNV_PRIME = 0x100000001b3ULL;
 constexpr uint64_t FNV_PRIME_MIX = 0xD6E8FEB86659FD93ULL;
 constexpr int STATUS_QUEUE_OVERFLOW = -5;
+constexpr int STATUS_COUNT_OVERFLOW = -7;          // an LFU/LHU access count outgrew 16 bits
 
 struct ReplayArgs {
     const EsimConfig* cfg;
@@ -99,7 +100,7 @@ __host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E,
     l.dsum = o; o += al8(ca ? L * 8 : 0);
     l.ctr = o; o += al8((int)sizeof(Ctr));
     l.dem_summed = o; o += al8(ca ? E * 8 : 0);
-    l.cnt = o; o += al8(has_cnt ? N * 4 : 0);
+    l.cnt = o; o += al8(has_cnt ? N * 2 : 0);      // 16-bit LFU/LHU access counts (host-checked bound)
     l.rscore = o; o += al8(gen ? S * 4 : 0);
     l.q_score = o; o += al8(Q * 4);
     l.pl = o; o += al8(L * ESIM_PL_FIELDS * 4);
@@ -148,7 +149,7 @@ struct Pt {
     double* dsum;
     Ctr* ctr;
     double* dem_summed_s;
-    int32_t* cnt;
+    uint16_t* cnt;                  // LFU / LHU access count per ident (< 65536: esim_replay_launch checks)
     float* rscore;
     float* q_score;
     int32_t* pl;
@@ -348,7 +349,8 @@ DFI void note_access(Pt& p, int ident, int slot, bool has_gate, double gate, int
     case ESIM_EV_LRU: set_key(p, slot, p.seq++); break;
     case ESIM_EV_LFU: case ESIM_EV_LHU: {
         const int step = (p.pol == ESIM_EV_LFU || prec == p.c->precisions[0]) ? 1 : 0;
-        if (p.lane == 0) p.cnt[ident] += step;
+        if (p.cnt[ident] + step > 0xFFFF) p.err = STATUS_COUNT_OVERFLOW;   // never silently wrap
+        else if (p.lane == 0) p.cnt[ident] = (uint16_t)(p.cnt[ident] + step);
         set_key(p, slot, p.seq++);
         break;
     }
@@ -1044,7 +1046,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     p.dsum = reinterpret_cast<double*>(base + lay.dsum);
     p.ctr = reinterpret_cast<Ctr*>(base + lay.ctr);
     p.dem_summed_s = reinterpret_cast<double*>(base + lay.dem_summed);
-    p.cnt = reinterpret_cast<int32_t*>(base + lay.cnt);
+    p.cnt = reinterpret_cast<uint16_t*>(base + lay.cnt);
     p.rscore = reinterpret_cast<float*>(base + lay.rscore);
     p.q_score = reinterpret_cast<float*>(base + lay.q_score);
     p.pl = reinterpret_cast<int32_t*>(base + lay.pl);
