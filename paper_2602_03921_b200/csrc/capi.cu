@@ -475,6 +475,7 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
             return fail(st, st == -4 ? "record buffer too small"
                             : st == -1 ? "config error during replay (an expert exceeds the cache capacity)"
                             : st == -7 ? "an LFU/LHU access count exceeded the device's 16-bit counters"
+                            : st == -8 ? "more than 2^31 policy stamps in one replay (trace too long)"
                                        : "runtime invariant broken during replay");
         }
     return 0;

@@ -45,6 +45,7 @@ constexpr uint64_t FNV_PRIME = 0x100000001b3ULL;
 constexpr uint64_t FNV_PRIME_MIX = 0xD6E8FEB86659FD93ULL;
 constexpr int STATUS_QUEUE_OVERFLOW = -5;
 constexpr int STATUS_COUNT_OVERFLOW = -7;          // an LFU/LHU access count outgrew 16 bits
+constexpr int STATUS_SEQ_OVERFLOW = -8;            // > 2^31 policy stamps in one replay
 
 struct ReplayArgs {
     const EsimConfig* cfg;
@@ -314,8 +315,11 @@ DFI void rec_prefetch(Pt& p, int ev, int target, int expert, int64_t t, float sc
 // ---------------------------------------------------------------------------
 // policies (eviction.py:29-294) on slot keys
 // ---------------------------------------------------------------------------
-constexpr uint64_t LS_CURRENT = 1ull << 50;   // stamps stay below 2^50; key << 12 fits 64 bits
-constexpr uint64_t KEY_FREE = 0x000FFFFFFFFFFFFFull; // free-slot key: above every live LRU/LS key,
+// LRU / LS keys are 32-bit: stamp (p.seq, kept below 2^31 - 1: STATUS_SEQ_OVERFLOW)
+// with the LS class in bit 31, so the victim scan compares one 32-bit word per slot
+constexpr uint64_t LS_CURRENT = 1ull << 31;
+constexpr uint64_t SEQ_LIMIT = 0x7FFF0000ull;        // checked once per layer (a layer adds < 2^16)
+constexpr uint64_t KEY_FREE = 0x000FFFFFFFFFFFFFull; // free-slot key: low word 0xFFFFFFFF is above every live LRU/LS key,
                                                      // also after begin_pass clears bit 50
 
 DFI uint64_t order_double(double d) {
@@ -402,19 +406,26 @@ DFI int select_victim(Pt& p, bool forced) {
         best = warp_min_u64(best);
         return (int)(best & 0xFFF);
     }
-    if (p.pol == ESIM_EV_LRU || p.pol == ESIM_EV_LS) {               // branch-free: free slots hold KEY_FREE
+    if (p.pol == ESIM_EV_LRU || p.pol == ESIM_EV_LS) {
+        // one 32-bit word per slot (the key's low word: class | stamp, free = 0xFFFFFFFF);
+        // stamps are unique, so the lane holding the warp minimum names the victim
+        const uint32_t* k32 = reinterpret_cast<const uint32_t*>(p.key);
+        uint32_t bk = 0xFFFFFFFFu;
+        int bs = 0;
         #pragma unroll 4
         for (int s = p.lane; s < p.S; s += 32) {
-            const uint64_t k = (p.key[s] << 12) | (uint64_t)s;
-            best = k < best ? k : best;
+            const uint32_t k = k32[2 * s];
+            bs = k < bk ? s : bs;
+            bk = k < bk ? k : bk;
         }
-        best = warp_min_u64(best);
-        if ((best >> 12) >= (KEY_FREE & ~LS_CURRENT)) return -1;
-        if (p.pol == ESIM_EV_LS && ((best >> 12) & LS_CURRENT)) {
+        const uint32_t m = __reduce_min_sync(FULL, bk);
+        if (m == 0xFFFFFFFFu) return -1;                                 // no resident
+        const int slot = __shfl_sync(FULL, bs, __ffs(__ballot_sync(FULL, bk == m)) - 1);
+        if (p.pol == ESIM_EV_LS && (m & (uint32_t)LS_CURRENT)) {
             if (!forced) { ctr_add(p, p.ctr->ls_refusals, 1); return -1; }
             ctr_add(p, p.ctr->ls_forced, 1);
         }
-        return (int)(best & 0xFFF);
+        return slot;
     }
     for (int s = p.lane; s < p.S; s += 32) {
         const int id = p.res_ident[s];
@@ -1103,7 +1114,10 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     for (int pass = 0; pass < tr.n_passes && !p.err; pass++) {
         p.pass_id = pass;
         if (p.pol == ESIM_EV_LS) {                                        // begin_pass (eviction.py:262-268)
-            for (int s = p.lane; s < p.S; s += 32) p.key[s] &= ~LS_CURRENT;
+            for (int s = p.lane; s < p.S; s += 32) {               // free slots keep KEY_FREE
+                const uint64_t k = p.key[s];
+                p.key[s] = k == KEY_FREE ? k : (k & ~LS_CURRENT);
+            }
         } else if (p.pol == ESIM_EV_SB) {                                 // eviction.py:195-197
             for (int s = p.lane; s < p.S; s += 32)
                 if (p.res_ident[s] >= 0)
@@ -1115,6 +1129,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
         int64_t pblocked = 0;
         for (int l = 0; l < p.L && !p.err; l++) {
             p.layer = l;
+            if (p.seq > SEQ_LIMIT) { p.err = STATUS_SEQ_OVERFLOW; break; }
             const int64_t ev = (int64_t)pass * p.L + l;
             settle(p);
             const int T = (int)(tr.row_offset[ev + 1] - tr.row_offset[ev]);
