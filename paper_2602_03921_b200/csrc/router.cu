@@ -234,10 +234,11 @@ __device__ __forceinline__ uint64_t u64max(uint64_t a, uint64_t b) { return a < 
 __device__ __forceinline__ int key_expert(uint64_t k) { return (int)(uint32_t)k; }
 __device__ __forceinline__ float key_score(uint64_t k) { return __uint_as_float(~(uint32_t)(k >> 32)); }
 
-// ascending bitonic sort of 32 (TWO = false) or 64 keys, element i = lane + 32 * reg
-template <bool TWO>
+// ascending bitonic sort of N = 8, 16, 32 or 64 keys, element i = lane + 32 * reg
+// (N < 32: lanes >= N sort their own padding, never mixed in)
+template <int N>
 __device__ __forceinline__ void bitonic_sort(uint64_t& a0, uint64_t& a1, int lane) {
-    constexpr int N = TWO ? 64 : 32;
+    constexpr bool TWO = N == 64;
 #pragma unroll
     for (int k = 2; k <= N; k <<= 1) {
 #pragma unroll
@@ -265,9 +266,10 @@ __device__ __forceinline__ void bitonic_sort(uint64_t& a0, uint64_t& a1, int lan
 
 // softmax_rows of one row (bit-exact, routing.py:22-29) -> sorted keys.
 // buf: this warp's E floats of shared memory (numpy's pairwise sum order).
-template <bool TWO>
+template <int N>
 __device__ __forceinline__ void row_keys64(const float* __restrict__ x, int E, int lane, float* buf, uint64_t& k0,
                                            uint64_t& k1) {
+    constexpr bool TWO = N == 64;
     const float ninf = -__int_as_float(0x7f800000);
     const bool h0 = lane < E, h1 = TWO && lane + 32 < E;
     const float v0 = h0 ? x[lane] : ninf;
@@ -284,12 +286,13 @@ __device__ __forceinline__ void row_keys64(const float* __restrict__ x, int E, i
     __syncwarp();
     k0 = h0 ? ((uint64_t)(~__float_as_uint(__fdiv_rn(e0, S))) << 32) | (uint32_t)lane : kNoKey;
     k1 = h1 ? ((uint64_t)(~__float_as_uint(__fdiv_rn(e1, S))) << 32) | (uint32_t)(lane + 32) : kNoKey;
-    bitonic_sort<TWO>(k0, k1, lane);
+    bitonic_sort<N>(k0, k1, lane);
 }
 
 // number of predicted experts of one row in sorted order (prefix length)
-template <bool TWO>
+template <int N>
 __device__ __forceinline__ int row_pred_count(const RouterArgs& a, int E, int K, uint64_t k0, uint64_t k1) {
+    constexpr bool TWO = N == 64;
     switch (a.pred_mode) {
     case ESIM_PF_TOPK: return a.pred_count;
     case ESIM_PF_ORACLE: return K;
@@ -319,12 +322,13 @@ __device__ __forceinline__ double row_mass(float w, int K, int lane) {
 }
 
 // a single-row event (decode passes): one warp does everything
-template <bool TWO>
+template <int N>
 __device__ __forceinline__ void route_single_warp(const RouterArgs& a, int64_t ev, float* buf, int lane) {
+    constexpr bool TWO = N == 64;
     const int E = a.tr.experts, K = a.tr.top_k;
     const int64_t r0 = a.tr.row_offset[ev];
     uint64_t k0, k1;
-    row_keys64<TWO>(a.tr.logits + r0 * E, E, lane, buf, k0, k1);
+    row_keys64<N>(a.tr.logits + r0 * E, E, lane, buf, k0, k1);
     const int x0 = key_expert(k0), x1 = key_expert(k1);
     const float s0 = key_score(k0), s1 = key_score(k1);
     const int64_t eb = ev * E;
@@ -337,7 +341,7 @@ __device__ __forceinline__ void route_single_warp(const RouterArgs& a, int64_t e
         a.out.dem_summed[eb + lane] = (double)s0;
         a.out.dem_tokens[eb + lane] = 1;
     }
-    const int c = row_pred_count<TWO>(a, E, K, k0, k1);
+    const int c = row_pred_count<N>(a, E, K, k0, k1);
     if (lane < c) { a.out.pred_expert[eb + lane] = x0; a.out.pred_score[eb + lane] = s0; }
     if (TWO && lane + 32 < c) { a.out.pred_expert[eb + lane + 32] = x1; a.out.pred_score[eb + lane + 32] = s1; }
     const double inner = row_mass(s0, K, lane);
@@ -374,8 +378,9 @@ struct Multi64Smem {
 // a multi-row event (prefill passes): rows spread over the warps in chunks
 // of 64; per expert the row-ordered fp64 sum of weights (engine.py:592) is
 // folded after each chunk from the row bitmask, so no O(E*T*K) rescans.
-template <bool TWO>
+template <int N>
 __device__ __forceinline__ void route_multi64_cta(const RouterArgs& a, int64_t ev, unsigned char* smem_raw) {
+    constexpr bool TWO = N == 64;
     Multi64Smem& s = *reinterpret_cast<Multi64Smem*>(smem_raw);
     const int E = a.tr.experts, K = a.tr.top_k;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -395,7 +400,7 @@ __device__ __forceinline__ void route_multi64_cta(const RouterArgs& a, int64_t e
         for (int rr = warp; rr < cn; rr += kRouterWarps) {
             const int64_t row = r0 + c0 + rr;
             uint64_t k0, k1;
-            row_keys64<TWO>(a.tr.logits + row * E, E, lane, s.rowbuf[warp], k0, k1);
+            row_keys64<N>(a.tr.logits + row * E, E, lane, s.rowbuf[warp], k0, k1);
             const int x0 = key_expert(k0), x1 = key_expert(k1);
             const float s0 = key_score(k0), s1 = key_score(k1);
             if (lane < K) {
@@ -406,7 +411,7 @@ __device__ __forceinline__ void route_multi64_cta(const RouterArgs& a, int64_t e
                 atomicMin(&s.rank[x0], lane + 1);
                 atomicMax(&s.gate[x0], __float_as_uint(s0));
             }
-            const int c = row_pred_count<TWO>(a, E, K, k0, k1);
+            const int c = row_pred_count<N>(a, E, K, k0, k1);
             if (lane < c) atomicMax(&s.best[x0], __float_as_uint(s0) + 1u);
             if (TWO && lane + 32 < c) atomicMax(&s.best[x1], __float_as_uint(s1) + 1u);
             const double inner = row_mass(s0, K, lane);
@@ -536,8 +541,11 @@ __global__ void __launch_bounds__(kRouterWarps * 32, 3) router_persistent_kernel
         const int t = trace_of(b.prefix, b.n, g);
         const RouterArgs a = router_args(b, t);
         const int64_t ev = g - b.prefix[t];
-        if (a.tr.experts <= 32) route_multi64_cta<false>(a, ev, smem);
-        else if (a.tr.experts <= 64) route_multi64_cta<true>(a, ev, smem);
+        const int E = a.tr.experts;
+        if (E <= 8) route_multi64_cta<8>(a, ev, smem);
+        else if (E <= 16) route_multi64_cta<16>(a, ev, smem);
+        else if (E <= 32) route_multi64_cta<32>(a, ev, smem);
+        else if (E <= 64) route_multi64_cta<64>(a, ev, smem);
         else route_event_cta_generic(a, ev, smem);
         __syncthreads();
     }
@@ -561,8 +569,11 @@ __global__ void __launch_bounds__(kRouterWarps * 32, 3) router_persistent_kernel
             }
             const int64_t ev = g - t_lo;
             if (a.tr.experts > 64 || a.tr.row_offset[ev + 1] - a.tr.row_offset[ev] != 1) continue;
-            if (a.tr.experts <= 32) route_single_warp<false>(a, ev, buf, lane);
-            else route_single_warp<true>(a, ev, buf, lane);
+            const int E = a.tr.experts;
+            if (E <= 8) route_single_warp<8>(a, ev, buf, lane);
+            else if (E <= 16) route_single_warp<16>(a, ev, buf, lane);
+            else if (E <= 32) route_single_warp<32>(a, ev, buf, lane);
+            else route_single_warp<64>(a, ev, buf, lane);
         }
     }
 }
