@@ -179,6 +179,9 @@ struct Pt {
     bool digest_on;
     uint32_t pf_ev[5];              // prefetch submitted/started/completed/skipped/dropped (registers)
     uint32_t n_evict, n_forced;
+    // this layer's access outcomes (registers; folded into the smem per-layer
+    // counters once per layer): misses (fetch + wait) by class, drops, substitutions
+    uint32_t lc_miss, lc_c0, lc_c1, lc_drop, lc_sub;
     int64_t n_recs, n_pe;
     int pass_id, layer;
     int err;
@@ -664,14 +667,35 @@ DFI void access_rec(Pt& p, int expert, int tokens, int rank, int outcome, int mc
                     int prec, int sub) {
     emit(p, ESIM_REC_ACCESS, p.layer, expert, tokens, rank,
          outcome | ((mclass < 0 ? 0xFF : mclass) << 8) | ((prec + 1) << 16), sub, blocked, 0, 0, wd);
-    // per-layer counters only; totals[0..7] are their sums (formed at the end)
+    // per-layer counters in registers (outcome is a literal at every call site);
+    // hits = demands - the rest, folded into smem after the layer (flush_layer_counts)
+    if (outcome == 1 || outcome == 2) {
+        p.lc_miss++;
+        p.lc_c0 += mclass == 0;
+        p.lc_c1 += mclass == 1;
+    } else if (outcome == 3) {
+        p.lc_drop++;
+    } else if (outcome == 4) {
+        p.lc_sub++;
+    }
+}
+
+// the layer's access outcomes -> per-layer counters (totals[0..7] are their sums,
+// formed at the end); n = the layer's demands, blocked = their summed blocked time
+DFI void flush_layer_counts(Pt& p, int layer, int n, int64_t blocked) {
     if (p.lane == 0) {
-        int32_t* pl = p.pl + p.layer * ESIM_PL_FIELDS;
-        pl[0]++;
-        pl[outcome == 0 ? 1 : outcome <= 2 ? 2 : outcome == 3 ? 6 : 7]++;
-        if (outcome == 1 || outcome == 2) pl[3 + mclass]++;
+        int32_t* pl = p.pl + layer * ESIM_PL_FIELDS;
+        pl[0] += n;
+        pl[1] += n - (int)(p.lc_miss + p.lc_drop + p.lc_sub);
+        pl[2] += p.lc_miss;
+        pl[3] += p.lc_c0;
+        pl[4] += p.lc_c1;
+        pl[5] += p.lc_miss - p.lc_c0 - p.lc_c1;
+        pl[6] += p.lc_drop;
+        pl[7] += p.lc_sub;
         if (blocked) p.ctr->sync_overhead += blocked;
     }
+    p.lc_miss = p.lc_c0 = p.lc_c1 = p.lc_drop = p.lc_sub = 0;
 }
 
 // nearest-rank percentile (prefetch.py:30-36) of n floats in smem, warp-parallel
@@ -1098,6 +1122,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     p.einv = ((1ull << 32) + (uint64_t)p.E - 1) / (uint64_t)p.E;
     p.digest = FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
     p.n_evict = 0; p.n_forced = 0;
+    p.lc_miss = p.lc_c0 = p.lc_c1 = p.lc_drop = p.lc_sub = 0;
     #pragma unroll
     for (int i = 0; i < 5; i++) p.pf_ev[i] = 0;
     p.err = 0;
@@ -1197,6 +1222,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
                 }
             }
             if (p.err) break;
+            flush_layer_counts(p, l, nd, blocked);
             int faithful = T, nmod = 0;                                   // RouteRec (engine.py:625-643)
             if (!GEN) {
                 // standard routing, every demand served: the record is the router's
