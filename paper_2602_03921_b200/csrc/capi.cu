@@ -401,12 +401,24 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
         std::memcpy(q, h.pass_kind, h.n_passes * 4); q += al256(h.n_passes * 4);
         std::memcpy(q, h.row_offset, (h.n_events + 1) * 8);
     }
-    cudaMemcpyAsync(base, P->small_img, P->small_bytes, cudaMemcpyHostToDevice, P->st);
+    // one batched submission of every input copy (cudaMemcpyBatchAsync), else one call each
+    std::vector<void*> dsts{base}, srcs{P->small_img};
+    std::vector<size_t> sizes{P->small_bytes};
     for (int t = 0; t < P->n_traces; t++) {
         const EsimTraceDesc& h = P->htr[t];
-        if (h.n_rows_total)
-            cudaMemcpyAsync(base + P->logit_off[t], h.logits, h.n_rows_total * h.experts * 4, cudaMemcpyHostToDevice,
-                            P->st);
+        if (!h.n_rows_total) continue;
+        dsts.push_back(base + P->logit_off[t]);
+        srcs.push_back(const_cast<float*>(h.logits));
+        sizes.push_back((size_t)h.n_rows_total * h.experts * 4);
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail_idx = 0;
+    if (cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1, &fail_idx,
+                             P->st) != cudaSuccess) {
+        cudaGetLastError();
+        for (size_t i = 0; i < dsts.size(); i++)
+            cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, P->st);
     }
     if (prof) { cudaStreamSynchronize(P->st); fprintf(stderr, "[plan_run] h2d done %.2f ms\n", now_ms() - t_start); }
     int rc = esim_router_launch_batch((EsimTraceDesc*)(base + P->td_off), (EsimRouterOut*)(base + P->rd_off),
