@@ -259,6 +259,13 @@ int esim_sweep_plan_create(const EsimConfig *cfg, int32_t n, const EsimTraceDesc
 int esim_sweep_plan_run(void *plan, EsimCounters *counters, int64_t *per_layer, EsimRec *recs,
                         int32_t *pred_experts);
 int esim_sweep_plan_destroy(void *plan);
+/* Pipelined steps over two device slabs (double buffering): submit enqueues one
+ * step (H2D, router, replays, D2H into the given buffers, which must stay
+ * untouched until its wait) and returns; wait blocks for the oldest submitted
+ * step and checks its statuses. At most two steps in flight. Step k+1's copies
+ * and router overlap step k's replays. esim_sweep_plan_run drains first. */
+int esim_sweep_plan_submit(void *plan, EsimCounters *counters, int64_t *per_layer);
+int esim_sweep_plan_wait(void *plan);
 
 /* ---- physical layer step (no reference equivalent; configs[1]) -------- */
 typedef struct {

@@ -52,6 +52,8 @@ def lib():
         L.esim_sweep_plan_create.argtypes = [vp, i32, vp, i32, i32, i64, i64, vp]
         L.esim_sweep_plan_run.argtypes = [vp, vp, vp, vp, vp]
         L.esim_sweep_plan_destroy.argtypes = [vp]
+        L.esim_sweep_plan_submit.argtypes = [vp, vp, vp]
+        L.esim_sweep_plan_wait.argtypes = [vp]
         L.esim_ffn_set_trace.argtypes = [vp]
         L.esim_host_unregister.argtypes = [vp]
         L.esim_router_launch_batch.argtypes = [vp, vp, vp, vp, i32, i64, i32, vp]

@@ -181,16 +181,29 @@ extern "C" int esim_router_launch_batch(const EsimTraceDesc* d_traces, const Esi
 
 // ---------------------------------------------------------------------------
 // Sweep plan: everything about a grid that does not change between runs is
-// resolved once (predictor per trace, geometry groups + costliest-first order,
-// the device slab layout, device descriptors). A run then moves the step's
-// inputs and outputs only:
-//   H2D  small per-trace arrays gathered into one pinned image -> 1 copy,
-//        logits straight from the caller's (page-locked) arrays, 1 copy each
+// resolved once (predictor per trace, launch groups and their order, the
+// device slab layout, device descriptors). A run then moves the step's inputs
+// and outputs only:
+//   H2D  small per-trace arrays gathered into one pinned image + the logits
+//        straight from the caller's (page-locked) arrays, one batched submission
 //   GPU  batched router, grouped concurrent replays writing their results at
 //        the caller's row (out_index), so
 //   D2H  counters / per-layer (/ logs) land directly in the caller's buffers.
+// run() is synchronous. submit()/wait() pipeline steps over two slabs (double
+// buffering): step k+1's copies and router overlap step k's replays, and its
+// replays fill the SMs that step k's tail leaves idle.
 // ---------------------------------------------------------------------------
 namespace {
+struct Slab {
+    char* dev = nullptr;                          // device: the layout below
+    char* small_img = nullptr;                    // pinned image of the small arrays
+    cudaStream_t st = nullptr;
+    std::vector<cudaStream_t> gs;
+    std::vector<cudaEvent_t> ge;
+    cudaEvent_t routed = nullptr;
+    EsimCounters* out_c = nullptr;                // pending step: the caller's counters
+};
+
 struct SweepPlan {
     int n = 0, n_traces = 0, pl_stride = 0, max_tokens = 0, max_e = 1;
     int64_t rec_cap = 0, pe_cap = 0, total_events = 0;
@@ -200,145 +213,58 @@ struct SweepPlan {
     int tune_runs = 2;                            // runs whose measured times re-sort the groups
     std::vector<std::pair<int, int>> groups;      // [begin, end) in pcfg
     std::vector<EsimTraceDesc> htr;               // caller descriptors (host pointers)
-    std::vector<size_t> small_off, logit_off;     // per trace, in the slab (small: relative to small image)
-    size_t small_bytes = 0, small_base = 0, cfg_off = 0, td_off = 0, rd_off = 0, par_off = 0, pre_off = 0;
+    std::vector<int32_t> params;                  // predictor per trace
+    std::vector<int64_t> prefix;                  // event prefix sums
+    std::vector<size_t> small_off, logit_off, roff;
+    size_t small_bytes = 0, cfg_off = 0, td_off = 0, rd_off = 0, par_off = 0, pre_off = 0;
     size_t idx_off = 0, cnt_off = 0, pl_off = 0, rec_off = 0, pe_off = 0, total = 0;
-    char* slab = nullptr;                         // device
-    char* small_img = nullptr;                    // pinned image of the small arrays
-    cudaStream_t st = nullptr;
-    std::vector<cudaStream_t> gs;
-    std::vector<cudaEvent_t> ge;
-    cudaEvent_t routed = nullptr;
+    Slab slab[2];
+    int next = 0;                                 // slab of the next submit
+    std::vector<int> pending;                     // submitted, not yet waited (oldest first)
 };
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
+void slab_free(Slab& S) {
+    if (S.st) cudaStreamSynchronize(S.st);
+    if (S.dev) cudaFree(S.dev);
+    if (S.small_img) cudaFreeHost(S.small_img);
+    for (auto s2 : S.gs) cudaStreamDestroy(s2);
+    for (auto e2 : S.ge) cudaEventDestroy(e2);
+    if (S.routed) cudaEventDestroy(S.routed);
+    if (S.st) cudaStreamDestroy(S.st);
+    S = Slab();
+}
+
 void plan_free(SweepPlan* P) {
     if (!P) return;
-    if (P->st) cudaStreamSynchronize(P->st);
-    if (P->slab) cudaFree(P->slab);
-    if (P->small_img) cudaFreeHost(P->small_img);
-    for (auto s2 : P->gs) cudaStreamDestroy(s2);
-    for (auto e2 : P->ge) cudaEventDestroy(e2);
-    if (P->routed) cudaEventDestroy(P->routed);
-    if (P->st) cudaStreamDestroy(P->st);
+    slab_free(P->slab[0]);
+    slab_free(P->slab[1]);
     delete P;
 }
-}  // namespace
 
-extern "C" int esim_sweep_plan_destroy(void* plan) {
-    plan_free(static_cast<SweepPlan*>(plan));
-    return 0;
-}
-
-extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const EsimTraceDesc* traces,
-                                      int32_t n_traces, int32_t pl_stride, int64_t rec_cap, int64_t pe_cap,
-                                      void** plan_out) {
-    if (!plan_out) return fail(-1, "null plan pointer");
-    *plan_out = nullptr;
-    if (n <= 0) return fail(-1, "empty grid");
-    SweepPlan* P = new SweepPlan();
-    auto bail = [&](int rc) { plan_free(P); return rc; };
+// allocate one slab, build its device descriptors, upload the fixed tables
+int slab_init(SweepPlan* P, Slab& S) {
     cudaError_t e;
-    P->n = n; P->n_traces = n_traces; P->pl_stride = pl_stride; P->rec_cap = rec_cap; P->pe_cap = pe_cap;
-    // predictor per trace (taken from the first config using it)
-    std::vector<int32_t> params(4 * n_traces, 0);
-    std::vector<char> seen(n_traces, 0);
-    std::vector<double> pover(n_traces), ppct(n_traces);
-    for (int i = 0; i < n; i++) {
-        const int t = cfg[i].trace_id;
-        if (t < 0 || t >= n_traces) return bail(fail(-1, "trace_id out of range"));
-        if (!seen[t]) {
-            seen[t] = 1;
-            pover[t] = cfg[i].overfetch;
-            ppct[t] = cfg[i].percentile;
-            esim_predictor_params(traces[t].top_k, traces[t].experts, cfg[i].prefetch, cfg[i].overfetch,
-                                  cfg[i].percentile, &params[4 * t]);
-        } else if (params[4 * t] != cfg[i].prefetch || pover[t] != cfg[i].overfetch || ppct[t] != cfg[i].percentile) {
-            return bail(fail(-1, "configs sharing a trace_id must share the predictor"));
-        }
-    }
-    // one launch group per kernel specialisation (policy x {common, general} path),
-    // every geometry in it (shared memory sized by the largest), each replayed on its
-    // own stream; first order = larger traces first, then after each of the first
-    // runs the measured per-point replay times (longest first, see plan_tune)
-    std::vector<int> order(n);
-    for (int i = 0; i < n; i++) order[i] = i;
-    auto gen_of = [&](int a) { return cfg[a].miss != ESIM_MISS_FETCH || cfg[a].routing != ESIM_ROUTE_STANDARD; };
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        if (cfg[a].eviction != cfg[b].eviction) return cfg[a].eviction < cfg[b].eviction;
-        if (gen_of(a) != gen_of(b)) return gen_of(a) < gen_of(b);
-        return cfg[a].num_layers * cfg[a].experts > cfg[b].num_layers * cfg[b].experts;
-    });
-    for (int i = 0; i < n; i++) {
-        if (i == 0 || cfg[order[i]].eviction != cfg[order[i - 1]].eviction || gen_of(order[i]) != gen_of(order[i - 1]))
-            P->groups.push_back({i, i + 1});
-        else
-            P->groups.back().second = i + 1;
-    }
-    P->order = order;
-    P->caller_cfg.assign(cfg, cfg + n);
-    P->pcfg.resize(n);
-    for (int i = 0; i < n; i++) P->pcfg[i] = cfg[order[i]];
-    // slab: [small arrays of every trace][logits per trace][router outputs][tables][outputs]
-    P->htr.assign(traces, traces + n_traces);
-    P->small_off.resize(n_traces);
-    P->logit_off.resize(n_traces);
-    std::vector<size_t> roff(n_traces);
-    std::vector<int64_t> prefix(n_traces + 1, 0);
-    for (int t = 0; t < n_traces; t++) {
-        const EsimTraceDesc& d = traces[t];
-        P->small_off[t] = P->small_bytes;
-        P->small_bytes += al256(d.n_passes * 4) * 2 + al256((d.n_events + 1) * 8);
-        prefix[t + 1] = prefix[t] + d.n_events;
-        P->max_e = std::max(P->max_e, (int)d.experts);
-        for (int p = 0; p < d.n_passes; p++) P->max_tokens = std::max(P->max_tokens, d.pass_tokens[p]);
-    }
-    P->total_events = prefix[n_traces];
-    size_t total = P->small_bytes;
-    for (int t = 0; t < n_traces; t++) {
-        const EsimTraceDesc& d = traces[t];
-        P->logit_off[t] = total;
-        total += al256(d.n_rows_total * d.experts * 4);
-    }
-    for (int t = 0; t < n_traces; t++) {
-        const EsimTraceDesc& d = traces[t];
-        const int64_t ne = d.n_events, nr = d.n_rows_total, E = d.experts, K = d.top_k;
-        roff[t] = total;
-        total += al256(ne * 4) * 3 + al256(ne * E * 4) * 6 + al256(ne * E * 8) + al256(ne * 8) +
-                 al256(nr * K * 2) + al256(nr * K * 4) + al256(ne * 4) * 2 + al256(d.num_layers * 16) +
-                 al256(sizeof(EsimRouteSummary));
-    }
-    P->cfg_off = total; total += al256(sizeof(EsimConfig) * n);
-    P->td_off = total; total += al256(sizeof(EsimTraceDesc) * n_traces);
-    P->rd_off = total; total += al256(sizeof(EsimRouterOut) * n_traces);
-    P->par_off = total; total += al256(sizeof(int32_t) * 4 * n_traces);
-    P->pre_off = total; total += al256(sizeof(int64_t) * (n_traces + 1));
-    P->idx_off = total; total += al256(sizeof(int32_t) * n);
-    P->cnt_off = total; total += al256(sizeof(EsimCounters) * n);
-    P->pl_off = total; total += al256(sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS);
-    P->rec_off = total; total += rec_cap ? al256(sizeof(EsimRec) * n * rec_cap) : 0;
-    P->pe_off = total; total += rec_cap ? al256(sizeof(int32_t) * n * pe_cap) : 0;
-    P->total = total;
-    if ((e = cudaMalloc((void**)&P->slab, total)) != cudaSuccess) return bail(cuda_fail(e, "device alloc"));
-    if ((e = cudaMallocHost((void**)&P->small_img, std::max<size_t>(P->small_bytes, 256))) != cudaSuccess)
-        return bail(cuda_fail(e, "pinned alloc"));
-    if ((e = cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking)) != cudaSuccess) return bail(cuda_fail(e, "stream"));
-    if ((e = cudaEventCreateWithFlags(&P->routed, cudaEventDisableTiming)) != cudaSuccess) return bail(cuda_fail(e, "event"));
+    const int n = P->n, n_traces = P->n_traces;
+    if ((e = cudaMalloc((void**)&S.dev, P->total)) != cudaSuccess) return cuda_fail(e, "device alloc");
+    if ((e = cudaMallocHost((void**)&S.small_img, std::max<size_t>(P->small_bytes, 256))) != cudaSuccess)
+        return cuda_fail(e, "pinned alloc");
+    if ((e = cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+    if ((e = cudaEventCreateWithFlags(&S.routed, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
     for (size_t g = 0; g < P->groups.size(); g++) {
         cudaStream_t s2;
         cudaEvent_t e2;
-        if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking)) != cudaSuccess) return bail(cuda_fail(e, "stream"));
-        P->gs.push_back(s2);
-        if ((e = cudaEventCreateWithFlags(&e2, cudaEventDisableTiming)) != cudaSuccess) return bail(cuda_fail(e, "event"));
-        P->ge.push_back(e2);
+        if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+        S.gs.push_back(s2);
+        if ((e = cudaEventCreateWithFlags(&e2, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+        S.ge.push_back(e2);
     }
-    // device descriptors of the slab (fixed for the plan)
-    char* base = P->slab;
+    char* base = S.dev;
     std::vector<EsimTraceDesc> dtr(n_traces);
     std::vector<EsimRouterOut> dro(n_traces);
     for (int t = 0; t < n_traces; t++) {
-        const EsimTraceDesc& h = traces[t];
+        const EsimTraceDesc& h = P->htr[t];
         const int64_t ne = h.n_events, nr = h.n_rows_total, E = h.experts, K = h.top_k;
         EsimTraceDesc d = h;
         char* q = base + P->small_off[t];
@@ -347,7 +273,7 @@ extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const Es
         d.row_offset = (const int64_t*)q;
         d.logits = (const float*)(base + P->logit_off[t]);
         dtr[t] = d;
-        char* r = base + roff[t];
+        char* r = base + P->roff[t];
         auto take = [&](size_t bytes) -> void* { void* x = r; r += al256(bytes); return x; };
         EsimRouterOut o;
         o.n_dem = (int32_t*)take(ne * 4);
@@ -369,40 +295,36 @@ extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const Es
         o.summary = (EsimRouteSummary*)take(sizeof(EsimRouteSummary));
         dro[t] = o;
     }
-    std::vector<int32_t> out_index(order.begin(), order.end());
+    std::vector<int32_t> out_index(P->order.begin(), P->order.end());
     cudaMemcpy(base + P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice);
     cudaMemcpy(base + P->td_off, dtr.data(), sizeof(EsimTraceDesc) * n_traces, cudaMemcpyHostToDevice);
     cudaMemcpy(base + P->rd_off, dro.data(), sizeof(EsimRouterOut) * n_traces, cudaMemcpyHostToDevice);
-    cudaMemcpy(base + P->par_off, params.data(), sizeof(int32_t) * 4 * n_traces, cudaMemcpyHostToDevice);
-    cudaMemcpy(base + P->pre_off, prefix.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(base + P->par_off, P->params.data(), sizeof(int32_t) * 4 * n_traces, cudaMemcpyHostToDevice);
+    cudaMemcpy(base + P->pre_off, P->prefix.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice);
     if ((e = cudaMemcpy(base + P->idx_off, out_index.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice)) !=
         cudaSuccess)
-        return bail(cuda_fail(e, "plan upload"));
-    *plan_out = P;
+        return cuda_fail(e, "plan upload");
     return 0;
 }
 
-extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* per_layer, EsimRec* recs,
-                                   int32_t* pred_experts) {
-    SweepPlan* P = static_cast<SweepPlan*>(plan);
-    if (!P) return fail(-1, "null plan");
+// one step on slab S, asynchronous: H2D, router, replays, D2H into the caller's buffers
+int slab_enqueue(SweepPlan* P, Slab& S, EsimCounters* counters, int64_t* per_layer, EsimRec* recs,
+                 int32_t* pred_experts, bool prof) {
     cudaError_t e;
-    const bool prof = getenv("ESIM_PROFILE_HOST") != nullptr;
     auto now_ms = []() { return std::chrono::duration<double, std::milli>(
                              std::chrono::steady_clock::now().time_since_epoch()).count(); };
     const double t_start = now_ms();
-    char* base = P->slab;
+    char* base = S.dev;
     const int n = P->n;
-    // ---- inputs: small arrays through one pinned image, logits straight from the caller
     for (int t = 0; t < P->n_traces; t++) {
         const EsimTraceDesc& h = P->htr[t];
-        char* q = P->small_img + P->small_off[t];
+        char* q = S.small_img + P->small_off[t];
         std::memcpy(q, h.pass_tokens, h.n_passes * 4); q += al256(h.n_passes * 4);
         std::memcpy(q, h.pass_kind, h.n_passes * 4); q += al256(h.n_passes * 4);
         std::memcpy(q, h.row_offset, (h.n_events + 1) * 8);
     }
     // one batched submission of every input copy (cudaMemcpyBatchAsync), else one call each
-    std::vector<void*> dsts{base}, srcs{P->small_img};
+    std::vector<void*> dsts{base}, srcs{S.small_img};
     std::vector<size_t> sizes{P->small_bytes};
     for (int t = 0; t < P->n_traces; t++) {
         const EsimTraceDesc& h = P->htr[t];
@@ -415,23 +337,22 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
     attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
     size_t attr_idx = 0, fail_idx = 0;
     if (cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1, &fail_idx,
-                             P->st) != cudaSuccess) {
+                             S.st) != cudaSuccess) {
         cudaGetLastError();
         for (size_t i = 0; i < dsts.size(); i++)
-            cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, P->st);
+            cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, S.st);
     }
-    if (prof) { cudaStreamSynchronize(P->st); fprintf(stderr, "[plan_run] h2d done %.2f ms\n", now_ms() - t_start); }
+    if (prof) { cudaStreamSynchronize(S.st); fprintf(stderr, "[plan_run] h2d done %.2f ms\n", now_ms() - t_start); }
     int rc = esim_router_launch_batch((EsimTraceDesc*)(base + P->td_off), (EsimRouterOut*)(base + P->rd_off),
                                       (int32_t*)(base + P->par_off), (int64_t*)(base + P->pre_off), P->n_traces,
-                                      P->total_events, P->max_e, P->st);
+                                      P->total_events, P->max_e, S.st);
     if (rc) return cuda_fail(cudaGetLastError(), "router batch");
-    if (prof) { cudaStreamSynchronize(P->st); fprintf(stderr, "[plan_run] router done %.2f ms\n", now_ms() - t_start); }
-    // ---- grouped concurrent replays, results at the caller's rows
-    cudaEventRecord(P->routed, P->st);
+    if (prof) { cudaStreamSynchronize(S.st); fprintf(stderr, "[plan_run] router done %.2f ms\n", now_ms() - t_start); }
+    cudaEventRecord(S.routed, S.st);
     const bool full = recs != nullptr && P->rec_cap > 0;
     for (size_t g = 0; g < P->groups.size(); g++) {
         const int b = P->groups[g].first, m = P->groups[g].second - b;
-        cudaStreamWaitEvent(P->gs[g], P->routed, 0);
+        cudaStreamWaitEvent(S.gs[g], S.routed, 0);
         Sizing z;
         if ((rc = replay_sizing(P->pcfg.data() + b, m, P->max_tokens, P->pl_stride, 0, &z))) return rc;
         const int per = esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt, z.general);
@@ -442,45 +363,26 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
                                     (EsimRouterOut*)(base + P->rd_off), (EsimCounters*)(base + P->cnt_off),
                                     (int64_t*)(base + P->pl_off), full ? (EsimRec*)(base + P->rec_off) : nullptr,
                                     P->rec_cap, full ? (int32_t*)(base + P->pe_off) : nullptr, P->pe_cap, z.N, z.S,
-                                    z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt, w, P->gs[g], nullptr, z.policy,
+                                    z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt, w, S.gs[g], nullptr, z.policy,
                                     z.general, (int32_t*)(base + P->idx_off) + b, z.log_rt);
         if (e != cudaSuccess) return cuda_fail(e, "replay launch");
-        cudaEventRecord(P->ge[g], P->gs[g]);
-        cudaStreamWaitEvent(P->st, P->ge[g], 0);
+        cudaEventRecord(S.ge[g], S.gs[g]);
+        cudaStreamWaitEvent(S.st, S.ge[g], 0);
     }
-    if (prof) { cudaStreamSynchronize(P->st); fprintf(stderr, "[plan_run] replay done %.2f ms\n", now_ms() - t_start); }
-    // ---- outputs straight into the caller's buffers
+    if (prof) { cudaStreamSynchronize(S.st); fprintf(stderr, "[plan_run] replay done %.2f ms\n", now_ms() - t_start); }
     const size_t pls = (size_t)P->pl_stride * ESIM_PL_FIELDS;
-    cudaMemcpyAsync(counters, base + P->cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, P->st);
-    cudaMemcpyAsync(per_layer, base + P->pl_off, sizeof(int64_t) * n * pls, cudaMemcpyDeviceToHost, P->st);
+    cudaMemcpyAsync(counters, base + P->cnt_off, sizeof(EsimCounters) * n, cudaMemcpyDeviceToHost, S.st);
+    cudaMemcpyAsync(per_layer, base + P->pl_off, sizeof(int64_t) * n * pls, cudaMemcpyDeviceToHost, S.st);
     if (full) {
-        cudaMemcpyAsync(recs, base + P->rec_off, sizeof(EsimRec) * n * P->rec_cap, cudaMemcpyDeviceToHost, P->st);
+        cudaMemcpyAsync(recs, base + P->rec_off, sizeof(EsimRec) * n * P->rec_cap, cudaMemcpyDeviceToHost, S.st);
         cudaMemcpyAsync(pred_experts, base + P->pe_off, sizeof(int32_t) * n * P->pe_cap, cudaMemcpyDeviceToHost,
-                        P->st);
+                        S.st);
     }
-    if ((e = cudaStreamSynchronize(P->st)) != cudaSuccess) return cuda_fail(e, "sweep plan run");
-    if (prof) fprintf(stderr, "[plan_run] d2h done %.2f ms\n", now_ms() - t_start);
-    if (P->tune_runs > 0) {
-        // profile-guided scheduling: every group longest-measured first (the kernel
-        // stamps each point's start/end globaltimer into counters.pad); the new
-        // order is uploaded on the plan's stream, ahead of the next run
-        P->tune_runs--;
-        auto dur = [&](int pos) { const EsimCounters& c = counters[P->order[pos]]; return c.pad[1] - c.pad[0]; };
-        std::vector<int64_t> d(n);
-        for (int pos = 0; pos < n; pos++) d[pos] = dur(pos);
-        std::vector<int> neworder(n);
-        for (const auto& g : P->groups) {
-            std::vector<int> pos(g.second - g.first);
-            for (int k = 0; k < (int)pos.size(); k++) pos[k] = g.first + k;
-            std::stable_sort(pos.begin(), pos.end(), [&](int a, int b) { return d[a] > d[b]; });
-            for (int k = 0; k < (int)pos.size(); k++) neworder[g.first + k] = P->order[pos[k]];
-        }
-        P->order = neworder;
-        std::vector<int32_t> out_index(neworder.begin(), neworder.end());
-        for (int i = 0; i < n; i++) P->pcfg[i] = P->caller_cfg[neworder[i]];
-        cudaMemcpy(base + P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice);
-        cudaMemcpy(base + P->idx_off, out_index.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice);
-    }
+    S.out_c = counters;
+    return 0;
+}
+
+int check_status(const EsimCounters* counters, int n) {
     for (int i = 0; i < n; i++)
         if (counters[i].status) {
             const int st = (int)counters[i].status;
@@ -491,6 +393,180 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
                                        : "runtime invariant broken during replay");
         }
     return 0;
+}
+
+// profile-guided scheduling: every group longest-measured first (the kernel stamps
+// each point's start/end globaltimer into counters.pad); uploaded to every slab
+void plan_tune(SweepPlan* P, const EsimCounters* counters) {
+    const int n = P->n;
+    std::vector<int64_t> d(n);
+    for (int pos = 0; pos < n; pos++) {
+        const EsimCounters& c = counters[P->order[pos]];
+        d[pos] = c.pad[1] - c.pad[0];
+    }
+    std::vector<int> neworder(n);
+    for (const auto& g : P->groups) {
+        std::vector<int> pos(g.second - g.first);
+        for (int k = 0; k < (int)pos.size(); k++) pos[k] = g.first + k;
+        std::stable_sort(pos.begin(), pos.end(), [&](int a, int b) { return d[a] > d[b]; });
+        for (int k = 0; k < (int)pos.size(); k++) neworder[g.first + k] = P->order[pos[k]];
+    }
+    P->order = neworder;
+    std::vector<int32_t> out_index(neworder.begin(), neworder.end());
+    for (int i = 0; i < n; i++) P->pcfg[i] = P->caller_cfg[neworder[i]];
+    for (auto& S : P->slab) {
+        if (!S.dev) continue;
+        cudaMemcpy(S.dev + P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice);
+        cudaMemcpy(S.dev + P->idx_off, out_index.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice);
+    }
+}
+}  // namespace
+
+extern "C" int esim_sweep_plan_destroy(void* plan) {
+    plan_free(static_cast<SweepPlan*>(plan));
+    return 0;
+}
+
+extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const EsimTraceDesc* traces,
+                                      int32_t n_traces, int32_t pl_stride, int64_t rec_cap, int64_t pe_cap,
+                                      void** plan_out) {
+    if (!plan_out) return fail(-1, "null plan pointer");
+    *plan_out = nullptr;
+    if (n <= 0) return fail(-1, "empty grid");
+    SweepPlan* P = new SweepPlan();
+    auto bail = [&](int rc) { plan_free(P); return rc; };
+    P->n = n; P->n_traces = n_traces; P->pl_stride = pl_stride; P->rec_cap = rec_cap; P->pe_cap = pe_cap;
+    // predictor per trace (taken from the first config using it)
+    P->params.assign(4 * n_traces, 0);
+    std::vector<char> seen(n_traces, 0);
+    std::vector<double> pover(n_traces), ppct(n_traces);
+    for (int i = 0; i < n; i++) {
+        const int t = cfg[i].trace_id;
+        if (t < 0 || t >= n_traces) return bail(fail(-1, "trace_id out of range"));
+        if (!seen[t]) {
+            seen[t] = 1;
+            pover[t] = cfg[i].overfetch;
+            ppct[t] = cfg[i].percentile;
+            esim_predictor_params(traces[t].top_k, traces[t].experts, cfg[i].prefetch, cfg[i].overfetch,
+                                  cfg[i].percentile, &P->params[4 * t]);
+        } else if (P->params[4 * t] != cfg[i].prefetch || pover[t] != cfg[i].overfetch || ppct[t] != cfg[i].percentile) {
+            return bail(fail(-1, "configs sharing a trace_id must share the predictor"));
+        }
+    }
+    // one launch group per kernel specialisation (policy x {common, general} path),
+    // every geometry in it (shared memory sized by the largest), each replayed on its
+    // own stream; first order = larger traces first, then after each of the first
+    // runs the measured per-point replay times (longest first, plan_tune)
+    std::vector<int> order(n);
+    for (int i = 0; i < n; i++) order[i] = i;
+    auto gen_of = [&](int a) { return cfg[a].miss != ESIM_MISS_FETCH || cfg[a].routing != ESIM_ROUTE_STANDARD; };
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        if (cfg[a].eviction != cfg[b].eviction) return cfg[a].eviction < cfg[b].eviction;
+        if (gen_of(a) != gen_of(b)) return gen_of(a) < gen_of(b);
+        return cfg[a].num_layers * cfg[a].experts > cfg[b].num_layers * cfg[b].experts;
+    });
+    for (int i = 0; i < n; i++) {
+        if (i == 0 || cfg[order[i]].eviction != cfg[order[i - 1]].eviction || gen_of(order[i]) != gen_of(order[i - 1]))
+            P->groups.push_back({i, i + 1});
+        else
+            P->groups.back().second = i + 1;
+    }
+    P->order = order;
+    P->caller_cfg.assign(cfg, cfg + n);
+    P->pcfg.resize(n);
+    for (int i = 0; i < n; i++) P->pcfg[i] = cfg[order[i]];
+    // slab layout: [small arrays of every trace][logits per trace][router outputs][tables][outputs]
+    P->htr.assign(traces, traces + n_traces);
+    P->small_off.resize(n_traces);
+    P->logit_off.resize(n_traces);
+    P->roff.resize(n_traces);
+    P->prefix.assign(n_traces + 1, 0);
+    for (int t = 0; t < n_traces; t++) {
+        const EsimTraceDesc& d = traces[t];
+        P->small_off[t] = P->small_bytes;
+        P->small_bytes += al256(d.n_passes * 4) * 2 + al256((d.n_events + 1) * 8);
+        P->prefix[t + 1] = P->prefix[t] + d.n_events;
+        P->max_e = std::max(P->max_e, (int)d.experts);
+        for (int p = 0; p < d.n_passes; p++) P->max_tokens = std::max(P->max_tokens, d.pass_tokens[p]);
+    }
+    P->total_events = P->prefix[n_traces];
+    size_t total = P->small_bytes;
+    for (int t = 0; t < n_traces; t++) {
+        const EsimTraceDesc& d = traces[t];
+        P->logit_off[t] = total;
+        total += al256(d.n_rows_total * d.experts * 4);
+    }
+    for (int t = 0; t < n_traces; t++) {
+        const EsimTraceDesc& d = traces[t];
+        const int64_t ne = d.n_events, nr = d.n_rows_total, E = d.experts, K = d.top_k;
+        P->roff[t] = total;
+        total += al256(ne * 4) * 3 + al256(ne * E * 4) * 6 + al256(ne * E * 8) + al256(ne * 8) +
+                 al256(nr * K * 2) + al256(nr * K * 4) + al256(ne * 4) * 2 + al256(d.num_layers * 16) +
+                 al256(sizeof(EsimRouteSummary));
+    }
+    P->cfg_off = total; total += al256(sizeof(EsimConfig) * n);
+    P->td_off = total; total += al256(sizeof(EsimTraceDesc) * n_traces);
+    P->rd_off = total; total += al256(sizeof(EsimRouterOut) * n_traces);
+    P->par_off = total; total += al256(sizeof(int32_t) * 4 * n_traces);
+    P->pre_off = total; total += al256(sizeof(int64_t) * (n_traces + 1));
+    P->idx_off = total; total += al256(sizeof(int32_t) * n);
+    P->cnt_off = total; total += al256(sizeof(EsimCounters) * n);
+    P->pl_off = total; total += al256(sizeof(int64_t) * n * pl_stride * ESIM_PL_FIELDS);
+    P->rec_off = total; total += rec_cap ? al256(sizeof(EsimRec) * n * rec_cap) : 0;
+    P->pe_off = total; total += rec_cap ? al256(sizeof(int32_t) * n * pe_cap) : 0;
+    P->total = total;
+    int rc = slab_init(P, P->slab[0]);
+    if (rc) return bail(rc);
+    *plan_out = P;
+    return 0;
+}
+
+extern "C" int esim_sweep_plan_wait(void* plan) {
+    SweepPlan* P = static_cast<SweepPlan*>(plan);
+    if (!P) return fail(-1, "null plan");
+    if (P->pending.empty()) return fail(-1, "no submitted step to wait for");
+    Slab& S = P->slab[P->pending.front()];
+    P->pending.erase(P->pending.begin());
+    cudaError_t e = cudaStreamSynchronize(S.st);
+    if (e != cudaSuccess) return cuda_fail(e, "sweep plan wait");
+    return check_status(S.out_c, P->n);
+}
+
+extern "C" int esim_sweep_plan_submit(void* plan, EsimCounters* counters, int64_t* per_layer) {
+    SweepPlan* P = static_cast<SweepPlan*>(plan);
+    if (!P) return fail(-1, "null plan");
+    if (P->pending.size() >= 2) return fail(-1, "two steps already in flight: wait first");
+    Slab& S = P->slab[P->next];
+    if (!S.dev) {
+        const int rc = slab_init(P, S);
+        if (rc) return rc;
+    }
+    const int rc = slab_enqueue(P, S, counters, per_layer, nullptr, nullptr, false);
+    if (rc) return rc;
+    P->pending.push_back(P->next);
+    P->next ^= 1;
+    return 0;
+}
+
+extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* per_layer, EsimRec* recs,
+                                   int32_t* pred_experts) {
+    SweepPlan* P = static_cast<SweepPlan*>(plan);
+    if (!P) return fail(-1, "null plan");
+    while (!P->pending.empty()) {                 // a synchronous run drains the pipeline first
+        const int rc = esim_sweep_plan_wait(plan);
+        if (rc) return rc;
+    }
+    const bool prof = getenv("ESIM_PROFILE_HOST") != nullptr;
+    Slab& S = P->slab[0];
+    int rc = slab_enqueue(P, S, counters, per_layer, recs, pred_experts, prof);
+    if (rc) return rc;
+    cudaError_t e = cudaStreamSynchronize(S.st);
+    if (e != cudaSuccess) return cuda_fail(e, "sweep plan run");
+    if (P->tune_runs > 0) {
+        P->tune_runs--;
+        plan_tune(P, counters);
+    }
+    return check_status(counters, P->n);
 }
 
 extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDesc* traces, int32_t n_traces,

@@ -159,13 +159,48 @@ class HostGrid:
             self._raise(rc)
         return self.counters, self.per_layer
 
+    # ---- pipelined steps (double-buffered plan: esim_sweep_plan_submit / wait) ----
+    def _out(self, slot: int):
+        if not hasattr(self, "_outs"):
+            self._outs = [(self.counters, self.per_layer)]
+            self._next, self._inflight = 0, []
+        while len(self._outs) <= slot:
+            cs = (_abi.EsimCounters * self.n)()
+            pl = np.zeros_like(self.per_layer)
+            for buf, nbytes in ((C.addressof(cs), C.sizeof(cs)), (pl.ctypes.data, pl.nbytes)):
+                if _lib().esim_host_register(buf, nbytes):
+                    raise RuntimeError(_lib().esim_last_error().decode())
+            self._outs.append((cs, pl))
+        return self._outs[slot]
+
+    def submit(self) -> None:
+        """Enqueue one step (inputs H2D, router, replays, results D2H) and return;
+        up to two steps in flight, the next one's copies and router overlapping
+        the current one's replays."""
+        cs, pl = self._out(getattr(self, "_next", 0))
+        rc = _lib().esim_sweep_plan_submit(self._plan, C.addressof(cs), pl.ctypes.data)
+        if rc != 0:
+            self._raise(rc)
+        self._inflight.append(self._next)
+        self._next ^= 1
+
+    def wait(self):
+        """Results of the oldest submitted step: (counters, per_layer), valid
+        until that buffer's next submit."""
+        slot = self._inflight.pop(0)
+        rc = _lib().esim_sweep_plan_wait(self._plan)
+        if rc != 0:
+            self._raise(rc)
+        return self._outs[slot]
+
     def close(self) -> None:
         if getattr(self, "_plan", None):
             _lib().esim_sweep_plan_destroy(self._plan)
             self._plan = None
         if getattr(self, "_registered", False):
-            _lib().esim_host_unregister(C.addressof(self.counters))
-            _lib().esim_host_unregister(self.per_layer.ctypes.data)
+            for cs, pl in getattr(self, "_outs", [(self.counters, self.per_layer)]):
+                _lib().esim_host_unregister(C.addressof(cs))
+                _lib().esim_host_unregister(pl.ctypes.data)
             self._registered = False
 
     def __del__(self):

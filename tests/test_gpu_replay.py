@@ -226,3 +226,28 @@ def test_sweep_plan_full_logs_match_reference():
                 assert json.dumps(rep) == json.dumps(c["report"]), c["name"]
     finally:
         lib().esim_sweep_plan_destroy(plan)
+
+
+def test_sweep_plan_pipelined_steps_match_run(oracle_lib):
+    """submit/wait over the plan's two slabs == the synchronous run, step by step."""
+    from paper_2602_03921_b200.models import builtin_spec
+    from paper_2602_03921_b200.sweep import C5_MODELS, HostGrid, c5_points, pin_traces
+    from paper_2602_03921_b200.trace import generate_synthetic
+    trs = {m: [generate_synthetic(builtin_spec(m), seed=s, prefill_tokens=16, decode_tokens=8) for s in (2, 3)]
+           for m in C5_MODELS}
+    cfgs, tl = c5_points(trs)
+    pin_traces(tl)
+    g = HostGrid(cfgs, tl)
+    try:
+        want = [int(c.digest) for c in g.run()[0]]
+        g.submit()
+        for _ in range(3):
+            g.submit()
+            cs, _ = g.wait()
+            assert [int(c.digest) for c in cs] == want
+        cs, _ = g.wait()
+        assert [int(c.digest) for c in cs] == want
+        o = oracle_lib.run(cfgs[5], tl[5], full_log=False)
+        assert int(o.counters.digest) == want[5]
+    finally:
+        g.close()
