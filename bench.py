@@ -315,14 +315,24 @@ def main():
         for _ in range(args.steps - 1):
             grid.submit()
             cs, _ = grid.wait()
-        cs, _ = grid.wait()
+        cs, last_pl = grid.wait()
         e2e_ms = 1e3 * (time.perf_counter() - t0) / args.steps
+        grid.wait_buffers_last_per_layer = last_pl
         e2e_match = [int(c.digest) for c in cs] == digests
+        # the reference sweep's output (one emit(report, "csv") row per point,
+        # cli.py:486-491) from the last step's host results, natively formatted
+        from paper_2602_03921_b200.sweep import csv_text
+        t_csv = time.perf_counter()
+        csv_out = csv_text(cfgs, cs, grid.wait_buffers_last_per_layer)
+        csv_ms = 1e3 * (time.perf_counter() - t_csv)
         te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": acc_all / (float(te[0]) / 1e3), "unit": "accesses/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": float(te[0]), "digests_match_device_path": e2e_match}
+               "d2h_bytes_per_step": d2h, "ms_per_step": float(te[0]), "digests_match_device_path": e2e_match,
+               "pipelined": "2 steps in flight (esim_sweep_plan_submit / wait)",
+               "report_csv": {"points": n_pts, "native_ms": csv_ms, "bytes": len(csv_out),
+                              "note": "reference-format sweep CSV of the last step (not in the timed region)"}}
 
     if rank != 0:
         dist.destroy_process_group()

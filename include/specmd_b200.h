@@ -267,6 +267,21 @@ int esim_sweep_plan_destroy(void *plan);
 int esim_sweep_plan_submit(void *plan, EsimCounters *counters, int64_t *per_layer);
 int esim_sweep_plan_wait(void *plan);
 
+/* Report assembly for sweeps (metrics.flatten_report + emit csv,
+ * metrics.py:190-316, 348-395): the result-dependent CSV columns (totals,
+ * rates, timing, fidelity, prefetch) of n points, formatted exactly as the
+ * reference's csv emission writes them (Python str(): shortest round-trip
+ * floats, True/False). With prefixes (point i's fixed config columns =
+ * prefixes[prefix_offsets[i] .. prefix_offsets[i+1]), ending in ","), each
+ * point is one complete CSV line ending "\r\n"; without, only the result
+ * columns. Point i's text is out[offsets[i] .. offsets[i+1]).
+ * per_layer: [n][pl_stride][ESIM_PL_FIELDS] (identity checks). Host code, no
+ * GPU needed. Returns 0, -1 (accounting identity broken), -4 (cap too small). */
+int esim_report_csv(const EsimCounters *counters, const int64_t *per_layer, int32_t pl_stride,
+                    const int32_t *num_layers, const int64_t *per_layer_compute_us, int32_t n,
+                    const char *prefixes, const int64_t *prefix_offsets, char *out, int64_t cap,
+                    int64_t *offsets);
+
 /* ---- physical layer step (no reference equivalent; configs[1]) -------- */
 typedef struct {
     int32_t num_layers, experts, top_k;

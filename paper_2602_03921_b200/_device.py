@@ -53,6 +53,7 @@ def lib():
         L.esim_sweep_plan_run.argtypes = [vp, vp, vp, vp, vp]
         L.esim_sweep_plan_destroy.argtypes = [vp]
         L.esim_sweep_plan_submit.argtypes = [vp, vp, vp]
+        L.esim_report_csv.argtypes = [vp, vp, i32, vp, vp, i32, vp, vp, vp, i64, vp]
         L.esim_sweep_plan_wait.argtypes = [vp]
         L.esim_ffn_set_trace.argtypes = [vp]
         L.esim_host_unregister.argtypes = [vp]

@@ -39,6 +39,10 @@ static int cuda_fail(cudaError_t e, const char* where) {
 }
 
 extern "C" const char* esim_last_error(void) { return g_err.c_str(); }
+const char* esim_set_error(const char* msg) {      // for the other translation units (report.cu)
+    g_err = msg;
+    return g_err.c_str();
+}
 
 // page-lock a caller buffer so the host API's copies are true async DMA
 extern "C" int esim_host_register(void* p, size_t bytes) {

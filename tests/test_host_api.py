@@ -3,6 +3,7 @@ config arithmetic (test_models.py), trace generation/IO (test_trace.py),
 report assembly/emission (test_metrics.py), prediction noise and
 percentiles (test_prefetch.py), SimConfig validation (test_engine.py)."""
 import copy
+import os
 import csv
 import json
 import warnings
@@ -193,3 +194,51 @@ def test_percentile_and_noise_semantics():
     assert len({e for e, _ in out}) == 2 and {e for e, _ in out} != {0, 1}
     assert [s for _, s in out] == [0.5, 0.2]
     assert apply_prediction_noise([(0, 0.6), (1, 0.4)], 2, 1.0, np.random.default_rng(2)) == [(0, 0.6), (1, 0.4)]
+
+
+def test_native_csv_report_matches_python_emit(tmp_path):
+    """esim_report_csv (native result columns) + config columns == metrics.emit
+    csv of every report, byte for byte (C5 grid, oracle results; host code only)."""
+    from oracle import oracle
+    from paper_2602_03921_b200.metrics import emit
+    from paper_2602_03921_b200.models import builtin_spec
+    from paper_2602_03921_b200.sweep import C5_MODELS, c5_points, csv_text, reports
+    from paper_2602_03921_b200.trace import generate_synthetic
+    trs = {m: [generate_synthetic(builtin_spec(m), seed=4, prefill_tokens=12, decode_tokens=6)] for m in C5_MODELS}
+    cfgs, tl = c5_points(trs)
+    ids, traces, cc = {}, [], []
+    for c, t in zip(cfgs, tl):
+        if id(t) not in ids:
+            ids[id(t)] = len(traces)
+            traces.append(t)
+        cc.append(c.to_c(ids[id(t)], False))
+    cs, pl = oracle.run_batch(cc, traces, 4)
+    path = tmp_path / "sweep.csv"
+    for rep in reports(cfgs, cs, pl):
+        emit(rep, "csv", path)
+    want = path.read_bytes().decode()
+    assert csv_text(cfgs, cs, pl) == want
+
+
+def test_native_csv_report_matches_reference_goldens(tmp_path, oracle_lib):
+    """csv_text from oracle counters == metrics.emit csv of the REAL reference's
+    reports (golden fixtures), over every policy / miss / routing variant."""
+    import sys as _sys
+    _sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from golden_cases import cases, config_from, trace_from
+    from paper_2602_03921_b200.metrics import emit
+    from paper_2602_03921_b200.sweep import csv_text
+    cs_ = [c for c in cases() if c["log_len"] <= 20000][::13][:60]
+    cfgs, counters, pls = [], [], []
+    L = max(config_from(c).model.num_layers for c in cs_)
+    import numpy as np
+    per_layer = np.zeros((len(cs_), L, 10), np.int64)
+    path = tmp_path / "golden.csv"
+    for i, c in enumerate(cs_):
+        cfg = config_from(c)
+        o = oracle_lib.run(cfg, trace_from(c["trace"]), full_log=False)
+        cfgs.append(cfg)
+        counters.append(o.counters)
+        per_layer[i, :cfg.model.num_layers] = o.per_layer[:cfg.model.num_layers]
+        emit(c["report"], "csv", path)
+    assert csv_text(cfgs, counters, per_layer) == path.read_bytes().decode()
