@@ -317,13 +317,12 @@ def main():
             cs, _ = grid.wait()
         cs, last_pl = grid.wait()
         e2e_ms = 1e3 * (time.perf_counter() - t0) / args.steps
-        grid.wait_buffers_last_per_layer = last_pl
         e2e_match = [int(c.digest) for c in cs] == digests
         # the reference sweep's output (one emit(report, "csv") row per point,
         # cli.py:486-491) from the last step's host results, natively formatted
         from paper_2602_03921_b200.sweep import csv_text
         t_csv = time.perf_counter()
-        csv_out = csv_text(cfgs, cs, grid.wait_buffers_last_per_layer)
+        csv_out = csv_text(cfgs, cs, last_pl)
         csv_ms = 1e3 * (time.perf_counter() - t_csv)
         te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         if world > 1:
