@@ -150,6 +150,10 @@ __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// programmatic dependent launch: the kernel starts while the previous one (token
+// gather) finishes; what reads the gathered tokens waits here first
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -266,7 +270,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_fused_kernel(const __grid_
                 if (x.kind == 0) {
                     const CUtensorMap* wm = g.w1_maps + slot;
                     const int nk = g.H / BK;
-                    for (int k = 0; k < nk; k++, k_all++) {
+                    int kb = 0;
+                    if (k_all == 0) {   // first unit: weight tiles stream before the gathered tokens exist
+                        const int pre = STAGES < nk ? STAGES : nk;
+                        for (int k = 0; k < pre; k++) {
+                            mbar_expect_tx(&s.full[k], ffn_stage_bytes(NPAD));
+                            tma_load_2d(s.a[k], wm, &s.full[k], 0, (x.tile * KT + k) * BM);
+                        }
+                        pdl_wait();
+                        for (int k = 0; k < pre; k++) tma_load_2d(s.b[k], g.x_map, &s.full[k], k * BK, x.e * NPAD);
+                        kb = pre;
+                        k_all = pre;
+                    }
+                    for (int k = kb; k < nk; k++, k_all++) {
                         const int st = k_all % STAGES;
                         if (k_all >= STAGES) mbar_wait(&s.empty[st], ((k_all / STAGES) - 1) & 1);
                         mbar_expect_tx(&s.full[st], ffn_stage_bytes(NPAD));
@@ -327,6 +343,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_fused_kernel(const __grid_
             }
         }
     } else {                                              // ---- epilogue, warps 2..5
+        pdl_wait();
         const int q = warp & 3;                           // TMEM lane quarter this warp may access
         const int row = q * 32 + lane;                    // accumulator row (TMEM lane)
         int j = 0;
@@ -499,7 +516,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_decode_kernel(const __grid
                 const CUtensorMap* w1 = g.w1_maps + slot;
                 const CUtensorMap* w2 = g.w2_maps + slot;
                 const int KT = g.H / 64;
-                for (int k = 0; k < g.H / BK; k++, k_all++) {
+                int k0 = 0;
+                if (k_all == 0) {       // first unit: its weight tiles stream before the gathered tokens exist
+                    const int pre = STAGES < g.H / BK ? STAGES : g.H / BK;
+                    for (int k = 0; k < pre; k++) {
+                        mbar_expect_tx(&s.full[k], A_BYTES + B_BYTES);
+                        tma_load_2d(s.a[k], w1, &s.full[k], 0, (mt * KT + k) * BM);
+                    }
+                    pdl_wait();
+                    for (int k = 0; k < pre; k++) tma_load_2d(s.b[k], g.x_map, &s.full[k], k * BK, e * NPAD);
+                    k0 = pre;
+                    k_all = pre;
+                }
+                for (int k = k0; k < g.H / BK; k++, k_all++) {
                     const int st = k_all % STAGES;
                     if (k_all >= STAGES) mbar_wait(&s.empty[st], ((k_all / STAGES) - 1) & 1);
                     mbar_expect_tx(&s.full[st], A_BYTES + B_BYTES);
@@ -549,6 +578,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_decode_kernel(const __grid
             }
         }
     } else {                                              // ---- epilogue, warps 2..5
+        pdl_wait();                                       // (the token tables / y precede the gather: belt and braces)
         const int q = warp & 3, row = q * 32 + lane;
         const uint32_t lanebase = (uint32_t)(q * 32) << 16;
         int j = 0;
@@ -628,14 +658,23 @@ cudaError_t launch_ffn(const FfnArgs& a, cudaStream_t st) {
                                          (int)ffn_smem<NPAD>());
     if (e != cudaSuccess) return e;
     const int n_units = a.n_exec * (a.I / 64) + a.n_exec * (a.H / BM) * a.n_kc;
-    const int grid = n_units < ffn_grid_cap() ? n_units : ffn_grid_cap();
-    ffn_fused_kernel<NPAD><<<grid, kFfnThreads, ffn_smem<NPAD>(), st>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(n_units < ffn_grid_cap() ? n_units : ffn_grid_cap());
+    lc.blockDim = dim3(kFfnThreads);
+    lc.dynamicSmemBytes = ffn_smem<NPAD>();
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue overlaps the gather
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, ffn_fused_kernel<NPAD>, a);
 }
 
 // gather token rows per executed expert: xg[e][n][:] = x[tok_index[e][n]][:] (zero for padding)
 __global__ void gather_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ tok_index,
                               __nv_bfloat16* __restrict__ xg, int npad, int H) {
+    pdl_launch_dependents();                          // let the FFN kernel start its prologue now
     const int row = blockIdx.x;                       // e * npad + n
     const int t = tok_index[row];
     const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(t < 0 ? 0 : t) * H);
@@ -748,8 +787,17 @@ extern "C" int esim_ffn_experts_ex(const void* d_w1_maps, const void* d_w2_maps,
             cudaSuccess)
             return -3;
         const int units = n_exec * (I / 64);
-        ffn_decode_kernel<<<units < ffn_grid_cap() ? units : ffn_grid_cap(), kFfnThreads, smem, st>>>(a);
-        return cudaGetLastError() == cudaSuccess ? 0 : -3;
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(units < ffn_grid_cap() ? units : ffn_grid_cap());
+        lc.blockDim = dim3(kFfnThreads);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        return cudaLaunchKernelEx(&lc, ffn_decode_kernel, a) == cudaSuccess ? 0 : -3;
     }
     // gemm2 split-K: enough units to cover the SMs, chunks of >= 256 columns
     int n_kc = 1;
