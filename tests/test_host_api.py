@@ -242,3 +242,16 @@ def test_native_csv_report_matches_reference_goldens(tmp_path, oracle_lib):
         per_layer[i, :cfg.model.num_layers] = o.per_layer[:cfg.model.num_layers]
         emit(c["report"], "csv", path)
     assert csv_text(cfgs, counters, per_layer) == path.read_bytes().decode()
+
+
+def test_native_csv_report_rejects_broken_identities():
+    """esim_report_csv refuses counters whose accounting identities do not hold
+    (metrics.check_identities, metrics.py:319-336)."""
+    from paper_2602_03921_b200 import SimConfig, HardwareSpec, builtin_spec, _abi
+    from paper_2602_03921_b200.sweep import csv_text
+    spec = builtin_spec("mixtral")
+    cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_fraction=0.05), working_precision="int4")
+    c = _abi.EsimCounters()
+    c.totals[0] = 5          # demanded 5, nothing resolved
+    with pytest.raises(ValueError):
+        csv_text([cfg], [c], np.zeros((1, spec.num_layers, _abi.ESIM_PL_FIELDS), np.int64))

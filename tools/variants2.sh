@@ -6,7 +6,7 @@ IFS=';' read -ra VS <<< "${VARIANTS}"
 i=0
 for V in "${VS[@]}"; do
   D=/tmp/var$i; mkdir -p $D; i=$((i+1))
-  for f in capi router replay ffn_gemm layer_step policy; do
+  for f in capi router replay ffn_gemm layer_step policy report; do
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC $V -c paper_2602_03921_b200/csrc/$f.cu -o $D/$f.o 2>&1 | grep -E "error" || true
   done
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $D/lib.so $D/*.o -lcudart
@@ -19,6 +19,7 @@ from paper_2602_03921_b200.sweep import DeviceSweep, c5_points
 cfgs, trs = c5_points(make_traces(list(range(1, 49))))
 ds = DeviceSweep(cfgs, trs)
 ds.step(); torch.cuda.synchronize()
+ds.tune_order(); ds.step(); torch.cuda.synchronize()
 ts = []
 for _ in range(3):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
