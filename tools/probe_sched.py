@@ -49,7 +49,7 @@ import json
 rows = []
 for i, c in enumerate(cfgs):
     r = res[i].counters
-    rows.append(dict(model=c.model.name, cap=c.hardware.capacity_fraction, bw=c.hardware.bandwidth_bytes_per_sec,
+    rows.append(dict(start_ms=float((st[i] - st.min()) / 1e6), sm=int(sm[i]), model=c.model.name, cap=c.hardware.capacity_fraction, bw=c.hardware.bandwidth_bytes_per_sec,
                      ev=c.eviction, seed=trs[i].seed if hasattr(trs[i], "seed") else 0, ms=float(dur[i]),
                      totals=[int(x) for x in r.totals], pf_pred=int(r.pf_pred_total), pf_dem=int(r.pf_dem_total),
                      n_recs=int(r.n_recs), ttft=int(r.ttft_us), total_us=int(r.total_us), passes=int(r.passes)))
