@@ -78,6 +78,43 @@ __global__ void build_tables_kernel(const int16_t* __restrict__ row_sel, const f
     }
 }
 
+// int8 expert (tile-major like the bf16 one, ffn.py; then fp32 scales: 2I
+// gate/up rows, H down rows) -> bf16 tile-major scratch entry: w = bf16(q * s_row).
+// One uint4 = 16 int8 of one row. grid: (chunks, n_entries)
+__global__ void dequant_int8_kernel(const int8_t* __restrict__ slots, int64_t slot_bytes,
+                                    const int32_t* __restrict__ entry_slot, __nv_bfloat16* __restrict__ scratch,
+                                    int I, int H) {
+    const int e = blockIdx.y;
+    const int8_t* src = slots + (int64_t)entry_slot[e] * slot_bytes;
+    const int64_t n1 = 2LL * I * H, n = 3LL * I * H;
+    const float* s1 = reinterpret_cast<const float*>(src + n);     // [2I]
+    const float* s2 = s1 + 2 * I;                                   // [H]
+    __nv_bfloat16* dst = scratch + (int64_t)e * n;
+    const int HT = H / 128;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n / 16; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = v * 16;
+        float sc;
+        if (j < n1) {                                   // w1 tile (m, k): [64 gate; 64 up] rows x 64
+            const int64_t t = j / 8192;
+            const int r = (int)((j % 8192) / 64);
+            const int m = (int)(t / (H / 64));
+            sc = r < 64 ? s1[m * 64 + r] : s1[I + m * 64 + (r - 64)];
+        } else {                                        // w2 tile (m, ht): 128 down rows x 64
+            const int64_t jj = j - n1;
+            const int64_t t = jj / 8192;
+            const int r = (int)((jj % 8192) / 64);
+            sc = s2[(int)(t % HT) * 128 + r];
+        }
+        const int4 q = reinterpret_cast<const int4*>(src)[v];
+        const int8_t* qb = reinterpret_cast<const int8_t*>(&q);
+        __align__(16) __nv_bfloat16 out[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) out[i] = __float2bfloat16((float)qb[i] * sc);
+        reinterpret_cast<uint4*>(dst + j)[0] = reinterpret_cast<const uint4*>(out)[0];
+        reinterpret_cast<uint4*>(dst + j)[1] = reinterpret_cast<const uint4*>(out)[1];
+    }
+}
+
 // rows of bf16 between device and mapped host memory (zero-copy over the link)
 __global__ void copy_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
@@ -108,6 +145,8 @@ struct Engine {
     int32_t* tables = nullptr;           // pool of [2][E] int32 (pos_of_expert, exec_slot) per flush
     int64_t table_cap = 0;
     int max_entries = 0;                 // FFN entries per flush: experts + token-count splits at 128
+    bool int8 = false;                   // weight_format 1: int8 slots, bf16 scratch per FFN entry
+    char* scratch = nullptr;             // int8: [max_entries][3*H*I] bf16 tile-major
     // per-run device scratch
     void* dev_scratch = nullptr;
     size_t dev_scratch_bytes = 0;
@@ -146,12 +185,21 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
     }
     // an expert with more than 128 tokens in a pass runs as several FFN entries of <= 128
     g->max_entries = E + (int)(((int64_t)p->max_tokens * p->top_k + 127) / 128);
-    g->expert_bytes = (size_t)3 * H * I * 2;
+    if (p->weight_format != 0 && p->weight_format != 1) { delete g; return ls_fail(-1, "unknown weight format"); }
+    g->int8 = p->weight_format == 1;
+    const size_t bf16_bytes = (size_t)3 * H * I * 2;
+    g->expert_bytes = g->int8 ? (size_t)3 * H * I + (size_t)4 * (2 * I + H) : bf16_bytes;
     CK(cudaHostAlloc(&g->store, g->expert_bytes * L * E, cudaHostAllocDefault));
     CK(cudaMalloc((void**)&g->slots, g->expert_bytes * p->n_slots));
-    std::vector<unsigned char> m1(128 * (size_t)p->n_slots), m2(128 * (size_t)p->n_slots);
-    for (int s = 0; s < p->n_slots; s++) {
-        const char* base = g->slots + g->expert_bytes * s;
+    // the FFN reads bf16 tile-major experts: the slots themselves (bf16) or the
+    // per-entry scratch pool the int8 slots are dequantised into
+    const int n_maps = g->int8 ? g->max_entries : p->n_slots;
+    if (g->int8) {
+        CK(cudaMalloc((void**)&g->scratch, bf16_bytes * g->max_entries));
+    }
+    std::vector<unsigned char> m1(128 * (size_t)n_maps), m2(128 * (size_t)n_maps);
+    for (int s = 0; s < n_maps; s++) {
+        const char* base = g->int8 ? g->scratch + bf16_bytes * s : g->slots + g->expert_bytes * s;
         // tile-major expert layout (ffn.py): every TMA box is one contiguous run
         if (esim_tmap_bf16(&m1[128 * s], base, (int64_t)2 * I * H / 64, 64, 128) ||
             esim_tmap_bf16(&m2[128 * s], base + (size_t)2 * I * H * 2, (int64_t)I * H / 64, 64, 128))
@@ -206,6 +254,7 @@ extern "C" int esim_ls_destroy(void* handle) {
     cudaDeviceSynchronize();
     cudaFreeHost(g->store);
     cudaFree(g->slots);
+    if (g->scratch) cudaFree(g->scratch);
     cudaFree(g->w1_maps);
     cudaFree(g->w2_maps);
     cudaFree(g->xg);
@@ -270,7 +319,7 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     CK(cudaHostAlloc((void**)&g->progress, (n_events + 2) * 8, cudaHostAllocMapped));
     volatile int64_t* prog = g->progress;
     for (int64_t i = 0; i < n_events + 2; i++) prog[i] = 0;
-    const int64_t table_need = (n_events * 2 + 64) * (E + g->max_entries);
+    const int64_t table_need = (n_events * 2 + 64) * (E + 2 * g->max_entries);
     if (table_need > g->table_cap) {
         if (g->tables) cudaFreeHost(g->tables);
         CK(cudaHostAlloc((void**)&g->tables, table_need * 4, cudaHostAllocMapped));
@@ -355,16 +404,22 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             for (int t : tok_of_pos) maxtok = std::max(maxtok, t);
             const int npad = npad_for(std::max(1, maxtok));
             if (npad < 0) return ls_fail(-1, "too many tokens per expert");
-            if (table_next + E + g->max_entries > g->table_cap) {                 // recycle the pool
+            if (table_next + E + 2 * g->max_entries > g->table_cap) {             // recycle the pool
                 CK(cudaStreamSynchronize(g->comp_st));
                 table_next = 0;
             }
             int32_t* tpos = g->tables + table_next;
-            int32_t* tslot = tpos + E;
-            table_next += E + g->max_entries;
+            int32_t* tslot = tpos + E;                  // FFN weight entry per position (slot, or scratch index)
+            int32_t* tsrc = tslot + g->max_entries;     // int8: the slot each scratch entry is dequantised from
+            table_next += E + 2 * g->max_entries;
             for (int e = 0; e < E; e++) tpos[e] = pos_of_expert[e];
-            for (int i = 0; i < n_exec; i++) tslot[i] = pend_slot[i];
+            for (int i = 0; i < n_exec; i++) tslot[i] = g->int8 ? i : pend_slot[i];
             for (int i = 0; i < n_exec; i++) CK(cudaStreamWaitEvent(g->comp_st, g->landed[pend_slot[i]], 0));
+            if (g->int8) {                          // int8 slots -> bf16 scratch entries 0..n_exec-1
+                for (int i = 0; i < n_exec; i++) tsrc[i] = pend_slot[i];
+                dequant_int8_kernel<<<dim3(96, n_exec), 256, 0, g->comp_st>>>(
+                    (const int8_t*)g->slots, (int64_t)g->expert_bytes, tsrc, (__nv_bfloat16*)g->scratch, I, H);
+            }
             build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
                                                                    g->tok_index, g->tok_weight);
             if (esim_ffn_gather(g->x, g->tok_index, g->xg, n_exec, npad, H, g->comp_st) ||

@@ -21,11 +21,17 @@ import numpy as np
 from . import _abi
 from ._device import DeviceTrace, _check, _torch, lib
 from .metrics import report_from_counters
+from .models import ConfigError
 
 
 class EsimLSParams(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("num_layers", "experts", "top_k", "hidden", "inter", "n_slots",
-                                         "max_tokens")]
+                                         "max_tokens", "weight_format")]
+
+
+# physical expert format per logical working precision: bf16 for fp16 (the
+# reference's "fp16" sizes), int8 + per-row fp32 scales for int8
+WEIGHT_FORMAT = {"fp16": 0, "int8": 1}
 
 
 class EsimLSResult(C.Structure):
@@ -80,7 +86,11 @@ class LayerStepEngine:
         m = cfg.model
         self.cfg, self.H, self.I = cfg, hidden, inter
         self.n_slots = cfg.capacity_bytes() // m.expert_bytes(cfg.working_precision)
-        p = EsimLSParams(m.num_layers, m.experts_per_layer, m.top_k, hidden, inter, self.n_slots, max_tokens)
+        if cfg.working_precision not in WEIGHT_FORMAT:
+            raise ConfigError(f"physical layer step stores fp16 (bf16) or int8 experts, not {cfg.working_precision}")
+        self.weight_format = WEIGHT_FORMAT[cfg.working_precision]
+        p = EsimLSParams(m.num_layers, m.experts_per_layer, m.top_k, hidden, inter, self.n_slots, max_tokens,
+                         self.weight_format)
         self._h = C.c_void_p()
         L = _bind()
         rc = L.esim_ls_create(C.addressof(p), C.addressof(self._h))
@@ -90,26 +100,59 @@ class LayerStepEngine:
         self.n_experts_total = m.num_layers * m.experts_per_layer
         nbytes = self.expert_bytes * self.n_experts_total
         buf = (C.c_uint8 * nbytes).from_address(L.esim_ls_store(self._h))
-        self.store = torch.frombuffer(buf, dtype=torch.bfloat16)   # pinned host view
+        self.store_bytes = torch.frombuffer(buf, dtype=torch.uint8)  # pinned host view
+        self.store = self.store_bytes.view(torch.bfloat16) if self.weight_format == 0 else self.store_bytes
         self.torch = torch
 
     def init_weights(self, seed: int = 0, std: float = 0.02) -> None:
-        """Random-init N(0, std) bf16 experts, generated on the GPU in chunks
-        and copied into the pinned store."""
+        """Random-init experts, generated on the GPU in chunks and copied into
+        the pinned store: bf16 N(0, std); int8: uniform codes in [-127, 127]
+        with per-row scales std*sqrt(3)/127 (the same std)."""
         torch = self.torch
         g = torch.Generator(device="cuda").manual_seed(seed)
-        per = self.expert_bytes // 2
-        chunk = max(1, min(64, (2 << 30) // self.expert_bytes))     # <= ~2 GiB of bf16 per generated chunk
-        for e0 in range(0, self.n_experts_total, chunk):
-            n = min(chunk, self.n_experts_total - e0)
-            w = (torch.randn(n * per, generator=g, device="cuda") * std).to(torch.bfloat16)
-            self.store[e0 * per:(e0 + n) * per].copy_(w)
+        chunk = max(1, min(64, (2 << 30) // self.expert_bytes))     # <= ~2 GiB generated per chunk
+        if self.weight_format == 0:
+            per = self.expert_bytes // 2
+            for e0 in range(0, self.n_experts_total, chunk):
+                n = min(chunk, self.n_experts_total - e0)
+                w = (torch.randn(n * per, generator=g, device="cuda") * std).to(torch.bfloat16)
+                self.store[e0 * per:(e0 + n) * per].copy_(w)
+        else:
+            H, I = self.H, self.I
+            nq, ns = 3 * H * I, 2 * I + H
+            for e0 in range(0, self.n_experts_total, chunk):
+                n = min(chunk, self.n_experts_total - e0)
+                q = torch.randint(-127, 128, (n, nq), generator=g, device="cuda", dtype=torch.int32).to(torch.int8)
+                sc = torch.full((n, ns), std * 3 ** 0.5 / 127, device="cuda") * \
+                    (0.5 + torch.rand((n, ns), generator=g, device="cuda"))
+                blob = torch.cat([q.view(torch.uint8), sc.contiguous().view(torch.uint8).view(n, ns * 4)], dim=1)
+                self.store_bytes[e0 * self.expert_bytes:(e0 + n) * self.expert_bytes].copy_(blob.reshape(-1))
         torch.cuda.synchronize()
 
     def expert_weights(self, layer: int, expert: int):
-        per = self.expert_bytes // 2
+        """The expert's stored bytes (bf16 elements, or raw int8 + scale bytes)."""
         i = layer * self.cfg.model.experts_per_layer + expert
-        return self.store[i * per:(i + 1) * per]
+        if self.weight_format == 0:
+            per = self.expert_bytes // 2
+            return self.store[i * per:(i + 1) * per]
+        return self.store_bytes[i * self.expert_bytes:(i + 1) * self.expert_bytes]
+
+    def expert_matrices(self, layer: int, expert: int):
+        """Logical (w1 [2I, H], wd [H, I]) as the FFN sees them (int8: bf16(q * scale)), fp32, on the GPU."""
+        from .ffn import expert_matrices
+        torch = self.torch
+        H, I = self.H, self.I
+        raw = self.expert_weights(layer, expert).cuda()
+        if self.weight_format == 0:
+            w1, wd = expert_matrices(raw, H, I)
+            return w1.float(), wd.float()
+        nq = 3 * H * I
+        q = raw[:nq].view(torch.int8).float()
+        sc = raw[nq:].view(torch.float32)
+        w1q, wdq = expert_matrices(q, H, I)
+        w1 = (w1q * sc[:2 * I, None]).to(torch.bfloat16).float()
+        wd = (wdq * sc[2 * I:, None]).to(torch.bfloat16).float()
+        return w1, wd
 
     def run(self, trace, x_prefill, x_decode, keep_outputs: bool = False) -> LayerStepResult:
         torch = self.torch

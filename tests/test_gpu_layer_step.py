@@ -19,7 +19,6 @@ def _reference(engine, trace, x0, xdec, served=None, I=1024):
     """No-cache fp32 forward; served[(pass, layer)][e] = the expert whose
     weights serve e's tokens (a substitute), or None when e was dropped."""
     import torch
-    from paper_2602_03921_b200.ffn import expert_matrices
     from paper_2602_03921_b200.routing import softmax_rows
     spec = trace.spec
     outs = []
@@ -33,8 +32,7 @@ def _reference(engine, trace, x0, xdec, served=None, I=1024):
                 we = (served or {}).get((p, ev.layer), {}).get(int(e), int(e))
                 if we is None:
                     continue
-                w = engine.expert_weights(ev.layer, we).cuda().float()
-                w1, wd = expert_matrices(w, H, I)
+                w1, wd = engine.expert_matrices(ev.layer, we)
                 act = (torch.nn.functional.silu(x.to(torch.bfloat16).float() @ w1[:I].T) *
                        (x.to(torch.bfloat16).float() @ w1[I:].T)).to(torch.bfloat16).float()
                 out = act @ wd.T
@@ -53,13 +51,22 @@ def test_layer_step_matches_nocache_reference(eviction, cap_experts, miss, inter
     _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts=16, top_k=4, prefill=8, decode=3)
 
 
+@pytest.mark.parametrize("eviction,cap_experts", [("ls", 6), ("lru", 3)])
+def test_layer_step_int8_experts(eviction, cap_experts, oracle_lib):
+    """int8 working precision: int8 experts (+ per-row scales) cross the link
+    and sit in the slots; each layer dequantises its executed experts into bf16
+    scratch for the FFN. Reference: the same dequantised weights in fp32."""
+    _run_case(eviction, cap_experts, "fetch", 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=3,
+              prec="int8")
+
+
 def test_layer_step_long_prefill_splits_experts(oracle_lib):
     """A 300-token prefill over 8 experts (top-4: ~150 tokens per expert): an
     expert with more than 128 tokens runs as several FFN entries."""
     _run_case("ls", 4, "fetch", 1024, oracle_lib, experts=8, top_k=4, prefill=300, decode=2)
 
 
-def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, prefill, decode):
+def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, prefill, decode, prec="fp16"):
     """I = 1408 is the Qwen1.5-MoE expert width (not a power of two); subst /
     drop follow the decision stream (substitute weights / no contribution)."""
     import torch
@@ -68,7 +75,8 @@ def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, pr
     I = inter
     eb = 3 * H * I * 2
     spec = ModelSpec("mini_moe", num_layers=4, experts_per_layer=experts, top_k=top_k, expert_bytes_fp16=eb)
-    cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=cap_experts * eb), working_precision="fp16",
+    cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=cap_experts * spec.expert_bytes(prec)),
+                    working_precision=prec,
                     eviction=eviction, prefetch="score", percentile=80.0, miss=miss, subst_tolerance=0.2,
                     drop_rank_threshold=2)
     tr = generate_synthetic(spec, seed=7, prefill_tokens=prefill, decode_tokens=decode)
