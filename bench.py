@@ -167,23 +167,24 @@ def layer_step_section(runs=2):
                    "logical_collision_rate": best.report["rates"]["collision_rate_demanded"],
                    "logical_ttft_us": best.report["timing"]["ttft_us"]}
     eng.close()
-    # the same request with int8 experts (int8 working precision: 102 slots in
-    # the same 0.6 GB, half the bytes per copy, dequantised per layer)
-    cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=614_400_000), working_precision="int8",
-                    eviction="ls", prefetch="score", percentile=80.0, miss="fetch")
-    eng = LayerStepEngine(cfg, 2048, 1024, max_tokens=64)
-    eng.init_weights(seed=0)
-    best = None
-    for _ in range(runs):
-        r = eng.run(tr, x0, xd)
-        best = r if best is None or r.total_ms < best.total_ms else best
-    out["ls_int8"] = {"ttft_ms": best.ttft_ms, "decode_tok_s": best.decode_tokens_per_sec, "total_ms": best.total_ms,
-                      "host_link_gbs": best.h2d_gbs, "host_link_frac": best.h2d_gbs / peak,
-                      "h2d_bytes": best.h2d_bytes, "copies": best.n_copies, "slots": eng.n_slots,
-                      "bytes_per_copy": eng.expert_bytes,
-                      "logical_hit_rate": best.report["rates"]["hit_rate"],
-                      "logical_ttft_us": best.report["timing"]["ttft_us"]}
-    eng.close()
+    # the same request with int8 / int4 experts (102 / 204 slots in the same
+    # 0.6 GB, 1/2 / 1/4 of the bytes per copy, dequantised per layer)
+    for prec in ("int8", "int4"):
+        cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=614_400_000), working_precision=prec,
+                        eviction="ls", prefetch="score", percentile=80.0, miss="fetch")
+        eng = LayerStepEngine(cfg, 2048, 1024, max_tokens=64)
+        eng.init_weights(seed=0)
+        best = None
+        for _ in range(runs):
+            r = eng.run(tr, x0, xd)
+            best = r if best is None or r.total_ms < best.total_ms else best
+        out["ls_" + prec] = {"ttft_ms": best.ttft_ms, "decode_tok_s": best.decode_tokens_per_sec,
+                             "total_ms": best.total_ms, "host_link_gbs": best.h2d_gbs,
+                             "host_link_frac": best.h2d_gbs / peak, "h2d_bytes": best.h2d_bytes,
+                             "copies": best.n_copies, "slots": eng.n_slots, "bytes_per_copy": eng.expert_bytes,
+                             "logical_hit_rate": best.report["rates"]["hit_rate"],
+                             "logical_ttft_us": best.report["timing"]["ttft_us"]}
+        eng.close()
     return out
 
 

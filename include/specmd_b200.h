@@ -288,8 +288,9 @@ typedef struct {
     int32_t hidden, inter;        /* OLMoE-1B-7B: 2048, 1024 (SwiGLU expert 3*H*I bf16) */
     int32_t n_slots;              /* HBM cache slots = capacity / working-precision expert bytes */
     int32_t max_tokens;           /* largest pass (<= 16384) */
-    int32_t weight_format;        /* 0: bf16 tile-major (3*H*I*2 B); 1: int8 tile-major + fp32 per-row
-                                     scales (3*H*I + 4*(2*I+H) B), copied as int8 and dequantised per
+    int32_t weight_format;        /* 0: bf16 tile-major (3*H*I*2 B); 1: int8 / 2: int4 (two per byte, low
+                                     nibble first) tile-major codes + fp32 per-row scales
+                                     (3*H*I*bits/8 + 4*(2*I+H) B), copied quantised and dequantised per
                                      layer into a bf16 scratch pool in front of the FFN */
 } EsimLSParams;
 

@@ -78,17 +78,20 @@ __global__ void build_tables_kernel(const int16_t* __restrict__ row_sel, const f
     }
 }
 
-// int8 expert (tile-major like the bf16 one, ffn.py; then fp32 scales: 2I
-// gate/up rows, H down rows) -> bf16 tile-major scratch entry: w = bf16(q * s_row).
-// One uint4 = 16 int8 of one row. grid: (chunks, n_entries)
-__global__ void dequant_int8_kernel(const int8_t* __restrict__ slots, int64_t slot_bytes,
-                                    const int32_t* __restrict__ entry_slot, __nv_bfloat16* __restrict__ scratch,
-                                    int I, int H) {
+// quantised expert (tile-major like the bf16 one, ffn.py; int8 codes, or
+// int4 codes two per byte, low nibble first, two's complement; then fp32
+// scales: 2I gate/up rows, H down rows) -> bf16 tile-major scratch entry:
+// w = bf16(q * s_row). A thread converts 16 consecutive codes of one row.
+// grid: (chunks, n_entries)
+template <int BITS>
+__global__ void dequant_kernel(const uint8_t* __restrict__ slots, int64_t slot_bytes,
+                               const int32_t* __restrict__ entry_slot, __nv_bfloat16* __restrict__ scratch, int I,
+                               int H) {
     const int e = blockIdx.y;
-    const int8_t* src = slots + (int64_t)entry_slot[e] * slot_bytes;
+    const uint8_t* src = slots + (int64_t)entry_slot[e] * slot_bytes;
     const int64_t n1 = 2LL * I * H, n = 3LL * I * H;
-    const float* s1 = reinterpret_cast<const float*>(src + n);     // [2I]
-    const float* s2 = s1 + 2 * I;                                   // [H]
+    const float* s1 = reinterpret_cast<const float*>(src + n * BITS / 8);   // [2I]
+    const float* s2 = s1 + 2 * I;                                          // [H]
     __nv_bfloat16* dst = scratch + (int64_t)e * n;
     const int HT = H / 128;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n / 16; v += (int64_t)gridDim.x * blockDim.x) {
@@ -105,8 +108,21 @@ __global__ void dequant_int8_kernel(const int8_t* __restrict__ slots, int64_t sl
             const int r = (int)((jj % 8192) / 64);
             sc = s2[(int)(t % HT) * 128 + r];
         }
-        const int4 q = reinterpret_cast<const int4*>(src)[v];
-        const int8_t* qb = reinterpret_cast<const int8_t*>(&q);
+        int8_t qb[16];
+        if (BITS == 8) {
+            const int4 q = reinterpret_cast<const int4*>(src)[v];
+            const int8_t* b = reinterpret_cast<const int8_t*>(&q);
+#pragma unroll
+            for (int i = 0; i < 16; i++) qb[i] = b[i];
+        } else {
+            const uint2 q = reinterpret_cast<const uint2*>(src)[v];
+            const uint8_t* b = reinterpret_cast<const uint8_t*>(&q);
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                qb[2 * i] = (int8_t)(b[i] << 4) >> 4;         // low nibble, sign-extended
+                qb[2 * i + 1] = (int8_t)b[i] >> 4;            // high nibble
+            }
+        }
         __align__(16) __nv_bfloat16 out[16];
 #pragma unroll
         for (int i = 0; i < 16; i++) out[i] = __float2bfloat16((float)qb[i] * sc);
@@ -145,7 +161,7 @@ struct Engine {
     int32_t* tables = nullptr;           // pool of [2][E] int32 (pos_of_expert, exec_slot) per flush
     int64_t table_cap = 0;
     int max_entries = 0;                 // FFN entries per flush: experts + token-count splits at 128
-    bool int8 = false;                   // weight_format 1: int8 slots, bf16 scratch per FFN entry
+    int qbits = 0;                       // weight_format 1: int8, 2: int4 slots (0: bf16), bf16 scratch per FFN entry
     char* scratch = nullptr;             // int8: [max_entries][3*H*I] bf16 tile-major
     // per-run device scratch
     void* dev_scratch = nullptr;
@@ -185,21 +201,21 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
     }
     // an expert with more than 128 tokens in a pass runs as several FFN entries of <= 128
     g->max_entries = E + (int)(((int64_t)p->max_tokens * p->top_k + 127) / 128);
-    if (p->weight_format != 0 && p->weight_format != 1) { delete g; return ls_fail(-1, "unknown weight format"); }
-    g->int8 = p->weight_format == 1;
+    if (p->weight_format < 0 || p->weight_format > 2) { delete g; return ls_fail(-1, "unknown weight format"); }
+    g->qbits = p->weight_format == 1 ? 8 : p->weight_format == 2 ? 4 : 0;
     const size_t bf16_bytes = (size_t)3 * H * I * 2;
-    g->expert_bytes = g->int8 ? (size_t)3 * H * I + (size_t)4 * (2 * I + H) : bf16_bytes;
+    g->expert_bytes = g->qbits ? (size_t)3 * H * I * g->qbits / 8 + (size_t)4 * (2 * I + H) : bf16_bytes;
     CK(cudaHostAlloc(&g->store, g->expert_bytes * L * E, cudaHostAllocDefault));
     CK(cudaMalloc((void**)&g->slots, g->expert_bytes * p->n_slots));
     // the FFN reads bf16 tile-major experts: the slots themselves (bf16) or the
     // per-entry scratch pool the int8 slots are dequantised into
-    const int n_maps = g->int8 ? g->max_entries : p->n_slots;
-    if (g->int8) {
+    const int n_maps = g->qbits ? g->max_entries : p->n_slots;
+    if (g->qbits) {
         CK(cudaMalloc((void**)&g->scratch, bf16_bytes * g->max_entries));
     }
     std::vector<unsigned char> m1(128 * (size_t)n_maps), m2(128 * (size_t)n_maps);
     for (int s = 0; s < n_maps; s++) {
-        const char* base = g->int8 ? g->scratch + bf16_bytes * s : g->slots + g->expert_bytes * s;
+        const char* base = g->qbits ? g->scratch + bf16_bytes * s : g->slots + g->expert_bytes * s;
         // tile-major expert layout (ffn.py): every TMA box is one contiguous run
         if (esim_tmap_bf16(&m1[128 * s], base, (int64_t)2 * I * H / 64, 64, 128) ||
             esim_tmap_bf16(&m2[128 * s], base + (size_t)2 * I * H * 2, (int64_t)I * H / 64, 64, 128))
@@ -413,12 +429,16 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             int32_t* tsrc = tslot + g->max_entries;     // int8: the slot each scratch entry is dequantised from
             table_next += E + 2 * g->max_entries;
             for (int e = 0; e < E; e++) tpos[e] = pos_of_expert[e];
-            for (int i = 0; i < n_exec; i++) tslot[i] = g->int8 ? i : pend_slot[i];
+            for (int i = 0; i < n_exec; i++) tslot[i] = g->qbits ? i : pend_slot[i];
             for (int i = 0; i < n_exec; i++) CK(cudaStreamWaitEvent(g->comp_st, g->landed[pend_slot[i]], 0));
-            if (g->int8) {                          // int8 slots -> bf16 scratch entries 0..n_exec-1
+            if (g->qbits) {                         // int8 / int4 slots -> bf16 scratch entries 0..n_exec-1
                 for (int i = 0; i < n_exec; i++) tsrc[i] = pend_slot[i];
-                dequant_int8_kernel<<<dim3(96, n_exec), 256, 0, g->comp_st>>>(
-                    (const int8_t*)g->slots, (int64_t)g->expert_bytes, tsrc, (__nv_bfloat16*)g->scratch, I, H);
+                if (g->qbits == 8)
+                    dequant_kernel<8><<<dim3(96, n_exec), 256, 0, g->comp_st>>>(
+                        (const uint8_t*)g->slots, (int64_t)g->expert_bytes, tsrc, (__nv_bfloat16*)g->scratch, I, H);
+                else
+                    dequant_kernel<4><<<dim3(96, n_exec), 256, 0, g->comp_st>>>(
+                        (const uint8_t*)g->slots, (int64_t)g->expert_bytes, tsrc, (__nv_bfloat16*)g->scratch, I, H);
             }
             build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
                                                                    g->tok_index, g->tok_weight);

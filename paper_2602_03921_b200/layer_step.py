@@ -30,8 +30,9 @@ class EsimLSParams(C.Structure):
 
 
 # physical expert format per logical working precision: bf16 for fp16 (the
-# reference's "fp16" sizes), int8 + per-row fp32 scales for int8
-WEIGHT_FORMAT = {"fp16": 0, "int8": 1}
+# reference's "fp16" sizes), int8 / int4 codes + per-row fp32 scales
+WEIGHT_FORMAT = {"fp16": 0, "int8": 1, "int4": 2}
+_QBITS = {0: 0, 1: 8, 2: 4}
 
 
 class EsimLSResult(C.Structure):
@@ -87,7 +88,8 @@ class LayerStepEngine:
         self.cfg, self.H, self.I = cfg, hidden, inter
         self.n_slots = cfg.capacity_bytes() // m.expert_bytes(cfg.working_precision)
         if cfg.working_precision not in WEIGHT_FORMAT:
-            raise ConfigError(f"physical layer step stores fp16 (bf16) or int8 experts, not {cfg.working_precision}")
+            raise ConfigError(f"physical layer step stores fp16 (bf16), int8 or int4 experts, not "
+                              f"{cfg.working_precision}")
         self.weight_format = WEIGHT_FORMAT[cfg.working_precision]
         p = EsimLSParams(m.num_layers, m.experts_per_layer, m.top_k, hidden, inter, self.n_slots, max_tokens,
                          self.weight_format)
@@ -119,13 +121,20 @@ class LayerStepEngine:
                 self.store[e0 * per:(e0 + n) * per].copy_(w)
         else:
             H, I = self.H, self.I
+            bits = _QBITS[self.weight_format]
+            qmax = 127 if bits == 8 else 7
             nq, ns = 3 * H * I, 2 * I + H
             for e0 in range(0, self.n_experts_total, chunk):
                 n = min(chunk, self.n_experts_total - e0)
-                q = torch.randint(-127, 128, (n, nq), generator=g, device="cuda", dtype=torch.int32).to(torch.int8)
-                sc = torch.full((n, ns), std * 3 ** 0.5 / 127, device="cuda") * \
+                q = torch.randint(-qmax, qmax + 1, (n, nq), generator=g, device="cuda", dtype=torch.int32)
+                if bits == 8:
+                    codes = q.to(torch.int8).view(torch.uint8)
+                else:                                    # two per byte, low nibble first
+                    u = (q & 0xF).to(torch.uint8).view(n, nq // 2, 2)
+                    codes = (u[:, :, 0] | (u[:, :, 1] << 4)).contiguous()
+                sc = torch.full((n, ns), std * 3 ** 0.5 / qmax, device="cuda") * \
                     (0.5 + torch.rand((n, ns), generator=g, device="cuda"))
-                blob = torch.cat([q.view(torch.uint8), sc.contiguous().view(torch.uint8).view(n, ns * 4)], dim=1)
+                blob = torch.cat([codes, sc.contiguous().view(torch.uint8).view(n, ns * 4)], dim=1)
                 self.store_bytes[e0 * self.expert_bytes:(e0 + n) * self.expert_bytes].copy_(blob.reshape(-1))
         torch.cuda.synchronize()
 
@@ -147,8 +156,15 @@ class LayerStepEngine:
             w1, wd = expert_matrices(raw, H, I)
             return w1.float(), wd.float()
         nq = 3 * H * I
-        q = raw[:nq].view(torch.int8).float()
-        sc = raw[nq:].view(torch.float32)
+        if _QBITS[self.weight_format] == 8:
+            q = raw[:nq].view(torch.int8).float()
+            sc = raw[nq:].view(torch.float32)
+        else:
+            b = raw[:nq // 2].to(torch.int16)
+            lo, hi = b & 0xF, (b >> 4) & 0xF
+            q = torch.stack([lo, hi], dim=1).reshape(-1)
+            q = torch.where(q >= 8, q - 16, q).float()
+            sc = raw[nq // 2:].view(torch.float32)
         w1q, wdq = expert_matrices(q, H, I)
         w1 = (w1q * sc[:2 * I, None]).to(torch.bfloat16).float()
         wd = (wdq * sc[2 * I:, None]).to(torch.bfloat16).float()

@@ -51,13 +51,13 @@ def test_layer_step_matches_nocache_reference(eviction, cap_experts, miss, inter
     _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts=16, top_k=4, prefill=8, decode=3)
 
 
-@pytest.mark.parametrize("eviction,cap_experts", [("ls", 6), ("lru", 3)])
-def test_layer_step_int8_experts(eviction, cap_experts, oracle_lib):
-    """int8 working precision: int8 experts (+ per-row scales) cross the link
-    and sit in the slots; each layer dequantises its executed experts into bf16
-    scratch for the FFN. Reference: the same dequantised weights in fp32."""
+@pytest.mark.parametrize("eviction,cap_experts,prec", [("ls", 6, "int8"), ("lru", 3, "int8"), ("ls", 7, "int4")])
+def test_layer_step_quantised_experts(eviction, cap_experts, prec, oracle_lib):
+    """int8 / int4 working precision: quantised experts (+ per-row scales) cross
+    the link and sit in the slots; each layer dequantises its executed experts
+    into bf16 scratch for the FFN. Reference: the same dequantised weights in fp32."""
     _run_case(eviction, cap_experts, "fetch", 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=3,
-              prec="int8")
+              prec=prec)
 
 
 def test_layer_step_long_prefill_splits_experts(oracle_lib):
