@@ -288,10 +288,15 @@ typedef struct {
     int32_t hidden, inter;        /* OLMoE-1B-7B: 2048, 1024 (SwiGLU expert 3*H*I bf16) */
     int32_t n_slots;              /* HBM cache slots = capacity / working-precision expert bytes */
     int32_t max_tokens;           /* largest pass (<= 16384) */
-    int32_t weight_format;        /* 0: bf16 tile-major (3*H*I*2 B); 1: int8 / 2: int4 (two per byte, low
-                                     nibble first) tile-major codes + fp32 per-row scales
-                                     (3*H*I*bits/8 + 4*(2*I+H) B), copied quantised and dequantised per
-                                     layer into a bf16 scratch pool in front of the FFN */
+    int32_t weight_format;        /* precision code of the working precision (models.PRECISION_ORDER):
+                                     0: bf16 tile-major (3*H*I*2 B); 1: int8 / 2: int4 / 3: int2 tile-major
+                                     codes (several per byte, lowest bits first, two's complement) +
+                                     fp32 per-row scales (3*H*I*bits/8 + 4*(2*I+H) B), copied quantised
+                                     and dequantised per layer into a bf16 scratch pool for the FFN */
+    int32_t prec_mask;            /* precisions held in the store (bit = code); 0 = just weight_format.
+                                     Mixed-precision miss policies (fetch_low / fetch_priority) need
+                                     every rung of the ladder: each slot then holds whichever
+                                     precision the decision stream fetched into it */
 } EsimLSParams;
 
 typedef struct {
@@ -301,12 +306,17 @@ typedef struct {
     int64_t status;
 } EsimLSResult;
 
-/* Engine: pinned host expert store [L][E][3*H*I] bf16 (esim_ls_store returns
- * it for initialisation), n_slots HBM slots with TMA descriptors, copy and
- * compute streams, per-slot RAW/WAR events. */
+/* Engine: pinned host expert store, one region [L][E][bytes(prec)] per
+ * precision in prec_mask, ascending code (esim_ls_store returns it for
+ * initialisation, esim_ls_format the per-expert bytes and region offset of
+ * one precision, 0 if absent), n_slots HBM slots sized for the largest
+ * precision with TMA descriptors, copy and compute streams, per-slot
+ * RAW/WAR events. esim_ls_expert_bytes: the working precision's bytes. */
 int esim_ls_create(const EsimLSParams *p, void **handle);
 void *esim_ls_store(void *handle);
 int64_t esim_ls_expert_bytes(void *handle);
+int64_t esim_ls_format(void *handle, int32_t prec, int64_t *store_offset);
+int64_t esim_ls_store_bytes(void *handle);
 void *esim_ls_slots(void *handle);
 int esim_ls_destroy(void *handle);
 const char *esim_ls_last_error(void);

@@ -79,20 +79,20 @@ __global__ void build_tables_kernel(const int16_t* __restrict__ row_sel, const f
 }
 
 // quantised expert (tile-major like the bf16 one, ffn.py; int8 codes, or
-// int4 codes two per byte, low nibble first, two's complement; then fp32
-// scales: 2I gate/up rows, H down rows) -> bf16 tile-major scratch entry:
-// w = bf16(q * s_row). A thread converts 16 consecutive codes of one row.
-// grid: (chunks, n_entries)
+// int4 / int2 codes two / four per byte, lowest bits first, two's
+// complement; then fp32 scales: 2I gate/up rows, H down rows) -> bf16
+// tile-major scratch entry: w = bf16(q * s_row). A thread converts 16
+// consecutive codes of one row. pairs[2e] = source slot, pairs[2e+1] =
+// scratch entry. grid: (chunks, n_entries of this precision)
 template <int BITS>
 __global__ void dequant_kernel(const uint8_t* __restrict__ slots, int64_t slot_bytes,
-                               const int32_t* __restrict__ entry_slot, __nv_bfloat16* __restrict__ scratch, int I,
+                               const int32_t* __restrict__ pairs, __nv_bfloat16* __restrict__ scratch, int I,
                                int H) {
-    const int e = blockIdx.y;
-    const uint8_t* src = slots + (int64_t)entry_slot[e] * slot_bytes;
+    const uint8_t* src = slots + (int64_t)pairs[2 * blockIdx.y] * slot_bytes;
     const int64_t n1 = 2LL * I * H, n = 3LL * I * H;
     const float* s1 = reinterpret_cast<const float*>(src + n * BITS / 8);   // [2I]
     const float* s2 = s1 + 2 * I;                                          // [H]
-    __nv_bfloat16* dst = scratch + (int64_t)e * n;
+    __nv_bfloat16* dst = scratch + (int64_t)pairs[2 * blockIdx.y + 1] * n;
     const int HT = H / 128;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n / 16; v += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = v * 16;
@@ -114,6 +114,10 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ slots, int64_t slot_b
             const int8_t* b = reinterpret_cast<const int8_t*>(&q);
 #pragma unroll
             for (int i = 0; i < 16; i++) qb[i] = b[i];
+        } else if (BITS == 2) {
+            const uint32_t q = reinterpret_cast<const uint32_t*>(src)[v];
+#pragma unroll
+            for (int i = 0; i < 16; i++) qb[i] = (int8_t)(q >> (2 * i) << 6) >> 6;   // sign-extended pair
         } else {
             const uint2 q = reinterpret_cast<const uint2*>(src)[v];
             const uint8_t* b = reinterpret_cast<const uint8_t*>(&q);
@@ -139,9 +143,14 @@ __global__ void copy_rows_kernel(const uint4* __restrict__ src, uint4* __restric
 
 struct Engine {
     EsimLSParams P;
-    size_t expert_bytes = 0;
-    void* store = nullptr;               // pinned host: [L][E][expert]
-    char* slots = nullptr;               // device: [n_slots][expert]
+    size_t expert_bytes = 0;             // working precision
+    int mask = 0;                        // precisions in the store
+    size_t fmt_bytes[4] = {};            // per expert, by precision code (0: absent)
+    size_t store_off[4] = {};            // region offsets in the store
+    size_t store_bytes = 0, slot_bytes = 0;
+    int n_slot_maps = 0;                 // FFN maps over the slots (bf16 present), then scratch maps
+    void* store = nullptr;               // pinned host: per precision [L][E][expert]
+    char* slots = nullptr;               // device: [n_slots][slot_bytes]
     void *w1_maps = nullptr, *w2_maps = nullptr;
     void *xg = nullptr, *act = nullptr;
     void *x_maps[4] = {}, *act_maps[4] = {};
@@ -161,8 +170,7 @@ struct Engine {
     int32_t* tables = nullptr;           // pool of [2][E] int32 (pos_of_expert, exec_slot) per flush
     int64_t table_cap = 0;
     int max_entries = 0;                 // FFN entries per flush: experts + token-count splits at 128
-    int qbits = 0;                       // weight_format 1: int8, 2: int4 slots (0: bf16), bf16 scratch per FFN entry
-    char* scratch = nullptr;             // int8: [max_entries][3*H*I] bf16 tile-major
+    char* scratch = nullptr;             // quantised: [max_entries][3*H*I] bf16 tile-major
     // per-run device scratch
     void* dev_scratch = nullptr;
     size_t dev_scratch_bytes = 0;
@@ -201,21 +209,35 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
     }
     // an expert with more than 128 tokens in a pass runs as several FFN entries of <= 128
     g->max_entries = E + (int)(((int64_t)p->max_tokens * p->top_k + 127) / 128);
-    if (p->weight_format < 0 || p->weight_format > 2) { delete g; return ls_fail(-1, "unknown weight format"); }
-    g->qbits = p->weight_format == 1 ? 8 : p->weight_format == 2 ? 4 : 0;
+    if (p->weight_format < 0 || p->weight_format > 3 || (p->prec_mask & ~0xF) ||
+        (p->prec_mask && !(p->prec_mask >> p->weight_format & 1))) {
+        delete g;
+        return ls_fail(-1, "unknown weight format / precision mask");
+    }
+    g->mask = p->prec_mask ? p->prec_mask : 1 << p->weight_format;
     const size_t bf16_bytes = (size_t)3 * H * I * 2;
-    g->expert_bytes = g->qbits ? (size_t)3 * H * I * g->qbits / 8 + (size_t)4 * (2 * I + H) : bf16_bytes;
-    CK(cudaHostAlloc(&g->store, g->expert_bytes * L * E, cudaHostAllocDefault));
-    CK(cudaMalloc((void**)&g->slots, g->expert_bytes * p->n_slots));
-    // the FFN reads bf16 tile-major experts: the slots themselves (bf16) or the
-    // per-entry scratch pool the int8 slots are dequantised into
-    const int n_maps = g->qbits ? g->max_entries : p->n_slots;
-    if (g->qbits) {
+    for (int pc = 0; pc < 4; pc++) {
+        if (!(g->mask >> pc & 1)) continue;
+        const int bits = 16 >> pc;                                    // 16, 8, 4, 2
+        g->fmt_bytes[pc] = pc == 0 ? bf16_bytes : (size_t)3 * H * I * bits / 8 + (size_t)4 * (2 * I + H);
+        g->store_off[pc] = g->store_bytes;
+        g->store_bytes += g->fmt_bytes[pc] * L * E;
+        g->slot_bytes = std::max(g->slot_bytes, (g->fmt_bytes[pc] + 255) & ~size_t(255));
+    }
+    g->expert_bytes = g->fmt_bytes[p->weight_format];
+    CK(cudaHostAlloc(&g->store, g->store_bytes, cudaHostAllocDefault));
+    CK(cudaMalloc((void**)&g->slots, g->slot_bytes * p->n_slots));
+    // the FFN reads bf16 tile-major experts: the slots themselves (bf16) and/or
+    // the per-entry scratch pool quantised slots are dequantised into
+    g->n_slot_maps = (g->mask & 1) ? p->n_slots : 0;
+    const int n_maps = g->n_slot_maps + ((g->mask & 0xE) ? g->max_entries : 0);
+    if (g->mask & 0xE) {
         CK(cudaMalloc((void**)&g->scratch, bf16_bytes * g->max_entries));
     }
     std::vector<unsigned char> m1(128 * (size_t)n_maps), m2(128 * (size_t)n_maps);
     for (int s = 0; s < n_maps; s++) {
-        const char* base = g->qbits ? g->scratch + bf16_bytes * s : g->slots + g->expert_bytes * s;
+        const char* base = s < g->n_slot_maps ? g->slots + g->slot_bytes * s
+                                               : g->scratch + bf16_bytes * (s - g->n_slot_maps);
         // tile-major expert layout (ffn.py): every TMA box is one contiguous run
         if (esim_tmap_bf16(&m1[128 * s], base, (int64_t)2 * I * H / 64, 64, 128) ||
             esim_tmap_bf16(&m2[128 * s], base + (size_t)2 * I * H * 2, (int64_t)I * H / 64, 64, 128))
@@ -262,6 +284,13 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
 
 extern "C" void* esim_ls_store(void* handle) { return static_cast<Engine*>(handle)->store; }
 extern "C" int64_t esim_ls_expert_bytes(void* handle) { return (int64_t) static_cast<Engine*>(handle)->expert_bytes; }
+extern "C" int64_t esim_ls_format(void* handle, int32_t prec, int64_t* store_offset) {
+    const Engine* g = static_cast<Engine*>(handle);
+    if (prec < 0 || prec > 3 || !g->fmt_bytes[prec]) return 0;
+    if (store_offset) *store_offset = (int64_t)g->store_off[prec];
+    return (int64_t)g->fmt_bytes[prec];
+}
+extern "C" int64_t esim_ls_store_bytes(void* handle) { return (int64_t) static_cast<Engine*>(handle)->store_bytes; }
 extern "C" void* esim_ls_slots(void* handle) { return static_cast<Engine*>(handle)->slots; }
 
 extern "C" int esim_ls_destroy(void* handle) {
@@ -312,9 +341,21 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     if (tr.num_layers != L || tr.experts != E || tr.top_k != K) return ls_fail(-1, "trace geometry mismatch");
     const int64_t n_events = tr.n_events;
     const int64_t wbytes = cfg->expert_bytes[cfg->working_prec];
-    if (cfg->miss == ESIM_MISS_FETCH_LOW || cfg->miss == ESIM_MISS_FETCH_PRIORITY)
-        return ls_fail(-1, "physical layer step stores bf16 experts: mixed-precision miss policies are logical only");
-    if (cfg->capacity_bytes / wbytes > P.n_slots) return ls_fail(-1, "more logical slots than physical slots");
+    // every precision the decisions can fetch must be in the store; the slot
+    // pool must hold the most residents the logical capacity allows
+    int64_t min_bytes = wbytes;
+    if (cfg->working_prec != P.weight_format || !g->fmt_bytes[cfg->working_prec])
+        return ls_fail(-1, "working precision differs from the engine's weight format");
+    if (cfg->miss == ESIM_MISS_FETCH_LOW || cfg->miss == ESIM_MISS_FETCH_PRIORITY) {
+        for (int i = 0; i < cfg->n_precisions; i++) {
+            const int pc = cfg->precisions[i];
+            if (pc < 0 || pc > 3 || !g->fmt_bytes[pc])
+                return ls_fail(-1, "mixed-precision miss policy: a ladder precision is missing from the store");
+            min_bytes = std::min(min_bytes, cfg->expert_bytes[pc]);
+        }
+    }
+    if (std::min<int64_t>(cfg->capacity_bytes / min_bytes, (int64_t)L * E) > P.n_slots)
+        return ls_fail(-1, "more logical slots than physical slots");
     int max_t = 0;
     for (int p = 0; p < tr.n_passes; p++) max_t = std::max(max_t, h_pass_tokens[p]);
     if (max_t > P.max_tokens) return ls_fail(-1, "pass has more tokens than the engine was sized for");
@@ -335,7 +376,7 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     CK(cudaHostAlloc((void**)&g->progress, (n_events + 2) * 8, cudaHostAllocMapped));
     volatile int64_t* prog = g->progress;
     for (int64_t i = 0; i < n_events + 2; i++) prog[i] = 0;
-    const int64_t table_need = (n_events * 2 + 64) * (E + 2 * g->max_entries);
+    const int64_t table_need = (n_events * 2 + 64) * (E + 3 * g->max_entries);
     if (table_need > g->table_cap) {
         if (g->tables) cudaFreeHost(g->tables);
         CK(cudaHostAlloc((void**)&g->tables, table_need * 4, cudaHostAllocMapped));
@@ -388,6 +429,8 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     if (rc) return ls_fail(rc, "replay launch");
 
     std::vector<int> phys(L * E, -1);                // ident -> physical slot
+    std::vector<int8_t> slot_prec(P.n_slots, -1);    // precision each slot holds
+    std::vector<int> scratch_of(P.n_slots, -1);      // per flush: slot -> its dequantised scratch entry
     std::vector<int> free_slots;
     for (int s = P.n_slots - 1; s >= 0; s--) free_slots.push_back(s);
     std::vector<int> pend_slot;                      // pending executed slots of the current layer (positions)
@@ -395,22 +438,25 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     std::vector<char> slot_pending(P.n_slots, 0);
     std::vector<int> tok_of_pos;
     int64_t table_next = 0;
-    int64_t n_copies = 0, n_demand = 0, n_prefetch = 0, n_cancel = 0, n_flush = 0, n_exec_total = 0;
+    int64_t n_copies = 0, n_demand = 0, n_prefetch = 0, n_cancel = 0, n_flush = 0, n_exec_total = 0, h2d = 0;
     int64_t row = 0;                                 // first token row of the current event
     int64_t rec_pos = 0;
     int64_t out_row = 0;
-    const int64_t expert_bytes = (int64_t)g->expert_bytes;
-
-    auto issue_copy = [&](int ident) -> int {
+    auto issue_copy = [&](int ident, int prec) -> int {
         if (free_slots.empty()) return ls_fail(-2, "no free physical slot (decision stream inconsistent)");
+        if (phys[ident] >= 0) return ls_fail(-2, "fetch of a resident expert (decision stream inconsistent)");
+        if (prec < 0 || prec > 3 || !g->fmt_bytes[prec]) return ls_fail(-2, "fetch precision not in the store");
         const int s = free_slots.back();
         free_slots.pop_back();
         phys[ident] = s;
+        slot_prec[s] = (int8_t)prec;
+        const size_t nb = g->fmt_bytes[prec];
         CK(cudaStreamWaitEvent(g->copy_st, g->freed[s], 0));                       // WAR
-        CK(cudaMemcpyAsync(g->slots + (size_t)s * expert_bytes, (char*)g->store + (size_t)ident * expert_bytes,
-                           expert_bytes, cudaMemcpyHostToDevice, g->copy_st));
+        CK(cudaMemcpyAsync(g->slots + (size_t)s * g->slot_bytes, (char*)g->store + g->store_off[prec] + ident * nb,
+                           nb, cudaMemcpyHostToDevice, g->copy_st));
         CK(cudaEventRecord(g->landed[s], g->copy_st));                              // RAW guard
         n_copies++;
+        h2d += (int64_t)nb;
         return 0;
     };
     auto flush = [&](int layer_rows, const int16_t* rs, const float* rw, bool residual) -> int {
@@ -420,25 +466,40 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             for (int t : tok_of_pos) maxtok = std::max(maxtok, t);
             const int npad = npad_for(std::max(1, maxtok));
             if (npad < 0) return ls_fail(-1, "too many tokens per expert");
-            if (table_next + E + 2 * g->max_entries > g->table_cap) {             // recycle the pool
+            if (table_next + E + 3 * g->max_entries > g->table_cap) {             // recycle the pool
                 CK(cudaStreamSynchronize(g->comp_st));
                 table_next = 0;
             }
             int32_t* tpos = g->tables + table_next;
-            int32_t* tslot = tpos + E;                  // FFN weight entry per position (slot, or scratch index)
-            int32_t* tsrc = tslot + g->max_entries;     // int8: the slot each scratch entry is dequantised from
-            table_next += E + 2 * g->max_entries;
+            int32_t* tslot = tpos + E;                  // FFN map per position: slot (bf16) or scratch entry
+            int32_t* tpair = tslot + g->max_entries;    // quantised: (slot, scratch entry) grouped by precision
+            table_next += E + 3 * g->max_entries;
             for (int e = 0; e < E; e++) tpos[e] = pos_of_expert[e];
-            for (int i = 0; i < n_exec; i++) tslot[i] = g->qbits ? i : pend_slot[i];
             for (int i = 0; i < n_exec; i++) CK(cudaStreamWaitEvent(g->comp_st, g->landed[pend_slot[i]], 0));
-            if (g->qbits) {                         // int8 / int4 slots -> bf16 scratch entries 0..n_exec-1
-                for (int i = 0; i < n_exec; i++) tsrc[i] = pend_slot[i];
-                if (g->qbits == 8)
-                    dequant_kernel<8><<<dim3(96, n_exec), 256, 0, g->comp_st>>>(
-                        (const uint8_t*)g->slots, (int64_t)g->expert_bytes, tsrc, (__nv_bfloat16*)g->scratch, I, H);
-                else
-                    dequant_kernel<4><<<dim3(96, n_exec), 256, 0, g->comp_st>>>(
-                        (const uint8_t*)g->slots, (int64_t)g->expert_bytes, tsrc, (__nv_bfloat16*)g->scratch, I, H);
+            int n_pair = 0;
+            for (int pc = 0; pc < 4; pc++) {            // slots holding precision pc
+                if (!(g->mask >> pc & 1)) continue;
+                const int first = n_pair;
+                for (int i = 0; i < n_exec; i++) {
+                    const int sl = pend_slot[i];
+                    if (slot_prec[sl] != pc) continue;
+                    if (pc == 0) { tslot[i] = sl; continue; }
+                    if (scratch_of[sl] < 0) {           // one dequant per slot (splits / substitutes share it)
+                        scratch_of[sl] = n_pair;
+                        tpair[2 * n_pair] = sl;
+                        tpair[2 * n_pair + 1] = n_pair;
+                        n_pair++;
+                    }
+                    tslot[i] = g->n_slot_maps + scratch_of[sl];
+                }
+                if (n_pair == first) continue;
+                const dim3 grid(96, n_pair - first);
+                const int32_t* pr = tpair + 2 * first;
+                const uint8_t* sl = (const uint8_t*)g->slots;
+                __nv_bfloat16* sc = (__nv_bfloat16*)g->scratch;
+                if (pc == 1) dequant_kernel<8><<<grid, 256, 0, g->comp_st>>>(sl, g->slot_bytes, pr, sc, I, H);
+                if (pc == 2) dequant_kernel<4><<<grid, 256, 0, g->comp_st>>>(sl, g->slot_bytes, pr, sc, I, H);
+                if (pc == 3) dequant_kernel<2><<<grid, 256, 0, g->comp_st>>>(sl, g->slot_bytes, pr, sc, I, H);
             }
             build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
                                                                    g->tok_index, g->tok_weight);
@@ -447,7 +508,10 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
                                     g->act_maps[npad_index(npad)], tslot, g->tok_index, g->tok_weight, g->act, g->y,
                                     n_exec, npad, I, H, std::max(1, maxtok), g->comp_st))
                 return ls_fail(-3, "ffn launch failed");
-            for (int i = 0; i < n_exec; i++) CK(cudaEventRecord(g->freed[pend_slot[i]], g->comp_st));
+            for (int i = 0; i < n_exec; i++) {
+                CK(cudaEventRecord(g->freed[pend_slot[i]], g->comp_st));
+                scratch_of[pend_slot[i]] = -1;
+            }
             n_exec_total += n_exec;
             n_flush++;
         }
@@ -463,7 +527,9 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     // experts appears once per expert (same slot, separate token lists), so
     // no entry ever holds more than one expert's tokens
     // (more than 128 tokens: consecutive entries of 128 on the same slot)
-    auto execute = [&](int expert, int slot, int tokens) {
+    auto execute = [&](int expert, int slot, int tokens, int prec) -> int {
+        if (slot < 0 || slot_prec[slot] != prec)
+            return ls_fail(-2, "executed expert not resident at its recorded precision (decision stream inconsistent)");
         slot_pending[slot] = 1;
         pos_of_expert[expert] = (int)pend_slot.size();
         do {
@@ -471,6 +537,7 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             tok_of_pos.push_back(std::min(tokens, 128));
             tokens -= 128;
         } while (tokens > 0);
+        return 0;
     };
 
     for (int64_t ev = 0; ev < n_events; ev++) {
@@ -499,8 +566,8 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
                     phys[v] = -1;
                 }
             } else if (r.kind == ESIM_REC_PREFETCH) {
-                if (r.i0 == 1) {                         // started
-                    if ((rc = issue_copy(r.i1 * E + r.i2))) return rc;
+                if (r.i0 == 1) {                         // started (working precision, engine.py:684)
+                    if ((rc = issue_copy(r.i1 * E + r.i2, cfg->working_prec))) return rc;
                     n_prefetch++;
                 } else if (r.i0 == 4 && r.i3 == 4) {     // dropped superseded: cancelled in flight
                     const int id = r.i1 * E + r.i2;
@@ -509,15 +576,16 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
                 }
             } else if (r.kind == ESIM_REC_ACCESS) {
                 const int outcome = r.i3 & 0xFF;
+                const int prec = ((r.i3 >> 16) & 0xFF) - 1;  // the precision it executes at
                 const int id = r.layer * E + r.i0;
-                if (outcome == 1) {                      // demand fetch
-                    if ((rc = issue_copy(id))) return rc;
+                if (outcome == 1) {                      // demand fetch (fetch_low / priority: below working)
+                    if ((rc = issue_copy(id, prec))) return rc;
                     n_demand++;
                 }
                 if (outcome <= 2) {
-                    execute(r.i0, phys[id], r.i1);
+                    if ((rc = execute(r.i0, phys[id], r.i1, prec))) return rc;
                 } else if (outcome == 4) {               // substitute runs the missing expert's tokens
-                    execute(r.i0, phys[r.layer * E + r.i4], r.i1);
+                    if ((rc = execute(r.i0, phys[r.layer * E + r.i4], r.i1, prec))) return rc;
                 }
             } else if (r.kind == ESIM_REC_ROUTE) {
                 if ((rc = flush(T, rs, rw, true))) return rc;
@@ -548,7 +616,7 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     res->total_ms = total;
     res->decode_ms = total - ttft;
     res->host_enqueue_ms = host_ms;
-    res->h2d_bytes = n_copies * expert_bytes;
+    res->h2d_bytes = h2d;
     res->n_copies = n_copies;
     res->n_demand_copies = n_demand;
     res->n_prefetch_copies = n_prefetch;

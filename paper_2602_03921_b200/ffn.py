@@ -107,6 +107,15 @@ def expert_matrices(flat, hidden: int, inter: int):
     return w1, wd
 
 
+def pack_expert(w1, wd, hidden: int, inter: int):
+    """Inverse of expert_matrices: logical w1 [2I, H] and wd [H, I] -> the
+    expert's tile-major flat 3*H*I elements."""
+    H, I = hidden, inter
+    t1 = w1.reshape(2, I // 64, 64, H // 64, 64).permute(1, 3, 0, 2, 4).reshape(-1)
+    t2 = wd.reshape(H // 128, 128, I // 64, 64).permute(2, 0, 1, 3).reshape(-1)
+    return _torch().cat([t1, t2])
+
+
 def routing_tables(row_sel: np.ndarray, row_w: np.ndarray, executed: dict, npad: int):
     """Per executed expert token lists: executed maps expert -> (position, substitute-or-self).
     Returns tok_index [n_exec*npad] (-1 pad) and tok_weight [n_exec*npad]."""

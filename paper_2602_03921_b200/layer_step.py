@@ -26,13 +26,16 @@ from .models import ConfigError
 
 class EsimLSParams(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("num_layers", "experts", "top_k", "hidden", "inter", "n_slots",
-                                         "max_tokens", "weight_format")]
+                                         "max_tokens", "weight_format", "prec_mask")]
 
 
-# physical expert format per logical working precision: bf16 for fp16 (the
-# reference's "fp16" sizes), int8 / int4 codes + per-row fp32 scales
-WEIGHT_FORMAT = {"fp16": 0, "int8": 1, "int4": 2}
-_QBITS = {0: 0, 1: 8, 2: 4}
+# physical expert format per logical precision (models.PRECISION_CODE): bf16
+# for fp16 (the reference's "fp16" sizes), int8 / int4 / int2 codes + per-row
+# fp32 scales
+WEIGHT_FORMAT = {"fp16": 0, "int8": 1, "int4": 2, "int2": 3}
+_QBITS = {0: 0, 1: 8, 2: 4, 3: 2}
+_QMAX = {8: 127, 4: 7, 2: 1}
+_MIXED_MISS = ("fetch_low", "fetch_priority")
 
 
 class EsimLSResult(C.Structure):
@@ -51,6 +54,10 @@ def _bind():
         L.esim_ls_store.restype = vp
         L.esim_ls_expert_bytes.argtypes = [vp]
         L.esim_ls_expert_bytes.restype = C.c_int64
+        L.esim_ls_format.argtypes = [vp, C.c_int32, vp]
+        L.esim_ls_format.restype = C.c_int64
+        L.esim_ls_store_bytes.argtypes = [vp]
+        L.esim_ls_store_bytes.restype = C.c_int64
         L.esim_ls_slots.argtypes = [vp]
         L.esim_ls_slots.restype = vp
         L.esim_ls_destroy.argtypes = [vp]
@@ -80,19 +87,27 @@ class LayerStepResult:
 
 
 class LayerStepEngine:
-    """Pinned expert store + HBM slots + copy/compute streams for one model."""
+    """Pinned expert store + HBM slots + copy/compute streams for one model.
+
+    The store holds the working precision, or -- for the mixed-precision miss
+    policies (fetch_low / fetch_priority, miss.py) -- every rung of the
+    model's precision ladder; each HBM slot then holds whichever precision
+    the decision stream fetched into it and the FFN dequantises per slot."""
 
     def __init__(self, cfg, hidden: int = 2048, inter: int = 1024, max_tokens: int = 64):
         torch = _torch()
         m = cfg.model
         self.cfg, self.H, self.I = cfg, hidden, inter
-        self.n_slots = cfg.capacity_bytes() // m.expert_bytes(cfg.working_precision)
         if cfg.working_precision not in WEIGHT_FORMAT:
-            raise ConfigError(f"physical layer step stores fp16 (bf16), int8 or int4 experts, not "
+            raise ConfigError(f"physical layer step stores fp16 (bf16), int8, int4 or int2 experts, not "
                               f"{cfg.working_precision}")
         self.weight_format = WEIGHT_FORMAT[cfg.working_precision]
+        self.precisions = tuple(m.precisions) if cfg.miss in _MIXED_MISS else (cfg.working_precision,)
+        self.prec_mask = sum(1 << WEIGHT_FORMAT[q] for q in set(self.precisions) | {cfg.working_precision})
+        lowest = min(m.expert_bytes(q) for q in self.precisions + (cfg.working_precision,))
+        self.n_slots = min(cfg.capacity_bytes() // lowest, m.num_layers * m.experts_per_layer)
         p = EsimLSParams(m.num_layers, m.experts_per_layer, m.top_k, hidden, inter, self.n_slots, max_tokens,
-                         self.weight_format)
+                         self.weight_format, self.prec_mask)
         self._h = C.c_void_p()
         L = _bind()
         rc = L.esim_ls_create(C.addressof(p), C.addressof(self._h))
@@ -100,71 +115,98 @@ class LayerStepEngine:
             raise RuntimeError(f"esim_ls_create failed ({rc}): {L.esim_ls_last_error().decode()}")
         self.expert_bytes = L.esim_ls_expert_bytes(self._h)
         self.n_experts_total = m.num_layers * m.experts_per_layer
-        nbytes = self.expert_bytes * self.n_experts_total
+        self.formats = {}                                # precision code -> (bytes per expert, store offset)
+        for code in range(4):
+            off = C.c_int64()
+            nb = L.esim_ls_format(self._h, code, C.addressof(off))
+            if nb:
+                self.formats[code] = (nb, off.value)
+        nbytes = L.esim_ls_store_bytes(self._h)
         buf = (C.c_uint8 * nbytes).from_address(L.esim_ls_store(self._h))
         self.store_bytes = torch.frombuffer(buf, dtype=torch.uint8)  # pinned host view
-        self.store = self.store_bytes.view(torch.bfloat16) if self.weight_format == 0 else self.store_bytes
         self.torch = torch
+
+    def _row_of_element(self):
+        """Scale row (0..2I+H) of every element of a tile-major expert."""
+        from .ffn import pack_expert
+        torch, H, I = self.torch, self.H, self.I
+        r1 = torch.arange(2 * I, device="cuda", dtype=torch.int64)[:, None].expand(2 * I, H)
+        r2 = (2 * I + torch.arange(H, device="cuda", dtype=torch.int64))[:, None].expand(H, I)
+        return pack_expert(r1, r2, H, I)
 
     def init_weights(self, seed: int = 0, std: float = 0.02) -> None:
         """Random-init experts, generated on the GPU in chunks and copied into
-        the pinned store: bf16 N(0, std); int8: uniform codes in [-127, 127]
-        with per-row scales std*sqrt(3)/127 (the same std)."""
+        the pinned store: bf16 masters N(0, std); every quantised precision
+        in the store is the per-row quantisation of the same master
+        (int8 / int4: symmetric absmax scales; int2: ternary codes with the
+        row's mean |w| as scale), so all rungs of one expert agree."""
         torch = self.torch
+        H, I = self.H, self.I
+        nq, ns = 3 * H * I, 2 * I + H
         g = torch.Generator(device="cuda").manual_seed(seed)
-        chunk = max(1, min(64, (2 << 30) // self.expert_bytes))     # <= ~2 GiB generated per chunk
-        if self.weight_format == 0:
-            per = self.expert_bytes // 2
-            for e0 in range(0, self.n_experts_total, chunk):
-                n = min(chunk, self.n_experts_total - e0)
-                w = (torch.randn(n * per, generator=g, device="cuda") * std).to(torch.bfloat16)
-                self.store[e0 * per:(e0 + n) * per].copy_(w)
-        else:
-            H, I = self.H, self.I
-            bits = _QBITS[self.weight_format]
-            qmax = 127 if bits == 8 else 7
-            nq, ns = 3 * H * I, 2 * I + H
-            for e0 in range(0, self.n_experts_total, chunk):
-                n = min(chunk, self.n_experts_total - e0)
-                q = torch.randint(-qmax, qmax + 1, (n, nq), generator=g, device="cuda", dtype=torch.int32)
+        chunk = max(1, min(32, (1 << 30) // (nq * 4)))
+        rows = self._row_of_element() if any(c for c in self.formats) else None
+        for e0 in range(0, self.n_experts_total, chunk):
+            n = min(chunk, self.n_experts_total - e0)
+            w = (torch.randn(n, nq, generator=g, device="cuda") * std).to(torch.bfloat16)
+            for code, (nb, off) in self.formats.items():
+                dst = self.store_bytes[off + e0 * nb:off + (e0 + n) * nb]
+                if code == 0:
+                    dst.copy_(w.view(torch.uint8).reshape(-1))
+                    continue
+                bits = _QBITS[code]
+                qmax = _QMAX[bits]
+                wf = w.float()
+                idx = rows.expand(n, nq)
+                if bits == 2:
+                    sc = torch.zeros(n, ns, device="cuda").scatter_add_(1, idx, wf.abs()) / \
+                        torch.bincount(rows, minlength=ns).float()
+                else:
+                    sc = torch.zeros(n, ns, device="cuda").scatter_reduce_(1, idx, wf.abs(), "amax") / qmax
+                sc = torch.clamp(sc, min=1e-12)
+                q = torch.clamp(torch.round(wf / torch.gather(sc, 1, idx)), -qmax, qmax).to(torch.int32)
                 if bits == 8:
                     codes = q.to(torch.int8).view(torch.uint8)
-                else:                                    # two per byte, low nibble first
-                    u = (q & 0xF).to(torch.uint8).view(n, nq // 2, 2)
-                    codes = (u[:, :, 0] | (u[:, :, 1] << 4)).contiguous()
-                sc = torch.full((n, ns), std * 3 ** 0.5 / qmax, device="cuda") * \
-                    (0.5 + torch.rand((n, ns), generator=g, device="cuda"))
+                else:                                    # 8/bits per byte, lowest bits first
+                    per = 8 // bits
+                    u = (q & ((1 << bits) - 1)).to(torch.uint8).view(n, nq // per, per)
+                    codes = u[:, :, 0].clone()
+                    for j in range(1, per):
+                        codes |= u[:, :, j] << (bits * j)
                 blob = torch.cat([codes, sc.contiguous().view(torch.uint8).view(n, ns * 4)], dim=1)
-                self.store_bytes[e0 * self.expert_bytes:(e0 + n) * self.expert_bytes].copy_(blob.reshape(-1))
+                dst.copy_(blob.reshape(-1))
         torch.cuda.synchronize()
 
-    def expert_weights(self, layer: int, expert: int):
-        """The expert's stored bytes (bf16 elements, or raw int8 + scale bytes)."""
+    def expert_weights(self, layer: int, expert: int, precision: str | None = None):
+        """The expert's stored bytes at `precision` (default: working):
+        bf16 elements, or raw codes + scale bytes."""
+        code = WEIGHT_FORMAT[precision or self.cfg.working_precision]
+        nb, off = self.formats[code]
         i = layer * self.cfg.model.experts_per_layer + expert
-        if self.weight_format == 0:
-            per = self.expert_bytes // 2
-            return self.store[i * per:(i + 1) * per]
-        return self.store_bytes[i * self.expert_bytes:(i + 1) * self.expert_bytes]
+        raw = self.store_bytes[off + i * nb:off + (i + 1) * nb]
+        return raw.view(self.torch.bfloat16) if code == 0 else raw
 
-    def expert_matrices(self, layer: int, expert: int):
-        """Logical (w1 [2I, H], wd [H, I]) as the FFN sees them (int8: bf16(q * scale)), fp32, on the GPU."""
+    def expert_matrices(self, layer: int, expert: int, precision: str | None = None):
+        """Logical (w1 [2I, H], wd [H, I]) as the FFN sees them (quantised:
+        bf16(q * scale)), fp32, on the GPU."""
         from .ffn import expert_matrices
         torch = self.torch
         H, I = self.H, self.I
-        raw = self.expert_weights(layer, expert).cuda()
-        if self.weight_format == 0:
+        code = WEIGHT_FORMAT[precision or self.cfg.working_precision]
+        raw = self.expert_weights(layer, expert, precision).cuda()
+        if code == 0:
             w1, wd = expert_matrices(raw, H, I)
             return w1.float(), wd.float()
         nq = 3 * H * I
-        if _QBITS[self.weight_format] == 8:
+        bits = _QBITS[code]
+        if bits == 8:
             q = raw[:nq].view(torch.int8).float()
-            sc = raw[nq:].view(torch.float32)
         else:
-            b = raw[:nq // 2].to(torch.int16)
-            lo, hi = b & 0xF, (b >> 4) & 0xF
-            q = torch.stack([lo, hi], dim=1).reshape(-1)
-            q = torch.where(q >= 8, q - 16, q).float()
-            sc = raw[nq // 2:].view(torch.float32)
+            per = 8 // bits
+            b = raw[:nq // per].to(torch.int16)
+            q = torch.stack([(b >> (bits * j)) & ((1 << bits) - 1) for j in range(per)], dim=1).reshape(-1)
+            q = torch.where(q >= (1 << (bits - 1)), q - (1 << bits), q).float()
+        sc = raw[nq * bits // 8:].view(torch.float32)
         w1q, wdq = expert_matrices(q, H, I)
         w1 = (w1q * sc[:2 * I, None]).to(torch.bfloat16).float()
         wd = (wdq * sc[2 * I:, None]).to(torch.bfloat16).float()

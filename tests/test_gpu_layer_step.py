@@ -15,9 +15,10 @@ pytestmark = pytest.mark.gpu
 H, I = 2048, 1024
 
 
-def _reference(engine, trace, x0, xdec, served=None, I=1024):
+def _reference(engine, trace, x0, xdec, served=None, I=1024, prec_of=None):
     """No-cache fp32 forward; served[(pass, layer)][e] = the expert whose
-    weights serve e's tokens (a substitute), or None when e was dropped."""
+    weights serve e's tokens (a substitute), or None when e was dropped;
+    prec_of[(pass, layer, e)] = the precision those weights run at."""
     import torch
     from paper_2602_03921_b200.routing import softmax_rows
     spec = trace.spec
@@ -32,7 +33,7 @@ def _reference(engine, trace, x0, xdec, served=None, I=1024):
                 we = (served or {}).get((p, ev.layer), {}).get(int(e), int(e))
                 if we is None:
                     continue
-                w1, wd = engine.expert_matrices(ev.layer, we)
+                w1, wd = engine.expert_matrices(ev.layer, we, (prec_of or {}).get((p, ev.layer, int(e))))
                 act = (torch.nn.functional.silu(x.to(torch.bfloat16).float() @ w1[:I].T) *
                        (x.to(torch.bfloat16).float() @ w1[I:].T)).to(torch.bfloat16).float()
                 out = act @ wd.T
@@ -51,13 +52,29 @@ def test_layer_step_matches_nocache_reference(eviction, cap_experts, miss, inter
     _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts=16, top_k=4, prefill=8, decode=3)
 
 
-@pytest.mark.parametrize("eviction,cap_experts,prec", [("ls", 6, "int8"), ("lru", 3, "int8"), ("ls", 7, "int4")])
+@pytest.mark.parametrize("eviction,cap_experts,prec", [("ls", 6, "int8"), ("lru", 3, "int8"), ("ls", 7, "int4"),
+                                                  ("ls", 5, "int2")])
 def test_layer_step_quantised_experts(eviction, cap_experts, prec, oracle_lib):
-    """int8 / int4 working precision: quantised experts (+ per-row scales) cross
-    the link and sit in the slots; each layer dequantises its executed experts
-    into bf16 scratch for the FFN. Reference: the same dequantised weights in fp32."""
+    """int8 / int4 / int2 working precision: quantised experts (+ per-row
+    scales) cross the link and sit in the slots; each layer dequantises its
+    executed experts into bf16 scratch for the FFN. Reference: the same
+    dequantised weights in fp32."""
     _run_case(eviction, cap_experts, "fetch", 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=3,
               prec=prec)
+
+
+@pytest.mark.parametrize("eviction,cap_experts,miss,working,ladder",
+                         [("ls", 5, "fetch_low", "fp16", ("fp16", "int8", "int4", "int2")),
+                          ("lru", 4, "fetch_priority", "fp16", ("fp16", "int8", "int4", "int2")),
+                          ("ls", 6, "fetch_priority", "int8", ("int8", "int4", "int2"))])
+def test_layer_step_mixed_precision(eviction, cap_experts, miss, working, ladder, oracle_lib):
+    """fetch_low / fetch_priority (miss.py): demand misses fetch a lower rung
+    of the ladder; slots hold mixed precisions, each executed expert runs at
+    the precision its AccessRec names (bf16 slots read directly, quantised
+    slots dequantised), and the copies carry that precision's bytes."""
+    res = _run_case(eviction, cap_experts, miss, 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=4,
+                    prec=working, ladder=ladder)
+    assert len(res["precisions"]) > 1, res["precisions"]
 
 
 def test_layer_step_long_prefill_splits_experts(oracle_lib):
@@ -66,7 +83,8 @@ def test_layer_step_long_prefill_splits_experts(oracle_lib):
     _run_case("ls", 4, "fetch", 1024, oracle_lib, experts=8, top_k=4, prefill=300, decode=2)
 
 
-def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, prefill, decode, prec="fp16"):
+def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, prefill, decode, prec="fp16",
+              ladder=None):
     """I = 1408 is the Qwen1.5-MoE expert width (not a power of two); subst /
     drop follow the decision stream (substitute weights / no contribution)."""
     import torch
@@ -74,7 +92,8 @@ def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, pr
     from paper_2602_03921_b200.layer_step import LayerStepEngine
     I = inter
     eb = 3 * H * I * 2
-    spec = ModelSpec("mini_moe", num_layers=4, experts_per_layer=experts, top_k=top_k, expert_bytes_fp16=eb)
+    spec = ModelSpec("mini_moe", num_layers=4, experts_per_layer=experts, top_k=top_k, expert_bytes_fp16=eb,
+                     **({"precisions": ladder} if ladder else {}))
     cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=cap_experts * spec.expert_bytes(prec)),
                     working_precision=prec,
                     eviction=eviction, prefetch="score", percentile=80.0, miss=miss, subst_tolerance=0.2,
@@ -88,15 +107,20 @@ def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, pr
     res = eng.run(tr, x0, xd, keep_outputs=True)
     o = oracle_lib.run(cfg, tr, full_log=True)
     assert json.dumps(o.report) == json.dumps(res.report)
-    served = {}
+    served, prec_of = {}, {}
     for r in o.log:
-        if type(r).__name__ == "AccessRec" and r.outcome in ("drop", "subst"):
+        if type(r).__name__ != "AccessRec":
+            continue
+        if r.outcome in ("drop", "subst"):
             served.setdefault((r.pass_id, r.layer), {})[r.expert] = r.substitute if r.outcome == "subst" else None
-    if miss != "fetch":
+        if r.precision is not None:
+            prec_of[(r.pass_id, r.layer, r.expert)] = r.precision
+    if miss in ("subst", "drop"):
         assert served, "the case must exercise its miss policy"
     got = res.out.view(-1, H).float()
-    ref = _reference(eng, tr, x0, xd, served, I).cpu()
+    ref = _reference(eng, tr, x0, xd, served, I, prec_of).cpu()
     err = (got - ref).abs().max().item() / ref.abs().max().item()
     assert err <= 1e-2, f"max rel err {err:.3e}"
     assert res.n_copies >= res.report["totals"]["misses"] - res.report["totals"]["prefetch_started"]
     eng.close()
+    return {"precisions": sorted(set(prec_of.values()))}

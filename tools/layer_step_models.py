@@ -4,7 +4,7 @@ Qwen1.5-MoE-A2.7B shape (24 x 60, top-4, H=2048, I=1408 -> 17,301,504 B/expert)
 at 5 % capacity with expert substitution. Decisions are checked against the C
 oracle (test infrastructure) for the same config; TTFT / decode tok/s / host
 link measured with CUDA events.
-usage: python tools/layer_step_models.py [model] [miss] [capacity_fraction or bytes,...] [policies] [decode_tokens] [fp16|int8]
+usage: python tools/layer_step_models.py [model] [miss] [capacity_fraction or bytes,...] [policies] [decode_tokens] [fp16|int8|int4|int2]
 Mixtral (configs[2]): 32 x 8 top-2, H=4096, I=14336, 352,321,536 B/expert -> a 90 GB pinned store."""
 import json, sys, time
 sys.path.insert(0, ".")
@@ -44,7 +44,8 @@ for frac in fracs:
         eng = LayerStepEngine(big, H, I, max_tokens=64)
         eng.init_weights(seed=0)
         out["n_slots_allocated"] = eng.n_slots
-        out["store_gb"] = eng.expert_bytes * eng.n_experts_total / 1e9
+        out["store_gb"] = eng.store_bytes.numel() / 1e9
+        out["store_precisions"] = list(eng.precisions)
         out["init_s"] = time.time() - t0
     eng.cfg = cfg
     best = None
@@ -54,7 +55,7 @@ for frac in fracs:
     ref = oracle.run(cfg, tr, full_log=False).report
     out[f"{ev}@{frac}"] = {"n_slots": cfg.capacity_bytes() // spec.expert_bytes(prec), "precision": prec,
                "copy_bytes": eng.expert_bytes, "ttft_ms": best.ttft_ms, "decode_tok_s": best.decode_tokens_per_sec, "total_ms": best.total_ms,
-               "host_link_gbs": best.h2d_gbs, "copies": best.n_copies, "ffn_batches": best.n_ffn_batches,
+               "host_link_gbs": best.h2d_gbs, "h2d_gb": best.h2d_bytes / 1e9, "copies": best.n_copies, "ffn_batches": best.n_ffn_batches,
                "logical_hit_rate": best.report["rates"]["hit_rate"],
                "substituted": best.report["totals"].get("substituted"),
                "decisions_match_oracle": json.dumps(ref) == json.dumps(best.report)}
