@@ -350,6 +350,14 @@ int esim_ffn_experts_ex(const void *d_w1_maps, const void *d_w2_maps, const void
                         int32_t max_tok, void *stream);
 int esim_ffn_residual(void *d_x, float *d_y, int64_t n, void *stream);
 int esim_ffn_set_trace(void *d_trace);
+/* Decode-like layers (<= 4 tokens per expert) over quantised slots: slot
+ * pool d_slots (slot_bytes apart, tile-major codes of `bits` 8 / 4 / 2 then
+ * fp32 row scales, as the layer step stores them), d_exec_slot = slot per
+ * executed expert; dequantisation is fused into the FFN's A operand
+ * (ffn_decode_q_kernel). x map: the gathered tokens, box 16 rows. */
+int esim_ffn_experts_q(const void *d_slots, int64_t slot_bytes, int32_t bits, const void *d_x_map,
+                       const int32_t *d_exec_slot, const int32_t *d_tok_index, const float *d_tok_weight,
+                       float *d_y, int32_t n_exec, int32_t inter, int32_t hidden, void *stream);
 
 #ifdef __cplusplus
 }

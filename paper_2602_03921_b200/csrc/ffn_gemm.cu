@@ -72,6 +72,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
         : "memory");
 }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -216,6 +222,8 @@ struct FfnArgs {
     uint32_t* sync;                  // [n_exec * n_kc] tile counters, [n_exec * n_kc] done counter (self-resetting)
     int I, H, n_exec, n_kc;
     unsigned long long* trace;       // optional [n_units][8] globaltimer ns: [0] first stage ready, [2] accumulator ready, [3] epilogue end
+    const uint8_t* qslots;           // quantised decode kernel: slot pool (codes + fp32 row scales per slot)
+    int64_t slot_bytes;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -652,6 +660,276 @@ static int ffn_grid_cap() {
     return sms;
 }
 
+// ---- decode path over quantised slots: dequantisation fused into the A operand ----
+// Same units and epilogue as ffn_decode_kernel, but the weight tiles stay in
+// their quantised form all the way into shared memory: the producer bulk-copies
+// each 128 x 64 tile's codes (8192 * BITS / 8 contiguous bytes of the
+// tile-major slot, layer_step.cu) into a code ring, four converter warps turn
+// them into the 128B-swizzled bf16 A tile (w = bf16(q * s_row), the row
+// scales read through L1), fence the generic writes into the async proxy and
+// arrive on the A ring's full barrier; the MMA issuer is unchanged. HBM reads
+// per expert: 3*H*I*BITS/8 + scales instead of the dequantise-to-scratch
+// path's codes + 2 x 3*H*I*2 B (scratch write + FFN read).
+// The unit's gathered tokens (NPAD x H bf16 <= 64 KB) are loaded once per
+// unit into their own buffer (every gemm1 step reuses them), and so are its
+// row scales (64 gate + 64 up + all H down rows, double-buffered by unit):
+// a scale read from global per tile put an HBM latency on every tile.
+// Warps: 0 producer, 1 MMA, 2-5 epilogue, 6-13 converters (two per SMSP: the
+// conversion is ALU work on the tile's critical path; int -> float goes through
+// the 1.5 * 2^23 magic-number add instead of the quarter-rate I2F).
+constexpr int kDecQConv = 256;
+constexpr int kDecQThreads = 192 + kDecQConv;
+
+template <int BITS>
+struct DecQSmem {
+    static constexpr int AS = 4, QS = 8;
+    static constexpr int QBYTES = BM * BK * BITS / 8;
+    alignas(1024) __nv_bfloat16 a[AS][BM * BK];
+    alignas(1024) __nv_bfloat16 xs[32][16 * BK];          // the unit's tokens, one 16 x 64 box per k (H <= 2048)
+    alignas(1024) __nv_bfloat16 act_tile[16 * 64];
+    alignas(128) uint8_t q[QS][QBYTES];
+    alignas(16) float sc[2][128 + 2048];                  // per unit: gate, up, then the H down-row scales
+    float xchg[64][17];
+    uint64_t full[AS], empty[AS], qfull[QS], qempty[QS], xfull, xempty, sfull[2], sempty[2];
+    uint64_t t1full, t1empty, actrdy, t2full, t2empty;
+    uint32_t tmem;
+};
+
+template <int BITS>
+__global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __grid_constant__ FfnArgs g) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    using S = DecQSmem<BITS>;
+    constexpr int AS = S::AS, QS = S::QS;
+    constexpr uint32_t QBYTES = S::QBYTES;
+    constexpr int NPAD = 16;
+    auto& s = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m1 = g.I / 64, n_units = g.n_exec * m1, n_ht = g.H / BM, KT = g.H / BK;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < AS; i++) { mbar_init(&s.full[i], kDecQConv); mbar_init(&s.empty[i], 1); }
+        for (int i = 0; i < QS; i++) { mbar_init(&s.qfull[i], 1); mbar_init(&s.qempty[i], kDecQConv); }
+        mbar_init(&s.xfull, 1); mbar_init(&s.xempty, 1);
+        for (int i = 0; i < 2; i++) { mbar_init(&s.sfull[i], 1); mbar_init(&s.sempty[i], kDecQConv); }
+        mbar_init(&s.t1full, 1); mbar_init(&s.t1empty, 4); mbar_init(&s.actrdy, 64);
+        mbar_init(&s.t2full, 1); mbar_init(&s.t2empty, 4);
+        fence_barrier_init();
+        prefetch_tmap(g.x_map);
+    }
+    if (warp == 0) tmem_alloc(&s.tmem, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s.tmem;
+    const int64_t n1 = 2LL * g.I * g.H;                   // w1 codes; then the w2 codes
+    const int64_t soff = 3LL * g.I * g.H * BITS / 8;      // fp32 scales: 2I gate/up rows, H down rows
+
+    if (warp == 0) {
+        if (lane == 0) {                                  // ---- producer: code tiles + the unit's tokens
+            int kq = 0, j = 0;
+            auto code_tile = [&](const uint8_t* src) {
+                const int st = kq % QS;
+                if (kq >= QS) mbar_wait(&s.qempty[st], ((kq / QS) - 1) & 1);
+                mbar_expect_tx(&s.qfull[st], QBYTES);
+                bulk_load(s.q[st], src, QBYTES, &s.qfull[st]);
+                kq++;
+            };
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
+                const int e = u / m1, mt = u - e * m1;
+                const uint8_t* base = g.qslots + (int64_t)g.exec_slot[e] * g.slot_bytes;
+                const float* s1 = reinterpret_cast<const float*>(base + soff);
+                const int sb = j & 1;
+                if (j >= 2) mbar_wait(&s.sempty[sb], ((j >> 1) - 1) & 1);
+                mbar_expect_tx(&s.sfull[sb], (uint32_t)(128 + g.H) * 4);
+                bulk_load(s.sc[sb], s1 + mt * 64, 256, &s.sfull[sb]);
+                bulk_load(s.sc[sb] + 64, s1 + g.I + mt * 64, 256, &s.sfull[sb]);
+                bulk_load(s.sc[sb] + 128, s1 + 2 * g.I, (uint32_t)g.H * 4, &s.sfull[sb]);
+                int k0 = 0;
+                if (j == 0) {                             // weights stream before the gathered tokens exist
+                    k0 = QS < KT ? QS : KT;
+                    for (int k = 0; k < k0; k++) code_tile(base + (int64_t)(mt * KT + k) * QBYTES);
+                    pdl_wait();
+                }
+                if (j >= 1) mbar_wait(&s.xempty, (j - 1) & 1);
+                mbar_expect_tx(&s.xfull, (uint32_t)(KT * NPAD * BK * 2));
+                for (int k = 0; k < KT; k++) tma_load_2d(s.xs[k], g.x_map, &s.xfull, k * BK, e * NPAD);
+                for (int k = k0; k < KT; k++) code_tile(base + (int64_t)(mt * KT + k) * QBYTES);
+                for (int ht = 0; ht < n_ht; ht++)
+                    code_tile(base + n1 * BITS / 8 + (int64_t)(mt * n_ht + ht) * QBYTES);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                                  // ---- MMA issuer
+            constexpr uint32_t idesc = idesc_bf16(BM, NPAD);
+            const uint64_t bact = umma_desc(s.act_tile);
+            int ka = 0, j = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
+                if (j >= 1) mbar_wait(&s.t1empty, (j - 1) & 1);
+                mbar_wait(&s.xfull, j & 1);
+                tc_fence_after();
+                for (int k = 0; k < KT; k++, ka++) {
+                    const int st = ka % AS;
+                    mbar_wait(&s.full[st], (ka / AS) & 1);
+                    tc_fence_after();
+                    const uint64_t a = umma_desc(s.a[st]), b = umma_desc(s.xs[k]);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; kk++) umma_bf16(tmem, a + 2 * kk, b + 2 * kk, idesc, (k | kk) ? 1u : 0u);
+                    umma_commit(&s.empty[st]);
+                }
+                umma_commit(&s.t1full);
+                umma_commit(&s.xempty);
+                mbar_wait(&s.actrdy, j & 1);
+                if (j >= 1) mbar_wait(&s.t2empty, (j - 1) & 1);
+                tc_fence_after();
+                for (int ht = 0; ht < n_ht; ht++, ka++) {
+                    const int st = ka % AS;
+                    mbar_wait(&s.full[st], (ka / AS) & 1);
+                    tc_fence_after();
+                    const uint64_t a = umma_desc(s.a[st]);
+                    const uint32_t d = tmem + 256u + (uint32_t)(ht * NPAD);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; kk++) umma_bf16(d, a + 2 * kk, bact + 2 * kk, idesc, kk ? 1u : 0u);
+                    umma_commit(&s.empty[st]);
+                }
+                umma_commit(&s.t2full);
+            }
+        }
+    } else if (warp >= 6) {                               // ---- converters: codes -> swizzled bf16 A tiles
+        const int ct = threadIdx.x - 192;
+        int kq = 0, j = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
+            const int sb = j & 1;
+            mbar_wait(&s.sfull[sb], (j >> 1) & 1);
+            constexpr int NI = BM * BK / 16 / kDecQConv;  // 16-code items per thread per tile
+            float sc[NI];
+#pragma unroll
+            for (int i = 0; i < NI; i++) sc[i] = s.sc[sb][(ct >> 2) + (kDecQConv / 4) * i];   // w1: gate 0-63, up 64-127
+            for (int t = 0; t < KT + n_ht; t++, kq++) {
+                const int qs = kq % QS, st = kq % AS;
+                if (t >= KT) {                             // down rows 128 (t - KT) + r
+#pragma unroll
+                    for (int i = 0; i < NI; i++) sc[i] = s.sc[sb][128 + (t - KT) * 128 + (ct >> 2) + (kDecQConv / 4) * i];
+                }
+                mbar_wait(&s.qfull[qs], (kq / QS) & 1);
+                if (kq >= AS) mbar_wait(&s.empty[st], ((kq / AS) - 1) & 1);
+                const uint32_t dst = smem_u32(s.a[st]);
+#pragma unroll
+                for (int i = 0; i < NI; i++) {
+                    const int it = ct + kDecQConv * i, r = it >> 2, c0 = (it & 3) * 2;   // row, first 16-B chunk
+                    uint32_t wq[4];                        // the 16 codes, BITS each, lowest bits first
+                    if (BITS == 8) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(s.q[qs] + it * 16);
+                        wq[0] = v.x; wq[1] = v.y; wq[2] = v.z; wq[3] = v.w;
+                    } else if (BITS == 4) {
+                        const uint2 v = *reinterpret_cast<const uint2*>(s.q[qs] + it * 8);
+                        wq[0] = v.x; wq[1] = v.y;
+                    } else {
+                        wq[0] = *reinterpret_cast<const uint32_t*>(s.q[qs] + it * 4);
+                    }
+                    constexpr int PER = 32 / BITS;         // codes per word
+                    uint32_t o[8];                         // bf16 pairs, element 2c in the low half
+#pragma unroll
+                    for (int c = 0; c < 8; c++) {
+                        const int e0 = 2 * c, e1 = 2 * c + 1;
+                        const int q0 = (int)(wq[e0 / PER] << (32 - BITS * (e0 % PER + 1))) >> (32 - BITS);
+                        const int q1 = (int)(wq[e1 / PER] << (32 - BITS * (e1 % PER + 1))) >> (32 - BITS);
+                        // (float)q exactly: bits(1.5 * 2^23) + q, minus 1.5 * 2^23
+                        const float f0 = __int_as_float(0x4B400000 + q0) - 12582912.0f;
+                        const float f1 = __int_as_float(0x4B400000 + q1) - 12582912.0f;
+                        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(o[c]) : "f"(f1 * sc[i]), "f"(f0 * sc[i]));
+                    }
+                    const uint4 w0 = make_uint4(o[0], o[1], o[2], o[3]), w1 = make_uint4(o[4], o[5], o[6], o[7]);
+                    const uint32_t row = dst + r * 128;
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((c0 ^ (r & 7)) << 4)),
+                                 "r"(w0.x), "r"(w0.y), "r"(w0.z), "r"(w0.w) : "memory");
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((c0 + 1) ^ (r & 7)) << 4)),
+                                 "r"(w1.x), "r"(w1.y), "r"(w1.z), "r"(w1.w) : "memory");
+                }
+                mbar_arrive(&s.qempty[qs]);
+                fence_proxy_async_smem();                 // generic smem writes -> the tensor core's view
+                mbar_arrive(&s.full[st]);
+            }
+            mbar_arrive(&s.sempty[sb]);                    // this unit's scales consumed
+        }
+    } else {                                              // ---- epilogue, warps 2..5 (ffn_decode_kernel's)
+        pdl_wait();
+        const int q = warp & 3, row = q * 32 + lane;
+        const uint32_t lanebase = (uint32_t)(q * 32) << 16;
+        int j = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
+            const int e = u / m1;
+            const int ti = lane < NPAD ? g.tok_index[e * NPAD + lane] : -1;
+            const float tw = lane < NPAD ? g.tok_weight[e * NPAD + lane] : 0.0f;
+            const int ncol = __reduce_max_sync(0xffffffffu, ti >= 0 ? lane + 1 : 0);
+            mbar_wait(&s.t1full, j & 1);
+            __syncwarp();
+            tc_fence_after();
+            float v[16];
+            tmem_ld16(tmem + lanebase, v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.t1empty);
+            if (row >= 64) {
+#pragma unroll
+                for (int c = 0; c < 16; c++) s.xchg[row - 64][c] = v[c];
+            }
+            epi_bar();
+            if (row < 64) {
+                unsigned char* tile = reinterpret_cast<unsigned char*>(s.act_tile);
+                const int cb = row * 2;
+#pragma unroll
+                for (int n = 0; n < 16; n++) {
+                    const float gg = v[n];
+                    const float a = n < ncol ? gg / (1.0f + __expf(-gg)) * s.xchg[row][n] : 0.0f;
+                    *reinterpret_cast<__nv_bfloat16*>(tile + n * 128 + ((((cb >> 4) ^ (n & 7)) << 4) | (cb & 15))) =
+                        __float2bfloat16(a);
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&s.actrdy);
+            }
+            mbar_wait(&s.t2full, j & 1);
+            __syncwarp();
+            tc_fence_after();
+            for (int ht = 0; ht < n_ht; ht++) {
+                float p[16];
+                tmem_ld16(tmem + lanebase + 256u + (uint32_t)(ht * NPAD), p);
+                const int h = ht * BM + row;
+                for (int c = 0; c < ncol; c++) {
+                    const int t = __shfl_sync(0xffffffffu, ti, c);
+                    const float w = __shfl_sync(0xffffffffu, tw, c);
+                    if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], w * p[c]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.t2empty);
+            epi_bar();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int BITS>
+cudaError_t launch_decode_q(const FfnArgs& a, cudaStream_t st) {
+    const size_t smem = sizeof(DecQSmem<BITS>) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(ffn_decode_q_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    const int units = a.n_exec * (a.I / 64);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(units < ffn_grid_cap() ? units : ffn_grid_cap());
+    lc.blockDim = dim3(kDecQThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, ffn_decode_q_kernel<BITS>, a);
+}
+
 template <int NPAD>
 cudaError_t launch_ffn(const FfnArgs& a, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(ffn_fused_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -813,6 +1091,25 @@ extern "C" int esim_ffn_experts_ex(const void* d_w1_maps, const void* d_w2_maps,
     case 32: e = launch_ffn<32>(a, st); break;
     case 64: e = launch_ffn<64>(a, st); break;
     case 128: e = launch_ffn<128>(a, st); break;
+    default: return -1;
+    }
+    return e == cudaSuccess ? 0 : -3;
+}
+
+// decode-like layers over quantised slots (BITS 8 / 4 / 2, the layout of
+// layer_step.cu): dequantisation fused into the FFN's A operand
+extern "C" int esim_ffn_experts_q(const void* d_slots, int64_t slot_bytes, int32_t bits, const void* d_x_map,
+                                  const int32_t* d_exec_slot, const int32_t* d_tok_index, const float* d_tok_weight,
+                                  float* d_y, int32_t n_exec, int32_t I, int32_t H, void* stream) {
+    if (n_exec <= 0) return 0;
+    if (I % BM || H % BM || H / BK > 32 || (slot_bytes & 127)) return -1;
+    FfnArgs a{nullptr, nullptr, (const CUtensorMap*)d_x_map, nullptr, d_exec_slot, d_tok_index, d_tok_weight,
+              nullptr, d_y, nullptr, I, H, n_exec, 1, nullptr, (const uint8_t*)d_slots, slot_bytes};
+    cudaError_t e;
+    switch (bits) {
+    case 8: e = launch_decode_q<8>(a, (cudaStream_t)stream); break;
+    case 4: e = launch_decode_q<4>(a, (cudaStream_t)stream); break;
+    case 2: e = launch_decode_q<2>(a, (cudaStream_t)stream); break;
     default: return -1;
     }
     return e == cudaSuccess ? 0 : -3;

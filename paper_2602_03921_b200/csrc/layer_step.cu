@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -44,6 +45,9 @@ extern "C" int esim_ffn_experts_ex(const void* d_w1_maps, const void* d_w2_maps,
                                    const void* d_act_map, const int32_t* d_exec_slot, const int32_t* d_tok_index,
                                    const float* d_tok_weight, void* d_act, float* d_y, int32_t n_exec, int32_t npad,
                                    int32_t I, int32_t H, int32_t max_tok, void* stream);
+extern "C" int esim_ffn_experts_q(const void* d_slots, int64_t slot_bytes, int32_t bits, const void* d_x_map,
+                                  const int32_t* d_exec_slot, const int32_t* d_tok_index, const float* d_tok_weight,
+                                  float* d_y, int32_t n_exec, int32_t I, int32_t H, void* stream);
 extern "C" int esim_ffn_experts(const void* d_w1_maps, const void* d_w2_maps, const void* d_x_map,
                                 const void* d_act_map, const int32_t* d_exec_slot, const int32_t* d_tok_index,
                                 const float* d_tok_weight, void* d_act, float* d_y, int32_t n_exec, int32_t npad,
@@ -171,6 +175,7 @@ struct Engine {
     int64_t table_cap = 0;
     int max_entries = 0;                 // FFN entries per flush: experts + token-count splits at 128
     char* scratch = nullptr;             // quantised: [max_entries][3*H*I] bf16 tile-major
+    bool fused_dequant = true;           // decode flushes over one quantised precision: ffn_decode_q_kernel
     // per-run device scratch
     void* dev_scratch = nullptr;
     size_t dev_scratch_bytes = 0;
@@ -215,6 +220,7 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
         return ls_fail(-1, "unknown weight format / precision mask");
     }
     g->mask = p->prec_mask ? p->prec_mask : 1 << p->weight_format;
+    if (const char* v = getenv("ESIM_LS_SCRATCH_DEQUANT")) g->fused_dequant = v[0] != '1';   // A/B switch
     const size_t bf16_bytes = (size_t)3 * H * I * 2;
     for (int pc = 0; pc < 4; pc++) {
         if (!(g->mask >> pc & 1)) continue;
@@ -476,8 +482,26 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             table_next += E + 3 * g->max_entries;
             for (int e = 0; e < E; e++) tpos[e] = pos_of_expert[e];
             for (int i = 0; i < n_exec; i++) CK(cudaStreamWaitEvent(g->comp_st, g->landed[pend_slot[i]], 0));
+            // decode-like flush whose slots all hold one quantised precision: the FFN
+            // dequantises in shared memory (no scratch round trip)
+            int fused_bits = 0;
+            if (g->fused_dequant && npad == 16 && maxtok <= 4 && H / 128 <= 16) {
+                const int pc = slot_prec[pend_slot[0]];
+                bool uniform = pc > 0;
+                for (int i = 1; i < n_exec && uniform; i++) uniform = slot_prec[pend_slot[i]] == pc;
+                if (uniform) fused_bits = 16 >> pc;
+            }
+            if (fused_bits) {
+                for (int i = 0; i < n_exec; i++) tslot[i] = pend_slot[i];
+                build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
+                                                                       g->tok_index, g->tok_weight);
+                if (esim_ffn_gather(g->x, g->tok_index, g->xg, n_exec, npad, H, g->comp_st) ||
+                    esim_ffn_experts_q(g->slots, (int64_t)g->slot_bytes, fused_bits, g->x_maps[npad_index(npad)],
+                                       tslot, g->tok_index, g->tok_weight, g->y, n_exec, I, H, g->comp_st))
+                    return ls_fail(-3, "quantised ffn launch failed");
+            }
             int n_pair = 0;
-            for (int pc = 0; pc < 4; pc++) {            // slots holding precision pc
+            for (int pc = 0; pc < 4 && !fused_bits; pc++) {   // slots holding precision pc
                 if (!(g->mask >> pc & 1)) continue;
                 const int first = n_pair;
                 for (int i = 0; i < n_exec; i++) {
@@ -501,12 +525,13 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
                 if (pc == 2) dequant_kernel<4><<<grid, 256, 0, g->comp_st>>>(sl, g->slot_bytes, pr, sc, I, H);
                 if (pc == 3) dequant_kernel<2><<<grid, 256, 0, g->comp_st>>>(sl, g->slot_bytes, pr, sc, I, H);
             }
-            build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
-                                                                   g->tok_index, g->tok_weight);
-            if (esim_ffn_gather(g->x, g->tok_index, g->xg, n_exec, npad, H, g->comp_st) ||
+            if (!fused_bits) build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos,
+                                                                                    n_exec, npad, g->tok_index,
+                                                                                    g->tok_weight);
+            if (!fused_bits && (esim_ffn_gather(g->x, g->tok_index, g->xg, n_exec, npad, H, g->comp_st) ||
                 esim_ffn_experts_ex(g->w1_maps, g->w2_maps, g->x_maps[npad_index(npad)],
                                     g->act_maps[npad_index(npad)], tslot, g->tok_index, g->tok_weight, g->act, g->y,
-                                    n_exec, npad, I, H, std::max(1, maxtok), g->comp_st))
+                                    n_exec, npad, I, H, std::max(1, maxtok), g->comp_st)))
                 return ls_fail(-3, "ffn launch failed");
             for (int i = 0; i < n_exec; i++) {
                 CK(cudaEventRecord(g->freed[pend_slot[i]], g->comp_st));

@@ -96,6 +96,24 @@ class ExpertSlots:
             T = x.numel() // self.H
             _check(L.esim_ffn_residual(x.data_ptr(), self.y.data_ptr(), T * self.H, st), "residual")
 
+    def run_layer_quant(self, qslots, slot_bytes: int, bits: int, x, exec_slot, tok_index, tok_weight,
+                        stream=None) -> None:
+        """Decode-like layer (<= 4 tokens per expert, npad 16) over quantised
+        slots: qslots uint8 (device) holding tile-major codes of `bits` then
+        fp32 row scales per slot (slot_bytes apart, layer_step.cu's format);
+        y += MoE(x) with the dequantisation fused into the FFN
+        (ffn_decode_q_kernel). No residual."""
+        n_exec = int(exec_slot.numel())
+        if n_exec > self.max_exec:
+            raise ValueError("more executed experts than staged")
+        st = stream or _stream()
+        L = lib()
+        _check(L.esim_ffn_gather(x.data_ptr(), tok_index.data_ptr(), self.xg.data_ptr(), n_exec, 16, self.H, st),
+               "gather")
+        _check(L.esim_ffn_experts_q(qslots.data_ptr(), slot_bytes, bits, self.x_maps[16].data_ptr(),
+                                    exec_slot.data_ptr(), tok_index.data_ptr(), tok_weight.data_ptr(),
+                                    self.y.data_ptr(), n_exec, self.I, self.H, st), "quantised ffn experts")
+
 
 def expert_matrices(flat, hidden: int, inter: int):
     """Logical (w1 [2I, H], wd [H, I]) views-turned-copies of one expert stored

@@ -86,6 +86,28 @@ class LayerStepResult:
     out: object = None           # last-layer hidden states of every pass (host bf16)
 
 
+def dequant_expert(raw, bits: int, hidden: int, inter: int):
+    """One quantised expert's bytes (tile-major codes of `bits`, lowest bits
+    first, two's complement, then fp32 row scales: 2I gate/up rows, H down
+    rows) -> logical (w1 [2I, H], wd [H, I]) = bf16(q * scale) as fp32."""
+    from .ffn import expert_matrices
+    torch = _torch()
+    H, I = hidden, inter
+    nq = 3 * H * I
+    if bits == 8:
+        q = raw[:nq].view(torch.int8).float()
+    else:
+        per = 8 // bits
+        b = raw[:nq // per].to(torch.int16)
+        q = torch.stack([(b >> (bits * j)) & ((1 << bits) - 1) for j in range(per)], dim=1).reshape(-1)
+        q = torch.where(q >= (1 << (bits - 1)), q - (1 << bits), q).float()
+    sc = raw[nq * bits // 8:nq * bits // 8 + 4 * (2 * I + H)].view(torch.float32)
+    w1q, wdq = expert_matrices(q, H, I)
+    w1 = (w1q * sc[:2 * I, None]).to(torch.bfloat16).float()
+    wd = (wdq * sc[2 * I:, None]).to(torch.bfloat16).float()
+    return w1, wd
+
+
 class LayerStepEngine:
     """Pinned expert store + HBM slots + copy/compute streams for one model.
 
@@ -190,27 +212,13 @@ class LayerStepEngine:
         """Logical (w1 [2I, H], wd [H, I]) as the FFN sees them (quantised:
         bf16(q * scale)), fp32, on the GPU."""
         from .ffn import expert_matrices
-        torch = self.torch
         H, I = self.H, self.I
         code = WEIGHT_FORMAT[precision or self.cfg.working_precision]
         raw = self.expert_weights(layer, expert, precision).cuda()
         if code == 0:
             w1, wd = expert_matrices(raw, H, I)
             return w1.float(), wd.float()
-        nq = 3 * H * I
-        bits = _QBITS[code]
-        if bits == 8:
-            q = raw[:nq].view(torch.int8).float()
-        else:
-            per = 8 // bits
-            b = raw[:nq // per].to(torch.int16)
-            q = torch.stack([(b >> (bits * j)) & ((1 << bits) - 1) for j in range(per)], dim=1).reshape(-1)
-            q = torch.where(q >= (1 << (bits - 1)), q - (1 << bits), q).float()
-        sc = raw[nq * bits // 8:].view(torch.float32)
-        w1q, wdq = expert_matrices(q, H, I)
-        w1 = (w1q * sc[:2 * I, None]).to(torch.bfloat16).float()
-        wd = (wdq * sc[2 * I:, None]).to(torch.bfloat16).float()
-        return w1, wd
+        return dequant_expert(raw, _QBITS[code], H, I)
 
     def run(self, trace, x_prefill, x_decode, keep_outputs: bool = False) -> LayerStepResult:
         torch = self.torch

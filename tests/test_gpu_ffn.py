@@ -68,3 +68,50 @@ def test_ffn_matches_torch_fp32(T, K, n_exp, npad, seed):
 def test_ffn_decode_kernel_matches_torch_fp32(T, K, n_exp, seed):
     """The fused per-slice decode kernel (<= 4 tokens per expert)."""
     _case(T, K, n_exp, 16, seed, fused=True)
+
+
+@pytest.mark.parametrize("bits,T,K,n_exp,seed", [(8, 1, 8, 8, 20), (4, 1, 8, 64, 21), (2, 3, 4, 16, 22),
+                                                 (4, 4, 8, 40, 23)])
+def test_ffn_quantised_decode_kernel_matches_torch_fp32(bits, T, K, n_exp, seed):
+    """ffn_decode_q_kernel: quantised slots (codes + fp32 row scales), the
+    dequantisation fused into the A operand; 64 experts x 16 units puts
+    several units on every CTA (ring phases wrap across units)."""
+    import torch
+    from paper_2602_03921_b200.ffn import ExpertSlots, routing_tables
+    from paper_2602_03921_b200.layer_step import dequant_expert
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    n_slots = n_exp + 3
+    nq, ns = 3 * H * I, 2 * I + H
+    per = nq * bits // 8 + 4 * ns
+    slot_bytes = (per + 255) // 256 * 256
+    q = torch.zeros(n_slots, slot_bytes, dtype=torch.uint8, device="cuda")
+    q[:, :nq * bits // 8] = torch.randint(0, 256, (n_slots, nq * bits // 8), generator=g, device="cuda",
+                                          dtype=torch.int32).to(torch.uint8)
+    qmax = {8: 127, 4: 7, 2: 1}[bits]
+    sc = (0.5 + torch.rand(n_slots, ns, generator=g, device="cuda")) * (0.02 / qmax)
+    q[:, nq * bits // 8:per] = sc.view(torch.uint8).view(n_slots, ns * 4)
+    slots = ExpertSlots(1, H, I, max_tokens=T, max_exec=n_exp)
+    x = torch.randn(T, H, generator=g, device="cuda").to(torch.bfloat16)
+    rng = np.random.default_rng(seed)
+    row_sel = np.stack([rng.choice(n_exp, size=K, replace=False) for _ in range(T)]).astype(np.int32)
+    row_w = rng.uniform(0.01, 0.3, size=(T, K)).astype(np.float32)
+    slot_of = rng.permutation(n_slots)[:n_exp]
+    assert np.bincount(row_sel.ravel()).max() <= 4
+    ti, tw = routing_tables(row_sel, row_w, {e: (e, e) for e in range(n_exp)}, 16)
+    slots.y.zero_()
+    slots.run_layer_quant(q, slot_bytes, bits, x, torch.tensor(slot_of, dtype=torch.int32, device="cuda"),
+                          torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda())
+    torch.cuda.synchronize()
+    y = slots.y[:T * H].view(T, H).float()
+    ref = torch.zeros(T, H, device="cuda")
+    xf = x.float()
+    for e in range(n_exp):
+        w1, wd = dequant_expert(q[int(slot_of[e])], bits, H, I)
+        act = (torch.nn.functional.silu(xf @ w1[:I].T) * (xf @ w1[I:].T)).to(torch.bfloat16).float()
+        out = act @ wd.T
+        for t in range(T):
+            for j in range(K):
+                if row_sel[t, j] == e:
+                    ref[t] += float(row_w[t, j]) * out[t]
+    err = (y - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= TOL, f"max rel err {err:.3e}"

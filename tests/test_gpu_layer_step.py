@@ -63,6 +63,13 @@ def test_layer_step_quantised_experts(eviction, cap_experts, prec, oracle_lib):
               prec=prec)
 
 
+def test_layer_step_quantised_scratch_path(oracle_lib, monkeypatch):
+    """The dequantise-to-scratch path for decode flushes too (the fused
+    ffn_decode_q_kernel is the default there): same reference, same bar."""
+    monkeypatch.setenv("ESIM_LS_SCRATCH_DEQUANT", "1")
+    _run_case("ls", 7, "fetch", 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=3, prec="int4")
+
+
 @pytest.mark.parametrize("eviction,cap_experts,miss,working,ladder",
                          [("ls", 5, "fetch_low", "fp16", ("fp16", "int8", "int4", "int2")),
                           ("lru", 4, "fetch_priority", "fp16", ("fp16", "int8", "int4", "int2")),

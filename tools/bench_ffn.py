@@ -42,4 +42,42 @@ for name, T, K, n_exp in (("prefill64", 64, 8, 28), ("decode", 1, 8, 8), ("prefi
     out[name] = {"ms": ms, "npad": npad, "n_exec": n_exp, "weight_gbs": byt / ms / 1e6,
                  "frac_of_hbm_peak": byt / ms / 1e6 / peak, "tflops": flops / ms / 1e9}
     print(name, out[name], flush=True)
+# decode over quantised slots (ffn_decode_q_kernel, dequantisation fused into the
+# A operand): algorithmic bytes = codes + fp32 row scales per executed expert
+for bits in (8, 4, 2):
+    nq, ns = 3 * H * I, 2 * I + H
+    per = nq * bits // 8 + 4 * ns
+    sb = (per + 255) // 256 * 256
+    qbuf = torch.randint(0, 256, (64 * sb,), device="cuda", dtype=torch.int32).to(torch.uint8)
+    qv = qbuf.view(64, sb)
+    qv[:, nq * bits // 8:per] = torch.full((64, ns), 0.01, device="cuda").view(torch.uint8).view(64, ns * 4)
+    for n_exp in (8, 64):
+        rng = np.random.default_rng(0)
+        row_sel = rng.choice(n_exp, size=8, replace=False).astype(np.int32).reshape(1, 8) if n_exp >= 8 else None
+        T = 1 if n_exp == 8 else 8
+        if n_exp == 64:
+            row_sel = np.arange(64, dtype=np.int32).reshape(8, 8)
+        row_w = rng.uniform(0.01, 0.3, size=row_sel.shape).astype(np.float32)
+        ti, tw = routing_tables(row_sel, row_w, {e: (e, e) for e in range(n_exp)}, 16)
+        ti, tw = torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda()
+        x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
+        es = torch.arange(n_exp, dtype=torch.int32, device="cuda")
+        for _ in range(3):
+            slots.run_layer_quant(qbuf, sb, bits, x, es, ti, tw)
+        torch.cuda.synchronize()
+        n = 30
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for i in range(n):
+            flush.zero_()
+            ev[i][0].record()
+            slots.run_layer_quant(qbuf, sb, bits, x, es, ti, tw)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+        byt = n_exp * per
+        name = f"decode_int{bits}_{n_exp}experts"
+        out[name] = {"ms": ms, "n_exec": n_exp, "quant_bytes_per_expert": per, "quant_gbs": byt / ms / 1e6,
+                     "frac_of_hbm_peak": byt / ms / 1e6 / peak,
+                     "bf16_equivalent_gbs": n_exp * 3 * H * I * 2 / ms / 1e6}
+        print(name, out[name], flush=True)
 json.dump(out, open("gpurun_out/bench_ffn.json", "w"), indent=1)
