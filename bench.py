@@ -185,6 +185,24 @@ def layer_step_section(runs=2):
                              "logical_hit_rate": best.report["rates"]["hit_rate"],
                              "logical_ttft_us": best.report["timing"]["ttft_us"]}
         eng.close()
+    # mixed precision (miss=fetch_low, miss.py): fp16 working, demand misses fetch
+    # the int2 rung; the store holds the whole ladder, slots hold what was fetched
+    cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=614_400_000), working_precision="fp16",
+                    eviction="ls", prefetch="score", percentile=80.0, miss="fetch_low")
+    eng = LayerStepEngine(cfg, 2048, 1024, max_tokens=64)
+    eng.init_weights(seed=0)
+    best = None
+    for _ in range(runs):
+        r = eng.run(tr, x0, xd)
+        best = r if best is None or r.total_ms < best.total_ms else best
+    out["ls_fetch_low"] = {"ttft_ms": best.ttft_ms, "decode_tok_s": best.decode_tokens_per_sec,
+                           "total_ms": best.total_ms, "host_link_gbs": best.h2d_gbs,
+                           "host_link_frac": best.h2d_gbs / peak, "h2d_bytes": best.h2d_bytes,
+                           "copies": best.n_copies, "demand_copies": best.n_demand_copies,
+                           "store_precisions": list(eng.precisions), "slots_allocated": eng.n_slots,
+                           "logical_hit_rate": best.report["rates"]["hit_rate"],
+                           "logical_ttft_us": best.report["timing"]["ttft_us"]}
+    eng.close()
     return out
 
 

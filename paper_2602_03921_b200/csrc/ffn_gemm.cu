@@ -630,7 +630,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_decode_kernel(const __grid
                 float p[16];
                 tmem_ld16(tmem + lanebase + 256u + (uint32_t)(ht * NPAD), p);
                 const int h = ht * BM + row;
-                for (int c = 0; c < ncol; c++) {
+#pragma unroll
+                for (int c = 0; c < 16; c++) {            // static index: p stays in registers
+                    if (c >= ncol) break;                 // (ncol is warp-uniform)
                     const int t = __shfl_sync(0xffffffffu, ti, c);
                     const float w = __shfl_sync(0xffffffffu, tw, c);
                     if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], w * p[c]);
@@ -893,7 +895,9 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
                 float p[16];
                 tmem_ld16(tmem + lanebase + 256u + (uint32_t)(ht * NPAD), p);
                 const int h = ht * BM + row;
-                for (int c = 0; c < ncol; c++) {
+#pragma unroll
+                for (int c = 0; c < 16; c++) {            // static index: p stays in registers
+                    if (c >= ncol) break;                 // (ncol is warp-uniform)
                     const int t = __shfl_sync(0xffffffffu, ti, c);
                     const float w = __shfl_sync(0xffffffffu, tw, c);
                     if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], w * p[c]);
