@@ -341,10 +341,12 @@ DFI void ls_touch(Pt& p, int slot) {                                  // evictio
     set_key(p, slot, LS_CURRENT | (p.seq++));
 }
 
-DFI void note_admit(Pt& p, int slot) {
+DFI void note_admit(Pt& p, int slot, int ident) {
     uint64_t nk;
     switch (p.pol) {
-    case ESIM_EV_LRU: case ESIM_EV_LFU: case ESIM_EV_LHU: nk = p.seq++; break;   // move_to_end / touch
+    case ESIM_EV_LRU: nk = p.seq++; break;                                       // move_to_end
+    case ESIM_EV_LFU: case ESIM_EV_LHU:                                          // count:16 | touch:32
+        nk = ((uint64_t)p.cnt[ident] << 32) | (uint64_t)(p.seq++); break;       // (counts persist)
     case ESIM_EV_LS: nk = LS_CURRENT | (p.seq++); break;                         // untracked -> current
     default: nk = 0; break;                                                      // FLD; SB signal 0.0
     }
@@ -356,9 +358,10 @@ DFI void note_access(Pt& p, int ident, int slot, bool has_gate, double gate, int
     case ESIM_EV_LRU: set_key(p, slot, p.seq++); break;
     case ESIM_EV_LFU: case ESIM_EV_LHU: {
         const int step = (p.pol == ESIM_EV_LFU || prec == p.c->precisions[0]) ? 1 : 0;
-        if (p.cnt[ident] + step > 0xFFFF) p.err = STATUS_COUNT_OVERFLOW;   // never silently wrap
-        else if (p.lane == 0) p.cnt[ident] = (uint16_t)(p.cnt[ident] + step);
-        set_key(p, slot, p.seq++);
+        const uint32_t c = p.cnt[ident] + step;
+        if (c > 0xFFFF) p.err = STATUS_COUNT_OVERFLOW;                      // never silently wrap
+        else if (p.lane == 0) p.cnt[ident] = (uint16_t)c;
+        set_key(p, slot, ((uint64_t)c << 32) | (uint64_t)(p.seq++));
         break;
     }
     case ESIM_EV_SB:
@@ -377,7 +380,7 @@ DFI void note_access(Pt& p, int ident, int slot, bool has_gate, double gate, int
 // Every policy's order is total, so one 64-bit key per slot with the slot
 // index in the low 12 bits reduces in a single shuffle chain:
 //   LRU / LS   (class | stamp) << 12 | slot      stamps are unique
-//   LFU / LHU  count:20 | touch:32 | slot:12      touches are unique
+//   LFU / LHU  the slot key itself: count:16 | touch:32 (touches are unique)
 //   FLD        (L-1-dist):8 | expert:16 | layer:16 | slot:12
 //   SB         two stages: min signal, then min ident among equal signals
 DFI uint64_t warp_min_u64(uint64_t v) {         // two redux.sync (hi word, then lo among ties)
@@ -430,18 +433,28 @@ DFI int select_victim(Pt& p, bool forced) {
         }
         return slot;
     }
-    for (int s = p.lane; s < p.S; s += 32) {
+    if (p.pol == ESIM_EV_LFU || p.pol == ESIM_EV_LHU) {
+        // the slot key holds (count, touch) and free slots hold KEY_FREE (above
+        // every live key), so the scan is one 64-bit load and compare per slot
+        uint64_t bk = KEY_FREE;
+        int bs = 0;
+        #pragma unroll 4
+        for (int s = p.lane; s < p.S; s += 32) {
+            const uint64_t k = p.key[s];
+            bs = k < bk ? s : bs;
+            bk = k < bk ? k : bk;
+        }
+        const uint64_t m = warp_min_u64(bk);
+        if (m == KEY_FREE) return -1;
+        return __shfl_sync(FULL, bs, __ffs(__ballot_sync(FULL, bk == m)) - 1);
+    }
+    for (int s = p.lane; s < p.S; s += 32) {                              // FLD
         const int id = p.res_ident[s];
         if (id < 0) continue;
-        uint64_t k;
-        if (p.pol == ESIM_EV_LFU || p.pol == ESIM_EV_LHU) {
-            k = ((uint64_t)(uint32_t)p.cnt[id] << 44) | ((uint64_t)(uint32_t)p.key[s] << 12) | (uint64_t)s;
-        } else {                                                          // FLD
-            const int l = ediv(p, id), e = id - l * p.E;
-            int d = l - c;
-            d = d < 0 ? d + p.L : d;
-            k = ((uint64_t)(p.L - 1 - d) << 44) | ((uint64_t)e << 28) | ((uint64_t)l << 12) | (uint64_t)s;
-        }
+        const int l = ediv(p, id), e = id - l * p.E;
+        int d = l - c;
+        d = d < 0 ? d + p.L : d;
+        const uint64_t k = ((uint64_t)(p.L - 1 - d) << 44) | ((uint64_t)e << 28) | ((uint64_t)l << 12) | (uint64_t)s;
         best = k < best ? k : best;
     }
     best = warp_min_u64(best);
@@ -605,7 +618,7 @@ DFI void settle(Pt& p) {                                                   // en
         }
         __syncwarp();
         if (p.resident_bytes + p.reserved_bytes > p.cap && !p.err) p.err = -2;
-        note_admit(p, slot);
+        note_admit(p, slot, ident);
         if (fl & 1) {
             const int il = ediv(p, ident);
             rec_prefetch(p, 2, il, ident - il * p.E, comp, score, 0);

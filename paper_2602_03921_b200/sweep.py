@@ -75,20 +75,31 @@ def _lib():
     return lib()
 
 
+def _torch():
+    from ._device import _torch as t
+    return t()
+
+
 def pin_traces(traces) -> None:
-    """Page-lock the packed arrays of each trace (idempotent) so run_grid_host's
-    host->device copies are DMA from pinned memory."""
-    seen = set()
+    """Move each trace's packed logits into page-locked memory (idempotent) so
+    run_grid_host's host->device copies are DMA from pinned memory (the small
+    per-trace arrays travel through the plan's own pinned image).
+
+    The pinned buffer is a cudaHostAlloc allocation owned by the array, not a
+    cudaHostRegister of the caller's heap memory: a registration outliving the
+    array it was made for leaves a stale page-locked range behind, and a later
+    copy into memory that reuses part of it fails (cudaErrorInvalidValue)."""
+    torch = _torch()
     for tr in traces:
-        if id(tr) in seen:
-            continue
-        seen.add(id(tr))
         pk = tr.packed()
-        for a in (pk.logits, pk.row_offset, pk.pass_tokens, pk.pass_kind):
-            if a.nbytes:
-                rc = _lib().esim_host_register(a.ctypes.data, a.nbytes)
-                if rc:
-                    raise RuntimeError(_lib().esim_last_error().decode())
+        a = pk.logits
+        if a.nbytes == 0 or getattr(pk, "_pinned", False):
+            continue
+        buf = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+        v = buf.numpy().view(a.dtype).reshape(a.shape)
+        v[...] = a
+        pk.logits = v
+        pk._pinned = True
 
 
 _CCFG_CACHE: dict = {}
@@ -130,19 +141,23 @@ class HostGrid:
         self.L = pl_stride or max(c.model.num_layers for c in cfgs)
         carr = (_abi.EsimConfig * n).from_buffer_copy(b"".join(ccfg))
         darr = (_abi.EsimTraceDesc * len(descs))(*descs)
-        self.counters = (_abi.EsimCounters * n)()
-        self.per_layer = np.zeros((n, self.L, _abi.ESIM_PL_FIELDS), np.int64)
-        for buf, nbytes in ((C.addressof(self.counters), C.sizeof(self.counters)),
-                            (self.per_layer.ctypes.data, self.per_layer.nbytes)):
-            if _lib().esim_host_register(buf, nbytes):
-                raise RuntimeError(_lib().esim_last_error().decode())
-        self._registered = True
+        self.counters, self.per_layer = self._pinned_outputs()
         h = C.c_void_p()
         rc = _lib().esim_sweep_plan_create(C.addressof(carr), n, C.addressof(darr), len(descs), self.L, 0, 0,
                                            C.byref(h))
         if rc != 0:
             self._raise(rc)
         self._plan = h
+
+    def _pinned_outputs(self):
+        """Counters + per-layer result buffers in page-locked (cudaHostAlloc)
+        memory, so the plan's D2H copies land directly in them."""
+        torch = _torch()
+        cb = torch.zeros(self.n * C.sizeof(_abi.EsimCounters), dtype=torch.uint8, pin_memory=True)
+        cs = (_abi.EsimCounters * self.n).from_address(cb.data_ptr())
+        cs._owner = cb                                   # keep the pinned storage alive with the view
+        pl = torch.zeros((self.n, self.L, _abi.ESIM_PL_FIELDS), dtype=torch.int64, pin_memory=True).numpy()
+        return cs, pl
 
     @staticmethod
     def _raise(rc):
@@ -166,12 +181,7 @@ class HostGrid:
             self._outs = [(self.counters, self.per_layer)]
             self._next, self._inflight = 0, []
         while len(self._outs) <= slot:
-            cs = (_abi.EsimCounters * self.n)()
-            pl = np.zeros_like(self.per_layer)
-            for buf, nbytes in ((C.addressof(cs), C.sizeof(cs)), (pl.ctypes.data, pl.nbytes)):
-                if _lib().esim_host_register(buf, nbytes):
-                    raise RuntimeError(_lib().esim_last_error().decode())
-            self._outs.append((cs, pl))
+            self._outs.append(self._pinned_outputs())
         return self._outs[slot]
 
     def submit(self) -> None:
@@ -198,11 +208,6 @@ class HostGrid:
         if getattr(self, "_plan", None):
             _lib().esim_sweep_plan_destroy(self._plan)
             self._plan = None
-        if getattr(self, "_registered", False):
-            for cs, pl in getattr(self, "_outs", [(self.counters, self.per_layer)]):
-                _lib().esim_host_unregister(C.addressof(cs))
-                _lib().esim_host_unregister(pl.ctypes.data)
-            self._registered = False
 
     def __del__(self):
         try:
