@@ -251,3 +251,29 @@ def test_sweep_plan_pipelined_steps_match_run(oracle_lib):
         assert int(o.counters.digest) == want[5]
     finally:
         g.close()
+
+
+def test_pinned_traces_leave_no_stale_registration(oracle_lib):
+    """pin_traces + a host-API grid, then the traces and the grid go away: later
+    host<->device copies into recycled host memory must keep working (a
+    cudaHostRegister that outlived its array used to break them)."""
+    import gc
+    import numpy as np
+    import torch
+    from paper_2602_03921_b200.models import builtin_spec
+    from paper_2602_03921_b200.sweep import C5_MODELS, c5_points, pin_traces, run_grid_host
+    from paper_2602_03921_b200.trace import generate_synthetic
+    trs = {m: [generate_synthetic(builtin_spec(m), seed=5, prefill_tokens=16, decode_tokens=8)] for m in C5_MODELS}
+    cfgs, tl = c5_points(trs)
+    pin_traces(tl)
+    cs, _ = run_grid_host(cfgs, tl)
+    assert all(c.status == 0 for c in cs)
+    del trs, cfgs, tl, cs
+    gc.collect()
+    x = torch.randn(1 << 20, device="cuda")
+    for n in (1 << 10, 1 << 14, 1 << 18, 1 << 20):
+        for _ in range(8):
+            host = [np.empty(n, np.float32) for _ in range(4)]       # recycle freed host ranges
+            y = x[:n].cpu()
+            assert torch.equal(y, x[:n].cpu())
+            del host
