@@ -317,6 +317,10 @@ void *esim_ls_store(void *handle);
 int64_t esim_ls_expert_bytes(void *handle);
 int64_t esim_ls_format(void *handle, int32_t prec, int64_t *store_offset);
 int64_t esim_ls_store_bytes(void *handle);
+/* The last request's executed routing [rows][K] (expert, weight): the
+ * router's top-k, or with routing=cache_aware the replay's re-routed
+ * selection and its original-softmax weights (routing.py:147-160). */
+int esim_ls_route_rows(void *handle, int16_t *sel_out, float *w_out, int64_t rows);
 void *esim_ls_slots(void *handle);
 int esim_ls_destroy(void *handle);
 const char *esim_ls_last_error(void);

@@ -179,6 +179,9 @@ struct Engine {
     // per-run device scratch
     void* dev_scratch = nullptr;
     size_t dev_scratch_bytes = 0;
+    const int16_t* last_sel = nullptr;   // the last request's executed routing (in dev_scratch)
+    const float* last_w = nullptr;
+    int64_t last_rows = 0;
 };
 
 std::string g_ls_err;
@@ -296,6 +299,17 @@ extern "C" int64_t esim_ls_format(void* handle, int32_t prec, int64_t* store_off
     if (store_offset) *store_offset = (int64_t)g->store_off[prec];
     return (int64_t)g->fmt_bytes[prec];
 }
+// the last request's executed routing, [rows][K] (the router's top-k, or the
+// cache-aware selection and its original-softmax weights for routing=cache_aware)
+extern "C" int esim_ls_route_rows(void* handle, int16_t* sel_out, float* w_out, int64_t rows) {
+    const Engine* g = static_cast<Engine*>(handle);
+    if (!g->last_sel || rows > g->last_rows) return ls_fail(-1, "no such rows in the last request");
+    const size_t n = (size_t)rows * g->P.top_k;
+    if (cudaMemcpy(sel_out, g->last_sel, n * 2, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(w_out, g->last_w, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return ls_fail(-3, "route rows copy failed");
+    return 0;
+}
 extern "C" int64_t esim_ls_store_bytes(void* handle) { return (int64_t) static_cast<Engine*>(handle)->store_bytes; }
 extern "C" void* esim_ls_slots(void* handle) { return static_cast<Engine*>(handle)->slots; }
 
@@ -410,6 +424,9 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     ro.row_sel = (int16_t*)take(nr * K * 2); ro.row_w = (float*)take(nr * K * 4);
     ro.route_mix = (uint32_t*)take(ne * 4); ro.pred_mix = (uint32_t*)take(ne * 4);
     ro.layer_pred = (int64_t*)take(L * 16); ro.summary = (EsimRouteSummary*)take(sizeof(EsimRouteSummary));
+    g->last_sel = ro.row_sel;
+    g->last_w = ro.row_w;
+    g->last_rows = nr;
     EsimConfig* d_cfg = (EsimConfig*)take(sizeof(EsimConfig));
     EsimTraceDesc* d_tr = (EsimTraceDesc*)take(sizeof(EsimTraceDesc));
     EsimRouterOut* d_ro = (EsimRouterOut*)take(sizeof(EsimRouterOut));

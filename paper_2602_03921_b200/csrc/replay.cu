@@ -1282,6 +1282,18 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
                  __double_as_longlong(exm), selm);
             if (p.lane == 0) { p.ctr->faithful += faithful; p.ctr->modified += nmod; }
             ps_add(p, 1, exm);                   // rows and the original mass: router summary
+            if (ca && A.progress) {
+                // streamed (physical layer step): the executed routing of this event's rows
+                // replaces the router's standard top-k in place before the layer is published
+                // (the FFN builds its token lists from these rows; routing.py:147-160)
+                const int64_t b0 = tr.row_offset[ev] * p.K;
+                for (int i = p.lane; i < T * p.K; i += 32) {
+                    R.row_sel[b0 + i] = p.ca_sel[i];
+                    R.row_w[b0 + i] = p.ca_w[i];
+                }
+                __threadfence();
+                __syncwarp();
+            }
             }
             if (cfg->prefetch != ESIM_PF_NONE && l + 1 < p.L) submit_prefetches(p, R, ev + 1);
             advance_to(p, p.now + cfg->compute_us);

@@ -58,6 +58,7 @@ def _bind():
         L.esim_ls_format.restype = C.c_int64
         L.esim_ls_store_bytes.argtypes = [vp]
         L.esim_ls_store_bytes.restype = C.c_int64
+        L.esim_ls_route_rows.argtypes = [vp, vp, vp, C.c_int64]
         L.esim_ls_slots.argtypes = [vp]
         L.esim_ls_slots.restype = vp
         L.esim_ls_destroy.argtypes = [vp]
@@ -248,6 +249,16 @@ class LayerStepEngine:
             n_copies=res.n_copies, n_demand_copies=res.n_demand_copies, n_prefetch_copies=res.n_prefetch_copies,
             n_cancelled=res.n_cancelled, n_ffn_batches=res.n_ffn_batches, n_exec_experts=res.n_exec_experts,
             host_enqueue_ms=res.host_enqueue_ms, report=rep, out=out if keep_outputs else None)
+
+    def route_rows(self, rows: int):
+        """The last run's executed routing: (sel int16 [rows, K], w float32 [rows, K])."""
+        K = self.cfg.model.top_k
+        sel = np.zeros((rows, K), np.int16)
+        w = np.zeros((rows, K), np.float32)
+        rc = _bind().esim_ls_route_rows(self._h, sel.ctypes.data, w.ctypes.data, rows)
+        if rc:
+            raise RuntimeError(f"esim_ls_route_rows failed ({rc}): {_bind().esim_ls_last_error().decode()}")
+        return sel, w
 
     def close(self) -> None:
         if self._h:

@@ -15,10 +15,12 @@ pytestmark = pytest.mark.gpu
 H, I = 2048, 1024
 
 
-def _reference(engine, trace, x0, xdec, served=None, I=1024, prec_of=None):
+def _reference(engine, trace, x0, xdec, served=None, I=1024, prec_of=None, route_sel=None):
     """No-cache fp32 forward; served[(pass, layer)][e] = the expert whose
     weights serve e's tokens (a substitute), or None when e was dropped;
-    prec_of[(pass, layer, e)] = the precision those weights run at."""
+    prec_of[(pass, layer, e)] = the precision those weights run at; route_sel:
+    the executed top-k per trace row (cache-aware routing re-selects; the
+    weights stay the original softmax at the selected experts)."""
     import torch
     from paper_2602_03921_b200.routing import softmax_rows
     spec = trace.spec
@@ -28,6 +30,9 @@ def _reference(engine, trace, x0, xdec, served=None, I=1024, prec_of=None):
         for ev in fp.events:
             sc = softmax_rows(ev.logits)
             idx = np.argsort(-sc, axis=1, kind="stable")[:, :spec.top_k]
+            if route_sel is not None:
+                r0 = int(trace.packed().row_offset[p * spec.num_layers + ev.layer])
+                idx = route_sel[r0:r0 + idx.shape[0]].astype(np.int64)
             y = torch.zeros_like(x)
             for e in np.unique(idx):
                 we = (served or {}).get((p, ev.layer), {}).get(int(e), int(e))
@@ -63,6 +68,14 @@ def test_layer_step_quantised_experts(eviction, cap_experts, prec, oracle_lib):
               prec=prec)
 
 
+def test_layer_step_cache_aware_routing(oracle_lib):
+    """config4 (cli.py:77-80): cache-aware routing (lambda 0.3, no prefetch,
+    LRU, int4): the replay re-routes rows toward cached experts and streams
+    the executed selection to the FFN; outputs follow it."""
+    _run_case("lru", 24, "fetch", 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=6, prec="int4",
+              routing="cache_aware", prefetch="none")      # 24 slots: residents survive a pass (4 rows re-routed)
+
+
 def test_layer_step_quantised_scratch_path(oracle_lib, monkeypatch):
     """The dequantise-to-scratch path for decode flushes too (the fused
     ffn_decode_q_kernel is the default there): same reference, same bar."""
@@ -91,7 +104,7 @@ def test_layer_step_long_prefill_splits_experts(oracle_lib):
 
 
 def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, prefill, decode, prec="fp16",
-              ladder=None):
+              ladder=None, routing="standard", prefetch="score"):
     """I = 1408 is the Qwen1.5-MoE expert width (not a power of two); subst /
     drop follow the decision stream (substitute weights / no contribution)."""
     import torch
@@ -103,8 +116,8 @@ def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, pr
                      **({"precisions": ladder} if ladder else {}))
     cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=cap_experts * spec.expert_bytes(prec)),
                     working_precision=prec,
-                    eviction=eviction, prefetch="score", percentile=80.0, miss=miss, subst_tolerance=0.2,
-                    drop_rank_threshold=2)
+                    eviction=eviction, prefetch=prefetch, percentile=80.0, miss=miss, subst_tolerance=0.2,
+                    drop_rank_threshold=2, routing=routing, lam=0.3)
     tr = generate_synthetic(spec, seed=7, prefill_tokens=prefill, decode_tokens=decode)
     eng = LayerStepEngine(cfg, H, I, max_tokens=prefill)
     eng.init_weights(seed=3)
@@ -125,7 +138,22 @@ def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, pr
     if miss in ("subst", "drop"):
         assert served, "the case must exercise its miss policy"
     got = res.out.view(-1, H).float()
-    ref = _reference(eng, tr, x0, xd, served, I, prec_of).cpu()
+    route_sel = None
+    if routing == "cache_aware":
+        rows = int(tr.packed().row_offset[-1])
+        route_sel, route_w = eng.route_rows(rows)
+        assert res.report["fidelity"]["modified_rows"] > 0, "the case must re-route some rows"
+        # the streamed selection differs from the standard top-k in exactly the
+        # rows the (oracle-equal) report counts as modified, and keeps the
+        # original softmax weights of the selected experts
+        from paper_2602_03921_b200.routing import softmax_rows
+        lg = tr.packed().logits
+        sc = softmax_rows(lg)
+        std = np.argsort(-sc, axis=1, kind="stable")[:, :top_k]
+        changed = sum(set(std[r].tolist()) != set(route_sel[r].tolist()) for r in range(rows))
+        assert changed == res.report["fidelity"]["modified_rows"]
+        assert np.array_equal(route_w, np.take_along_axis(sc, route_sel.astype(np.int64), axis=1))
+    ref = _reference(eng, tr, x0, xd, served, I, prec_of, route_sel).cpu()
     err = (got - ref).abs().max().item() / ref.abs().max().item()
     assert err <= 1e-2, f"max rel err {err:.3e}"
     assert res.n_copies >= res.report["totals"]["misses"] - res.report["totals"]["prefetch_started"]
