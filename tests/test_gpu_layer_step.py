@@ -68,6 +68,19 @@ def test_layer_step_quantised_experts(eviction, cap_experts, prec, oracle_lib):
               prec=prec)
 
 
+@pytest.mark.parametrize("preset,eviction,cap_experts,miss,prec,ladder,prefetch", [
+    ("config1", "lru", 8, "fetch", "int4", None, "topk"),
+    ("config2", "sb", 8, "subst", "int4", None, "score"),
+    ("config3", "lhu", 8, "fetch_priority", "int8", ("int8", "int4", "int2"), "topk"),
+    ("config5", "ls", 8, "fetch", "int4", None, "score")])
+def test_layer_step_reference_presets(preset, eviction, cap_experts, miss, prec, ladder, prefetch, oracle_lib):
+    """The reference's bundled stacks (cli.py:63-85) on the physical path:
+    decisions == the oracle's report, outputs == the reference forward at the
+    executed experts / precisions (config4 below: cache-aware routing)."""
+    _run_case(eviction, cap_experts, miss, 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=4, prec=prec,
+              ladder=ladder, prefetch=prefetch)
+
+
 def test_layer_step_cache_aware_routing(oracle_lib):
     """config4 (cli.py:77-80): cache-aware routing (lambda 0.3, no prefetch,
     LRU, int4): the replay re-routes rows toward cached experts and streams
