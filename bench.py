@@ -339,6 +339,10 @@ def main():
         grid = HostGrid(cfgs, trs)          # configs packed once (a plan); each run() = one C-ABI call
         for _ in range(max(1, args.warmup)):
             grid.run()
+        grid.submit()                       # warm the pipelined path too: the second slab and its
+        grid.submit()                       # pinned result buffers are created on first use
+        grid.wait()
+        grid.wait()
         h2d = sum(t.packed().logits.nbytes + t.packed().row_offset.nbytes + t.packed().pass_tokens.nbytes * 2
                   for t in {id(x): x for x in trs}.values()) + 168 * n_pts
         d2h = n_pts * (360 + max(c.model.num_layers for c in cfgs) * 80)
