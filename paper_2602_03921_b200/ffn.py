@@ -131,7 +131,8 @@ def pack_expert(w1, wd, hidden: int, inter: int):
     H, I = hidden, inter
     t1 = w1.reshape(2, I // 64, 64, H // 64, 64).permute(1, 3, 0, 2, 4).reshape(-1)
     t2 = wd.reshape(H // 128, 128, I // 64, 64).permute(2, 0, 1, 3).reshape(-1)
-    return _torch().cat([t1, t2])
+    import torch                     # layout helper on caller tensors (any device), not a compute path
+    return torch.cat([t1, t2])
 
 
 def routing_tables(row_sel: np.ndarray, row_w: np.ndarray, executed: dict, npad: int):

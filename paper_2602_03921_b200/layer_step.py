@@ -90,9 +90,11 @@ class LayerStepResult:
 def dequant_expert(raw, bits: int, hidden: int, inter: int):
     """One quantised expert's bytes (tile-major codes of `bits`, lowest bits
     first, two's complement, then fp32 row scales: 2I gate/up rows, H down
-    rows) -> logical (w1 [2I, H], wd [H, I]) = bf16(q * scale) as fp32."""
+    rows) -> logical (w1 [2I, H], wd [H, I]) = bf16(q * scale) as fp32, on
+    raw's device (the test reference / weight inspection; the device path
+    dequantises in dequant_kernel / ffn_decode_q_kernel)."""
     from .ffn import expert_matrices
-    torch = _torch()
+    import torch
     H, I = hidden, inter
     nq = 3 * H * I
     if bits == 8:

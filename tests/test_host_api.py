@@ -255,3 +255,37 @@ def test_native_csv_report_rejects_broken_identities():
     c.totals[0] = 5          # demanded 5, nothing resolved
     with pytest.raises(ValueError):
         csv_text([cfg], [c], np.zeros((1, spec.num_layers, _abi.ESIM_PL_FIELDS), np.int64))
+
+
+def test_tile_major_pack_and_quantised_decode_on_cpu():
+    """Host halves of the physical expert formats (CPU): pack_expert inverts
+    expert_matrices (the tile-major layout the TMA boxes read), and
+    dequant_expert decodes int8 / int4 / int2 codes (lowest bits first, two's
+    complement) + fp32 row scales exactly like the device dequantisers."""
+    import numpy as np
+    import torch
+    from paper_2602_03921_b200.ffn import expert_matrices, pack_expert
+    from paper_2602_03921_b200.layer_step import dequant_expert
+    H, I = 256, 128
+    g = torch.Generator().manual_seed(0)
+    w1, wd = torch.randn(2 * I, H, generator=g), torch.randn(H, I, generator=g)
+    a, b = expert_matrices(pack_expert(w1, wd, H, I), H, I)
+    assert torch.equal(a, w1) and torch.equal(b, wd)
+    rows = pack_expert(torch.arange(2 * I)[:, None].expand(2 * I, H),
+                       (2 * I + torch.arange(H))[:, None].expand(H, I), H, I).numpy()
+    rng = np.random.default_rng(1)
+    nq, ns = 3 * H * I, 2 * I + H
+    for bits in (8, 4, 2):
+        lo, hi = -(1 << (bits - 1)), (1 << (bits - 1)) - 1
+        q = rng.integers(lo, hi + 1, nq)
+        sc = rng.uniform(0.01, 0.02, ns).astype(np.float32)
+        per = 8 // bits
+        u = (q & ((1 << bits) - 1)).astype(np.uint8).reshape(-1, per)
+        codes = np.zeros(nq // per, np.uint8)
+        for j in range(per):
+            codes |= (u[:, j] << (bits * j)).astype(np.uint8)
+        raw = torch.from_numpy(np.concatenate([codes, sc.view(np.uint8)]))
+        d1, d2 = dequant_expert(raw, bits, H, I)
+        want = torch.from_numpy((q.astype(np.float32) * sc[rows]).astype(np.float32)).to(torch.bfloat16).float()
+        w1w, wdw = expert_matrices(want, H, I)
+        assert torch.equal(d1, w1w) and torch.equal(d2, wdw), bits
