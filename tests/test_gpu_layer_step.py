@@ -172,3 +172,31 @@ def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, pr
     assert res.n_copies >= res.report["totals"]["misses"] - res.report["totals"]["prefetch_started"]
     eng.close()
     return {"precisions": sorted(set(prec_of.values()))}
+
+
+def test_layer_step_rejects_configs_its_store_cannot_serve():
+    """The engine fails loudly (no silent fallback) when a request's config
+    needs precisions or slots its store / pool was not built for."""
+    from dataclasses import replace
+
+    import torch
+    from paper_2602_03921_b200 import HardwareSpec, ModelSpec, SimConfig, generate_synthetic
+    from paper_2602_03921_b200.layer_step import LayerStepEngine
+    spec = ModelSpec("mini_moe", num_layers=2, experts_per_layer=8, top_k=2, expert_bytes_fp16=3 * H * I * 2)
+    cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=3 * spec.expert_bytes("fp16")),
+                    working_precision="fp16", eviction="ls", prefetch="score")
+    tr = generate_synthetic(spec, seed=1, prefill_tokens=4, decode_tokens=2)
+    eng = LayerStepEngine(cfg, H, I, max_tokens=4)
+    eng.init_weights(seed=0)
+    x0 = torch.zeros(4, H, dtype=torch.bfloat16).pin_memory()
+    xd = torch.zeros(2, H, dtype=torch.bfloat16).pin_memory()
+    bad = [replace(cfg, miss="fetch_low"),                                   # ladder not in the store
+           replace(cfg, working_precision="int4"),                           # other weight format
+           replace(cfg, hardware=HardwareSpec(capacity_bytes=8 * spec.expert_bytes("fp16")))]   # > slots
+    for c in bad:
+        eng.cfg = c
+        with pytest.raises(RuntimeError):
+            eng.run(tr, x0, xd)
+    eng.cfg = cfg
+    assert eng.run(tr, x0, xd).n_copies > 0                               # still usable afterwards
+    eng.close()
