@@ -35,3 +35,6 @@ def test_struct_sizes_match_the_header():
     assert ctypes.sizeof(_abi.EsimTraceDesc) == 64
     assert ctypes.sizeof(_abi.EsimRouterOut) == 17 * 8
     assert REC_DTYPE.itemsize == 64
+    from paper_2602_03921_b200.layer_step import EsimLSParams, EsimLSResult
+    assert ctypes.sizeof(EsimLSParams) == 9 * 4           # incl. weight_format, prec_mask
+    assert ctypes.sizeof(EsimLSResult) == 4 * 8 + 9 * 8
