@@ -73,7 +73,9 @@ typedef struct {
     double  subst_tolerance, degrade_percentile;
     int32_t flags;
     int32_t trace_id;             /* which router/trace buffer set this point replays */
-} EsimConfig;                     /* 168 bytes */
+    double  prefetch_noise;       /* SimConfig.prefetch_noise (engine.py:92): prefetch.py:110-136 */
+    uint64_t seed;                /* SimConfig.seed (engine.py:97): np.random.default_rng(seed) */
+} EsimConfig;                     /* 184 bytes */
 
 /* One event-log record, 64 bytes; field mapping per kind is documented in
  * paper_2602_03921_b200/records.py:decode_records. */
@@ -176,6 +178,14 @@ int esim_router_launch_batch(const EsimTraceDesc *d_traces, const EsimRouterOut 
  * holding device pointers; pred_mode as for esim_router_launch. */
 int esim_route_summary_launch(const EsimTraceDesc *trace, const EsimRouterOut *out, int32_t pred_mode,
                               void *stream);
+/* prefetch.apply_prediction_noise (prefetch.py:110-136) over a routed
+ * trace's whole prediction stream, in place, drawing from numpy's
+ * default_rng(seed) (SeedSequence -> PCG64, restated on the device) in the
+ * reference's submission order (engine.py:413, 653-666); then the router
+ * summary is recomputed (as esim_route_summary_launch). noise 0 or pred_mode
+ * NONE consumes nothing. Host structs holding device pointers. */
+int esim_noise_launch(const EsimTraceDesc *trace, const EsimRouterOut *out, int32_t pred_mode, double noise,
+                      uint64_t seed, void *stream);
 int esim_predictor_params(int32_t top_k, int32_t experts, int32_t pred_mode, double overfetch,
                           double percentile, int32_t *out4);
 
@@ -241,7 +251,9 @@ int esim_replay_launch(const EsimConfig *h_cfg, const EsimConfig *d_cfg, int32_t
 /* End-to-end host API (engine.run_simulation over many configs): host
  * traces (host pointers) and configs in; router + replay on the device;
  * host counters/per-layer/records out. Synchronous. Configs sharing a
- * trace_id must share the predictor (prefetch mode/overfetch/percentile). */
+ * trace_id must share the predictor (prefetch mode/overfetch/percentile)
+ * and the prediction noise stream (prefetch_noise, seed): the noise is
+ * applied on the device once per trace_id (esim_noise_launch). */
 int esim_run_host(const EsimConfig *cfg, int32_t n, const EsimTraceDesc *traces, int32_t n_traces,
                   EsimCounters *counters, int64_t *per_layer, int32_t pl_stride,
                   EsimRec *recs, int64_t rec_cap, int32_t *pred_experts, int64_t pe_cap);

@@ -16,7 +16,7 @@ import numpy as np
 
 from paper_2602_03921_b200 import _abi
 from paper_2602_03921_b200.metrics import report_from_counters
-from paper_2602_03921_b200.prefetch import noised_prediction_stream, PREFETCH_CODE
+from paper_2602_03921_b200.prefetch import PREFETCH_CODE, apply_prediction_noise
 from paper_2602_03921_b200.records import REC_DTYPE, decode_records
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -79,6 +79,39 @@ def predictions(pk, mode: int, overfetch: float, percentile: float):
     desc, keep = _abi.trace_desc_host(pk)
     lib().esim_oracle_predict(C.addressof(desc), mode, overfetch, percentile, _p(off), _p(ex), _p(sc), _p(cl))
     return off, ex, sc, cl
+
+
+def noised_prediction_stream(offsets, experts, scores, clamped, num_layers: int, n_passes: int,
+                             num_experts: int, noise: float, seed: int):
+    """Apply prediction noise to a whole trace's prediction stream.
+
+    Inputs are the per-event predictions (event = pass*L + layer, each event
+    as a TARGET layer). The reference draws noise in submission order --
+    pass by pass, layer 0..L-2 predicting layer+1 -- from one
+    default_rng(seed) (engine.py:413, 653-666); this replays that order and
+    returns new (offsets, experts, scores, clamped) arrays.
+    """
+    rng = np.random.default_rng(seed)
+    n_events = num_layers * n_passes
+    out_e, out_s = [], []
+    new_off = np.zeros(n_events + 1, np.int32)
+    lists: dict = {}
+    for p in range(n_passes):
+        for layer in range(num_layers - 1):
+            ev = p * num_layers + layer + 1
+            a, b = int(offsets[ev]), int(offsets[ev + 1])
+            preds = [(int(experts[i]), float(scores[i])) for i in range(a, b)]
+            lists[ev] = apply_prediction_noise(preds, num_experts, noise, rng)
+    pos = 0
+    for ev in range(n_events):
+        new_off[ev] = pos
+        for e, s in lists.get(ev, []):
+            out_e.append(e)
+            out_s.append(s)
+            pos += 1
+    new_off[n_events] = pos
+    return (new_off, np.asarray(out_e, np.int32), np.asarray(out_s, np.float32),
+            np.asarray(clamped, np.int32).copy())
 
 
 @dataclass

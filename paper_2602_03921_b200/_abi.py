@@ -22,7 +22,8 @@ class EsimConfig(C.Structure):
                 ("sb_decay", C.c_double), ("overfetch", C.c_double), ("percentile", C.c_double),
                 ("miss", C.c_int32), ("drop_rank_threshold", C.c_int32),
                 ("subst_tolerance", C.c_double), ("degrade_percentile", C.c_double),
-                ("flags", C.c_int32), ("trace_id", C.c_int32)]
+                ("flags", C.c_int32), ("trace_id", C.c_int32),
+                ("prefetch_noise", C.c_double), ("seed", C.c_uint64)]
 
 
 class EsimCounters(C.Structure):
@@ -60,7 +61,7 @@ class EsimRouteSummary(C.Structure):
                [(n, C.c_double) for n in ("orig_f", "orig_c", "prec_f", "prec_c", "rec_f", "rec_c")]
 
 
-assert C.sizeof(EsimConfig) == 168, C.sizeof(EsimConfig)
+assert C.sizeof(EsimConfig) == 184, C.sizeof(EsimConfig)
 assert C.sizeof(EsimCounters) == 360, C.sizeof(EsimCounters)
 assert C.sizeof(EsimRouteSummary) == 112, C.sizeof(EsimRouteSummary)
 COUNTERS_DTYPE = np.dtype((np.void, C.sizeof(EsimCounters)))

@@ -18,7 +18,7 @@ import numpy as np
 from . import _abi
 from .metrics import report_from_counters
 from .models import ConfigError
-from .prefetch import PREFETCH_CODE, noised_prediction_stream
+from .prefetch import PREFETCH_CODE
 from .records import REC_DTYPE, decode_records
 from .routing import RoutingDecision
 
@@ -62,6 +62,10 @@ def lib():
         L.esim_predictor_params.argtypes = [i32, i32, i32, f64, f64, vp]
         L.esim_topk_launch.argtypes = [vp, i32, i32, i32, vp, vp]
         L.esim_route_summary_launch.argtypes = [vp, vp, i32, vp]
+        L.esim_noise_launch.argtypes = [vp, vp, i32, f64, C.c_uint64, vp]
+        L.esim_version.restype = C.c_int
+        if L.esim_version() != 2:
+            raise RuntimeError(f"{LIB_PATH}: C ABI version {L.esim_version()} != 2 (stale build)")
         _lib = L
     return _lib
 
@@ -175,27 +179,13 @@ def route_trace(dt: DeviceTrace, prefetch: str, overfetch: float, percentile: fl
     return out
 
 
-def _noised(dt: DeviceTrace, ro: RouterOut, cfg) -> RouterOut:
-    """Apply numpy-PCG64 prediction noise (engine.py:661-666) to the device predictions."""
-    pk = dt.pk
-    E = pk.experts
-    n_pred = ro.t["n_pred"].cpu().numpy()[:pk.n_events]
-    pe = ro.t["pred_expert"].cpu().numpy()[:pk.n_events * E].reshape(pk.n_events, E)
-    ps = ro.t["pred_score"].cpu().numpy()[:pk.n_events * E].reshape(pk.n_events, E)
-    cl = ro.t["pred_clamped"].cpu().numpy()[:pk.n_events]
-    off = np.zeros(pk.n_events + 1, np.int32)
-    np.cumsum(n_pred, out=off[1:])
-    flat_e = np.concatenate([pe[i, :n_pred[i]] for i in range(pk.n_events)]) if pk.n_events else pe[:0, 0]
-    flat_s = np.concatenate([ps[i, :n_pred[i]] for i in range(pk.n_events)]) if pk.n_events else ps[:0, 0]
-    noff, ne_, ns_, ncl = noised_prediction_stream(off, flat_e, flat_s, cl, pk.num_layers, pk.n_passes, E,
-                                                   cfg.prefetch_noise, cfg.seed)
-    npred = np.diff(noff).astype(np.int32)
-    pe2 = np.zeros((pk.n_events, E), np.int32)
-    ps2 = np.zeros((pk.n_events, E), np.float32)
-    for i in range(pk.n_events):
-        pe2[i, :npred[i]] = ne_[noff[i]:noff[i + 1]]
-        ps2[i, :npred[i]] = ns_[noff[i]:noff[i + 1]]
-    return ro.with_predictions(dt, PREFETCH_CODE[cfg.prefetch], npred, pe2.ravel(), ps2.ravel(), ncl)
+def apply_noise(dt: DeviceTrace, ro: RouterOut, prefetch: str, noise: float, seed: int, stream=None) -> None:
+    """Prediction noise on the device (esim_noise_launch): numpy's
+    default_rng(seed) PCG64 stream restated in CUDA, drawn in the reference's
+    submission order (prefetch.py:110-136, engine.py:413, 653-666), applied
+    to the router output in place; the router summary is recomputed."""
+    _check(lib().esim_noise_launch(C.addressof(dt.desc), C.addressof(ro.desc), PREFETCH_CODE[prefetch],
+                                   float(noise), int(seed), stream or _stream()), "prediction noise")
 
 
 # ---------------------------------------------------------------------------
@@ -236,9 +226,9 @@ class ReplayBatch:
                 dt = self.dtraces[key]
                 ro = route_trace(dt, cfg.prefetch, cfg.overfetch, cfg.percentile, stream)
                 if skey[4] is not None:
-                    ro = _noised(dt, ro, cfg)
+                    apply_noise(dt, ro, cfg.prefetch, cfg.prefetch_noise, cfg.seed, stream)
                 streams[skey] = (len(streams), dt, ro, (cfg.prefetch, cfg.overfetch, cfg.percentile),
-                                 skey[4] is not None)
+                                 skey[4])          # (noise, seed) or None
         self.sets = list(streams.values())
         torch.cuda.synchronize()
         self.d_traces = self._blob([s[1].desc for s in self.sets])

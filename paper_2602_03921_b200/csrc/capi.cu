@@ -55,7 +55,7 @@ extern "C" int esim_host_unregister(void* p) {
     if (e == cudaErrorHostMemoryNotRegistered) { cudaGetLastError(); return 0; }
     return e == cudaSuccess ? 0 : cuda_fail(e, "cudaHostUnregister");
 }
-extern "C" int esim_version(void) { return 1; }
+extern "C" int esim_version(void) { return 2; }   // 2: EsimConfig gained prefetch_noise + seed (184 B)
 
 // predictor constants resolved on the host exactly as the reference does in
 // Python floats: count = ceil(k * overfetch) (prefetch.py:48), rank =
@@ -182,6 +182,8 @@ int esim_replay_launch_streamed(const EsimConfig* h_cfg, const EsimConfig* d_cfg
 extern "C" int esim_router_launch_batch(const EsimTraceDesc* d_traces, const EsimRouterOut* d_outs,
                                         const int32_t* d_params, const int64_t* d_prefix, int32_t n_traces,
                                         int64_t total_events, int32_t max_experts, void* stream);
+extern "C" int esim_noise_launch(const EsimTraceDesc* tr, const EsimRouterOut* out, int32_t pred_mode, double noise,
+                                 uint64_t seed, void* stream);
 
 // ---------------------------------------------------------------------------
 // Sweep plan: everything about a grid that does not change between runs is
@@ -206,6 +208,8 @@ struct Slab {
     std::vector<cudaEvent_t> ge;
     cudaEvent_t routed = nullptr;
     EsimCounters* out_c = nullptr;                // pending step: the caller's counters
+    std::vector<EsimTraceDesc> dtr;               // host copies of the device descriptors
+    std::vector<EsimRouterOut> dro;               // (esim_noise_launch takes host structs)
 };
 
 struct SweepPlan {
@@ -218,6 +222,8 @@ struct SweepPlan {
     std::vector<std::pair<int, int>> groups;      // [begin, end) in pcfg
     std::vector<EsimTraceDesc> htr;               // caller descriptors (host pointers)
     std::vector<int32_t> params;                  // predictor per trace
+    std::vector<double> noise;                    // prediction noise per trace (0 = none)
+    std::vector<uint64_t> seed;                   // its default_rng seed
     std::vector<int64_t> prefix;                  // event prefix sums
     std::vector<size_t> small_off, logit_off, roff;
     size_t small_bytes = 0, cfg_off = 0, td_off = 0, rd_off = 0, par_off = 0, pre_off = 0;
@@ -299,6 +305,8 @@ int slab_init(SweepPlan* P, Slab& S) {
         o.summary = (EsimRouteSummary*)take(sizeof(EsimRouteSummary));
         dro[t] = o;
     }
+    S.dtr = dtr;
+    S.dro = dro;
     std::vector<int32_t> out_index(P->order.begin(), P->order.end());
     cudaMemcpy(base + P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice);
     cudaMemcpy(base + P->td_off, dtr.data(), sizeof(EsimTraceDesc) * n_traces, cudaMemcpyHostToDevice);
@@ -351,6 +359,11 @@ int slab_enqueue(SweepPlan* P, Slab& S, EsimCounters* counters, int64_t* per_lay
                                       (int32_t*)(base + P->par_off), (int64_t*)(base + P->pre_off), P->n_traces,
                                       P->total_events, P->max_e, S.st);
     if (rc) return cuda_fail(cudaGetLastError(), "router batch");
+    // prediction noise: one serial PCG64 stream per noised trace (prefetch.py:110-136)
+    for (int t = 0; t < P->n_traces; t++)
+        if (P->noise[t] > 0.0 &&
+            (rc = esim_noise_launch(&S.dtr[t], &S.dro[t], P->params[4 * t], P->noise[t], P->seed[t], S.st)))
+            return rc;
     if (prof) { cudaStreamSynchronize(S.st); fprintf(stderr, "[plan_run] router done %.2f ms\n", now_ms() - t_start); }
     cudaEventRecord(S.routed, S.st);
     const bool full = recs != nullptr && P->rec_cap > 0;
@@ -444,17 +457,28 @@ extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const Es
     P->params.assign(4 * n_traces, 0);
     std::vector<char> seen(n_traces, 0);
     std::vector<double> pover(n_traces), ppct(n_traces);
+    P->noise.assign(n_traces, 0.0);
+    P->seed.assign(n_traces, 0);
     for (int i = 0; i < n; i++) {
         const int t = cfg[i].trace_id;
         if (t < 0 || t >= n_traces) return bail(fail(-1, "trace_id out of range"));
+        if (!(cfg[i].prefetch_noise >= 0.0 && cfg[i].prefetch_noise <= 1.0))
+            return bail(fail(-1, "prefetch_noise must be in [0, 1], got " + std::to_string(cfg[i].prefetch_noise)));
+        // noise draws only when something is predicted (engine.py:651-666)
+        const double nz = cfg[i].prefetch != ESIM_PF_NONE ? cfg[i].prefetch_noise : 0.0;
+        const uint64_t sd = nz > 0.0 ? cfg[i].seed : 0;
         if (!seen[t]) {
             seen[t] = 1;
             pover[t] = cfg[i].overfetch;
             ppct[t] = cfg[i].percentile;
+            P->noise[t] = nz;
+            P->seed[t] = sd;
             esim_predictor_params(traces[t].top_k, traces[t].experts, cfg[i].prefetch, cfg[i].overfetch,
                                   cfg[i].percentile, &P->params[4 * t]);
         } else if (P->params[4 * t] != cfg[i].prefetch || pover[t] != cfg[i].overfetch || ppct[t] != cfg[i].percentile) {
             return bail(fail(-1, "configs sharing a trace_id must share the predictor"));
+        } else if (P->noise[t] != nz || P->seed[t] != sd) {
+            return bail(fail(-1, "configs sharing a trace_id must share the prediction noise stream (prefetch_noise, seed)"));
         }
     }
     // one launch group per kernel specialisation (policy x {common, general} path),

@@ -54,6 +54,8 @@ extern "C" int esim_ffn_experts(const void* d_w1_maps, const void* d_w2_maps, co
                                 int32_t I, int32_t H, void* stream);
 extern "C" int esim_router_launch(const EsimTraceDesc* tr, const EsimRouterOut* out, int32_t pred_mode,
                                   double overfetch, double percentile, void* stream);
+extern "C" int esim_noise_launch(const EsimTraceDesc* tr, const EsimRouterOut* out, int32_t pred_mode, double noise,
+                                 uint64_t seed, void* stream);
 int esim_replay_launch_streamed(const EsimConfig* h_cfg, const EsimConfig* d_cfg, const EsimTraceDesc* d_traces,
                                 const EsimRouterOut* d_routers, int32_t max_tokens, EsimCounters* d_counters,
                                 int64_t* d_per_layer, int32_t pl_stride, EsimRec* d_recs, int64_t rec_cap,
@@ -447,6 +449,9 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     CK(cudaStreamWaitEvent(g->ctl_st, g->ev_start, 0));
     int rc = esim_router_launch(&tr, &ro, hc.prefetch, hc.overfetch, hc.percentile, g->ctl_st);
     if (rc) return ls_fail(rc, "router launch");
+    if (hc.prefetch != ESIM_PF_NONE && hc.prefetch_noise > 0.0 &&      // prefetch.py:110-136 on the device
+        (rc = esim_noise_launch(&tr, &ro, hc.prefetch, hc.prefetch_noise, hc.seed, g->ctl_st)))
+        return ls_fail(rc, "prediction noise");
     rc = esim_replay_launch_streamed(&hc, d_cfg, d_tr, d_ro, max_t, d_cnt, d_pl, L, g->recs, rec_cap, g->pexp, pe_cap,
                                      g->progress, g->ctl_st);
     if (rc) return ls_fail(rc, "replay launch");

@@ -68,16 +68,26 @@ __device__ __forceinline__ float warp_pw_block(const float* a, int n, int lane) 
 }
 
 // numpy pairwise sum for n <= 256 (ESIM_MAX_E): blocks of <= 128 are
-// summed directly; larger n split once at n2 = n/2 - (n/2)%8 (numpy's
-// recursion, which never nests deeper for n <= 256). No recursion on the
+// summed directly; larger n split at n2 = n/2 - (n/2)%8 as numpy does. For
+// n in 249..255 the upper half (129..135 elements) is itself over the block
+// size and numpy splits it again; for n <= 256 the recursion never goes
+// deeper than that (the lower half is always <= 128). No recursion on the
 // device: the stack size stays statically known.
+__device__ __forceinline__ int pw_split(int n) {
+    int n2 = n / 2;
+    return n2 - n2 % 8;
+}
+
+__device__ __forceinline__ float warp_pw_mid(const float* a, int n, int lane) {   // n <= 256, hi half <= 128
+    if (n <= 128) return warp_pw_block(a, n, lane);
+    const int n2 = pw_split(n);
+    return __fadd_rn(warp_pw_block(a, n2, lane), warp_pw_block(a + n2, n - n2, lane));
+}
+
 __device__ __forceinline__ float warp_pw_sum(const float* a, int n, int lane) {
     if (n <= 128) return warp_pw_block(a, n, lane);
-    int n2 = n / 2;
-    n2 -= n2 % 8;
-    float lo = warp_pw_block(a, n2, lane);
-    float hi = warp_pw_block(a + n2, n - n2, lane);
-    return __fadd_rn(lo, hi);
+    const int n2 = pw_split(n);
+    return __fadd_rn(warp_pw_block(a, n2, lane), warp_pw_mid(a + n2, n - n2, lane));
 }
 
 // CPython >= 3.12 builtin sum() over floats (Neumaier compensation).

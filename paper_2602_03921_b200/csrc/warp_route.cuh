@@ -49,7 +49,7 @@ DFI void warp_topk(const float* s, int E, int K, int lane, int16_t* out) {
     __syncwarp();
 }
 
-// numpy DOUBLE_pairwise_sum of a float32 row cast to float64; n <= 256 splits at most once
+// numpy DOUBLE_pairwise_sum of a float32 row cast to float64 (block of <= 128)
 DFI double warp_pw_block_f64(const float* a, int n, int lane) {
     if (n < 8) {
         double res = 0.0;
@@ -70,11 +70,17 @@ DFI double warp_pw_block_f64(const float* a, int n, int lane) {
     return res;
 }
 
+DFI double warp_pw_mid_f64(const float* a, int n, int lane) {   // n <= 256: the halves are <= 128
+    if (n <= 128) return warp_pw_block_f64(a, n, lane);
+    const int n2 = pw_split(n);
+    return __dadd_rn(warp_pw_block_f64(a, n2, lane), warp_pw_block_f64(a + n2, n - n2, lane));
+}
+
+// numpy's recursion: the upper half of n in 249..255 (129..135) splits again
 DFI double warp_pw_sum_f64(const float* a, int n, int lane) {
     if (n <= 128) return warp_pw_block_f64(a, n, lane);
-    int n2 = n / 2;
-    n2 -= n2 % 8;
-    return __dadd_rn(warp_pw_block_f64(a, n2, lane), warp_pw_block_f64(a + n2, n - n2, lane));
+    const int n2 = pw_split(n);
+    return __dadd_rn(warp_pw_block_f64(a, n2, lane), warp_pw_mid_f64(a + n2, n - n2, lane));
 }
 
 

@@ -125,6 +125,9 @@ class SimConfig:
         c.subst_tolerance, c.degrade_percentile = self.subst_tolerance, self.degrade_percentile
         c.flags = _abi.ESIM_FLAG_FULL_LOG if full_log else 0
         c.trace_id = trace_id
+        # noise is only drawn when something is predicted (engine.py:651-666)
+        c.prefetch_noise = self.prefetch_noise if self.prefetch != "none" else 0.0
+        c.seed = self.seed if c.prefetch_noise > 0 else 0
         return c
 
 

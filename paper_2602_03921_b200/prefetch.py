@@ -3,9 +3,11 @@
 Prediction (topk / score-percentile / oracle over the NEXT layer's router
 scores, unioned over token rows) runs inside the fused router kernel
 (csrc/router.cu). The watchdog's two sweeps run inside the replay kernel
-(csrc/replay.cu). Prediction noise is host input preparation: it consumes
-numpy's PCG64 stream in the reference's order (prefetch.py:110-136,
-engine.py:661-666) and is applied to the device predictions before replay.
+(csrc/replay.cu). Prediction noise over a whole trace runs on the device
+(csrc/noise.cu: numpy's default_rng PCG64 stream restated in CUDA, drawn in
+the reference's order, prefetch.py:110-136, engine.py:413, 661-666).
+`apply_prediction_noise` below is the plug-in itself, for callers that hold
+their own numpy Generator.
 """
 from __future__ import annotations
 
@@ -86,36 +88,3 @@ class PrefetchQueue:
 
     def pop(self) -> PrefetchRequest:
         return self._q.popleft()
-
-
-def noised_prediction_stream(offsets, experts, scores, clamped, num_layers: int, n_passes: int,
-                             num_experts: int, noise: float, seed: int):
-    """Apply prediction noise to a whole trace's prediction stream.
-
-    Inputs are the per-event predictions (event = pass*L + layer, each event
-    as a TARGET layer). The reference draws noise in submission order --
-    pass by pass, layer 0..L-2 predicting layer+1 -- from one
-    default_rng(seed) (engine.py:413, 653-666); this replays that order and
-    returns new (offsets, experts, scores, clamped) arrays.
-    """
-    rng = np.random.default_rng(seed)
-    n_events = num_layers * n_passes
-    out_e, out_s = [], []
-    new_off = np.zeros(n_events + 1, np.int32)
-    lists: dict = {}
-    for p in range(n_passes):
-        for layer in range(num_layers - 1):
-            ev = p * num_layers + layer + 1
-            a, b = int(offsets[ev]), int(offsets[ev + 1])
-            preds = [(int(experts[i]), float(scores[i])) for i in range(a, b)]
-            lists[ev] = apply_prediction_noise(preds, num_experts, noise, rng)
-    pos = 0
-    for ev in range(n_events):
-        new_off[ev] = pos
-        for e, s in lists.get(ev, []):
-            out_e.append(e)
-            out_s.append(s)
-            pos += 1
-    new_off[n_events] = pos
-    return (new_off, np.asarray(out_e, np.int32), np.asarray(out_s, np.float32),
-            np.asarray(clamped, np.int32).copy())

@@ -105,6 +105,11 @@ def pin_traces(traces) -> None:
 _CCFG_CACHE: dict = {}
 
 
+def _noise_key(cfg):
+    """The prediction-noise stream a point draws (None: no draws, engine.py:651-666)."""
+    return (cfg.prefetch_noise, cfg.seed) if cfg.prefetch != "none" and cfg.prefetch_noise > 0 else None
+
+
 def _c_config(cfg, trace_id: int):
     key = (cfg, trace_id)
     c = _CCFG_CACHE.get(key)
@@ -120,17 +125,16 @@ class HostGrid:
     trace H2D, router, replays, results D2H straight into this object's
     page-locked output arrays, in config order.
 
-    Configs that share a trace object must share the predictor; prediction
-    noise is not supported on this path (use engine.Simulation)."""
+    Points get one trace_id per (trace, predictor, noise stream): the plan
+    routes each trace_id once and applies its prediction noise on the device
+    (esim_noise_launch)."""
 
     def __init__(self, cfgs, traces, pl_stride: int | None = None):
-        if any(c.prefetch != "none" and c.prefetch_noise > 0 for c in cfgs):
-            raise ConfigError("run_grid_host: prediction noise needs the Simulation path")
         ids, descs, self._keep = {}, [], []
         ccfg = []
         for cfg, tr in zip(cfgs, traces):
             check_geometry(cfg, tr)
-            key = (id(tr), cfg.prefetch, cfg.overfetch, cfg.percentile)
+            key = (id(tr), cfg.prefetch, cfg.overfetch, cfg.percentile, _noise_key(cfg))
             if key not in ids:
                 ids[key] = len(descs)
                 d, k = _abi.trace_desc_host(tr.packed())
@@ -326,8 +330,6 @@ class DeviceSweep:
         from ._device import PREFETCH_CODE, lib
         params, prefix = [], [0]
         for _, dt, ro, (mode, over, pct), noised in self.batch.sets:
-            if noised:
-                raise ConfigError("DeviceSweep.route: noised prediction streams are host-prepared")
             out4 = (C.c_int32 * 4)()
             lib().esim_predictor_params(dt.pk.top_k, dt.pk.experts, PREFETCH_CODE[mode], float(over), float(pct), out4)
             params += list(out4)
@@ -339,7 +341,7 @@ class DeviceSweep:
 
     def route(self, stream=None) -> None:
         """Fused router over every trace of the sweep in one launch."""
-        from ._device import _check, _stream, lib
+        from ._device import _check, _stream, apply_noise, lib
         if not hasattr(self, "_rparams"):
             self._router_tables()
         rc = lib().esim_router_launch_batch(self.batch.d_traces.data_ptr(), self.batch.d_routers.data_ptr(),
@@ -347,6 +349,9 @@ class DeviceSweep:
                                             len(self.batch.sets), self._total_events, self._max_e,
                                             stream or _stream())
         _check(rc, "router batch")
+        for _, dt, ro, (mode, _o, _p), noised in self.batch.sets:      # prefetch.py:110-136 on the device
+            if noised:
+                apply_noise(dt, ro, mode, noised[0], noised[1], stream)
 
     def replay(self, stream=None) -> None:
         self.batch.launch(stream)

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_sizes_match_the_header():
     from paper_2602_03921_b200 import _abi
     from paper_2602_03921_b200.records import REC_DTYPE
-    assert ctypes.sizeof(_abi.EsimConfig) == 168
+    assert ctypes.sizeof(_abi.EsimConfig) == 184
     assert ctypes.sizeof(_abi.EsimCounters) == 360
     assert ctypes.sizeof(_abi.EsimTraceDesc) == 64
     assert ctypes.sizeof(_abi.EsimRouterOut) == 17 * 8

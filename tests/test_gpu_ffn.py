@@ -11,7 +11,7 @@ H, I = 2048, 1024
 TOL = 1e-2
 
 
-def _case(T, K, n_exp, npad_expected, seed, fused):
+def _case(T, K, n_exp, npad_expected, seed, fused, H=H, I=I):
     import torch
     from paper_2602_03921_b200.ffn import ExpertSlots, expert_matrices, npad_for, routing_tables
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -68,6 +68,23 @@ def test_ffn_matches_torch_fp32(T, K, n_exp, npad, seed):
 def test_ffn_decode_kernel_matches_torch_fp32(T, K, n_exp, seed):
     """The fused per-slice decode kernel (<= 4 tokens per expert)."""
     _case(T, K, n_exp, 16, seed, fused=True)
+
+
+# BASELINE.json configs[2]: Mixtral-8x7B experts, H=4096, I=14336 (352 MB bf16
+# per expert). Decode takes ffn_fused_kernel<16> (H/BM = 32 > 16 rows of
+# output tiles per unit: the split-K n_kc = 4 path, ffn_gemm.cu), prefill the
+# persistent two-phase kernel; top-2 of 8 experts.
+@pytest.mark.parametrize("T,K,n_exp,npad,seed,fused", [(1, 2, 2, 16, 30, True), (2, 2, 4, 16, 31, True),
+                                                       (64, 2, 8, 32, 32, False), (16, 2, 8, 16, 33, False)])
+def test_ffn_mixtral_shape_matches_torch_fp32(T, K, n_exp, npad, seed, fused):
+    _case(T, K, n_exp, npad, seed, fused=fused, H=4096, I=14336)
+
+
+# configs[3]: Qwen1.5-MoE routed experts (I = 1408) and its shared expert (I = 5632)
+@pytest.mark.parametrize("T,K,n_exp,npad,seed,fused,inter", [(1, 4, 4, 16, 40, True, 1408), (64, 4, 24, 32, 41, False, 1408),
+                                                             (1, 1, 1, 16, 42, True, 5632), (64, 1, 1, 64, 43, False, 5632)])
+def test_ffn_qwen_shapes_match_torch_fp32(T, K, n_exp, npad, seed, fused, inter):
+    _case(T, K, n_exp, npad, seed, fused=fused, H=2048, I=inter)
 
 
 @pytest.mark.parametrize("bits,T,K,n_exp,seed", [(8, 1, 8, 8, 20), (4, 1, 8, 64, 21), (2, 3, 4, 16, 22),
