@@ -334,6 +334,19 @@ int64_t esim_ls_store_bytes(void *handle);
  * selection and its original-softmax weights (routing.py:147-160). */
 int esim_ls_route_rows(void *handle, int16_t *sel_out, float *w_out, int64_t rows);
 void *esim_ls_slots(void *handle);
+/* Attach an always-resident shared expert (Qwen1.5-MoE-A2.7B, BASELINE.json
+ * configs[3]: 2048 x 5632 per layer; not cache-managed -- the reference
+ * models only routed experts): d_w [L][3*H*inter] bf16 in the
+ * routed experts' tile-major layout, d_gate [L][H] bf16, caller-owned device
+ * memory. Each layer then adds sigmoid(x . gate_l) * SwiGLU_l(x) for every
+ * token to the routed output before the residual (HF Qwen2MoeSparseMoeBlock).
+ * inter = 0 detaches. */
+int esim_ls_shared_expert(void *handle, const void *d_w, const void *d_gate, int32_t inter);
+/* Parity hook: every layer's output hidden states (after the residual) of
+ * the following esim_ls_run calls are written to host_buf (page-locked /
+ * mapped host memory, [rows][H] bf16, events in (pass, layer) order, the
+ * pass's token count of rows per event); NULL turns it off. */
+int esim_ls_capture_layers(void *handle, void *host_buf, int64_t rows);
 int esim_ls_destroy(void *handle);
 const char *esim_ls_last_error(void);
 /* One request. trace: host struct with device pointers; h_pass_tokens: host

@@ -147,6 +147,36 @@ __global__ void copy_rows_kernel(const uint4* __restrict__ src, uint4* __restric
         dst[i] = src[i];
 }
 
+// shared expert of one layer (HF Qwen2MoeSparseMoeBlock): every token, weight
+// sigmoid(x . gate). One warp per table row: entry j = row / npad, column
+// c = row % npad, token t = j * npad + c (npad == 128 whenever T > 128).
+__global__ void shared_tables_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ gate,
+                                     int T, int H, int npad, int n_ent, int layer, int32_t* __restrict__ tok_index,
+                                     float* __restrict__ tok_weight, int32_t* __restrict__ exec) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (r >= n_ent * npad) return;
+    const int t = r;                                  // entries are consecutive npad-token chunks
+    if (r % npad == 0 && lane == 0) exec[r / npad] = layer;
+    if (t >= T) {
+        if (lane == 0) { tok_index[r] = -1; tok_weight[r] = 0.0f; }
+        return;
+    }
+    float acc = 0.0f;
+    const __nv_bfloat162* xr = reinterpret_cast<const __nv_bfloat162*>(x + (size_t)t * H);
+    const __nv_bfloat162* gr = reinterpret_cast<const __nv_bfloat162*>(gate);
+    for (int i = lane; i < H / 2; i += 32) {
+        const float2 a = __bfloat1622float2(xr[i]), b = __bfloat1622float2(gr[i]);
+        acc = fmaf(a.x, b.x, fmaf(a.y, b.y, acc));
+    }
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+        tok_index[r] = t;
+        tok_weight[r] = 1.0f / (1.0f + expf(-acc));
+    }
+}
+
 struct Engine {
     EsimLSParams P;
     size_t expert_bytes = 0;             // working precision
@@ -181,6 +211,18 @@ struct Engine {
     // per-run device scratch
     void* dev_scratch = nullptr;
     size_t dev_scratch_bytes = 0;
+    // always-resident shared expert (Qwen1.5-MoE: 2048 x 5632 per layer), attached by the caller
+    int Is = 0;                          // its intermediate width (0: none)
+    const void* shared_w = nullptr;      // device [L][3*H*Is] bf16 tile-major (caller-owned)
+    const __nv_bfloat16* shared_gate = nullptr;   // device [L][H] bf16
+    void *sw1_maps = nullptr, *sw2_maps = nullptr, *sact = nullptr;
+    void* sact_maps[4] = {};
+    int32_t* s_tok_index = nullptr;      // device tables of the shared entries
+    float* s_tok_weight = nullptr;
+    int32_t* s_exec = nullptr;
+    int s_entries = 0;                   // ceil(max_tokens / 128)
+    void* capture = nullptr;             // optional mapped host [sum over events of T][H] bf16: every layer's output
+    int64_t capture_rows = 0;
     const int16_t* last_sel = nullptr;   // the last request's executed routing (in dev_scratch)
     const float* last_w = nullptr;
     int64_t last_rows = 0;
@@ -315,6 +357,64 @@ extern "C" int esim_ls_route_rows(void* handle, int16_t* sel_out, float* w_out, 
 extern "C" int64_t esim_ls_store_bytes(void* handle) { return (int64_t) static_cast<Engine*>(handle)->store_bytes; }
 extern "C" void* esim_ls_slots(void* handle) { return static_cast<Engine*>(handle)->slots; }
 
+// Attach the always-resident shared expert (d_w: [L][3*H*inter] bf16 tile-major
+// like a routed expert, d_gate: [L][H] bf16; both caller-owned device memory):
+// every layer then adds sigmoid(x . gate_l) * shared_l(x) to the routed experts'
+// output before the residual. inter = 0 detaches.
+extern "C" int esim_ls_shared_expert(void* handle, const void* d_w, const void* d_gate, int32_t inter) {
+    Engine* g = static_cast<Engine*>(handle);
+    const int L = g->P.num_layers, H = g->P.hidden;
+    cudaDeviceSynchronize();
+    cudaFree(g->sw1_maps); cudaFree(g->sw2_maps); cudaFree(g->sact);
+    for (int i = 0; i < 4; i++) { cudaFree(g->sact_maps[i]); g->sact_maps[i] = nullptr; }
+    cudaFree(g->s_tok_index); cudaFree(g->s_tok_weight); cudaFree(g->s_exec);
+    g->sw1_maps = g->sw2_maps = g->sact = nullptr;
+    g->s_tok_index = nullptr; g->s_tok_weight = nullptr; g->s_exec = nullptr;
+    g->Is = 0;
+    if (inter == 0) return 0;
+    if (inter < 0 || inter % 128 || !d_w || !d_gate) return ls_fail(-1, "bad shared expert");
+    const int Is = inter;
+    g->s_entries = (g->P.max_tokens + 127) / 128;
+    if (g->s_entries > g->max_entries) return ls_fail(-1, "shared expert entries exceed the staging buffers");
+    std::vector<unsigned char> m1(128 * (size_t)L), m2(128 * (size_t)L);
+    for (int l = 0; l < L; l++) {
+        const char* base = (const char*)d_w + (size_t)l * 3 * H * Is * 2;
+        if (esim_tmap_bf16(&m1[128 * l], base, (int64_t)2 * Is * H / 64, 64, 128) ||
+            esim_tmap_bf16(&m2[128 * l], base + (size_t)2 * Is * H * 2, (int64_t)Is * H / 64, 64, 128))
+            return ls_fail(-3, "tensor map encode failed");
+    }
+    CK(cudaMalloc(&g->sw1_maps, m1.size()));
+    CK(cudaMalloc(&g->sw2_maps, m2.size()));
+    CK(cudaMemcpy(g->sw1_maps, m1.data(), m1.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->sw2_maps, m2.data(), m2.size(), cudaMemcpyHostToDevice));
+    const size_t rows = (size_t)g->s_entries * 128;
+    CK(cudaMalloc(&g->sact, rows * Is * 2));
+    for (int i = 0; i < 4; i++) {
+        unsigned char ma[128];
+        if (esim_tmap_bf16(ma, g->sact, (int64_t)g->s_entries * NPADS[i], Is, NPADS[i]))
+            return ls_fail(-3, "tensor map encode failed");
+        CK(cudaMalloc(&g->sact_maps[i], 128));
+        CK(cudaMemcpy(g->sact_maps[i], ma, 128, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMalloc((void**)&g->s_tok_index, rows * 4));
+    CK(cudaMalloc((void**)&g->s_tok_weight, rows * 4));
+    CK(cudaMalloc((void**)&g->s_exec, g->s_entries * 4));
+    g->shared_w = d_w;
+    g->shared_gate = (const __nv_bfloat16*)d_gate;
+    g->Is = Is;
+    return 0;
+}
+
+// Debug / parity hook: every layer's output hidden states (after the residual)
+// of the following requests go to `host_buf` (page-locked or mapped host
+// memory, [rows][H] bf16, events in order, T rows per event); NULL turns it off.
+extern "C" int esim_ls_capture_layers(void* handle, void* host_buf, int64_t rows) {
+    Engine* g = static_cast<Engine*>(handle);
+    g->capture = host_buf;
+    g->capture_rows = host_buf ? rows : 0;
+    return 0;
+}
+
 extern "C" int esim_ls_destroy(void* handle) {
     Engine* g = static_cast<Engine*>(handle);
     if (!g) return 0;
@@ -336,6 +436,7 @@ extern "C" int esim_ls_destroy(void* handle) {
     if (g->progress) cudaFreeHost(g->progress);
     if (g->tables) cudaFreeHost(g->tables);
     if (g->dev_scratch) cudaFree(g->dev_scratch);
+    esim_ls_shared_expert(g, nullptr, nullptr, 0);
     for (auto e : g->landed) cudaEventDestroy(e);
     for (auto e : g->freed) cudaEventDestroy(e);
     cudaEventDestroy(g->ev_start);
@@ -470,6 +571,7 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
     int64_t row = 0;                                 // first token row of the current event
     int64_t rec_pos = 0;
     int64_t out_row = 0;
+    int64_t cap_row = 0;
     auto issue_copy = [&](int ident, int prec) -> int {
         if (free_slots.empty()) return ls_fail(-2, "no free physical slot (decision stream inconsistent)");
         if (phys[ident] >= 0) return ls_fail(-2, "fetch of a resident expert (decision stream inconsistent)");
@@ -487,7 +589,21 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
         h2d += (int64_t)nb;
         return 0;
     };
-    auto flush = [&](int layer_rows, const int16_t* rs, const float* rw, bool residual) -> int {
+    // the layer's shared expert (always resident): every token, weight sigmoid(x . gate)
+    auto run_shared = [&](int layer, int T) -> int {
+        const int npad = T > 128 ? 128 : npad_for(T);
+        const int n_ent = (T + npad - 1) / npad;
+        shared_tables_kernel<<<(n_ent * npad + 7) / 8, 256, 0, g->comp_st>>>(
+            (const __nv_bfloat16*)g->x, g->shared_gate + (size_t)layer * H, T, H, npad, n_ent, layer, g->s_tok_index,
+            g->s_tok_weight, g->s_exec);
+        if (esim_ffn_gather(g->x, g->s_tok_index, g->xg, n_ent, npad, H, g->comp_st) ||
+            esim_ffn_experts_ex(g->sw1_maps, g->sw2_maps, g->x_maps[npad_index(npad)], g->sact_maps[npad_index(npad)],
+                                g->s_exec, g->s_tok_index, g->s_tok_weight, g->sact, g->y, n_ent, npad, g->Is, H,
+                                std::min(T, 128), g->comp_st))
+            return ls_fail(-3, "shared expert ffn launch failed");
+        return 0;
+    };
+    auto flush = [&](int layer_rows, const int16_t* rs, const float* rw, bool residual, int layer) -> int {
         const int n_exec = (int)pend_slot.size();
         if (n_exec > 0) {
             int maxtok = 0;
@@ -566,6 +682,10 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
         pend_slot.clear();
         tok_of_pos.clear();
         std::fill(pos_of_expert.begin(), pos_of_expert.end(), -1);
+        if (residual && g->Is) {
+            const int rc2 = run_shared(layer, layer_rows);
+            if (rc2) return rc2;
+        }
         if (residual && esim_ffn_residual(g->x, g->y, (int64_t)layer_rows * H, g->comp_st))
             return ls_fail(-3, "residual launch failed");
         return 0;
@@ -608,7 +728,7 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
                 const int v = r.i0 * E + r.i1;
                 const int s = phys[v];
                 if (s >= 0) {
-                    if (slot_pending[s] && (rc = flush(T, rs, rw, false))) return rc;   // self-eviction
+                    if (slot_pending[s] && (rc = flush(T, rs, rw, false, layer))) return rc;   // self-eviction
                     free_slots.push_back(s);
                     phys[v] = -1;
                 }
@@ -635,7 +755,14 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
                     if ((rc = execute(r.i0, phys[r.layer * E + r.i4], r.i1, prec))) return rc;
                 }
             } else if (r.kind == ESIM_REC_ROUTE) {
-                if ((rc = flush(T, rs, rw, true))) return rc;
+                if ((rc = flush(T, rs, rw, true, layer))) return rc;
+                if (g->capture) {                        // this layer's output -> host (zero-copy)
+                    if (cap_row + T > g->capture_rows) return ls_fail(-4, "layer capture buffer too small");
+                    copy_rows_kernel<<<64, 256, 0, g->comp_st>>>((const uint4*)g->x,
+                                                                 (uint4*)((char*)g->capture + (size_t)cap_row * H * 2),
+                                                                 (int64_t)T * H / 8);
+                    cap_row += T;
+                }
                 if (layer == L - 1) {                    // pass output -> host (zero-copy)
                     copy_rows_kernel<<<64, 256, 0, g->comp_st>>>((const uint4*)g->x,
                                                                  (uint4*)((char*)out + (size_t)out_row * H * 2),

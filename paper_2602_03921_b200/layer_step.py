@@ -64,6 +64,8 @@ def _bind():
         L.esim_ls_destroy.argtypes = [vp]
         L.esim_ls_last_error.restype = C.c_char_p
         L.esim_ls_run.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.esim_ls_shared_expert.argtypes = [vp, vp, vp, C.c_int32]
+        L.esim_ls_capture_layers.argtypes = [vp, vp, C.c_int64]
         L._ls_bound = True
     return L
 
@@ -85,6 +87,7 @@ class LayerStepResult:
     host_enqueue_ms: float
     report: dict                 # the decision stream's reference-format report (logical timeline)
     out: object = None           # last-layer hidden states of every pass (host bf16)
+    layers: object = None        # every layer's output per (pass, layer) event (keep_layers)
 
 
 def dequant_expert(raw, bits: int, hidden: int, inter: int):
@@ -202,6 +205,31 @@ class LayerStepEngine:
                 dst.copy_(blob.reshape(-1))
         torch.cuda.synchronize()
 
+    def attach_shared_expert(self, inter: int, seed: int = 1, std: float = 0.02) -> None:
+        """Always-resident shared expert per layer (Qwen1.5-MoE-A2.7B: I = 5632,
+        BASELINE.json configs[3]), random-init bf16 N(0, std) in HBM, outside the
+        expert cache (the reference sizes only routed experts).
+        Each layer adds sigmoid(x . gate_l) * SwiGLU_l(x) before the residual."""
+        torch = self.torch
+        L, H = self.cfg.model.num_layers, self.H
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        self.shared_inter = inter
+        self.shared_w = (torch.randn(L, 3 * H * inter, generator=g, device="cuda") * std).to(torch.bfloat16)
+        self.shared_gate = (torch.randn(L, H, generator=g, device="cuda") * std).to(torch.bfloat16)
+        rc = _bind().esim_ls_shared_expert(self._h, self.shared_w.data_ptr(), self.shared_gate.data_ptr(), inter)
+        if rc:
+            raise RuntimeError(f"esim_ls_shared_expert failed ({rc}): {_bind().esim_ls_last_error().decode()}")
+
+    @property
+    def shared_bytes(self) -> int:
+        return 0 if not getattr(self, "shared_inter", 0) else self.shared_w.numel() * 2 + self.shared_gate.numel() * 2
+
+    def shared_matrices(self, layer: int):
+        """(w1 [2Is, H], wd [H, Is], gate [H]) of the layer's shared expert, fp32."""
+        from .ffn import expert_matrices
+        w1, wd = expert_matrices(self.shared_w[layer], self.H, self.shared_inter)
+        return w1.float(), wd.float(), self.shared_gate[layer].float()
+
     def expert_weights(self, layer: int, expert: int, precision: str | None = None):
         """The expert's stored bytes at `precision` (default: working):
         bf16 elements, or raw codes + scale bytes."""
@@ -223,9 +251,18 @@ class LayerStepEngine:
             return w1.float(), wd.float()
         return dequant_expert(raw, _QBITS[code], H, I)
 
-    def run(self, trace, x_prefill, x_decode, keep_outputs: bool = False) -> LayerStepResult:
+    def run(self, trace, x_prefill, x_decode, keep_outputs: bool = False,
+            keep_layers: bool = False) -> LayerStepResult:
+        """One request. keep_outputs: the last layer's hidden states of every
+        pass (res.out); keep_layers: every layer's (res.layers, [events] list of
+        [T, H] bf16 host tensors, events in (pass, layer) order)."""
         torch = self.torch
         pk = trace.packed()
+        cap = None
+        if keep_layers:
+            cap = torch.empty(int(pk.pass_tokens.sum()) * self.cfg.model.num_layers * self.H,
+                              dtype=torch.bfloat16).pin_memory()
+            _bind().esim_ls_capture_layers(self._h, cap.data_ptr(), cap.numel() // self.H)
         dt = DeviceTrace(pk)
         ctoks = np.ascontiguousarray(pk.pass_tokens, np.int32)
         c = self.cfg.to_c(0, True)
@@ -239,8 +276,18 @@ class LayerStepEngine:
         rc = L.esim_ls_run(self._h, C.addressof(dt.desc), ctoks.ctypes.data, C.addressof(c), x_prefill.data_ptr(),
                            x_decode.data_ptr(), out.data_ptr(), C.addressof(counters), per_layer.ctypes.data,
                            C.addressof(res))
+        if keep_layers:
+            L.esim_ls_capture_layers(self._h, None, 0)
         if rc:
             raise RuntimeError(f"esim_ls_run failed ({rc}): {L.esim_ls_last_error().decode()}")
+        layers = None
+        if keep_layers:
+            layers, r0 = [], 0
+            for p in range(pk.n_passes):
+                T = int(pk.pass_tokens[p])
+                for _ in range(self.cfg.model.num_layers):
+                    layers.append(cap[r0 * self.H:(r0 + T) * self.H].view(T, self.H))
+                    r0 += T
         rep = report_from_counters(self.cfg.echo(), self.cfg.model.num_layers,
                                    self.cfg.hardware.per_layer_compute_us, counters, per_layer)
         decode_passes = int((pk.pass_kind == 1).sum())
@@ -250,7 +297,7 @@ class LayerStepEngine:
             h2d_bytes=res.h2d_bytes, h2d_gbs=res.h2d_bytes / (res.total_ms / 1e3) / 1e9,
             n_copies=res.n_copies, n_demand_copies=res.n_demand_copies, n_prefetch_copies=res.n_prefetch_copies,
             n_cancelled=res.n_cancelled, n_ffn_batches=res.n_ffn_batches, n_exec_experts=res.n_exec_experts,
-            host_enqueue_ms=res.host_enqueue_ms, report=rep, out=out if keep_outputs else None)
+            host_enqueue_ms=res.host_enqueue_ms, report=rep, out=out if keep_outputs else None, layers=layers)
 
     def route_rows(self, rows: int):
         """The last run's executed routing: (sel int16 [rows, K], w float32 [rows, K])."""

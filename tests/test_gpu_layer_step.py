@@ -16,18 +16,22 @@ H, I = 2048, 1024
 
 
 def _reference(engine, trace, x0, xdec, served=None, I=1024, prec_of=None, route_sel=None):
-    """No-cache fp32 forward; served[(pass, layer)][e] = the expert whose
-    weights serve e's tokens (a substitute), or None when e was dropped;
-    prec_of[(pass, layer, e)] = the precision those weights run at; route_sel:
-    the executed top-k per trace row (cache-aware routing re-selects; the
-    weights stay the original softmax at the selected experts)."""
+    return _reference_ex(engine, trace, x0, xdec, served, I, prec_of, route_sel)
+
+
+def _reference_ex(engine, trace, x0, xdec, served=None, I=1024, prec_of=None, route_sel=None, layers=None):
+    """layers: the engine's captured per-layer outputs ([events] of [T, H]);
+    given, every layer runs teacher-forced on the engine's own input to it and
+    the per-layer max relative error list is returned with the outputs."""
     import torch
     from paper_2602_03921_b200.routing import softmax_rows
     spec = trace.spec
-    outs = []
+    outs, layer_err = [], []
     for p, fp in enumerate(trace.passes):
         x = (x0 if p == 0 else xdec[p - 1:p]).cuda().float()
         for ev in fp.events:
+            if layers is not None and ev.layer > 0:
+                x = layers[p * spec.num_layers + ev.layer - 1].cuda().float()
             sc = softmax_rows(ev.logits)
             idx = np.argsort(-sc, axis=1, kind="stable")[:, :spec.top_k]
             if route_sel is not None:
@@ -45,9 +49,18 @@ def _reference(engine, trace, x0, xdec, served=None, I=1024, prec_of=None, route
                 wt = torch.tensor(np.where((idx == e).any(axis=1), sc[:, e], 0.0), dtype=torch.float32,
                                   device=out.device)
                 y += wt[:, None] * out
+            if getattr(engine, "shared_inter", 0):     # HF Qwen2MoeSparseMoeBlock shared expert
+                Is = engine.shared_inter
+                w1, wd, gw = engine.shared_matrices(ev.layer)
+                xb = x.to(torch.bfloat16).float()
+                act = (torch.nn.functional.silu(xb @ w1[:Is].T) * (xb @ w1[Is:].T)).to(torch.bfloat16).float()
+                y += torch.sigmoid(xb @ gw)[:, None] * (act @ wd.T)
             x = (x.to(torch.bfloat16).float() + y).to(torch.bfloat16).float()
+            if layers is not None:
+                got = layers[p * spec.num_layers + ev.layer].cuda().float()
+                layer_err.append((got - x).abs().max().item() / x.abs().max().item())
         outs.append(x)
-    return torch.cat(outs)
+    return (torch.cat(outs), layer_err) if layers is not None else torch.cat(outs)
 
 
 @pytest.mark.parametrize("eviction,cap_experts,miss,inter", [("ls", 12, "fetch", 1024), ("lru", 6, "fetch", 1024),
@@ -117,7 +130,8 @@ def test_layer_step_long_prefill_splits_experts(oracle_lib):
 
 
 def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, prefill, decode, prec="fp16",
-              ladder=None, routing="standard", prefetch="score"):
+              ladder=None, routing="standard", prefetch="score", spec=None, cap_bytes=None, shared_inter=0,
+              noise=0.0, trace_seed=7, layers=4, e2e_tol=1e-2):
     """I = 1408 is the Qwen1.5-MoE expert width (not a power of two); subst /
     drop follow the decision stream (substitute weights / no contribution)."""
     import torch
@@ -125,19 +139,23 @@ def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, pr
     from paper_2602_03921_b200.layer_step import LayerStepEngine
     I = inter
     eb = 3 * H * I * 2
-    spec = ModelSpec("mini_moe", num_layers=4, experts_per_layer=experts, top_k=top_k, expert_bytes_fp16=eb,
-                     **({"precisions": ladder} if ladder else {}))
-    cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=cap_experts * spec.expert_bytes(prec)),
+    if spec is None:
+        spec = ModelSpec("mini_moe", num_layers=layers, experts_per_layer=experts, top_k=top_k,
+                         expert_bytes_fp16=eb, **({"precisions": ladder} if ladder else {}))
+    cap = cap_bytes if cap_bytes is not None else cap_experts * spec.expert_bytes(prec)
+    cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=cap),
                     working_precision=prec,
                     eviction=eviction, prefetch=prefetch, percentile=80.0, miss=miss, subst_tolerance=0.2,
-                    drop_rank_threshold=2, routing=routing, lam=0.3)
-    tr = generate_synthetic(spec, seed=7, prefill_tokens=prefill, decode_tokens=decode)
+                    drop_rank_threshold=2, routing=routing, lam=0.3, prefetch_noise=noise, seed=11)
+    tr = generate_synthetic(spec, seed=trace_seed, prefill_tokens=prefill, decode_tokens=decode)
     eng = LayerStepEngine(cfg, H, I, max_tokens=prefill)
     eng.init_weights(seed=3)
+    if shared_inter:
+        eng.attach_shared_expert(shared_inter, seed=5)
     g = torch.Generator().manual_seed(1)
     x0 = torch.randn(prefill, H, generator=g).to(torch.bfloat16).pin_memory()
     xd = torch.randn(decode, H, generator=g).to(torch.bfloat16).pin_memory()
-    res = eng.run(tr, x0, xd, keep_outputs=True)
+    res = eng.run(tr, x0, xd, keep_outputs=True, keep_layers=True)
     o = oracle_lib.run(cfg, tr, full_log=True)
     assert json.dumps(o.report) == json.dumps(res.report)
     served, prec_of = {}, {}
@@ -166,12 +184,60 @@ def _run_case(eviction, cap_experts, miss, inter, oracle_lib, experts, top_k, pr
         changed = sum(set(std[r].tolist()) != set(route_sel[r].tolist()) for r in range(rows))
         assert changed == res.report["fidelity"]["modified_rows"]
         assert np.array_equal(route_w, np.take_along_axis(sc, route_sel.astype(np.int64), axis=1))
-    ref = _reference(eng, tr, x0, xd, served, I, prec_of, route_sel).cpu()
+    # every layer's output, teacher-forced on the engine's own input to it (the
+    # layer-output contract: <= 1e-2 of max |x|), then the whole chain from the
+    # pass inputs alone
+    _, layer_err = _reference_ex(eng, tr, x0, xd, served, I, prec_of, route_sel, layers=res.layers)
+    assert max(layer_err) <= 1e-2, f"layer output max rel err {max(layer_err):.3e}"
+    ref = _reference_ex(eng, tr, x0, xd, served, I, prec_of, route_sel).cpu()
     err = (got - ref).abs().max().item() / ref.abs().max().item()
-    assert err <= 1e-2, f"max rel err {err:.3e}"
+    assert err <= e2e_tol, f"max rel err {err:.3e}"
     assert res.n_copies >= res.report["totals"]["misses"] - res.report["totals"]["prefetch_started"]
     eng.close()
-    return {"precisions": sorted(set(prec_of.values()))}
+    return {"precisions": sorted(set(prec_of.values())), "err": err, "layer_err": max(layer_err),
+            "report": res.report, "copies": res.n_copies}
+
+
+def test_layer_step_full_olmoe_configs1_request(oracle_lib):
+    """BASELINE.json configs[1] at full size: OLMoE-1B-7B 16 layers x 64
+    experts, top-8, H 2048 / I 1024 (12,582,912 B bf16 experts, 12.9 GB pinned
+    store), 0.6 GB cache (51 slots), score:80 + Least-Stale, 64 prefill + 4
+    decode tokens. Decisions == the oracle; the final hidden states of every
+    pass == a layer-by-layer no-cache fp32 forward (<= 1e-2)."""
+    from paper_2602_03921_b200 import builtin_spec
+    spec = builtin_spec("olmoe")
+    r = _run_case("ls", None, "fetch", 1024, oracle_lib, experts=64, top_k=8, prefill=64, decode=4, spec=spec,
+                  cap_bytes=614_400_000, trace_seed=1)
+    assert r["report"]["totals"]["demanded"] > 400
+
+
+def test_layer_step_qwen_configs3_with_shared_expert(oracle_lib):
+    """BASELINE.json configs[3] shape: Qwen1.5-MoE-A2.7B routed experts (60 per
+    layer, top-4, H 2048 / I 1408) with expert-substitution misses, plus the
+    always-resident shared expert (I 5632, sigmoid-gated) on every layer; 6
+    of 24 layers keep the fp32 reference affordable. Every layer's output is
+    within 1e-2 of the fp32 layer on the same input; end to end the chain
+    drifts further (measured 1.2-1.3e-2 after 6 layers, 0.34e-2 after 1):
+    each layer re-rounds the residual stream to bf16, a 1-ulp flip upstream
+    (2^-8 relative) propagates through every later layer, and the shared
+    expert roughly doubles each layer's contribution -- so the chain is
+    held to 2e-2."""
+    from paper_2602_03921_b200 import ModelSpec
+    from paper_2602_03921_b200.models import builtin_spec
+    q = builtin_spec("qwen15moe")
+    spec = ModelSpec("qwen15moe_6l", num_layers=6, experts_per_layer=q.experts_per_layer, top_k=q.top_k,
+                     expert_bytes_fp16=3 * H * 1408 * 2)
+    r = _run_case("ls", 18, "subst", 1408, oracle_lib, experts=60, top_k=4, prefill=32, decode=4, spec=spec,
+                  shared_inter=5632, trace_seed=2, e2e_tol=2e-2)
+    assert r["report"]["totals"]["substituted"] > 0
+
+
+def test_layer_step_prediction_noise(oracle_lib):
+    """prefetch_noise 0.3 (prefetch.py:110-136) on the physical path: the
+    device PCG64 stream drives the prefetches; decisions == the oracle (numpy's
+    own generator), outputs == the reference forward."""
+    r = _run_case("ls", 6, "fetch", 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=4, noise=0.3)
+    assert r["report"]["totals"]["prefetch_started"] > 0
 
 
 def test_layer_step_rejects_configs_its_store_cannot_serve():
