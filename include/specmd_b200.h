@@ -247,6 +247,17 @@ int esim_replay_launch(const EsimConfig *h_cfg, const EsimConfig *d_cfg, int32_t
                        EsimCounters *d_counters, int64_t *d_per_layer, int32_t pl_stride,
                        EsimRec *d_recs, int64_t rec_cap, int32_t *d_pred_experts, int64_t pe_cap,
                        int32_t warps_per_cta, int32_t queue_cap, void *stream);
+/* The same with a cap on the launch's CTAs. Common-path points (miss=fetch,
+ * standard routing) replay in a persistent launch: one CTA of up to 12 warps
+ * per SM, every warp pulling the next point of the launch order (put the
+ * longest first). max_ctas > 0 limits the launch to that many CTAs (SMs), so
+ * concurrent launches of different policies on different streams split the
+ * GPU instead of interleaving; 0 = as many as fit. */
+int esim_replay_launch_ex(const EsimConfig *h_cfg, const EsimConfig *d_cfg, int32_t n,
+                          const EsimTraceDesc *d_traces, const EsimRouterOut *d_routers, int32_t max_tokens,
+                          EsimCounters *d_counters, int64_t *d_per_layer, int32_t pl_stride,
+                          EsimRec *d_recs, int64_t rec_cap, int32_t *d_pexp, int64_t pe_cap,
+                          int32_t warps_per_cta, int32_t queue_cap, int32_t max_ctas, void *stream);
 
 /* End-to-end host API (engine.run_simulation over many configs): host
  * traces (host pointers) and configs in; router + replay on the device;
@@ -277,6 +288,11 @@ int esim_sweep_plan_destroy(void *plan);
  * step and checks its statuses. At most two steps in flight. Step k+1's copies
  * and router overlap step k's replays. esim_sweep_plan_run drains first. */
 int esim_sweep_plan_submit(void *plan, EsimCounters *counters, int64_t *per_layer);
+/* Opt-in profile-guided schedule: re-order every launch group longest-measured
+ * first using the per-point replay times in `counters` (the output of one of
+ * this plan's previous runs). Plans are created with a static order (the
+ * traces' token-expert selections, longest first). */
+int esim_sweep_plan_tune(void *plan, const EsimCounters *counters);
 int esim_sweep_plan_wait(void *plan);
 
 /* Report assembly for sweeps (metrics.flatten_report + emit csv,

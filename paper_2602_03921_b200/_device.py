@@ -39,6 +39,7 @@ def lib():
         L.esim_last_error.restype = C.c_char_p
         L.esim_router_launch.argtypes = [vp, vp, i32, f64, f64, vp]
         L.esim_replay_launch.argtypes = [vp, vp, i32, vp, vp, i32, vp, vp, i32, vp, i64, vp, i64, i32, i32, vp]
+        L.esim_replay_launch_ex.argtypes = [vp, vp, i32, vp, vp, i32, vp, vp, i32, vp, i64, vp, i64, i32, i32, i32, vp]
         L.esim_replay_smem_per_point.argtypes = [vp, i32, i32, i32, i32]
         L.esim_run_host.argtypes = [vp, i32, vp, i32, vp, vp, i32, vp, i64, vp, i64]
         L.esim_softmax_launch.argtypes = [vp, i32, i32, vp, vp]
@@ -245,19 +246,26 @@ class ReplayBatch:
         n = len(self.ccfg)
         self.Lmax = max(c.num_layers for c in self.ccfg)
         groups: dict = {}
-        # one launch per (policy, general) -- the kernel specialisations; every
-        # geometry shares it, shared memory sized by the largest (measured on the
-        # C5 step: 61.5 ms for 3 launches against 66 ms for 12 per-geometry
-        # launches, which the SMs could not co-schedule from the start)
+        # one launch per kernel specialisation (policy x {common, general} path),
+        # shared memory sized by the largest geometry of the launch; the
+        # common-path launches are persistent (one CTA per SM, warps pull points
+        # in launch order)
         for i, c in enumerate(self.ccfg):
             general = c.miss != 0 or c.routing != 0
             groups.setdefault((c.eviction, general), []).append(i)
-        # first launch: larger traces first (a rough cost); tune_order() then sorts
-        # by the replay times measured on the device (longest first, LPT)
+        # static order: longest estimated first (the trace's token-expert
+        # selections); tune_order() re-sorts by measured replay times (opt-in)
+        rows_k = {id(s_[1]): int(s_[1].pk.row_offset[-1]) * s_[1].pk.top_k for s_ in self.sets}
+        tcost = [rows_k[id(self.sets[c.trace_id][1])] for c in self.ccfg]
+
         def cost(i):
-            c = self.ccfg[i]
-            return (-c.num_layers * c.experts, i)
+            return (-tcost[i], i)
         self.groups = [sorted(g, key=cost) for g in groups.values()]
+        # concurrent group launches split the SMs by estimated work (persistent
+        # common-path launches: one CTA per SM, policies never share an SM)
+        sms = _torch().cuda.get_device_properties(0).multi_processor_count
+        gw = [sum(tcost[i] for i in g) for g in self.groups]
+        self.group_ctas = [max(1, round(sms * w / max(1, sum(gw)))) for w in gw]
         self.order = [i for g in self.groups for i in g]
         harr = (_abi.EsimConfig * n)(*[self.ccfg[i] for i in self.order])
         self.h_cfg = harr
@@ -327,13 +335,13 @@ class ReplayBatch:
                 gs.wait_event(self._fork)
                 sh = gs.cuda_stream
             hptr = C.addressof(self.h_cfg) + base * csz
-            rc = lib().esim_replay_launch(
+            rc = lib().esim_replay_launch_ex(
                 hptr, self.d_cfg.data_ptr() + base * csz, n, self.d_traces.data_ptr(), self.d_routers.data_ptr(),
                 self.max_tokens, self.counters.data_ptr() + base * cntsz,
                 self.per_layer.data_ptr() + base * self.Lmax * _abi.ESIM_PL_FIELDS * 8, self.Lmax,
                 self.recs.data_ptr() + base * self.rec_cap * 64 if self.full_log else None, self.rec_cap,
                 self.pexp.data_ptr() + base * self.pe_cap * 4 if self.full_log else None, self.pe_cap,
-                warps_per_cta, queue_cap, sh)
+                warps_per_cta, queue_cap, self.group_ctas[gi], sh)
             _check(rc, "replay")
             if not single:
                 self._joins[gi].record(self._streams[gi])

@@ -25,7 +25,7 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
                                     int policy, bool general, const int32_t* out_index = nullptr,
-                                    bool log_rt = true);
+                                    bool log_rt = true, int max_ctas = 0);
 int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt, bool gen);
 
 static thread_local std::string g_err;
@@ -137,11 +137,11 @@ extern "C" int esim_replay_smem_per_point(const EsimConfig* h_cfg, int32_t n, in
     return esim_replay_smem_bytes(z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.ca, z.has_cnt, z.general);
 }
 
-extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_cfg, int32_t n,
+extern "C" int esim_replay_launch_ex(const EsimConfig* h_cfg, const EsimConfig* d_cfg, int32_t n,
                                   const EsimTraceDesc* d_traces, const EsimRouterOut* d_routers, int32_t max_tokens,
                                   EsimCounters* d_counters, int64_t* d_per_layer, int32_t pl_stride,
                                   EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp, int64_t pe_cap,
-                                  int32_t warps_per_cta, int32_t queue_cap, void* stream) {
+                                  int32_t warps_per_cta, int32_t queue_cap, int32_t max_ctas, void* stream) {
     if (n <= 0) return 0;
     Sizing z;
     int rc = replay_sizing(h_cfg, n, max_tokens, pl_stride, queue_cap, &z);
@@ -155,9 +155,18 @@ extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_c
     cudaError_t e = esim_replay_launch_impl(d_cfg, n, d_traces, d_routers, d_counters, d_per_layer, d_recs, rec_cap,
                                             d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
                                             w, (cudaStream_t)stream, nullptr, z.policy, z.general, nullptr,
-                                            z.log_rt);
+                                            z.log_rt, max_ctas);
     if (e != cudaSuccess) return cuda_fail(e, "replay launch");
     return 0;
+}
+
+extern "C" int esim_replay_launch(const EsimConfig* h_cfg, const EsimConfig* d_cfg, int32_t n,
+                                  const EsimTraceDesc* d_traces, const EsimRouterOut* d_routers, int32_t max_tokens,
+                                  EsimCounters* d_counters, int64_t* d_per_layer, int32_t pl_stride,
+                                  EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp, int64_t pe_cap,
+                                  int32_t warps_per_cta, int32_t queue_cap, void* stream) {
+    return esim_replay_launch_ex(h_cfg, d_cfg, n, d_traces, d_routers, max_tokens, d_counters, d_per_layer, pl_stride,
+                                 d_recs, rec_cap, d_pexp, pe_cap, warps_per_cta, queue_cap, 0, stream);
 }
 
 // single point with its decisions streamed to mapped host memory (layer_step.cu)
@@ -218,8 +227,9 @@ struct SweepPlan {
     std::vector<EsimConfig> pcfg;                 // group-sorted configs
     std::vector<EsimConfig> caller_cfg;           // the caller's configs (caller order)
     std::vector<int> order;                       // launch position -> caller row
-    int tune_runs = 2;                            // runs whose measured times re-sort the groups
+    int tune_runs = 0;                            // runs whose measured times re-sort the groups (opt-in)
     std::vector<std::pair<int, int>> groups;      // [begin, end) in pcfg
+    std::vector<int> group_ctas;                  // persistent launches: CTAs (SMs) per group
     std::vector<EsimTraceDesc> htr;               // caller descriptors (host pointers)
     std::vector<int32_t> params;                  // predictor per trace
     std::vector<double> noise;                    // prediction noise per trace (0 = none)
@@ -381,7 +391,7 @@ int slab_enqueue(SweepPlan* P, Slab& S, EsimCounters* counters, int64_t* per_lay
                                     (int64_t*)(base + P->pl_off), full ? (EsimRec*)(base + P->rec_off) : nullptr,
                                     P->rec_cap, full ? (int32_t*)(base + P->pe_off) : nullptr, P->pe_cap, z.N, z.S,
                                     z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt, w, S.gs[g], nullptr, z.policy,
-                                    z.general, (int32_t*)(base + P->idx_off) + b, z.log_rt);
+                                    z.general, (int32_t*)(base + P->idx_off) + b, z.log_rt, P->group_ctas[g]);
         if (e != cudaSuccess) return cuda_fail(e, "replay launch");
         cudaEventRecord(S.ge[g], S.gs[g]);
         cudaStreamWaitEvent(S.st, S.ge[g], 0);
@@ -414,7 +424,7 @@ int check_status(const EsimCounters* counters, int n) {
 
 // profile-guided scheduling: every group longest-measured first (the kernel stamps
 // each point's start/end globaltimer into counters.pad); uploaded to every slab
-void plan_tune(SweepPlan* P, const EsimCounters* counters) {
+int plan_tune(SweepPlan* P, const EsimCounters* counters) {
     const int n = P->n;
     std::vector<int64_t> d(n);
     for (int pos = 0; pos < n; pos++) {
@@ -433,9 +443,12 @@ void plan_tune(SweepPlan* P, const EsimCounters* counters) {
     for (int i = 0; i < n; i++) P->pcfg[i] = P->caller_cfg[neworder[i]];
     for (auto& S : P->slab) {
         if (!S.dev) continue;
-        cudaMemcpy(S.dev + P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice);
-        cudaMemcpy(S.dev + P->idx_off, out_index.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice);
+        cudaError_t e = cudaMemcpy(S.dev + P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(S.dev + P->idx_off, out_index.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "plan tune upload");
     }
+    return 0;
 }
 }  // namespace
 
@@ -482,22 +495,43 @@ extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const Es
         }
     }
     // one launch group per kernel specialisation (policy x {common, general} path),
-    // every geometry in it (shared memory sized by the largest), each replayed on its
-    // own stream; first order = larger traces first, then after each of the first
-    // runs the measured per-point replay times (longest first, plan_tune)
+    // each on its own stream; within a group the points go longest estimated first
+    // (static cost model: the trace's token-expert selections), so the persistent
+    // common-path launches pull the long replays first -- greedy LPT
     std::vector<int> order(n);
     for (int i = 0; i < n; i++) order[i] = i;
     auto gen_of = [&](int a) { return cfg[a].miss != ESIM_MISS_FETCH || cfg[a].routing != ESIM_ROUTE_STANDARD; };
+    auto grp_of = [&](int a) { return (gen_of(a) ? 16 : 0) + cfg[a].eviction; };
+    auto cost_of = [&](int a) {
+        const EsimTraceDesc& t = traces[cfg[a].trace_id];
+        return (double)t.n_rows_total * t.top_k;
+    };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        if (cfg[a].eviction != cfg[b].eviction) return cfg[a].eviction < cfg[b].eviction;
-        if (gen_of(a) != gen_of(b)) return gen_of(a) < gen_of(b);
-        return cfg[a].num_layers * cfg[a].experts > cfg[b].num_layers * cfg[b].experts;
+        if (grp_of(a) != grp_of(b)) return grp_of(a) < grp_of(b);
+        return cost_of(a) > cost_of(b);
     });
     for (int i = 0; i < n; i++) {
-        if (i == 0 || cfg[order[i]].eviction != cfg[order[i - 1]].eviction || gen_of(order[i]) != gen_of(order[i - 1]))
+        if (i == 0 || grp_of(order[i]) != grp_of(order[i - 1]))
             P->groups.push_back({i, i + 1});
         else
             P->groups.back().second = i + 1;
+    }
+    // the concurrent group launches split the SMs in proportion to their estimated
+    // work (one persistent CTA per SM each), so every group's warps loop over
+    // several points and the policies never share an SM
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        std::vector<double> gw;
+        double tw = 0;
+        for (auto& gr : P->groups) {
+            double w = 0;
+            for (int i = gr.first; i < gr.second; i++) w += cost_of(order[i]);
+            gw.push_back(w);
+            tw += w;
+        }
+        for (double w : gw) P->group_ctas.push_back(std::max(1, (int)std::lround(sms * w / (tw > 0 ? tw : 1))));
     }
     P->order = order;
     P->caller_cfg.assign(cfg, cfg + n);
@@ -592,9 +626,21 @@ extern "C" int esim_sweep_plan_run(void* plan, EsimCounters* counters, int64_t* 
     if (e != cudaSuccess) return cuda_fail(e, "sweep plan run");
     if (P->tune_runs > 0) {
         P->tune_runs--;
-        plan_tune(P, counters);
+        if ((rc = plan_tune(P, counters))) return rc;
     }
     return check_status(counters, P->n);
+}
+
+// profile-guided re-order (opt-in): every group longest-measured first by the
+// per-point replay times of a previous run's counters (the caller's buffer)
+extern "C" int esim_sweep_plan_tune(void* plan, const EsimCounters* counters) {
+    SweepPlan* P = static_cast<SweepPlan*>(plan);
+    if (!P || !counters) return fail(-1, "null argument");
+    while (!P->pending.empty()) {
+        const int rc = esim_sweep_plan_wait(plan);
+        if (rc) return rc;
+    }
+    return plan_tune(P, counters);
 }
 
 extern "C" int esim_run_host(const EsimConfig* cfg, int32_t n, const EsimTraceDesc* traces, int32_t n_traces,

@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 
 #include "../../include/specmd_b200.h"
 #include "numpy_f32.cuh"
@@ -63,6 +65,7 @@ struct ReplayArgs {
     int warps_per_cta;
     int point_bytes;
     const int32_t* out_index;      // optional: output row of launch point pid (counters, per_layer, logs)
+    int* work;                     // optional: persistent launch, next point of the launch order
     volatile int64_t* progress;    // optional (single point, streamed decisions): [0] events done
                                    // (-1 on error), [1 + ev] records emitted through event ev
 };
@@ -81,7 +84,7 @@ struct Ctr {                       // 32-bit counts: native ATOMS.ADD (64-bit is
 struct Layout {
     int key, q_submit, q_comp, dsum, ctr, dem_summed;     // 8-byte
     int cnt, rscore, q_score, pl, demmask, lsc, ca_w, ca_row, dem_gate, dem_tokens, dem_expert, dem_rank;  // 4-byte
-    int rs, hist, res_ident, fs, q_ident, ca_sel;         // 2-byte
+    int rs, hist, res_ident, fs, q_ident, ca_sel, vict;   // 2-byte
     int q_flags, tofetch, ca_mod;                         // 1-byte
     int total;
 };
@@ -119,6 +122,7 @@ __host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E,
     l.fs = o; o += al8(S * 2);
     l.q_ident = o; o += al8(Q * 2);
     l.ca_sel = o; o += al8(ca ? T * K * 2 : 0);
+    l.vict = o; o += al8(gen ? 0 : E * 2);          // batched watchdog sweep 2 (uniform instances)
     l.q_flags = o; o += al8(Q);
     l.tofetch = o; o += al8(E);
     l.ca_mod = o; o += al8(ca ? T : 0);
@@ -168,6 +172,7 @@ struct Pt {
     uint16_t* fs;
     int16_t* q_ident;
     int16_t* ca_sel;
+    int16_t* vict;                  // sweep-2 victims in eviction order (uniform instances)
     uint8_t* q_flags;
     uint8_t* tofetch;
     uint8_t* ca_mod;
@@ -309,6 +314,38 @@ DFI void emit_lanes(Pt& p, bool act, int rank, int cnt, int kind, int layer, int
 }
 
 DFI unsigned lanes_below(int lane) { return (1u << lane) - 1u; }
+
+// one record at absolute log index idx from this lane (batched phases: every
+// lane owns a record at a position fixed by prefix counts); returns its digest
+// term (0 when inactive) for the caller's one warp-sum per batch
+DFI uint64_t lane_rec(Pt& p, bool act, int64_t idx, int kind, int layer, int i0, int i1, int i2, int i3, int i4,
+                      int64_t t0, int64_t t1, int64_t t2, double x0) {
+    if (!act) return 0;
+    if (p.full) {
+        if (idx < p.rec_cap) {
+            EsimRec r;
+            r.kind = kind; r.pass_id = p.pass_id; r.layer = layer;
+            r.i0 = i0; r.i1 = i1; r.i2 = i2; r.i3 = i3; r.i4 = i4;
+            r.t0 = t0; r.t1 = t1; r.t2 = t2; r.x0 = x0;
+            p.recs[idx] = r;
+        } else {
+            p.err = -4;                          // lane-local; folded by the caller
+        }
+    }
+    return p.digest_on ? fold(rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0), idx) : 0;
+}
+
+DFI void digest_add_warp(Pt& p, uint64_t v) {
+    if (!p.digest_on) return;
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    p.digest += v;
+}
+
+DFI void err_fold(Pt& p) {                       // a lane-local record-capacity error -> warp-uniform
+    const int e = __reduce_min_sync(FULL, p.err);
+    p.err = e;
+}
 
 DFI void rec_prefetch(Pt& p, int ev, int target, int expert, int64_t t, float score, int reason) {
     emit(p, ESIM_REC_PREFETCH, p.layer, ev, target, expert, reason, 0, t, 0, 0, (double)score);
@@ -590,7 +627,70 @@ DFI int q_find(const Pt& p, int ident) {
     return -1;
 }
 
+// Uniform instances: entry i of the settled queue completes at qc0 + i * dur, so
+// the k entries landed by `now` are known up front and admitted lane-parallel:
+// slot = i-th pop of the free-slot stack, policy key stamp = seq + i, and the
+// prefetch "completed" records at the positions their order fixes.
+DFI void settle_uniform(Pt& p) {
+    if (p.qn == 0 || p.qc0 > p.now) return;
+    int k = p.qn;
+    if (p.dur_w > 0) {
+        const int64_t t = (p.now - p.qc0) / p.dur_w + 1;
+        if (t < k) k = (int)t;
+    }
+    if (p.fs_top < k) { p.err = -2; return; }
+    const int wp = p.c->working_prec;
+    const unsigned below = lanes_below(p.lane);
+    uint64_t dg = 0;
+    int npf = 0;
+    for (int b = 0; b < k; b += 32) {
+        const int i = b + p.lane;
+        const bool act = i < k;
+        bool pf = false;
+        int ident = 0, slot = 0;
+        float score = 0.0f;
+        if (act) {
+            const int x = qphys(p, i);
+            ident = p.q_ident[x];
+            pf = p.q_flags[x] & 1;
+            score = p.q_score[x];
+            slot = p.fs[p.fs_top - 1 - i];
+            p.rs[ident] = rs_make(wp, slot);
+            p.res_ident[slot] = (int16_t)ident;
+            if (p.hist[ident] == -2) p.hist[ident] = -1;
+            const uint64_t st = p.seq + (uint64_t)i;            // note_admit, in pop order
+            uint64_t nk = 0;
+            if (p.pol == ESIM_EV_LRU) nk = st;
+            else if (p.pol == ESIM_EV_LS) nk = LS_CURRENT | st;
+            else if (p.pol == ESIM_EV_LFU || p.pol == ESIM_EV_LHU) nk = ((uint64_t)p.cnt[ident] << 32) | st;
+            p.key[slot] = nk;
+        }
+        const unsigned pm = __ballot_sync(FULL, pf);
+        const int il = ediv(p, ident);
+        dg += lane_rec(p, pf, p.n_recs + npf + __popc(pm & below), ESIM_REC_PREFETCH, p.layer, 2, il,
+                       ident - il * p.E, 0, 0, p.qc0 + (int64_t)i * p.dur_w, 0, 0, (double)score);
+        npf += __popc(pm);
+    }
+    digest_add_warp(p, dg);
+    if (p.full) err_fold(p);
+    __syncwarp();
+    const int64_t nb = p.eb_w;
+    p.seq += (uint64_t)k;
+    p.fs_top -= k;
+    p.qh += k;
+    if (p.qh >= p.Q) p.qh -= p.Q;
+    p.qn -= k;
+    p.qc0 += (int64_t)k * p.dur_w;
+    p.nA = p.nA > k ? p.nA - k : 0;
+    p.reserved_bytes -= nb * k;
+    p.resident_bytes += nb * k;
+    p.n_recs += npf;
+    p.pf_ev[2] += npf;
+    if (p.resident_bytes + p.reserved_bytes > p.cap && !p.err) p.err = -2;
+}
+
 DFI void settle(Pt& p) {                                                   // engine.py:422-442
+    if (p.uniform) { settle_uniform(p); return; }
     while (p.qn > 0) {
         const int h = p.qh;
         const int64_t comp = qcomp(p, 0);
@@ -846,6 +946,118 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
     return 1;
 }
 
+// Watchdog sweep 2 (prefetch.py:199-221) for uniform instances under LRU / LS /
+// LFU / LHU, batched. Every candidate needs exactly one expert's bytes, so the
+// first `room` candidates start without evicting; each later one evicts the
+// current minimum-key resident -- sweep 2 changes no key, so these victims
+// are the residents in ascending key order (LS: stale ones only; a current
+// minimum is a refusal, and so is every later candidate's); once no victim is
+// left the rest are dropped "no_space". The victims are extracted with one
+// warp min-reduction each; records (evict + started, or dropped) land at the
+// positions their candidate order fixes and are written lane-parallel.
+DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int target) {
+    const int64_t nb = p.eb_w;
+    const int wp = p.c->working_prec;
+    int64_t room = (p.cap - p.resident_bytes - p.reserved_bytes) / nb;
+    if (room < 0) room = 0;
+    const int F = nt < room ? nt : (int)room;
+    const int need = nt - F;
+    int r = 0;
+    bool refusals = false;                     // LS: a current resident was the minimum
+    if (need > 0) {
+        const bool wide = p.pol == ESIM_EV_LFU || p.pol == ESIM_EV_LHU;   // 64-bit (count, touch) keys
+        const uint32_t* k32 = reinterpret_cast<const uint32_t*>(p.key);
+        // this lane's smallest key above `lo` (keys are unique; free slots hold the maximum)
+        auto lane_min = [&](uint64_t lo, int& slot) -> uint64_t {
+            uint64_t bk = wide ? KEY_FREE : 0xFFFFFFFFull;
+            int bs = 0;
+            for (int sl = p.lane; sl < p.S; sl += 32) {
+                const uint64_t k = wide ? p.key[sl] : (uint64_t)k32[2 * sl];
+                const bool better = k > lo && k < bk;
+                bs = better ? sl : bs;
+                bk = better ? k : bk;
+            }
+            slot = bs;
+            return bk;
+        };
+        int lslot;
+        uint64_t lk;
+        {                                                              // first pass: no lower bound
+            uint64_t bk = wide ? KEY_FREE : 0xFFFFFFFFull;
+            int bs = 0;
+            for (int sl = p.lane; sl < p.S; sl += 32) {
+                const uint64_t k = wide ? p.key[sl] : (uint64_t)k32[2 * sl];
+                bs = k < bk ? sl : bs;
+                bk = k < bk ? k : bk;
+            }
+            lk = bk;
+            lslot = bs;
+        }
+        const uint64_t FREE = wide ? KEY_FREE : 0xFFFFFFFFull;
+        while (r < need) {
+            const uint64_t m = wide ? warp_min_u64(lk) : (uint64_t)__reduce_min_sync(FULL, (uint32_t)lk);
+            if (m == FREE) break;                                     // no resident left: no_space drops
+            if (p.pol == ESIM_EV_LS && (m & LS_CURRENT)) { refusals = true; break; }
+            const int wl = __ffs(__ballot_sync(FULL, lk == m)) - 1;
+            const int vs = __shfl_sync(FULL, lslot, wl);
+            if (p.lane == 0) p.vict[r] = (int16_t)vs;
+            r++;
+            if (p.lane == wl) lk = lane_min(m, lslot);
+        }
+        __syncwarp();
+    }
+    const int started = F + r, dropped = nt - started;
+    if (p.qn + started > p.Q) { p.err = STATUS_QUEUE_OVERFLOW; return; }
+    const int64_t base = p.n_recs;
+    uint64_t dg = 0;
+    for (int b = 0; b < nt; b += 32) {
+        const int t = b + p.lane;
+        const bool act = t < nt;
+        int e = 0;
+        float sc = 0.0f;
+        if (act) { const int j = p.tofetch[t]; e = pe[j]; sc = ps[j]; }
+        const bool ev_rec = act && t >= F && t < started;
+        const bool st = act && t < started;
+        const bool dr = act && t >= started;
+        const int64_t ri = base + (t < F ? t : (t < started ? F + 2 * (t - F) : F + 2 * r + (t - started)));
+        int vid = 0, vslot = 0;
+        if (ev_rec) { vslot = p.vict[t - F]; vid = p.res_ident[vslot]; }
+        const int vl = ediv(p, vid);
+        dg += lane_rec(p, ev_rec, ri, ESIM_REC_EVICT, p.layer, vl, vid - vl * p.E, wp, 1, 0, 0, 0, 0, 0.0);
+        dg += lane_rec(p, st, ri + (ev_rec ? 1 : 0), ESIM_REC_PREFETCH, p.layer, 1, target, e, 0, 0, p.now, 0, 0,
+                       (double)sc);
+        dg += lane_rec(p, dr, ri, ESIM_REC_PREFETCH, p.layer, 4, target, e, 3, 0, p.now, 0, 0, (double)sc);
+        __syncwarp();
+        if (ev_rec) {                                                  // evict (engine.py:451-460)
+            p.rs[vid] = 0;
+            p.hist[vid] = (int16_t)p.pass_id;
+            p.res_ident[vslot] = -1;
+            p.key[vslot] = KEY_FREE;
+            p.fs[p.fs_top + (t - F)] = (uint16_t)vslot;
+        }
+        if (st) {                                                      // reserve + channel.append
+            const int x = qphys(p, p.qn + t);
+            p.q_ident[x] = (int16_t)(target * p.E + e);
+            p.q_flags[x] = (uint8_t)(1 | (wp << 2));
+            p.q_score[x] = sc;
+            p.rs[target * p.E + e] = RS_INF;
+        }
+    }
+    digest_add_warp(p, dg);
+    if (p.full) err_fold(p);
+    __syncwarp();
+    if (p.qn == 0 && started > 0) p.qc0 = p.now + p.dur_w;
+    p.qn += started;
+    p.fs_top += r;
+    p.resident_bytes -= nb * r;
+    p.reserved_bytes += nb * started;
+    p.n_evict += r;
+    p.pf_ev[1] += started;
+    p.pf_ev[4] += dropped;
+    p.n_recs += F + 2 * r + dropped;
+    if (p.pol == ESIM_EV_LS && refusals) ctr_add(p, p.ctr->ls_refusals, dropped);
+}
+
 // _submit_prefetches + watchdog_step (engine.py:651-725, prefetch.py:163-221)
 DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
     const int target = p.layer + 1;
@@ -898,7 +1110,12 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
         nt += __popc(fm);
     }
     __syncwarp();
-    for (int t = 0; t < nt && !p.err; t++) {                              // sweep 2
+    if (p.uniform && (p.pol == ESIM_EV_LRU || p.pol == ESIM_EV_LS || p.pol == ESIM_EV_LFU ||
+                      p.pol == ESIM_EV_LHU)) {
+        sweep2_uniform(p, pe, ps, nt, target);
+        return;
+    }
+    for (int t = 0; t < nt && !p.err; t++) {                              // sweep 2 (serial)
         const int j = p.tofetch[t];
         const int e = pe[j];
         const float sc = ps[j];
@@ -1026,28 +1243,22 @@ DFI int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int
 }
 
 // ---------------------------------------------------------------------------
-#ifndef ESIM_REPLAY_MINB
-#define ESIM_REPLAY_MINB 1
-#endif
-#ifndef ESIM_SIMPLE_MINB
-#define ESIM_SIMPLE_MINB 1          // blocks/SM hint for the common-path instances
-#endif
+// Common-path launches are persistent with one CTA of kPersistWarps warps per SM
+// (registers <= 65536 / (32 * 12) = 170 per thread): an SM then only ever runs
+// one policy's kernel -- two policies' ~80 KB instruction streams sharing an SM
+// thrash its instruction cache -- and its warps pull points longest-first.
+constexpr int kPersistWarps = 12;
 // POL: eviction policy; GEN: 0 = the common case (miss=fetch, standard routing) with every
 // other miss/routing path compiled out, 1 = all paths. Every helper is force-inlined, so the
 // compile-time policy/miss constants delete the other policies' code from the kernel.
 // LOG: 0 = digest only, no record log (compile-time: the log-writing code is gone
 // from the kernel), 1 = per-point runtime flags (full log and/or digest)
 template <int POL, int GEN, int LOG>
-__global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB) replay_kernel(ReplayArgs A) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int wid = threadIdx.x >> 5;
-    const int pid = blockIdx.x * A.warps_per_cta + wid;
-    if (pid >= A.n_points) return;
+DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     const int64_t orow = A.out_index ? A.out_index[pid] : pid;      // where this point's results go
     const EsimConfig* cfg = &A.cfg[pid];
     const EsimTraceDesc tr = A.traces[cfg->trace_id];
     const EsimRouterOut R = A.routers[cfg->trace_id];
-    unsigned char* base = smem_raw + (size_t)wid * A.point_bytes;
     const bool ca = GEN && cfg->routing == ESIM_ROUTE_CACHE_AWARE;
     const Layout lay = make_layout(A.N, A.S, A.Q, A.Lmax, A.Emax, A.Tmax, A.Kmax, A.Tmax > 0, A.has_cnt != 0, GEN != 0);
 
@@ -1112,6 +1323,7 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     p.fs = reinterpret_cast<uint16_t*>(base + lay.fs);
     p.q_ident = reinterpret_cast<int16_t*>(base + lay.q_ident);
     p.ca_sel = reinterpret_cast<int16_t*>(base + lay.ca_sel);
+    p.vict = reinterpret_cast<int16_t*>(base + lay.vict);
     p.q_flags = base + lay.q_flags;
     p.tofetch = base + lay.tofetch;
     p.ca_mod = base + lay.ca_mod;
@@ -1378,7 +1590,43 @@ __global__ void __launch_bounds__(128, GEN ? ESIM_REPLAY_MINB : ESIM_SIMPLE_MINB
     }
 }
 
+template <int POL, int GEN, int LOG>
+__global__ void __launch_bounds__(GEN ? 128 : 32 * kPersistWarps, 1) replay_kernel(ReplayArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int wid = threadIdx.x >> 5;
+    unsigned char* base = smem_raw + (size_t)wid * A.point_bytes;
+    if (A.work == nullptr) {                         // one point per warp
+        const int pid = blockIdx.x * A.warps_per_cta + wid;
+        if (pid < A.n_points) replay_point<POL, GEN, LOG>(A, pid, base);
+        return;
+    }
+    // persistent: every warp pulls the next point of the launch order (longest
+    // first) as soon as it is free -- greedy LPT packing across the whole grid
+    for (;;) {
+        int pid = 0;
+        if ((threadIdx.x & 31) == 0) pid = atomicAdd(A.work, 1);
+        pid = __shfl_sync(FULL, pid, 0);
+        if (pid >= A.n_points) break;
+        replay_point<POL, GEN, LOG>(A, pid, base);
+        __syncwarp();
+    }
+}
+
 }  // namespace esim
+
+// one work counter per stream (launches on a stream are ordered, so they share it)
+static cudaError_t work_counter(cudaStream_t st, int** out) {
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, int*> ctr;
+    std::lock_guard<std::mutex> lock(mu);
+    int*& c = ctr[st];
+    if (!c) {
+        const cudaError_t e = cudaMalloc((void**)&c, sizeof(int));
+        if (e != cudaSuccess) { c = nullptr; return e; }
+    }
+    *out = c;
+    return cudaSuccess;
+}
 
 int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt, bool gen) {
     return esim::make_layout(N, S, Q, L, E, T, K, ca, has_cnt, gen).total;
@@ -1389,7 +1637,8 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     int64_t* d_per_layer, EsimRec* d_recs, int64_t rec_cap, int32_t* d_pexp,
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
-                                    int policy, bool general, const int32_t* out_index, bool log_rt) {
+                                    int policy, bool general, const int32_t* out_index, bool log_rt,
+                                    int max_ctas) {
     esim::ReplayArgs a;
     a.progress = progress;
     a.out_index = out_index;
@@ -1400,8 +1649,9 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
     a.has_cnt = has_cnt ? 1 : 0;
     a.warps_per_cta = warps_per_cta;
     a.point_bytes = esim::make_layout(N, S, Q, Lmax, Emax, Tmax, Kmax, Tmax > 0, has_cnt, general).total;
+    a.work = nullptr;
     const size_t smem = (size_t)a.point_bytes * warps_per_cta;
-    const int blocks = (n + warps_per_cta - 1) / warps_per_cta;
+    int blocks = (n + warps_per_cta - 1) / warps_per_cta;
     void (*k)(esim::ReplayArgs) = nullptr;
 #define ESIM_PICK(P)                                                                   \
     case P: k = general ? esim::replay_kernel<P, 1, 1>                                 \
@@ -1423,6 +1673,28 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
         e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         if (e != cudaSuccess) return e;
     }
-    k<<<blocks, 32 * warps_per_cta, smem, st>>>(a);
+    if (!general && !progress) {
+        // persistent: one resident wave of warps pulls the points (launch order =
+        // longest estimated first) from a per-stream work counter; as many warps
+        // per CTA as shared memory allows, up to one SM's worth
+        int w = esim::kPersistWarps;
+        while (w > 1 && (size_t)a.point_bytes * w > 227 * 1024) w--;
+        a.warps_per_cta = w;
+        warps_per_cta = w;
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const size_t psmem = (size_t)a.point_bytes * w;
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem)) != cudaSuccess)
+            return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 32 * w, psmem)) != cudaSuccess) return e;
+        blocks = (n + w - 1) / w;
+        const int wave = sms * (per > 0 ? per : 1);
+        if (blocks > wave) blocks = wave;
+        if (max_ctas > 0 && blocks > max_ctas) blocks = max_ctas;   // this launch's share of the SMs
+        if ((e = work_counter(st, &a.work)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(a.work, 0, sizeof(int), st)) != cudaSuccess) return e;
+    }
+    k<<<blocks, 32 * warps_per_cta, (size_t)a.point_bytes * warps_per_cta, st>>>(a);
     return cudaGetLastError();
 }
