@@ -37,6 +37,19 @@ def _digest() -> str:
     return h.hexdigest()
 
 
+def _obj_digest(src: str) -> str:
+    """Per-object hash: the .cu itself plus every shared header and the flags."""
+    import hashlib
+    h = hashlib.sha256(" ".join(FLAGS).encode())
+    deps = [os.path.join(CSRC, src)] + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh"))
+    deps.append(os.path.join(HERE, "..", "include", "specmd_b200.h"))
+    for d in deps:
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
@@ -61,8 +74,15 @@ def _build_locked(verbose: bool) -> str:
 
     def compile_one(src):
         obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
+        stamp, want = obj + ".sha256", _obj_digest(src)
+        if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read().strip() == want:
+            return src, obj, subprocess.CompletedProcess([], 0, "", "")   # unchanged translation unit
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode == 0:
+            with open(stamp, "w") as f:
+                f.write(want + "\n")
+        return src, obj, r
 
     objs = []
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:

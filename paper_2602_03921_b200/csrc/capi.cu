@@ -318,14 +318,17 @@ int slab_init(SweepPlan* P, Slab& S) {
     S.dtr = dtr;
     S.dro = dro;
     std::vector<int32_t> out_index(P->order.begin(), P->order.end());
-    cudaMemcpy(base + P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n, cudaMemcpyHostToDevice);
-    cudaMemcpy(base + P->td_off, dtr.data(), sizeof(EsimTraceDesc) * n_traces, cudaMemcpyHostToDevice);
-    cudaMemcpy(base + P->rd_off, dro.data(), sizeof(EsimRouterOut) * n_traces, cudaMemcpyHostToDevice);
-    cudaMemcpy(base + P->par_off, P->params.data(), sizeof(int32_t) * 4 * n_traces, cudaMemcpyHostToDevice);
-    cudaMemcpy(base + P->pre_off, P->prefix.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice);
-    if ((e = cudaMemcpy(base + P->idx_off, out_index.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice)) !=
-        cudaSuccess)
-        return cuda_fail(e, "plan upload");
+    const struct { size_t off; const void* src; size_t bytes; } up[] = {
+        {P->cfg_off, P->pcfg.data(), sizeof(EsimConfig) * n},
+        {P->td_off, dtr.data(), sizeof(EsimTraceDesc) * n_traces},
+        {P->rd_off, dro.data(), sizeof(EsimRouterOut) * n_traces},
+        {P->par_off, P->params.data(), sizeof(int32_t) * 4 * n_traces},
+        {P->pre_off, P->prefix.data(), sizeof(int64_t) * (n_traces + 1)},
+        {P->idx_off, out_index.data(), sizeof(int32_t) * n},
+    };
+    for (const auto& u : up)      // once per slab, at plan creation
+        if ((e = cudaMemcpy(base + u.off, u.src, u.bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return cuda_fail(e, "plan upload");
     return 0;
 }
 
@@ -345,24 +348,15 @@ int slab_enqueue(SweepPlan* P, Slab& S, EsimCounters* counters, int64_t* per_lay
         std::memcpy(q, h.pass_kind, h.n_passes * 4); q += al256(h.n_passes * 4);
         std::memcpy(q, h.row_offset, (h.n_events + 1) * 8);
     }
-    // one batched submission of every input copy (cudaMemcpyBatchAsync), else one call each
-    std::vector<void*> dsts{base}, srcs{S.small_img};
-    std::vector<size_t> sizes{P->small_bytes};
+    // every input copy on the slab's stream: the small image, then one logits block per trace
+    if ((e = cudaMemcpyAsync(base, S.small_img, P->small_bytes, cudaMemcpyHostToDevice, S.st)) != cudaSuccess)
+        return cuda_fail(e, "h2d small");
     for (int t = 0; t < P->n_traces; t++) {
         const EsimTraceDesc& h = P->htr[t];
         if (!h.n_rows_total) continue;
-        dsts.push_back(base + P->logit_off[t]);
-        srcs.push_back(const_cast<float*>(h.logits));
-        sizes.push_back((size_t)h.n_rows_total * h.experts * 4);
-    }
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail_idx = 0;
-    if (cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1, &fail_idx,
-                             S.st) != cudaSuccess) {
-        cudaGetLastError();
-        for (size_t i = 0; i < dsts.size(); i++)
-            cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, S.st);
+        if ((e = cudaMemcpyAsync(base + P->logit_off[t], h.logits, (size_t)h.n_rows_total * h.experts * 4,
+                                 cudaMemcpyHostToDevice, S.st)) != cudaSuccess)
+            return cuda_fail(e, "h2d logits");
     }
     if (prof) { cudaStreamSynchronize(S.st); fprintf(stderr, "[plan_run] h2d done %.2f ms\n", now_ms() - t_start); }
     int rc = esim_router_launch_batch((EsimTraceDesc*)(base + P->td_off), (EsimRouterOut*)(base + P->rd_off),

@@ -7,12 +7,18 @@
 // round-trip repr for floats, True/False for bools). The config columns are
 // fixed per point, so the host formats them once; per step only these
 // columns change. Host code (no kernel): a few hundred bytes per point,
-// ~1 us instead of ~180 us of Python report assembly.
+// ~1 us instead of ~180 us of Python report assembly; large sweeps format
+// in parallel row chunks.
 #include <charconv>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
-#include <string>
+#include <algorithm>
+#include <thread>
+#include <vector>
+
+extern const char* esim_set_error(const char* msg);
 
 #include "../../include/specmd_b200.h"
 
@@ -41,71 +47,59 @@ struct Out {
         if (std::isinf(x)) { put(x > 0 ? "inf" : "-inf"); return; }
         if (x == 0.0) { put(std::signbit(x) ? "-0.0" : "0.0"); return; }
         char b[64];
-        auto r = std::to_chars(b, b + sizeof b, x, std::chars_format::scientific);   // shortest round-trip
-        std::string sci(b, r.ptr);
-        std::string sign;
-        if (sci[0] == '-') { sign = "-"; sci.erase(0, 1); }
-        const size_t epos = sci.find('e');
-        std::string mant = sci.substr(0, epos);
-        const int exp10 = std::atoi(sci.c_str() + epos + 1);
-        std::string digits;
-        for (char c : mant) if (c != '.') digits += c;
-        const int n = (int)digits.size();
+        auto r = std::to_chars(b, b + sizeof b - 1, x, std::chars_format::scientific);   // shortest round-trip
+        *r.ptr = 0;                                  // to_chars does not terminate
+        const char* q = b;
+        char s[64];
+        int m = 0;
+        if (*q == '-') { s[m++] = '-'; q++; }
+        char digits[32];
+        int n = 0;
+        for (; q < r.ptr && *q != 'e'; q++)
+            if (*q != '.') digits[n++] = *q;
+        const int exp10 = std::atoi(q + 1);
         const int decpt = exp10 + 1;                 // value = 0.d1d2... x 10^decpt
-        std::string s = sign;
         if (decpt <= -4 || decpt > 16) {
-            s += digits[0];
-            if (n > 1) { s += '.'; s += digits.substr(1); }
-            char eb[16];
-            std::snprintf(eb, sizeof eb, "e%c%02d", exp10 < 0 ? '-' : '+', std::abs(exp10));
-            s += eb;
+            s[m++] = digits[0];
+            if (n > 1) { s[m++] = '.'; std::memcpy(s + m, digits + 1, n - 1); m += n - 1; }
+            m += std::snprintf(s + m, sizeof s - m, "e%c%02d", exp10 < 0 ? '-' : '+', std::abs(exp10));
         } else if (decpt <= 0) {
-            s += "0.";
-            s.append((size_t)(-decpt), '0');
-            s += digits;
+            s[m++] = '0'; s[m++] = '.';
+            for (int k = 0; k < -decpt; k++) s[m++] = '0';
+            std::memcpy(s + m, digits, n); m += n;
         } else if (decpt >= n) {
-            s += digits;
-            s.append((size_t)(decpt - n), '0');
-            s += ".0";
+            std::memcpy(s + m, digits, n); m += n;
+            for (int k = 0; k < decpt - n; k++) s[m++] = '0';
+            s[m++] = '.'; s[m++] = '0';
         } else {
-            s += digits.substr(0, (size_t)decpt);
-            s += '.';
-            s += digits.substr((size_t)decpt);
+            std::memcpy(s + m, digits, decpt); m += decpt;
+            s[m++] = '.';
+            std::memcpy(s + m, digits + decpt, n - decpt); m += n - decpt;
         }
-        put(s.c_str(), s.size());
+        put(s, (size_t)m);
     }
 };
 
 double ratio(double a, double b) { return b != 0.0 ? a / b : 0.0; }
 
-}  // namespace
 
-extern const char* esim_set_error(const char* msg);
-
-extern "C" int esim_report_csv(const EsimCounters* cs, const int64_t* per_layer, int32_t pl_stride,
-                               const int32_t* num_layers, const int64_t* per_layer_compute_us, int32_t n,
-                               const char* prefixes, const int64_t* prefix_offsets, char* out, int64_t cap,
-                               int64_t* offsets) {
-    Out o{out, out + cap};
-    for (int i = 0; i < n; i++) {
-        offsets[i] = o.p - out;
+// rows [lo, hi) into o; offsets relative to `base`
+int format_rows(const EsimCounters* cs, const int64_t* per_layer, int32_t pl_stride, const int32_t* num_layers,
+                const int64_t* per_layer_compute_us, int lo, int hi, const char* prefixes,
+                const int64_t* prefix_offsets, Out& o, const char* base, int64_t* offsets) {
+    for (int i = lo; i < hi; i++) {
+        offsets[i] = o.p - base;
         if (prefixes) o.put(prefixes + prefix_offsets[i], (size_t)(prefix_offsets[i + 1] - prefix_offsets[i]));
         const EsimCounters& c = cs[i];
         const int64_t* t = c.totals;            // TOTAL_FIELDS order
         const int64_t demanded = t[0], hits = t[1], misses = t[2], comp = t[3], coll = t[4], capm = t[5];
         const int64_t dropped = t[6], subst = t[7];
         // check_identities (metrics.py:319-336)
-        if (hits + misses + dropped + subst != demanded || comp + coll + capm != misses) {
-            esim_set_error("accounting identity broken in a replay's totals");
-            return -1;
-        }
+        if (hits + misses + dropped + subst != demanded || comp + coll + capm != misses) return -1;
         const int64_t* pl = per_layer + (int64_t)i * pl_stride * ESIM_PL_FIELDS;
         for (int l = 0; l < num_layers[i]; l++) {
             const int64_t* r = pl + (int64_t)l * ESIM_PL_FIELDS;
-            if (r[1] + r[2] + r[6] + r[7] != r[0]) {
-                esim_set_error("per-layer accounting identity broken in a replay");
-                return -1;
-            }
+            if (r[1] + r[2] + r[6] + r[7] != r[0]) return -2;
         }
         for (int k = 0; k < 15; k++) { o.put_int(t[k]); o.put(","); }                       // totals
         const double d = (double)demanded;
@@ -134,6 +128,53 @@ extern "C" int esim_report_csv(const EsimCounters* cs, const int64_t* per_layer,
         if (prefixes) o.put("\r\n", 2);
         if (!o.ok) return -4;
     }
-    offsets[n] = o.p - out;
     return 0;
+}
+
+}  // namespace
+
+extern "C" int esim_report_csv(const EsimCounters* cs, const int64_t* per_layer, int32_t pl_stride,
+                               const int32_t* num_layers, const int64_t* per_layer_compute_us, int32_t n,
+                               const char* prefixes, const int64_t* prefix_offsets, char* out, int64_t cap,
+                               int64_t* offsets) {
+    // rows are independent: large sweeps format in parallel chunks (each into
+    // its own buffer, bounded by its prefixes + 512 B per row), then the chunks
+    // are concatenated in row order
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int nth = n >= 512 ? std::min(hw, std::min(16, n / 256)) : 1;
+    int rc = 0;
+    if (nth <= 1) {
+        Out o{out, out + cap};
+        rc = format_rows(cs, per_layer, pl_stride, num_layers, per_layer_compute_us, 0, n, prefixes, prefix_offsets,
+                         o, out, offsets);
+        if (rc == 0) offsets[n] = o.p - out;
+    } else {
+        std::vector<std::vector<char>> bufs(nth);
+        std::vector<int> rcs(nth, 0), lo(nth + 1);
+        std::vector<int64_t> used(nth, 0);
+        for (int k = 0; k <= nth; k++) lo[k] = (int)((int64_t)n * k / nth);
+        std::vector<std::thread> th;
+        for (int k = 0; k < nth; k++)
+            th.emplace_back([&, k] {
+                const int64_t pb = prefixes ? prefix_offsets[lo[k + 1]] - prefix_offsets[lo[k]] : 0;
+                bufs[k].resize((size_t)(pb + 512 * (int64_t)(lo[k + 1] - lo[k]) + 64));
+                Out o{bufs[k].data(), bufs[k].data() + bufs[k].size()};
+                rcs[k] = format_rows(cs, per_layer, pl_stride, num_layers, per_layer_compute_us, lo[k], lo[k + 1],
+                                     prefixes, prefix_offsets, o, bufs[k].data(), offsets);
+                used[k] = o.p - bufs[k].data();
+            });
+        for (auto& t : th) t.join();
+        int64_t pos = 0;
+        for (int k = 0; k < nth && rc == 0; k++) {
+            if ((rc = rcs[k])) break;
+            if (pos + used[k] > cap) { rc = -4; break; }
+            std::memcpy(out + pos, bufs[k].data(), (size_t)used[k]);
+            for (int i = lo[k]; i < lo[k + 1]; i++) offsets[i] += pos;
+            pos += used[k];
+        }
+        if (rc == 0) offsets[n] = pos;
+    }
+    if (rc == -1) { esim_set_error("accounting identity broken in a replay's totals"); return -1; }
+    if (rc == -2) { esim_set_error("per-layer accounting identity broken in a replay"); return -1; }
+    return rc;
 }

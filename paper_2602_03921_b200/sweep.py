@@ -403,13 +403,18 @@ def gather_counter_records(local: bytes, bounds: list, group=None, device=None) 
     bounds[r][0]:bounds[r][1]) and return all records in global point order.
     One all_gather_into_tensor of equal-size (padded) buffers: NCCL on GPU
     ranks, gloo on CPU."""
+    return gather_records(local, bounds, RECORD_BYTES, group, device)
+
+
+def gather_records(local: bytes, bounds: list, rec_bytes: int, group=None, device=None) -> bytes:
+    """gather_counter_records for any fixed-size per-point record."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    lens = [(hi - lo) * RECORD_BYTES for lo, hi in bounds]
+    lens = [(hi - lo) * rec_bytes for lo, hi in bounds]
     assert len(local) == lens[rank], (len(local), lens[rank])
-    width = max(lens) if lens else 0
+    width = max(max(lens), 1)
     dev = device if device is not None else torch.device("cpu")
     buf = torch.zeros(width, dtype=torch.uint8, device=dev)
     if local:
@@ -418,3 +423,68 @@ def gather_counter_records(local: bytes, bounds: list, group=None, device=None) 
     dist.all_gather_into_tensor(out, buf, group=group)
     host = out.cpu().numpy().tobytes()
     return b"".join(host[r * width:r * width + lens[r]] for r in range(world))
+
+
+class ShardedSweep:
+    """One sweep grid split across the ranks of a process group (SURVEY.md
+    section 8(e); the replacement for the reference's process pool,
+    cli.py:462-482): every rank replays a contiguous, cost-balanced block
+    [lo:hi) of the grid (the cli.py:446 product order) on its own GPU through
+    the C-ABI plan, then the fixed-size result records (EsimCounters + the
+    per-layer rows) are all-gathered in point order -- one collective per
+    record kind, no data-path collective -- and rank 0 formats the reference
+    sweep CSV (cli.py:486-491). NCCL between GPU ranks, gloo when ranks share
+    a device or run on CPU hosts."""
+
+    def __init__(self, cfgs, traces, group=None, pl_stride: int | None = None):
+        import torch
+        import torch.distributed as dist
+        self.cfgs, self.traces, self.group = list(cfgs), list(traces), group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.L = pl_stride or max(c.model.num_layers for c in self.cfgs)
+        self.bounds = [shard_bounds(point_costs(self.cfgs, self.traces), r, self.world) for r in range(self.world)]
+        lo, hi = self.bounds[self.rank]
+        self.lo, self.hi = lo, hi
+        self.grid = HostGrid(self.cfgs[lo:hi], self.traces[lo:hi], self.L) if hi > lo else None
+        nccl = self.world > 1 and dist.get_backend(group) == "nccl"
+        self.device = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+
+    def run(self):
+        """Replay this rank's block and gather everyone's results.
+        Returns (counters [n], per_layer [n][L][ESIM_PL_FIELDS]) for the whole
+        grid, in point order, on every rank."""
+        n = len(self.cfgs)
+        pl_rec = self.L * _abi.ESIM_PL_FIELDS * 8
+        if self.grid is not None:
+            cs, pl = self.grid.run()
+            loc_c, loc_p = bytes(cs), np.ascontiguousarray(pl).tobytes()
+        else:
+            loc_c, loc_p = b"", b""
+        if self.world > 1:
+            all_c = gather_records(loc_c, self.bounds, RECORD_BYTES, self.group, self.device)
+            all_p = gather_records(loc_p, self.bounds, pl_rec, self.group, self.device)
+        else:
+            all_c, all_p = loc_c, loc_p
+        counters = (_abi.EsimCounters * n).from_buffer_copy(all_c)
+        per_layer = np.frombuffer(all_p, np.int64).reshape(n, self.L, _abi.ESIM_PL_FIELDS).copy()
+        return counters, per_layer
+
+    def csv(self, header: bool = True):
+        """The whole grid's reference-format CSV on rank 0 (None elsewhere)."""
+        cs, pl = self.run()
+        return csv_text(self.cfgs, cs, pl, header) if self.rank == 0 else None
+
+    def close(self) -> None:
+        if self.grid is not None:
+            self.grid.close()
+            self.grid = None
+
+
+def run_sharded(cfgs, traces, group=None) -> str | None:
+    """shard_bounds -> device replay of [lo:hi) -> all-gather -> rank-0 CSV."""
+    s = ShardedSweep(cfgs, traces, group)
+    try:
+        return s.csv()
+    finally:
+        s.close()
