@@ -310,6 +310,30 @@ int esim_report_csv(const EsimCounters *counters, const int64_t *per_layer, int3
                     const char *prefixes, const int64_t *prefix_offsets, char *out, int64_t cap,
                     int64_t *offsets);
 
+/* ---- trace ingestion (trace.py:219-279 read_trace) --
+ * esim_trace_jsonl_parse: the event lines of a reference JSON-lines trace
+ * (text = the whole file, line 1 = the spec record, parsed by the host),
+ * parsed natively in parallel line blocks (n_threads <= 0: all cores) into
+ * float32 rows bit-identical to json.loads + np.asarray(float32). Returns 0
+ * with *handle, *n_rows and *n_passes set; ESIM_TRACE_SLOW when the file
+ * needs the reference-exact reader (malformed line, unexpected record or
+ * key, out-of-order pass/layer, mixed kinds or row counts within a pass,
+ * NaN/Infinity, truncated last pass): *bad_line = first such line (-1: end of
+ * file), and the host re-parses to raise the reference's TraceFormatError.
+ * esim_trace_jsonl_take copies rows (row-major [n_rows][experts]) and the
+ * per-pass token counts / kinds (0 prefill, 1 decode) out and frees the
+ * handle; esim_trace_jsonl_free drops it. Host code, no GPU needed.
+ * Replaces: read_trace (trace.py:219-279) -- json.loads + np.asarray per line. */
+#define ESIM_TRACE_SLOW 1
+int esim_trace_jsonl_parse(const char *text, int64_t len, int32_t num_layers, int32_t experts, int32_t n_threads,
+                           void **handle, int64_t *n_rows, int32_t *n_passes, int64_t *bad_line);
+int esim_trace_jsonl_take(void *handle, float *logits, int32_t *pass_tokens, int32_t *pass_kind);
+int esim_trace_jsonl_free(void *handle);
+/* Device-side validation of uploaded logits (trace.py:94-95 "non-finite
+ * logit value"): *d_first_bad (device int64) = index of the first
+ * non-finite element, or -1. d_logits 16-byte aligned. Async on `stream`. */
+int esim_trace_check_finite(const float *d_logits, int64_t n, int64_t *d_first_bad, void *stream);
+
 /* ---- physical layer step (no reference equivalent; configs[1]) -------- */
 typedef struct {
     int32_t num_layers, experts, top_k;

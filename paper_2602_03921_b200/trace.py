@@ -92,6 +92,16 @@ class Trace:
     def validate(self) -> None:
         """Structural checks; messages name the pass/layer (trace.py:62-95)."""
         L, E = self.spec.num_layers, self.spec.experts_per_layer
+        if isinstance(self.passes, _LazyPasses) and self.passes._src is not None:
+            # packed layout: structure holds by construction; check the values
+            # in one vectorised pass and name the first bad event like the loop
+            pk = self._packed
+            if pk is not None and (pk.pass_tokens <= 0).any():
+                p = int(np.argmax(pk.pass_tokens <= 0))
+                raise TraceFormatError(f"pass {p} layer 0: empty logits matrix")
+            if pk is not None and pk.logits.size and not np.isfinite(pk.logits).all():
+                raise TraceFormatError(_nonfinite_where(pk, int(np.argmax((~np.isfinite(pk.logits)).any(axis=1)))))
+            return
         for want, fp in enumerate(self.passes):
             if fp.pass_id != want:
                 raise TraceFormatError(f"pass {fp.pass_id}: expected pass_id {want}")
@@ -130,23 +140,62 @@ class Trace:
         return self._packed
 
 
+class _LazyPasses(list):
+    """Trace.passes of a packed trace: the ForwardPass / LayerEvent view
+    objects are built on first use (the device path never needs them; a
+    C5 sweep trace would otherwise carry 65 x L Python objects)."""
+
+    def __init__(self, spec: ModelSpec, toks, kinds, logits: np.ndarray):
+        super().__init__()
+        self._src = (spec, list(toks), list(kinds), logits)
+
+    def _build(self):
+        if self._src is None:
+            return
+        spec, toks, kinds, logits = self._src
+        self._src = None
+        L, row = spec.num_layers, 0
+        for p, (t, k) in enumerate(zip(toks, kinds)):
+            kind = PREFILL if k == 0 else DECODE
+            events = []
+            for layer in range(L):
+                events.append(LayerEvent(p, kind, layer, logits[row:row + t]))
+                row += t
+            list.append(self, ForwardPass(p, kind, events))
+
+    def __len__(self):
+        return len(self._src[1]) if self._src is not None else list.__len__(self)
+
+
+def _lazy_method(name):
+    def m(self, *a, **k):
+        self._build()
+        return getattr(list, name)(self, *a, **k)
+    m.__name__ = name
+    return m
+
+
+for _n in ("__getitem__", "__iter__", "__reversed__", "__contains__", "__eq__", "__repr__", "index", "count",
+           "append", "extend", "insert", "pop", "remove", "__setitem__", "__delitem__", "copy", "__add__",
+           "__iadd__", "__mul__", "sort", "reverse", "clear"):
+    setattr(_LazyPasses, _n, _lazy_method(_n))
+
+
 def _from_packed(spec: ModelSpec, toks, kinds, logits: np.ndarray, meta: dict) -> Trace:
     L = spec.num_layers
-    passes, row = [], 0
-    for p, (t, k) in enumerate(zip(toks, kinds)):
-        kind = PREFILL if k == 0 else DECODE
-        events = []
-        for layer in range(L):
-            events.append(LayerEvent(p, kind, layer, logits[row:row + t]))
-            row += t
-        passes.append(ForwardPass(p, kind, events))
-    tr = Trace(spec, passes, meta)
+    tr = Trace(spec, _LazyPasses(spec, toks, kinds, logits), meta)
     per_event = np.repeat(np.asarray(toks, np.int64), L)
     off = np.zeros(per_event.shape[0] + 1, np.int64)
     np.cumsum(per_event, out=off[1:])
     tr._packed = PackedTrace(L, spec.experts_per_layer, spec.top_k, np.asarray(toks, np.int32),
                              np.asarray(kinds, np.int32), off, logits)
     return tr
+
+
+def _nonfinite_where(pk: PackedTrace, row: int) -> str:
+    """trace.py:94-95's message for the event holding packed row `row`."""
+    ev = int(np.searchsorted(pk.row_offset, row, side="right")) - 1
+    return f"pass {ev // pk.num_layers} layer {ev % pk.num_layers}: non-finite logit value"
 
 
 def generate_synthetic(spec: ModelSpec, seed: int, prefill_tokens: int, decode_tokens: int,
@@ -236,18 +285,58 @@ def _spec_from_header(path, header: dict) -> ModelSpec:
         raise TraceFormatError(f"{path}:1: bad spec record: {exc}") from None
 
 
-def read_trace(path) -> Trace:
-    """Read either format; errors name file and line / pass and layer (trace.py:219-279)."""
+def _alloc_rows(rows: int, experts: int, alloc):
+    """float32 [rows, experts] from `alloc(nbytes) -> writable uint8 buffer`
+    (e.g. page-locked memory) or plain numpy."""
+    if alloc is None:
+        return np.empty((rows, experts), np.float32)
+    buf = alloc(rows * experts * 4)
+    return np.frombuffer(buf, np.float32, count=rows * experts).reshape(rows, experts)
+
+
+def read_trace(path, alloc=None, check_values: bool = True) -> Trace:
+    """Read either format; errors name file and line / pass and layer (trace.py:219-279).
+
+    JSON lines: the spec line is parsed here, the event lines by the native
+    parallel parser (esim_trace_jsonl_parse) straight into the packed float32
+    matrix -- bit-identical to json.loads + np.asarray(float32); a file the
+    fast parser refuses is re-read by the reference-exact reader below, which
+    raises the reference's TraceFormatError. Binary: the logits are read from
+    the file straight into the packed matrix. `alloc` places that matrix
+    (e.g. pinned host memory for the H2D path, see load_trace_device);
+    check_values=False leaves the binary format's finite-value check to the
+    caller (the device path checks in HBM)."""
     path = Path(path)
-    raw = path.read_bytes()
-    if raw.startswith(_BIN_MAGIC):
-        (hl,) = struct.unpack("<Q", raw[8:16])
-        head = json.loads(raw[16:16 + hl])
-        spec = _spec_from_header(path, head)
-        logits = np.frombuffer(raw, "<f4", offset=16 + hl).reshape(-1, spec.experts_per_layer).copy()
-        tr = _from_packed(spec, head["pass_tokens"], head["pass_kind"], logits, head.get("meta", {}))
-        tr.validate()
-        return tr
+    with open(path, "rb") as fh:
+        magic = fh.read(len(_BIN_MAGIC))
+        if magic == _BIN_MAGIC:
+            (hl,) = struct.unpack("<Q", fh.read(8))
+            head = json.loads(fh.read(hl))
+            spec = _spec_from_header(path, head)
+            toks = np.asarray(head["pass_tokens"], np.int32)
+            rows = int(toks.astype(np.int64).sum()) * spec.num_layers
+            logits = _alloc_rows(rows, spec.experts_per_layer, alloc)
+            got = fh.readinto(memoryview(logits.reshape(-1).view(np.uint8)))   # file -> destination, no copy
+            if got != logits.nbytes or fh.read(1):
+                raise TraceFormatError(f"{path}: binary trace holds {got} logit bytes, header implies "
+                                       f"{logits.nbytes}")
+            tr = _from_packed(spec, toks, head["pass_kind"], logits, head.get("meta", {}))
+            if check_values:
+                tr.validate()
+            elif (toks <= 0).any():
+                tr.validate()
+            return tr
+        raw = magic + fh.read()
+    fast = _read_jsonl_native(path, raw, alloc)
+    if fast is not None:
+        return fast
+    return _read_jsonl_python(path, raw)
+
+
+def _read_jsonl_python(path, raw: bytes) -> Trace:
+    """The reference-exact JSON-lines reader (trace.py:219-279): every error
+    message, and the files the native parser hands back."""
+    path = Path(path)
     lines = raw.decode().splitlines()
     if not lines:
         raise TraceFormatError(f"{path}: empty trace file")
@@ -285,3 +374,39 @@ def read_trace(path) -> Trace:
     tr = Trace(spec, passes, head.get("meta", {}))
     tr.validate()
     return tr
+
+
+def _read_jsonl_native(path, raw: bytes, alloc):
+    """The native fast path of read_trace for JSON lines (None: use the
+    reference-exact reader, which also produces every error message)."""
+    import ctypes as C
+    # the native parser splits lines on \n only; str.splitlines() also splits
+    # on these, so such files take the reference-exact reader
+    if any(raw.find(b) >= 0 for b in (b"\x0b", b"\x0c", b"\x1c", b"\x1d", b"\x1e", b"\xc2\x85",
+                                      b"\xe2\x80\xa8", b"\xe2\x80\xa9")) or \
+            raw.count(b"\r") != raw.count(b"\r\n"):
+        return None
+    nl = raw.find(b"\n")
+    first = raw[:nl if nl >= 0 else len(raw)]
+    try:
+        head = json.loads(first)
+    except (json.JSONDecodeError, UnicodeDecodeError):
+        return None
+    if not isinstance(head, dict) or head.get("record") != "spec":
+        return None
+    try:
+        spec = _spec_from_header(path, head)
+    except TraceFormatError:
+        return None
+    from ._device import lib
+    L = lib()
+    h, rows, npass, bad = C.c_void_p(), C.c_int64(), C.c_int32(), C.c_int64()
+    rc = L.esim_trace_jsonl_parse(raw, len(raw), spec.num_layers, spec.experts_per_layer, 0, C.byref(h),
+                                  C.byref(rows), C.byref(npass), C.byref(bad))
+    if rc != 0:
+        return None
+    logits = _alloc_rows(rows.value, spec.experts_per_layer, alloc)
+    toks = np.zeros(npass.value, np.int32)
+    kinds = np.zeros(npass.value, np.int32)
+    L.esim_trace_jsonl_take(h, logits.ctypes.data, toks.ctypes.data, kinds.ctypes.data)
+    return _from_packed(spec, toks, kinds, logits, head.get("meta", {}))
