@@ -399,16 +399,29 @@ class ReplayBatch:
         for pos, i in enumerate(self.order):
             c = cs[pos]
             if c.status != 0:
-                code = int(c.status)
-                if code == -1:
-                    raise ConfigError("replay: an expert exceeds the cache capacity")
-                raise RuntimeError(f"replay failed on point {i} (status {code})")
+                raise point_error(self.cfgs[i], int(c.status))
             cfg = self.cfgs[i]
             L = cfg.model.num_layers
             log = decode_records(recs[pos][:c.n_recs], pexp[pos]) if self.full_log else None
             rep = report_from_counters(cfg.echo(), L, cfg.hardware.per_layer_compute_us, c, pl[pos][:L])
             out[i] = SimResult(rep, log, c, pl[pos][:L].copy())
         return out
+
+
+def point_error(cfg, status: int) -> Exception:
+    """The exception the reference raises for a replay that ended with
+    `status` (EsimCounters.status)."""
+    if status == -1:
+        # _fetch's final call (engine.py:470-477): the miss policy's last
+        # rung -- the lowest precision for fetch_low / fetch_priority
+        # (miss.py:120-136), else the working precision
+        spec = cfg.model
+        prec = spec.lowest_precision if cfg.miss in ("fetch_low", "fetch_priority") else cfg.working_precision
+        return ConfigError(f"{prec} expert ({spec.expert_bytes(prec)} B) exceeds capacity {cfg.capacity_bytes()} B")
+    what = {-7: "an LFU/LHU access count exceeded the device's 16-bit counters",
+            -8: "more than 2^31 policy stamps in one replay (trace too long)",
+            -4: "record buffer too small"}.get(status, "runtime invariant broken during replay")
+    return RuntimeError(f"replay failed (status {status}): {what}")
 
 
 def run_simulations(cfgs, traces, full_log: bool = False) -> list:

@@ -170,12 +170,15 @@ class HostGrid:
             raise ConfigError(msg)
         raise RuntimeError(f"esim_run_host failed ({rc}): {msg}")
 
-    def run(self):
+    def run(self, check: bool = True):
         """Returns (counters, per_layer [n][pl_stride][ESIM_PL_FIELDS]): this grid's
-        own output buffers (no copy), overwritten by the next run()."""
+        own output buffers (no copy), overwritten by the next run().
+        check=False: a point that failed (EsimCounters.status != 0, e.g. an
+        expert larger than the cache) does not raise; the other points'
+        results are valid and the caller inspects each status."""
         rc = _lib().esim_sweep_plan_run(self._plan, C.addressof(self.counters), self.per_layer.ctypes.data,
                                         None, None)
-        if rc != 0:
+        if rc != 0 and (check or not any(c.status for c in self.counters)):
             self._raise(rc)
         return self.counters, self.per_layer
 
@@ -436,10 +439,10 @@ class ShardedSweep:
     sweep CSV (cli.py:486-491). NCCL between GPU ranks, gloo when ranks share
     a device or run on CPU hosts."""
 
-    def __init__(self, cfgs, traces, group=None, pl_stride: int | None = None):
+    def __init__(self, cfgs, traces, group=None, pl_stride: int | None = None, check: bool = True):
         import torch
         import torch.distributed as dist
-        self.cfgs, self.traces, self.group = list(cfgs), list(traces), group
+        self.cfgs, self.traces, self.group, self.check = list(cfgs), list(traces), group, check
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.L = pl_stride or max(c.model.num_layers for c in self.cfgs)
@@ -457,7 +460,7 @@ class ShardedSweep:
         n = len(self.cfgs)
         pl_rec = self.L * _abi.ESIM_PL_FIELDS * 8
         if self.grid is not None:
-            cs, pl = self.grid.run()
+            cs, pl = self.grid.run(check=self.check)       # check=False: failed points carry their status
             loc_c, loc_p = bytes(cs), np.ascontiguousarray(pl).tobytes()
         else:
             loc_c, loc_p = b"", b""
