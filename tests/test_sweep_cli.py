@@ -69,5 +69,5 @@ def test_sweep_cli_matches_reference_byte_for_byte(tmp_path, case):
     assert out.replace(d, "<DIR>") == case["stdout"]
     fails = [ln for ln in err.replace(d, "<DIR>").splitlines() if ": FAILED: " in ln]
     assert fails == [ln for ln in case["stderr"].splitlines() if ": FAILED: " in ln]
-    got_csv = out_csv.read_text(newline="") if out_csv.exists() else None
+    got_csv = open(out_csv, newline="").read() if out_csv.exists() else None
     assert got_csv == case["csv"]
