@@ -156,6 +156,13 @@ const char *esim_last_error(void);
 int esim_host_register(void *ptr, size_t bytes);
 int esim_host_unregister(void *ptr);
 int esim_version(void);
+/* Host-semantics switch: the builtin sum() of the interpreter the device
+ * must match (RouteRec masses engine.py:630-631, report sums
+ * metrics.py:168-180, 267-270): neumaier = 1 for CPython >= 3.12 (the
+ * compensated float path; the default), 0 for CPython <= 3.11 (plain left
+ * fold). Process-wide; needs a device context. esim_get_host_sum reads it. */
+int esim_set_host_sum(int neumaier);
+int esim_get_host_sum(void);
 
 /* Fused router over a whole trace: one CTA per event. `trace` and `out`
  * are host structs holding DEVICE pointers. pred_mode/overfetch/percentile
@@ -224,6 +231,26 @@ typedef struct {
     double *signal;                /* SB */
     int32_t *layer, *expert;
 } EsimPolicyState;
+
+/* Miss-handler plug-in decision (miss.py:66-140 resolve_miss/find_substitute):
+ * policy = ESIM_MISS_* (models MISS_CODE order), rank = the missing expert's
+ * 1-based rank by routing weight, scores = the gate scores demanded at this
+ * layer event (degrade percentile, fetch_priority), residents = (expert,
+ * recorded score) of the layer, pct_rank = max(1, ceil(p/100 * n_scores)).
+ * Decision: kind DROP / SUBST (substitute = expert: min (|rec - gate|,
+ * expert) within tolerance) / FETCH with fetch = WORKING, LOWEST, or CASCADE
+ * down the ladder from `start` (1 when gate < the percentile). The caller
+ * runs the fetch. Synchronous; host buffers in and out. */
+enum { ESIM_MISS_OUT_FETCH = 0, ESIM_MISS_OUT_DROP = 1, ESIM_MISS_OUT_SUBST = 2 };
+enum { ESIM_MISS_FETCH_WORKING = 0, ESIM_MISS_FETCH_LOWEST = 1, ESIM_MISS_FETCH_CASCADE = 2 };
+typedef struct {
+    int32_t policy, rank, drop_rank_threshold, n_scores;
+    int32_t n_residents, ladder_len, pct_rank, pad;
+    double gate_score, subst_tolerance;
+} EsimMissQuery;
+typedef struct { int32_t kind, substitute, fetch, start; } EsimMissDecision;
+int esim_miss_decide(const EsimMissQuery *q, const double *scores, const int32_t *res_expert, const double *res_rec,
+                     EsimMissDecision *decision);
 
 int esim_policy_apply(const EsimPolicyState *state, const EsimPolicyOp *d_ops, int32_t n_ops, int32_t *d_results,
                       void *stream);

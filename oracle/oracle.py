@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import subprocess
 from dataclasses import dataclass
 
@@ -35,6 +36,7 @@ def lib():
         if not os.path.exists(LIB_PATH):
             build()
         L = C.CDLL(LIB_PATH)
+        L.esim_oracle_set_host_sum(1 if sys.version_info >= (3, 12) else 0)   # this interpreter's sum()
         vp = C.c_void_p
         L.esim_oracle_run.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64, vp, C.c_int64]
         L.esim_oracle_run_batch.argtypes = [vp, C.c_int, vp, C.c_int, vp, vp, C.c_int]
@@ -165,3 +167,8 @@ def run_batch(cfgs, traces_by_id, nthreads: int):
     if rc != 0:
         raise RuntimeError(f"oracle batch failed ({rc}): {lib().esim_oracle_last_error().decode()}")
     return list(counters), per_layer
+
+
+def set_host_sum(neumaier: bool) -> None:
+    """Reproduce CPython >= 3.12 (True) or <= 3.11 (False) builtin sum()."""
+    lib().esim_oracle_set_host_sum(1 if neumaier else 0)

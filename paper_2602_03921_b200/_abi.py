@@ -93,3 +93,14 @@ class EsimPolicyState(C.Structure):
 
 
 assert C.sizeof(EsimPolicyOp) == 32
+
+
+class EsimMissQuery(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("rank", C.c_int32), ("drop_rank_threshold", C.c_int32),
+                ("n_scores", C.c_int32), ("n_residents", C.c_int32), ("ladder_len", C.c_int32),
+                ("pct_rank", C.c_int32), ("pad", C.c_int32), ("gate_score", C.c_double),
+                ("subst_tolerance", C.c_double)]
+
+
+class EsimMissDecision(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("substitute", C.c_int32), ("fetch", C.c_int32), ("start", C.c_int32)]

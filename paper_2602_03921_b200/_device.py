@@ -69,10 +69,53 @@ def lib():
         L.esim_route_summary_launch.argtypes = [vp, vp, i32, vp]
         L.esim_noise_launch.argtypes = [vp, vp, i32, f64, C.c_uint64, vp]
         L.esim_version.restype = C.c_int
+        L.esim_set_host_sum.argtypes = [i32]
+        L.esim_miss_decide.argtypes = [vp, vp, vp, vp, vp]
         if L.esim_version() != 2:
             raise RuntimeError(f"{LIB_PATH}: C ABI version {L.esim_version()} != 2 (stale build)")
         _lib = L
     return _lib
+
+
+_host_checked = False
+
+
+def ensure_host_semantics() -> None:
+    """Once per process, before the first device computation: (1) tell the
+    device which builtin sum() the host interpreter has (CPython >= 3.12
+    Neumaier vs a plain fold; RouteRec masses engine.py:630-631, report sums
+    metrics.py:168-180); (2) check the device's float32 exp / pairwise-sum
+    restatement against THIS host's numpy softmax (routing.py:22-29) on a
+    fixed grid -- a host whose np.exp differs (another SIMD path, an ARM
+    build) would make every routing decision differ silently, so raise."""
+    global _host_checked
+    if _host_checked:
+        return
+    import sys
+    L = lib()
+    _check(L.esim_set_host_sum(1 if sys.version_info >= (3, 12) else 0), "esim_set_host_sum")
+    torch = _torch()
+    rng = np.random.default_rng(20260)
+    rows = []
+    grid = np.linspace(-103.9, 0.0, 4096, dtype=np.float32)          # the exp domain after x - max
+    for E in (8, 60, 64, 128, 200, 249, 255, 256):
+        g = np.resize(grid, ((len(grid) + E - 1) // E) * E).reshape(-1, E)
+        r = (rng.standard_normal((64, E)) * rng.choice([0.5, 1.0, 4.0, 30.0], (64, 1))).astype(np.float32)
+        rows.append((E, np.concatenate([g, r])))
+    for E, x in rows:
+        want = np.exp(x - x.max(axis=1, keepdims=True), dtype=np.float32)
+        want = want / want.sum(axis=1, keepdims=True, dtype=np.float32)
+        dx = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        out = torch.empty_like(dx)
+        _check(L.esim_softmax_launch(dx.data_ptr(), x.shape[0], E, out.data_ptr(), _stream()), "softmax selfcheck")
+        got = out.cpu().numpy()
+        if not np.array_equal(got.view(np.uint32), want.view(np.uint32)):
+            bad = int(np.argmax((got.view(np.uint32) != want.view(np.uint32)).any(axis=1)))
+            raise RuntimeError(
+                f"host numpy float32 softmax differs from the device restatement (E={E}, row {bad}): this "
+                f"host's np.exp / pairwise sum is not the AVX2/AVX-512 numpy path the device reproduces "
+                f"(SURVEY.md Appendix A), so routing would not be bit-exact here")
+    _host_checked = True
 
 
 def _torch():
@@ -102,6 +145,7 @@ class DeviceTrace:
     """A PackedTrace uploaded to HBM, plus its EsimTraceDesc."""
 
     def __init__(self, pk, non_blocking: bool = False):
+        ensure_host_semantics()
         torch = _torch()
         dev = torch.device("cuda")
         self.pk = pk

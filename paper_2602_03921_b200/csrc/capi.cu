@@ -55,6 +55,23 @@ extern "C" int esim_host_unregister(void* p) {
     if (e == cudaErrorHostMemoryNotRegistered) { cudaGetLastError(); return 0; }
     return e == cudaSuccess ? 0 : cuda_fail(e, "cudaHostUnregister");
 }
+int esim_router_set_sum_plain(int plain);
+int esim_replay_set_sum_plain(int plain);
+
+// builtin sum() semantics of the host interpreter whose results the device
+// must reproduce (RouteRec masses engine.py:630-631, report sums
+// metrics.py:168-180, 267-270): 1 = CPython >= 3.12 (Neumaier-compensated
+// float path, the default), 0 = CPython <= 3.11 (plain left fold)
+static int g_host_sum_neumaier = 1;
+extern "C" int esim_set_host_sum(int neumaier) {
+    const int plain = neumaier ? 0 : 1;
+    if (esim_router_set_sum_plain(plain) || esim_replay_set_sum_plain(plain))
+        return cuda_fail(cudaGetLastError(), "esim_set_host_sum");
+    g_host_sum_neumaier = neumaier ? 1 : 0;
+    return 0;
+}
+extern "C" int esim_get_host_sum(void) { return g_host_sum_neumaier; }
+
 extern "C" int esim_version(void) { return 2; }   // 2: EsimConfig gained prefetch_noise + seed (184 B)
 
 // predictor constants resolved on the host exactly as the reference does in

@@ -90,11 +90,18 @@ __device__ __forceinline__ float warp_pw_sum(const float* a, int n, int lane) {
     return __fadd_rn(warp_pw_block(a, n2, lane), warp_pw_mid(a + n2, n - n2, lane));
 }
 
-// CPython >= 3.12 builtin sum() over floats (Neumaier compensation).
+// The host interpreter's builtin sum() over floats (bltinmodule.c
+// builtin_sum_impl float path): CPython >= 3.12 adds Neumaier compensation,
+// earlier versions a plain left fold. Which one is a per-translation-unit
+// device global set by esim_set_host_sum() (the Python wrapper passes
+// sys.version_info at load), default 3.12+.
+static __device__ int g_pysum_plain = 0;
+
 struct PySum {
     double f, c;
     __device__ __forceinline__ void init() { f = 0.0; c = 0.0; }
     __device__ __forceinline__ void add(double x) {
+        if (g_pysum_plain) { f = __dadd_rn(f, x); return; }
         double t = __dadd_rn(f, x);
         if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
         else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));

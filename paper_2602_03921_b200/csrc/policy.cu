@@ -175,3 +175,93 @@ extern "C" int esim_policy_apply(const EsimPolicyState* state, const EsimPolicyO
     esim::pol::policy_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*state, d_ops, n_ops, d_results);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
+
+// ---------------------------------------------------------------------------
+// miss-handler plug-in decision (miss.py:66-140): one warp over the layer's
+// demanded gate scores and the layer's residents. The fetch itself (making
+// space, the transfer, blocking) belongs to the caller's fetch_fn.
+// ---------------------------------------------------------------------------
+namespace esim {
+namespace pol {
+
+__global__ void miss_decide_kernel(EsimMissQuery q, const double* __restrict__ scores,
+                                   const int32_t* __restrict__ res_expert, const double* __restrict__ res_rec,
+                                   EsimMissDecision* out) {
+    const int lane = threadIdx.x;
+    EsimMissDecision d{ESIM_MISS_OUT_FETCH, -1, ESIM_MISS_FETCH_WORKING, 0};
+    if (q.policy == ESIM_MISS_DROP && q.rank > q.drop_rank_threshold) {
+        d.kind = ESIM_MISS_OUT_DROP;                                   // miss.py:109-110
+    } else {
+        bool decided = false;
+        if (q.policy == ESIM_MISS_SUBST) {
+            // find_substitute (miss.py:66-79): min (|rec - gate|, expert) within tolerance
+            // two passes: min diff, then min expert among equal diffs
+            double bd = INFINITY;
+            for (int i = lane; i < q.n_residents; i += 32) {
+                const double diff = fabs(__dsub_rn(res_rec[i], q.gate_score));
+                if (diff <= q.subst_tolerance && diff < bd) bd = diff;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) bd = fmin(bd, __shfl_xor_sync(FULL, bd, o));
+            int be = INT32_MAX;
+            if (bd != INFINITY)
+                for (int i = lane; i < q.n_residents; i += 32)
+                    if (fabs(__dsub_rn(res_rec[i], q.gate_score)) == bd && res_expert[i] < be) be = res_expert[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) be = min(be, __shfl_xor_sync(FULL, be, o));
+            if (bd != INFINITY) { d.kind = ESIM_MISS_OUT_SUBST; d.substitute = be; decided = true; }
+        }
+        if (!decided) {
+            if (q.policy == ESIM_MISS_FETCH_LOW) {
+                d.fetch = ESIM_MISS_FETCH_LOWEST;                       // miss.py:116-118
+            } else if (q.policy == ESIM_MISS_FETCH_PRIORITY) {
+                d.fetch = ESIM_MISS_FETCH_CASCADE;                      // miss.py:120-136
+                if (q.ladder_len > 1 && q.n_scores > 0) {
+                    // nearest-rank percentile (prefetch.py:30-36): the value whose
+                    // ascending position holds rank - 1
+                    double thr = 0.0;
+                    bool found = false;
+                    for (int i = lane; i < q.n_scores; i += 32) {
+                        int lt = 0, le = 0;
+                        for (int j = 0; j < q.n_scores; j++) {
+                            lt += scores[j] < scores[i];
+                            le += scores[j] <= scores[i];
+                        }
+                        if (lt <= q.pct_rank - 1 && q.pct_rank - 1 < le) { thr = scores[i]; found = true; }
+                    }
+                    const unsigned m = __ballot_sync(FULL, found);
+                    thr = __shfl_sync(FULL, thr, __ffs(m) - 1);
+                    if (q.gate_score < thr) d.start = 1;                // low-importance: one level lower
+                }
+            }
+        }
+    }
+    if (lane == 0) *out = d;
+}
+
+}  // namespace pol
+}  // namespace esim
+
+extern "C" int esim_miss_decide(const EsimMissQuery* q, const double* h_scores, const int32_t* h_res_expert,
+                                const double* h_res_rec, EsimMissDecision* decision) {
+    if (!q || !decision || q->n_scores < 0 || q->n_residents < 0) return -1;
+    const size_t ns = (size_t)q->n_scores, nr = (size_t)q->n_residents;
+    char* d = nullptr;
+    const size_t bytes = 8 * ns + 4 * nr + 8 * nr + sizeof(EsimMissDecision) + 64;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return -2;
+    double* ds = (double*)d;
+    double* dr = ds + ns;
+    int32_t* de = (int32_t*)(dr + nr);
+    EsimMissDecision* dd = (EsimMissDecision*)(((uintptr_t)(de + nr) + 15) & ~(uintptr_t)15);
+    cudaError_t e = cudaSuccess;
+    if (ns) e = cudaMemcpy(ds, h_scores, 8 * ns, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && nr) e = cudaMemcpy(dr, h_res_rec, 8 * nr, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && nr) e = cudaMemcpy(de, h_res_expert, 4 * nr, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        esim::pol::miss_decide_kernel<<<1, 32>>>(*q, ds, de, dr, dd);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(decision, dd, sizeof(EsimMissDecision), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? 0 : -2;
+}

@@ -230,7 +230,8 @@ DFI void ps_add(Pt& p, int which, double x) {
     if (p.lane == 0) {
         double f = p.ctr->ps[2 * which], c = p.ctr->ps[2 * which + 1];
         double t = __dadd_rn(f, x);
-        if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+        if (g_pysum_plain) {}                                    // CPython < 3.12: no compensation
+        else if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
         else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
         p.ctr->ps[2 * which] = t;
         p.ctr->ps[2 * which + 1] = c;
@@ -1697,4 +1698,8 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
     }
     k<<<blocks, 32 * warps_per_cta, (size_t)a.point_bytes * warps_per_cta, st>>>(a);
     return cudaGetLastError();
+}
+
+int esim_replay_set_sum_plain(int plain) {          // see esim_set_host_sum
+    return cudaMemcpyToSymbol(esim::g_pysum_plain, &plain, sizeof(int)) == cudaSuccess ? 0 : -2;
 }

@@ -641,7 +641,8 @@ __global__ void __launch_bounds__(256) route_events_kernel(SumArgs a, int64_t to
 
 __device__ __forceinline__ void nsum_add(double& f, double& c, double x) {   // PySum step (ps_add)
     const double t = __dadd_rn(f, x);
-    if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+    if (g_pysum_plain) {}                                        // CPython < 3.12: no compensation
+    else if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
     else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
     f = t;
 }
@@ -711,7 +712,8 @@ __global__ void __launch_bounds__(256) route_totals_kernel(SumArgs a) {
             for (int k = 0; k < cnt; k++) {
                 const double x = (need == 0 || (s_flags[k] & need)) ? src[k] : 0.0;
                 const double t = __dadd_rn(f, x);
-                const double e = fabs(f) >= fabs(x) ? __dadd_rn(__dsub_rn(f, t), x) : __dadd_rn(__dsub_rn(x, t), f);
+                const double e = g_pysum_plain ? 0.0
+                                 : fabs(f) >= fabs(x) ? __dadd_rn(__dsub_rn(f, t), x) : __dadd_rn(__dsub_rn(x, t), f);
                 c = __dadd_rn(c, e);
                 f = t;
             }
@@ -1003,4 +1005,10 @@ extern "C" int esim_route_cache_aware_launch(const float* d_x, int32_t rows, int
     esim::route_cache_aware_kernel<<<1, 32, 2 * experts * 4, (cudaStream_t)stream>>>(
         d_x, rows, experts, top_k, d_cached_mask, lam, d_delta, d_sel, d_w, d_orig, d_ow, d_modified);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// the host interpreter's sum() semantics for this translation unit's PySum
+// chains (numpy_f32.cuh g_pysum_plain); called by esim_set_host_sum
+int esim_router_set_sum_plain(int plain) {
+    return cudaMemcpyToSymbol(esim::g_pysum_plain, &plain, sizeof(int)) == cudaSuccess ? 0 : -2;
 }

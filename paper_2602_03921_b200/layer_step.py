@@ -123,6 +123,8 @@ class LayerStepEngine:
     the decision stream fetched into it and the FFN dequantises per slot."""
 
     def __init__(self, cfg, hidden: int = 2048, inter: int = 1024, max_tokens: int = 64):
+        from ._device import ensure_host_semantics
+        ensure_host_semantics()
         torch = _torch()
         m = cfg.model
         self.cfg, self.H, self.I = cfg, hidden, inter

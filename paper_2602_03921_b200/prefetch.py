@@ -88,3 +88,44 @@ class PrefetchQueue:
 
     def pop(self) -> PrefetchRequest:
         return self._q.popleft()
+
+
+def watchdog_step(queue: PrefetchQueue, cache, policy, channel, now_us: int, ctx, nbytes: int, precision: str,
+                  evict_fn, on_start, on_skip, on_drop) -> int:
+    """Drain the prefetch queue (prefetch.py:163-221), the plug-in form for
+    callers with their own engine objects; inside a run the replay kernel
+    executes the same two sweeps on its device directory. Sweep 1 settles
+    what needs no transfer -- residents are marked prefetch-selected via
+    policy.note_prefetch_hit (so a peer request of the same prediction can
+    never evict them), in-flight experts are skipped; sweep 2 admits the
+    rest, evicting unforced (policy.select_victim: a device-backed policy
+    object, eviction.make_eviction_policy) until `nbytes` fit or dropping the
+    request ("no_space"), then reserves and appends the transfer. This
+    function only sequences decisions; cache, channel and the callbacks are
+    the caller's. Returns the number of transfers started."""
+    pending = []
+    while len(queue):
+        req = queue.pop()
+        ident = (req.target_layer, req.expert)
+        if cache.is_resident(ident):
+            policy.note_prefetch_hit(ident, ctx)
+            on_skip(req, "resident")
+        elif channel.in_flight(ident) is not None:
+            on_skip(req, "in_flight")
+        else:
+            pending.append(req)
+    started = 0
+    for req in pending:
+        ident = (req.target_layer, req.expert)
+        while cache.free_bytes < nbytes:
+            victim = policy.select_victim(ctx, forced=False)
+            if victim is None:
+                on_drop(req, "no_space")
+                break
+            evict_fn(victim, "prefetch", False)
+        else:
+            cache.reserve(nbytes)
+            channel.append(ident, nbytes, "prefetch", now_us, req.score, precision)
+            on_start(req)
+            started += 1
+    return started

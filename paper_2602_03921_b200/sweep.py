@@ -130,6 +130,8 @@ class HostGrid:
     (esim_noise_launch)."""
 
     def __init__(self, cfgs, traces, pl_stride: int | None = None):
+        from ._device import ensure_host_semantics
+        ensure_host_semantics()
         ids, descs, self._keep = {}, [], []
         ccfg = []
         for cfg, tr in zip(cfgs, traces):

@@ -16,7 +16,8 @@ def declared_functions():
 def test_header_declares_the_boundary():
     names = declared_functions()
     for must in ("esim_router_launch", "esim_replay_launch", "esim_run_host", "esim_softmax_launch",
-                 "esim_topk_launch", "esim_ls_create", "esim_ls_run", "esim_ffn_experts", "esim_last_error"):
+                 "esim_topk_launch", "esim_ls_create", "esim_ls_run", "esim_ffn_experts", "esim_last_error",
+                 "esim_trace_jsonl_parse", "esim_trace_check_finite", "esim_set_host_sum", "esim_miss_decide"):
         assert must in names
 
 
@@ -34,6 +35,7 @@ def test_struct_sizes_match_the_header():
     assert ctypes.sizeof(_abi.EsimCounters) == 360
     assert ctypes.sizeof(_abi.EsimTraceDesc) == 64
     assert ctypes.sizeof(_abi.EsimRouterOut) == 17 * 8
+    assert ctypes.sizeof(_abi.EsimMissQuery) == 48 and ctypes.sizeof(_abi.EsimMissDecision) == 16
     assert REC_DTYPE.itemsize == 64
     from paper_2602_03921_b200.layer_step import EsimLSParams, EsimLSResult
     assert ctypes.sizeof(EsimLSParams) == 9 * 4           # incl. weight_format, prec_mask
