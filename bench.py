@@ -112,25 +112,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def host_link_peak_gbs(nbytes=1 << 30, reps=5):
-    """Pinned host->device copy bandwidth measured in this run (the layer step's link roofline)."""
-    import torch
-    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
-    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-    s = torch.cuda.Stream()
-    with torch.cuda.stream(s):
-        d.copy_(h, non_blocking=True)
-    s.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(s):
-        e0.record()
-        for _ in range(reps):
-            d.copy_(h, non_blocking=True)
-        e1.record()
-    s.synchronize()
-    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
-
-
 def layer_step_section(runs=2):
     """configs[1]: OLMoE-1B-7B bf16 prefill 64 + decode 64 with a 0.6 GB HBM expert cache,
     score:80 prefetch + Least-Stale (and LRU for contrast), experts in pinned host memory."""
@@ -142,7 +123,8 @@ def layer_step_section(runs=2):
     g = torch.Generator().manual_seed(0)
     x0 = torch.randn(64, 2048, generator=g).to(torch.bfloat16).pin_memory()
     xd = torch.randn(64, 2048, generator=g).to(torch.bfloat16).pin_memory()
-    peak = host_link_peak_gbs()
+    from paper_2602_03921_b200.calibrate import measure_link_gbs
+    peak = measure_link_gbs()
     out = {"config": "olmoe 16x64 top-8, SwiGLU H=2048 I=1024 bf16 (12,582,912 B/expert, 12.9 GB pinned store, "
                      "N(0,0.02) seed 0), cache 614,400,000 B -> 51 HBM slots, score:80 + fetch, "
                      "logical clock 5 GB/s / 2000 us (reference defaults), 64 prefill + 64 decode tokens",
@@ -203,6 +185,46 @@ def layer_step_section(runs=2):
                            "logical_hit_rate": best.report["rates"]["hit_rate"],
                            "logical_ttft_us": best.report["timing"]["ttft_us"]}
     eng.close()
+    out["calibrated"] = calibrated_section(spec, tr, x0, xd, peak, runs)
+    return out
+
+
+def calibrated_section(spec, tr, x0, xd, link_gbs, runs=2):
+    """The same request with the logical clock calibrated to this box
+    (calibrate.py: measured host-link bytes/s and per-layer FFN us), so the
+    policies decide at the B200's own fetch/compute ratio; LS vs LRU at fp16
+    and int4, logical (decision-stream) and physical numbers side by side."""
+    from paper_2602_03921_b200 import SimConfig
+    from paper_2602_03921_b200.calibrate import calibrated_hardware
+    from paper_2602_03921_b200.layer_step import LayerStepEngine
+    out = {}
+    for prec in ("fp16", "int4"):
+        hw, meas = calibrated_hardware(spec, tr, 2048, 1024, prec, 614_400_000, link_gbs)
+        sec = {"hardware": meas}
+        eng = None
+        for ev in ("ls", "lru"):
+            cfg = SimConfig(model=spec, hardware=hw, working_precision=prec, eviction=ev, prefetch="score",
+                            percentile=80.0, miss="fetch")
+            if eng is None:
+                eng = LayerStepEngine(cfg, 2048, 1024, max_tokens=64)
+                eng.init_weights(seed=0)
+            eng.cfg = cfg
+            best = None
+            for _ in range(runs):
+                r = eng.run(tr, x0, xd)
+                best = r if best is None or r.total_ms < best.total_ms else best
+            rep = best.report
+            sec[ev] = {"ttft_ms": best.ttft_ms, "decode_tok_s": best.decode_tokens_per_sec,
+                       "total_ms": best.total_ms, "host_link_gbs": best.h2d_gbs,
+                       "host_link_frac": best.h2d_gbs / link_gbs, "h2d_bytes": best.h2d_bytes,
+                       "copies": best.n_copies, "demand_copies": best.n_demand_copies,
+                       "prefetch_copies": best.n_prefetch_copies,
+                       "logical_hit_rate": rep["rates"]["hit_rate"],
+                       "logical_collision_rate": rep["rates"]["collision_rate_demanded"],
+                       "logical_ttft_us": rep["timing"]["ttft_us"],
+                       "logical_decode_tok_s": rep["timing"]["decode_tokens_per_sec"]}
+        eng.close()
+        out[prec] = sec
     return out
 
 

@@ -266,3 +266,33 @@ def test_layer_step_rejects_configs_its_store_cannot_serve():
     eng.cfg = cfg
     assert eng.run(tr, x0, xd).n_copies > 0                               # still usable afterwards
     eng.close()
+
+
+def test_calibrated_hardware_decisions_match_oracle(oracle_lib):
+    """A HardwareSpec calibrated on this box (measured host-link bytes/s and
+    per-layer FFN us, calibrate.py) changes only the config's integers: the
+    physical OLMoE layer step's decisions under it equal the oracle's, for
+    Least-Stale and LRU at fp16 and int4."""
+    import torch
+    from paper_2602_03921_b200 import SimConfig, builtin_spec, generate_synthetic
+    from paper_2602_03921_b200.calibrate import calibrated_hardware
+    from paper_2602_03921_b200.layer_step import LayerStepEngine
+    spec = builtin_spec("olmoe")
+    tr = generate_synthetic(spec, seed=1, prefill_tokens=64, decode_tokens=8)
+    g = torch.Generator().manual_seed(0)
+    x0 = torch.randn(64, H, generator=g).to(torch.bfloat16).pin_memory()
+    xd = torch.randn(8, H, generator=g).to(torch.bfloat16).pin_memory()
+    for prec in ("fp16", "int4"):
+        hw, meas = calibrated_hardware(spec, tr, H, 1024, prec, 614_400_000)
+        assert 10 < meas["link_gbs"] < 2000 and 1 <= meas["per_layer_compute_us"] < 2000
+        eng = None
+        for ev in ("ls", "lru"):
+            cfg = SimConfig(model=spec, hardware=hw, working_precision=prec, eviction=ev, prefetch="score",
+                            percentile=80.0, miss="fetch")
+            if eng is None:
+                eng = LayerStepEngine(cfg, H, 1024, max_tokens=64)
+                eng.init_weights(seed=0)
+            eng.cfg = cfg
+            res = eng.run(tr, x0, xd)
+            assert json.dumps(res.report) == json.dumps(oracle_lib.run(cfg, tr, full_log=False).report), (prec, ev)
+        eng.close()
