@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <cstdint>
 #include <mutex>
 #include <unordered_map>
@@ -51,7 +52,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef MBAR_SPIN
+#define MBAR_SPIN 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#if MBAR_SPIN
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+#else
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
@@ -61,6 +76,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -503,7 +519,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_decode_kernel(const __grid
     const int m1 = g.I / 64, n_units = g.n_exec * m1, n_ht = g.H / BM;
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; i++) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
-        mbar_init(&s.t1full, 1); mbar_init(&s.t1empty, 4); mbar_init(&s.actrdy, 64);
+        mbar_init(&s.t1full, 1); mbar_init(&s.t1empty, 4); mbar_init(&s.actrdy, 2);   // one per act-writing warp
         mbar_init(&s.t2full, 1); mbar_init(&s.t2empty, 4);
         fence_barrier_init();
         prefetch_tmap(g.x_map);
@@ -620,7 +636,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_decode_kernel(const __grid
                         __float2bfloat16(a);
                 }
                 fence_proxy_async_smem();                 // generic smem writes -> the tensor core's view
-                mbar_arrive(&s.actrdy);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.actrdy);
             }
             // gemm2 epilogue: partial sums of the H rows, scaled, into y
             mbar_wait(&s.t2full, j & 1);
@@ -673,19 +690,29 @@ static int ffn_grid_cap() {
 // per expert: 3*H*I*BITS/8 + scales instead of the dequantise-to-scratch
 // path's codes + 2 x 3*H*I*2 B (scratch write + FFN read).
 // The unit's gathered tokens (NPAD x H bf16 <= 64 KB) are loaded once per
-// unit into their own buffer (every gemm1 step reuses them), and so are its
-// row scales (64 gate + 64 up + all H down rows, double-buffered by unit):
-// a scale read from global per tile put an HBM latency on every tile.
-// Warps: 0 producer, 1 MMA, 2-5 epilogue, 6-13 converters (two per SMSP: the
-// conversion is ALU work on the tile's critical path; int -> float goes through
-// the 1.5 * 2^23 magic-number add instead of the quarter-rate I2F).
+// unit into their own buffer (every gemm1 step reuses them); the row scales (64 gate + 64 up + all H down rows,
+// double-buffered by unit) are applied by the epilogue to the fp32
+// accumulators (the A tile carries the integer codes, exact in bf16).
+// Warps: 0 code producer, 1 MMA, 2-5 epilogue, 6-13 converters (two per SMSP:
+// the conversion is ALU work on the tile's critical path: int4 / int2 pairs are
+// one LOP3 + one bf16x2 subtract).
 constexpr int kDecQConv = 256;
 constexpr int kDecQThreads = 192 + kDecQConv;
 
+#ifndef DECQ_DIAG
+#define DECQ_DIAG 0                                       // A/B diagnostics: 1 no conversion, 2 no gemm1 MMAs, 3 phase stamps
+#endif
+#ifndef DECQ_AS
+#define DECQ_AS 4                                         // A (bf16) ring stages
+#endif
+#ifndef DECQ_QRING
+#define DECQ_QRING (32 * 1024)                            // code ring bytes
+#endif
 template <int BITS>
 struct DecQSmem {
-    static constexpr int AS = 4, QS = 8;
+    static constexpr int AS = DECQ_AS;
     static constexpr int QBYTES = BM * BK * BITS / 8;
+    static constexpr int QS = DECQ_QRING / QBYTES;
     alignas(1024) __nv_bfloat16 a[AS][BM * BK];
     alignas(1024) __nv_bfloat16 xs[32][16 * BK];          // the unit's tokens, one 16 x 64 box per k (H <= 2048)
     alignas(1024) __nv_bfloat16 act_tile[16 * 64];
@@ -700,6 +727,12 @@ struct DecQSmem {
 template <int BITS>
 __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __grid_constant__ FfnArgs g) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+#if DECQ_DIAG == 3
+    __shared__ unsigned long long dq_t[16];
+#define DQ_STAMP(i) do { unsigned long long _t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t)); dq_t[i] = _t; } while (0)
+#else
+#define DQ_STAMP(i) do {} while (0)
+#endif
     using S = DecQSmem<BITS>;
     constexpr int AS = S::AS, QS = S::QS;
     constexpr uint32_t QBYTES = S::QBYTES;
@@ -707,12 +740,14 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
     auto& s = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m1 = g.I / 64, n_units = g.n_exec * m1, n_ht = g.H / BM, KT = g.H / BK;
+    if (threadIdx.x == 0) DQ_STAMP(0);
     if (threadIdx.x == 0) {
-        for (int i = 0; i < AS; i++) { mbar_init(&s.full[i], kDecQConv); mbar_init(&s.empty[i], 1); }
-        for (int i = 0; i < QS; i++) { mbar_init(&s.qfull[i], 1); mbar_init(&s.qempty[i], kDecQConv); }
+        // converter hand-offs arrive once per warp
+        for (int i = 0; i < AS; i++) { mbar_init(&s.full[i], kDecQConv / 32); mbar_init(&s.empty[i], 1); }
+        for (int i = 0; i < QS; i++) { mbar_init(&s.qfull[i], 1); mbar_init(&s.qempty[i], kDecQConv / 32); }
         mbar_init(&s.xfull, 1); mbar_init(&s.xempty, 1);
-        for (int i = 0; i < 2; i++) { mbar_init(&s.sfull[i], 1); mbar_init(&s.sempty[i], kDecQConv); }
-        mbar_init(&s.t1full, 1); mbar_init(&s.t1empty, 4); mbar_init(&s.actrdy, 64);
+        for (int i = 0; i < 2; i++) { mbar_init(&s.sfull[i], 1); mbar_init(&s.sempty[i], 4); }
+        mbar_init(&s.t1full, 1); mbar_init(&s.t1empty, 4); mbar_init(&s.actrdy, 2);   // one per act-writing warp
         mbar_init(&s.t2full, 1); mbar_init(&s.t2empty, 4);
         fence_barrier_init();
         prefetch_tmap(g.x_map);
@@ -726,7 +761,7 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
     const int64_t soff = 3LL * g.I * g.H * BITS / 8;      // fp32 scales: 2I gate/up rows, H down rows
 
     if (warp == 0) {
-        if (lane == 0) {                                  // ---- producer: code tiles + the unit's tokens
+        if (lane == 0) {                                  // ---- producer: code tiles + row scales
             int kq = 0, j = 0;
             auto code_tile = [&](const uint8_t* src) {
                 const int st = kq % QS;
@@ -750,6 +785,7 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
                     k0 = QS < KT ? QS : KT;
                     for (int k = 0; k < k0; k++) code_tile(base + (int64_t)(mt * KT + k) * QBYTES);
                     pdl_wait();
+                    DQ_STAMP(1);
                 }
                 if (j >= 1) mbar_wait(&s.xempty, (j - 1) & 1);
                 mbar_expect_tx(&s.xfull, (uint32_t)(KT * NPAD * BK * 2));
@@ -767,6 +803,7 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
             for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
                 if (j >= 1) mbar_wait(&s.t1empty, (j - 1) & 1);
                 mbar_wait(&s.xfull, j & 1);
+                if (j == 0) DQ_STAMP(2);
                 tc_fence_after();
                 for (int k = 0; k < KT; k++, ka++) {
                     const int st = ka % AS;
@@ -774,12 +811,15 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
                     tc_fence_after();
                     const uint64_t a = umma_desc(s.a[st]), b = umma_desc(s.xs[k]);
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; kk++) umma_bf16(tmem, a + 2 * kk, b + 2 * kk, idesc, (k | kk) ? 1u : 0u);
+                    for (int kk = 0; kk < (DECQ_DIAG == 2 ? 0 : BK / 16); kk++)
+                        umma_bf16(tmem, a + 2 * kk, b + 2 * kk, idesc, (k | kk) ? 1u : 0u);
                     umma_commit(&s.empty[st]);
                 }
+                if (j == 0) DQ_STAMP(3);
                 umma_commit(&s.t1full);
                 umma_commit(&s.xempty);
                 mbar_wait(&s.actrdy, j & 1);
+                if (j == 0) DQ_STAMP(6);
                 if (j >= 1) mbar_wait(&s.t2empty, (j - 1) & 1);
                 tc_fence_after();
                 for (int ht = 0; ht < n_ht; ht++, ka++) {
@@ -796,61 +836,72 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
             }
         }
     } else if (warp >= 6) {                               // ---- converters: codes -> swizzled bf16 A tiles
+        // The A tile holds the integer codes themselves (exact in bf16); the
+        // per-row scale is applied to the fp32 accumulator in the epilogue
+        // (the TMEM lane is the weight row: y = s_row * (q . x)).
+        // int4 / int2 words are interleaved (layer_step.py code_positions):
+        // (w >> BITS*j) & 0x000F000F (0x00030003) holds elements (2j, 2j+1) in
+        // its two half-words, so one LOP3 makes the pair's bf16x2 128 + u
+        // (u = q + 2^(BITS-1), offset binary) and one bf16x2 subtract gives q.
         const int ct = threadIdx.x - 192;
-        int kq = 0, j = 0;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x, j++) {
-            const int sb = j & 1;
-            mbar_wait(&s.sfull[sb], (j >> 1) & 1);
-            constexpr int NI = BM * BK / 16 / kDecQConv;  // 16-code items per thread per tile
-            float sc[NI];
-#pragma unroll
-            for (int i = 0; i < NI; i++) sc[i] = s.sc[sb][(ct >> 2) + (kDecQConv / 4) * i];   // w1: gate 0-63, up 64-127
+        constexpr int NI = BM * BK / 16 / kDecQConv;      // 16-code items per thread per tile
+        int kq = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             for (int t = 0; t < KT + n_ht; t++, kq++) {
                 const int qs = kq % QS, st = kq % AS;
-                if (t >= KT) {                             // down rows 128 (t - KT) + r
-#pragma unroll
-                    for (int i = 0; i < NI; i++) sc[i] = s.sc[sb][128 + (t - KT) * 128 + (ct >> 2) + (kDecQConv / 4) * i];
-                }
                 mbar_wait(&s.qfull[qs], (kq / QS) & 1);
                 if (kq >= AS) mbar_wait(&s.empty[st], ((kq / AS) - 1) & 1);
                 const uint32_t dst = smem_u32(s.a[st]);
 #pragma unroll
-                for (int i = 0; i < NI; i++) {
+                for (int i = 0; i < (DECQ_DIAG == 1 ? 0 : NI); i++) {
                     const int it = ct + kDecQConv * i, r = it >> 2, c0 = (it & 3) * 2;   // row, first 16-B chunk
-                    uint32_t wq[4];                        // the 16 codes, BITS each, lowest bits first
+                    uint32_t o[8];                         // bf16 pairs, element 2c in the low half
                     if (BITS == 8) {
                         const uint4 v = *reinterpret_cast<const uint4*>(s.q[qs] + it * 16);
-                        wq[0] = v.x; wq[1] = v.y; wq[2] = v.z; wq[3] = v.w;
-                    } else if (BITS == 4) {
-                        const uint2 v = *reinterpret_cast<const uint2*>(s.q[qs] + it * 8);
-                        wq[0] = v.x; wq[1] = v.y;
-                    } else {
-                        wq[0] = *reinterpret_cast<const uint32_t*>(s.q[qs] + it * 4);
-                    }
-                    constexpr int PER = 32 / BITS;         // codes per word
-                    uint32_t o[8];                         // bf16 pairs, element 2c in the low half
+                        const uint32_t wq[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int c = 0; c < 8; c++) {
-                        const int e0 = 2 * c, e1 = 2 * c + 1;
-                        const int q0 = (int)(wq[e0 / PER] << (32 - BITS * (e0 % PER + 1))) >> (32 - BITS);
-                        const int q1 = (int)(wq[e1 / PER] << (32 - BITS * (e1 % PER + 1))) >> (32 - BITS);
-                        // (float)q exactly: bits(1.5 * 2^23) + q, minus 1.5 * 2^23
-                        const float f0 = __int_as_float(0x4B400000 + q0) - 12582912.0f;
-                        const float f1 = __int_as_float(0x4B400000 + q1) - 12582912.0f;
-                        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(o[c]) : "f"(f1 * sc[i]), "f"(f0 * sc[i]));
+                        for (int c = 0; c < 8; c++) {
+                            const uint32_t w = wq[c >> 1], sh = (c & 1) * 16;
+                            // (float)q exactly: bits(1.5 * 2^23) + q, minus 1.5 * 2^23
+                            const int q0 = (int)(w << (24 - sh)) >> 24, q1 = (int)(w << (16 - sh)) >> 24;
+                            const float f0 = __int_as_float(0x4B400000 + q0) - 12582912.0f;
+                            const float f1 = __int_as_float(0x4B400000 + q1) - 12582912.0f;
+                            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(o[c]) : "f"(f1), "f"(f0));
+                        }
+                    } else {
+                        constexpr uint32_t MASK = BITS == 4 ? 0x000F000Fu : 0x00030003u;
+                        constexpr uint32_t BIAS = BITS == 4 ? 0x43084308u : 0x43024302u;   // 128 + 2^(BITS-1)
+                        constexpr int PAIRS = 16 / BITS;                                  // pairs per word
+                        uint32_t wq[2];
+                        if (BITS == 4) {
+                            const uint2 v = *reinterpret_cast<const uint2*>(s.q[qs] + it * 8);
+                            wq[0] = v.x; wq[1] = v.y;
+                        } else {
+                            wq[0] = *reinterpret_cast<const uint32_t*>(s.q[qs] + it * 4);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 8; c++) {
+                            const uint32_t w = wq[c / PAIRS] >> (BITS * (c % PAIRS));
+                            uint32_t h;                    // ((w & MASK) ^ BIAS): 128 + u in each half
+                            asm("lop3.b32 %0, %1, %2, %3, 0x6a;" : "=r"(h) : "r"(w), "r"(MASK), "r"(BIAS));
+                            asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(o[c]) : "r"(h), "r"(BIAS));
+                        }
                     }
-                    const uint4 w0 = make_uint4(o[0], o[1], o[2], o[3]), w1 = make_uint4(o[4], o[5], o[6], o[7]);
                     const uint32_t row = dst + r * 128;
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((c0 ^ (r & 7)) << 4)),
-                                 "r"(w0.x), "r"(w0.y), "r"(w0.z), "r"(w0.w) : "memory");
+                                 "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]) : "memory");
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((c0 + 1) ^ (r & 7)) << 4)),
-                                 "r"(w1.x), "r"(w1.y), "r"(w1.z), "r"(w1.w) : "memory");
+                                 "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]) : "memory");
                 }
-                mbar_arrive(&s.qempty[qs]);
                 fence_proxy_async_smem();                 // generic smem writes -> the tensor core's view
-                mbar_arrive(&s.full[st]);
+                __syncwarp();                             // the warp's codes read, its tile rows written + fenced
+                if (lane == 0) {
+                    mbar_arrive(&s.qempty[qs]);
+                    mbar_arrive(&s.full[st]);
+                }
+                if (ct == 0 && kq == 0) DQ_STAMP(9);
+                if (ct == 0 && kq == KT - 1) DQ_STAMP(10);
             }
-            mbar_arrive(&s.sempty[sb]);                    // this unit's scales consumed
         }
     } else {                                              // ---- epilogue, warps 2..5 (ffn_decode_kernel's)
         pdl_wait();
@@ -862,7 +913,11 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
             const int ti = lane < NPAD ? g.tok_index[e * NPAD + lane] : -1;
             const float tw = lane < NPAD ? g.tok_weight[e * NPAD + lane] : 0.0f;
             const int ncol = __reduce_max_sync(0xffffffffu, ti >= 0 ? lane + 1 : 0);
+            const int sb = j & 1;
+            mbar_wait(&s.sfull[sb], (j >> 1) & 1);        // this unit's row scales
+            const float s1 = s.sc[sb][row];               // gate rows 0-63, up rows 64-127
             mbar_wait(&s.t1full, j & 1);
+            if (j == 0 && threadIdx.x == 64) DQ_STAMP(4);
             __syncwarp();
             tc_fence_after();
             float v[16];
@@ -870,6 +925,8 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.t1empty);
+#pragma unroll
+            for (int c = 0; c < 16; c++) v[c] *= s1;      // w = q * s_row
             if (row >= 64) {
 #pragma unroll
                 for (int c = 0; c < 16; c++) s.xchg[row - 64][c] = v[c];
@@ -886,31 +943,45 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
                         __float2bfloat16(a);
                 }
                 fence_proxy_async_smem();
-                mbar_arrive(&s.actrdy);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.actrdy);
+                if (j == 0 && threadIdx.x == 64) DQ_STAMP(5);
             }
             mbar_wait(&s.t2full, j & 1);
+            if (j == 0 && threadIdx.x == 64) DQ_STAMP(7);
             __syncwarp();
             tc_fence_after();
             for (int ht = 0; ht < n_ht; ht++) {
                 float p[16];
                 tmem_ld16(tmem + lanebase + 256u + (uint32_t)(ht * NPAD), p);
                 const int h = ht * BM + row;
+                const float s2 = s.sc[sb][128 + h];       // down row h
 #pragma unroll
                 for (int c = 0; c < 16; c++) {            // static index: p stays in registers
                     if (c >= ncol) break;                 // (ncol is warp-uniform)
                     const int t = __shfl_sync(0xffffffffu, ti, c);
                     const float w = __shfl_sync(0xffffffffu, tw, c);
-                    if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], w * p[c]);
+                    if (t >= 0) atomicAdd(&g.y[(size_t)t * g.H + h], w * (p[c] * s2));
                 }
             }
             tc_fence_before();
             __syncwarp();
+            if (lane == 0) mbar_arrive(&s.sempty[sb]);    // this unit's scales consumed (one per warp)
+            if (j == 0 && threadIdx.x == 64) DQ_STAMP(8);
             if (lane == 0) mbar_arrive(&s.t2empty);
             epi_bar();
         }
     }
     tc_fence_before();
     __syncthreads();
+#if DECQ_DIAG == 3
+    if (threadIdx.x == 0 && blockIdx.x < 3) {
+        DQ_STAMP(11);
+        printf("dq blk %d: pdl %lld xfull %lld g1issued %lld t1full %lld act %lld mma_act %lld t2full %lld unitend %lld conv0 %lld convKT %lld end %lld (ns from entry)\n",
+               blockIdx.x, dq_t[1] - dq_t[0], dq_t[2] - dq_t[0], dq_t[3] - dq_t[0], dq_t[4] - dq_t[0], dq_t[5] - dq_t[0],
+               dq_t[6] - dq_t[0], dq_t[7] - dq_t[0], dq_t[8] - dq_t[0], dq_t[9] - dq_t[0], dq_t[10] - dq_t[0], dq_t[11] - dq_t[0]);
+    }
+#endif
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 

@@ -85,8 +85,8 @@ __global__ void build_tables_kernel(const int16_t* __restrict__ row_sel, const f
 }
 
 // quantised expert (tile-major like the bf16 one, ffn.py; int8 codes, or
-// int4 / int2 codes two / four per byte, lowest bits first, two's
-// complement; then fp32 scales: 2I gate/up rows, H down rows) -> bf16
+// int4 / int2 codes word-interleaved in 32-bit words (layer_step.py
+// code_positions), two's complement; then fp32 scales: 2I gate/up rows, H down rows) -> bf16
 // tile-major scratch entry: w = bf16(q * s_row). A thread converts 16
 // consecutive codes of one row. pairs[2e] = source slot, pairs[2e+1] =
 // scratch entry. grid: (chunks, n_entries of this precision)
@@ -120,17 +120,21 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ slots, int64_t slot_b
             const int8_t* b = reinterpret_cast<const int8_t*>(&q);
 #pragma unroll
             for (int i = 0; i < 16; i++) qb[i] = b[i];
-        } else if (BITS == 2) {
-            const uint32_t q = reinterpret_cast<const uint32_t*>(src)[v];
-#pragma unroll
-            for (int i = 0; i < 16; i++) qb[i] = (int8_t)(q >> (2 * i) << 6) >> 6;   // sign-extended pair
         } else {
-            const uint2 q = reinterpret_cast<const uint2*>(src)[v];
-            const uint8_t* b = reinterpret_cast<const uint8_t*>(&q);
+            // word-interleaved codes (layer_step.py code_positions): element 2j at
+            // position j, element 2j+1 at position PER/2 + j of its 32-bit word
+            constexpr int PER = 32 / BITS;
+            uint32_t w[2];
+            if (BITS == 2) {
+                w[0] = reinterpret_cast<const uint32_t*>(src)[v];
+            } else {
+                const uint2 q = reinterpret_cast<const uint2*>(src)[v];
+                w[0] = q.x; w[1] = q.y;
+            }
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                qb[2 * i] = (int8_t)(b[i] << 4) >> 4;         // low nibble, sign-extended
-                qb[2 * i + 1] = (int8_t)b[i] >> 4;            // high nibble
+            for (int i = 0; i < 16; i++) {
+                const int wi = i / PER, k = i % PER, pos = (k & 1) ? PER / 2 + k / 2 : k / 2;
+                qb[i] = (int8_t)((int)(w[wi] << (32 - BITS * (pos + 1))) >> (32 - BITS));   // sign-extended
             }
         }
         __align__(16) __nv_bfloat16 out[16];

@@ -90,6 +90,53 @@ class LayerStepResult:
     layers: object = None        # every layer's output per (pass, layer) event (keep_layers)
 
 
+def code_positions(bits: int) -> list:
+    """Bit position (in units of `bits`) of element i of each 32-bit code word
+    (int4 / int2): even elements fill the low half-word, odd ones the high
+    half-word, pair j at positions (j, PER/2 + j) -- so one shift + one
+    LOP3 with 0x000F000F (int4) / 0x00030003 (int2) puts elements (2j, 2j+1)
+    into the two halves of a bf16x2 register (ffn_decode_q_kernel)."""
+    per = 32 // bits
+    return [i // 2 if i % 2 == 0 else per // 2 + i // 2 for i in range(per)]
+
+
+def pack_codes(q, bits: int):
+    """int codes [..., n] (two's complement in `bits`) -> uint8 bytes of the
+    slot format: int8 one per byte; int4 / int2 word-interleaved
+    (code_positions) in little-endian 32-bit words."""
+    import torch
+    if bits == 8:
+        return q.to(torch.int8).view(torch.uint8)
+    per = 32 // bits
+    u = (q.to(torch.int64) & ((1 << bits) - 1)).reshape(*q.shape[:-1], q.shape[-1] // per, per)
+    w = torch.zeros(u.shape[:-1], dtype=torch.int64, device=q.device)
+    for i, pos in enumerate(code_positions(bits)):
+        w |= u[..., i] << (bits * pos)
+    return _words_to_bytes(w).reshape(*q.shape[:-1], q.shape[-1] * bits // 8)
+
+
+def _words_to_bytes(w):
+    import torch
+    w = w & 0xFFFFFFFF
+    b = torch.stack([(w >> (8 * k)) & 0xFF for k in range(4)], dim=-1)
+    return b.to(torch.uint8)
+
+
+def unpack_codes(raw, bits: int, n: int):
+    """Inverse of pack_codes: the first n codes of `raw` (uint8) as float."""
+    import torch
+    if bits == 8:
+        return raw[:n].view(torch.int8).float()
+    per = 32 // bits
+    b = raw[:n * bits // 8].to(torch.int64).view(-1, 4)
+    w = b[:, 0] | (b[:, 1] << 8) | (b[:, 2] << 16) | (b[:, 3] << 24)
+    cols = []
+    for i, pos in enumerate(code_positions(bits)):
+        c = (w >> (bits * pos)) & ((1 << bits) - 1)
+        cols.append(torch.where(c >= (1 << (bits - 1)), c - (1 << bits), c))
+    return torch.stack(cols, dim=1).reshape(-1).float()
+
+
 def dequant_expert(raw, bits: int, hidden: int, inter: int):
     """One quantised expert's bytes (tile-major codes of `bits`, lowest bits
     first, two's complement, then fp32 row scales: 2I gate/up rows, H down
@@ -100,13 +147,7 @@ def dequant_expert(raw, bits: int, hidden: int, inter: int):
     import torch
     H, I = hidden, inter
     nq = 3 * H * I
-    if bits == 8:
-        q = raw[:nq].view(torch.int8).float()
-    else:
-        per = 8 // bits
-        b = raw[:nq // per].to(torch.int16)
-        q = torch.stack([(b >> (bits * j)) & ((1 << bits) - 1) for j in range(per)], dim=1).reshape(-1)
-        q = torch.where(q >= (1 << (bits - 1)), q - (1 << bits), q).float()
+    q = unpack_codes(raw, bits, nq)
     sc = raw[nq * bits // 8:nq * bits // 8 + 4 * (2 * I + H)].view(torch.float32)
     w1q, wdq = expert_matrices(q, H, I)
     w1 = (w1q * sc[:2 * I, None]).to(torch.bfloat16).float()
@@ -195,14 +236,7 @@ class LayerStepEngine:
                     sc = torch.zeros(n, ns, device="cuda").scatter_reduce_(1, idx, wf.abs(), "amax") / qmax
                 sc = torch.clamp(sc, min=1e-12)
                 q = torch.clamp(torch.round(wf / torch.gather(sc, 1, idx)), -qmax, qmax).to(torch.int32)
-                if bits == 8:
-                    codes = q.to(torch.int8).view(torch.uint8)
-                else:                                    # 8/bits per byte, lowest bits first
-                    per = 8 // bits
-                    u = (q & ((1 << bits) - 1)).to(torch.uint8).view(n, nq // per, per)
-                    codes = u[:, :, 0].clone()
-                    for j in range(1, per):
-                        codes |= u[:, :, j] << (bits * j)
+                codes = pack_codes(q, bits)              # int8 bytes / word-interleaved int4, int2
                 blob = torch.cat([codes, sc.contiguous().view(torch.uint8).view(n, ns * 4)], dim=1)
                 dst.copy_(blob.reshape(-1))
         torch.cuda.synchronize()

@@ -260,8 +260,9 @@ def test_native_csv_report_rejects_broken_identities():
 def test_tile_major_pack_and_quantised_decode_on_cpu():
     """Host halves of the physical expert formats (CPU): pack_expert inverts
     expert_matrices (the tile-major layout the TMA boxes read), and
-    dequant_expert decodes int8 / int4 / int2 codes (lowest bits first, two's
-    complement) + fp32 row scales exactly like the device dequantisers."""
+    dequant_expert decodes int8 / int4 / int2 codes (int8 one per byte,
+    int4 / int2 word-interleaved, two's complement) + fp32 row scales exactly
+    like the device dequantisers; pack_codes is their inverse."""
     import numpy as np
     import torch
     from paper_2602_03921_b200.ffn import expert_matrices, pack_expert
@@ -279,13 +280,20 @@ def test_tile_major_pack_and_quantised_decode_on_cpu():
         lo, hi = -(1 << (bits - 1)), (1 << (bits - 1)) - 1
         q = rng.integers(lo, hi + 1, nq)
         sc = rng.uniform(0.01, 0.02, ns).astype(np.float32)
-        per = 8 // bits
-        u = (q & ((1 << bits) - 1)).astype(np.uint8).reshape(-1, per)
-        codes = np.zeros(nq // per, np.uint8)
-        for j in range(per):
-            codes |= (u[:, j] << (bits * j)).astype(np.uint8)
+        if bits == 8:
+            codes = q.astype(np.int8).view(np.uint8)
+        else:       # independent encoding of the word-interleaved layout: element 2j -> slot j, 2j+1 -> PER/2 + j
+            per = 32 // bits
+            u = (q & ((1 << bits) - 1)).astype(np.uint64).reshape(-1, per)
+            words = np.zeros(nq // per, np.uint64)
+            for i in range(per):
+                slot = i // 2 if i % 2 == 0 else per // 2 + i // 2
+                words |= u[:, i] << np.uint64(bits * slot)
+            codes = words.astype("<u4").view(np.uint8)
         raw = torch.from_numpy(np.concatenate([codes, sc.view(np.uint8)]))
         d1, d2 = dequant_expert(raw, bits, H, I)
         want = torch.from_numpy((q.astype(np.float32) * sc[rows]).astype(np.float32)).to(torch.bfloat16).float()
         w1w, wdw = expert_matrices(want, H, I)
         assert torch.equal(d1, w1w) and torch.equal(d2, wdw), bits
+        from paper_2602_03921_b200.layer_step import pack_codes
+        assert torch.equal(pack_codes(torch.from_numpy(q), bits), torch.from_numpy(codes)), bits
