@@ -145,6 +145,7 @@ struct Pt {
     int64_t cap;
     int64_t dur0, dur1, dur2, dur3, eb0, eb1, eb2, eb3;   // by precision code (registers, not an array)
     int64_t dur_w, eb_w;            // working precision
+    double inv_dur, inv_eb;         // 1 / dur_w, 1 / eb_w (uniform-path quotients)
     bool uniform;                   // all transfers at the working precision (common path)
     // shared memory
     uint64_t* key;
@@ -209,6 +210,15 @@ DFI int64_t peb(const Pt& p, int c) {
     return c == 0 ? p.eb0 : c == 1 ? p.eb1 : c == 2 ? p.eb2 : p.eb3;
 }
 
+// x / d for 0 <= x < 2^53, d > 0, with inv = 1.0 / d: one double multiply and an
+// exact integer correction instead of a ~70-instruction 64-bit division
+DFI int64_t udiv_rcp(int64_t x, int64_t d, double inv) {
+    int64_t q = (int64_t)((double)x * inv);
+    if (q * d > x) q--;
+    else if ((q + 1) * d <= x) q++;
+    return q;
+}
+
 DFI int ediv(const Pt& p, int ident) {             // ident / E, exact for ident < 2^24
     return (int)(((uint64_t)(uint32_t)ident * p.einv) >> 32);
 }
@@ -255,8 +265,11 @@ DFI uint64_t fold(uint32_t mix, int64_t idx) {
 DFI void emit_mixed(Pt& p, uint32_t mix, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0,
                     int64_t t1, int64_t t2, double x0, const int32_t* pe = nullptr, int npe = 0) {
     if (p.digest_on) {
-        // order-sensitive through the record index, associative across records
-        p.digest += fold(mix, p.n_recs);
+        // order-sensitive through the record index, associative across records;
+        // the digest is lane-partial (summed over the warp once, at the end), so a
+        // warp-uniform record is added by lane 0 only
+        const uint64_t f = fold(mix, p.n_recs);
+        p.digest += p.lane == 0 ? f : 0ull;
     }
     if (p.full) {
         const int64_t n = p.n_recs, m = p.n_pe;
@@ -294,9 +307,8 @@ DFI void emit_lanes(Pt& p, bool act, int rank, int cnt, int kind, int layer, int
         if (act) {
             v = fold(rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0), p.n_recs + rank);
         }
-        #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-        p.digest += v;
+        p.digest += v;                                   // lane-partial
+
     }
     if (p.full) {
         if (p.n_recs + cnt <= p.rec_cap) {
@@ -336,10 +348,8 @@ DFI uint64_t lane_rec(Pt& p, bool act, int64_t idx, int kind, int layer, int i0,
     return p.digest_on ? fold(rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0), idx) : 0;
 }
 
-DFI void digest_add_warp(Pt& p, uint64_t v) {
+DFI void digest_add_warp(Pt& p, uint64_t v) {        // this lane's records of a batch (lane-partial digest)
     if (!p.digest_on) return;
-    #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     p.digest += v;
 }
 
@@ -636,7 +646,7 @@ DFI void settle_uniform(Pt& p) {
     if (p.qn == 0 || p.qc0 > p.now) return;
     int k = p.qn;
     if (p.dur_w > 0) {
-        const int64_t t = (p.now - p.qc0) / p.dur_w + 1;
+        const int64_t t = udiv_rcp(p.now - p.qc0, p.dur_w, p.inv_dur) + 1;
         if (t < k) k = (int)t;
     }
     if (p.fs_top < k) { p.err = -2; return; }
@@ -959,8 +969,8 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
 DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int target) {
     const int64_t nb = p.eb_w;
     const int wp = p.c->working_prec;
-    int64_t room = (p.cap - p.resident_bytes - p.reserved_bytes) / nb;
-    if (room < 0) room = 0;
+    const int64_t freeb = p.cap - p.resident_bytes - p.reserved_bytes;
+    int64_t room = freeb <= 0 ? 0 : udiv_rcp(freeb, nb, p.inv_eb);
     const int F = nt < room ? nt : (int)room;
     const int need = nt - F;
     int r = 0;
@@ -1292,6 +1302,8 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     p.uniform = !GEN;
     p.eb_w = ebs[cfg->working_prec & 3];
     p.dur_w = durs[cfg->working_prec & 3];
+    p.inv_dur = p.dur_w > 0 ? 1.0 / (double)p.dur_w : 0.0;
+    p.inv_eb = p.eb_w > 0 ? 1.0 / (double)p.eb_w : 0.0;
     // residents + queued transfers <= capacity / (smallest expert this point can admit):
     // only fetch_low / fetch_priority ever admit below the working precision
     if (p.miss != ESIM_MISS_FETCH_LOW && p.miss != ESIM_MISS_FETCH_PRIORITY) minb = peb(p, cfg->working_prec);
@@ -1346,7 +1358,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     p.now = 0; p.resident_bytes = 0; p.reserved_bytes = 0;
     p.qh = 0; p.qn = 0; p.nA = 0; p.fs_top = p.S; p.seq = 0; p.qc0 = 0;
     p.einv = ((1ull << 32) + (uint64_t)p.E - 1) / (uint64_t)p.E;
-    p.digest = FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
+    p.digest = p.lane == 0 ? FNV_OFFSET : 0ull; p.n_recs = 0; p.n_pe = 0;   // lane-partial sum
     p.n_evict = 0; p.n_forced = 0;
     p.lc_miss = p.lc_c0 = p.lc_c1 = p.lc_drop = p.lc_sub = 0;
     #pragma unroll
@@ -1530,6 +1542,8 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
         rows_before += tr.pass_tokens[pass];
     }
     __syncwarp();
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p.digest += __shfl_xor_sync(FULL, p.digest, o);   // fold the lane partials
     if (A.progress && p.lane == 0) {
         __threadfence_system();
         A.progress[0] = p.err ? -1 : (int64_t)tr.n_passes * p.L + 1;    // +1: final PassRec written
