@@ -991,9 +991,9 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
             slot = bs;
             return bk;
         };
-        int lslot;
-        uint64_t lk;
-        {                                                              // first pass: no lower bound
+        int lslot = 0;
+        uint64_t lk = 0;
+        if (p.S > 128) {                                               // first pass: no lower bound
             uint64_t bk = wide ? KEY_FREE : 0xFFFFFFFFull;
             int bs = 0;
             for (int sl = p.lane; sl < p.S; sl += 32) {
@@ -1005,15 +1005,52 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
             lslot = bs;
         }
         const uint64_t FREE = wide ? KEY_FREE : 0xFFFFFFFFull;
-        while (r < need) {
-            const uint64_t m = wide ? warp_min_u64(lk) : (uint64_t)__reduce_min_sync(FULL, (uint32_t)lk);
-            if (m == FREE) break;                                     // no resident left: no_space drops
-            if (p.pol == ESIM_EV_LS && (m & LS_CURRENT)) { refusals = true; break; }
-            const int wl = __ffs(__ballot_sync(FULL, lk == m)) - 1;
-            const int vs = __shfl_sync(FULL, lslot, wl);
-            if (p.lane == 0) p.vict[r] = (int16_t)vs;
-            r++;
-            if (p.lane == wl) lk = lane_min(m, lslot);
+        if (p.S <= 128) {
+            // <= 4 slots per lane: each lane sorts its keys once (a 5-exchange
+            // network in registers); the victims are then a 32-way merge of the
+            // lanes' sorted lists -- the winner shifts its list instead of
+            // rescanning its slots for the next key
+            uint64_t kk[4];
+            int ss[4];
+            #pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int sl = p.lane + 32 * j;
+                const bool in = sl < p.S;
+                kk[j] = in ? (wide ? p.key[sl] : (uint64_t)k32[2 * sl]) : FREE;
+                ss[j] = sl;
+            }
+            auto cx = [&](int a, int b) {
+                const bool sw = kk[b] < kk[a];
+                const uint64_t ka = kk[a], kb = kk[b];
+                const int sa = ss[a], sb = ss[b];
+                kk[a] = sw ? kb : ka; kk[b] = sw ? ka : kb;
+                ss[a] = sw ? sb : sa; ss[b] = sw ? sa : sb;
+            };
+            cx(0, 1); cx(2, 3); cx(0, 2); cx(1, 3); cx(1, 2);
+            while (r < need) {
+                const uint64_t m = wide ? warp_min_u64(kk[0]) : (uint64_t)__reduce_min_sync(FULL, (uint32_t)kk[0]);
+                if (m == FREE) break;                                 // no resident left: no_space drops
+                if (p.pol == ESIM_EV_LS && (m & LS_CURRENT)) { refusals = true; break; }
+                const int wl = __ffs(__ballot_sync(FULL, kk[0] == m)) - 1;
+                const int vs = __shfl_sync(FULL, ss[0], wl);
+                if (p.lane == 0) p.vict[r] = (int16_t)vs;
+                r++;
+                if (p.lane == wl) {
+                    kk[0] = kk[1]; kk[1] = kk[2]; kk[2] = kk[3]; kk[3] = FREE;
+                    ss[0] = ss[1]; ss[1] = ss[2]; ss[2] = ss[3];
+                }
+            }
+        } else {
+            while (r < need) {
+                const uint64_t m = wide ? warp_min_u64(lk) : (uint64_t)__reduce_min_sync(FULL, (uint32_t)lk);
+                if (m == FREE) break;                                 // no resident left: no_space drops
+                if (p.pol == ESIM_EV_LS && (m & LS_CURRENT)) { refusals = true; break; }
+                const int wl = __ffs(__ballot_sync(FULL, lk == m)) - 1;
+                const int vs = __shfl_sync(FULL, lslot, wl);
+                if (p.lane == 0) p.vict[r] = (int16_t)vs;
+                r++;
+                if (p.lane == wl) lk = lane_min(m, lslot);
+            }
         }
         __syncwarp();
     }
