@@ -82,10 +82,10 @@ struct Ctr {                       // 32-bit counts: native ATOMS.ADD (64-bit is
 };
 
 struct Layout {
-    int key, q_submit, q_comp, dsum, ctr, dem_summed;     // 8-byte
-    int cnt, rscore, q_score, pl, demmask, lsc, ca_w, ca_row, dem_gate, dem_tokens, dem_expert, dem_rank;  // 4-byte
-    int rs, hist, res_ident, fs, q_ident, ca_sel, vict;   // 2-byte
-    int q_flags, tofetch, ca_mod;                         // 1-byte
+    int key, q_submit, q_comp, dsum, ctr, dem_summed, q_ent;   // 8-byte
+    int cnt, rscore, pl, demmask, lsc, ca_w, ca_row, dem_gate, dem_tokens, dem_expert, dem_rank;  // 4-byte
+    int rs, hist, res_ident, fs, ca_sel, vict;            // 2-byte
+    int tofetch, ca_mod;                                  // 1-byte
     int total;
 };
 
@@ -104,9 +104,9 @@ __host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E,
     l.dsum = o; o += al8(ca ? L * 8 : 0);
     l.ctr = o; o += al8((int)sizeof(Ctr));
     l.dem_summed = o; o += al8(ca ? E * 8 : 0);
+    l.q_ent = o; o += al8(Q * 8);                   // channel entries: ident | flags | score, one word each
     l.cnt = o; o += al8(has_cnt ? N * 2 : 0);      // 16-bit LFU/LHU access counts (host-checked bound)
     l.rscore = o; o += al8(gen ? S * 4 : 0);
-    l.q_score = o; o += al8(Q * 4);
     l.pl = o; o += al8(L * ESIM_PL_FIELDS * 4);
     l.demmask = o; o += al8(((E + 31) / 32) * 4);
     l.lsc = o; o += al8(E * 4);
@@ -120,10 +120,8 @@ __host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E,
     l.hist = o; o += al8(N * 2);
     l.res_ident = o; o += al8(S * 2);
     l.fs = o; o += al8(S * 2);
-    l.q_ident = o; o += al8(Q * 2);
     l.ca_sel = o; o += al8(ca ? T * K * 2 : 0);
     l.vict = o; o += al8(gen ? 0 : E * 2);          // batched watchdog sweep 2 (uniform instances)
-    l.q_flags = o; o += al8(Q);
     l.tofetch = o; o += al8(E);
     l.ca_mod = o; o += al8(ca ? T : 0);
     l.total = o;
@@ -157,7 +155,6 @@ struct Pt {
     double* dem_summed_s;
     uint16_t* cnt;                  // LFU / LHU access count per ident (< 65536: esim_replay_launch checks)
     float* rscore;
-    float* q_score;
     int32_t* pl;
     uint32_t* demmask;
     float* lsc;
@@ -171,10 +168,9 @@ struct Pt {
     int16_t* hist;
     int16_t* res_ident;
     uint16_t* fs;
-    int16_t* q_ident;
+    uint64_t* q_ent;                // channel ring: ident:16 | flags:8 (bits 16-23) | score f32 (bits 32-63)
     int16_t* ca_sel;
     int16_t* vict;                  // sweep-2 victims in eviction order (uniform instances)
-    uint8_t* q_flags;
     uint8_t* tofetch;
     uint8_t* ca_mod;
     // warp-uniform scalars
@@ -542,6 +538,13 @@ DFI void evict(Pt& p, int slot, int cause, bool forced) {                 // eng
 // ---------------------------------------------------------------------------
 struct QEntry { int16_t ident; uint8_t flags; float score; int64_t submit, comp; };
 
+DFI uint64_t qe_make(int16_t ident, uint8_t flags, float score) {
+    return (uint64_t)(uint16_t)ident | ((uint64_t)flags << 16) | ((uint64_t)__float_as_uint(score) << 32);
+}
+DFI int16_t qe_ident(uint64_t w) { return (int16_t)(uint16_t)w; }
+DFI uint8_t qe_flags(uint64_t w) { return (uint8_t)(w >> 16); }
+DFI float qe_score(uint64_t w) { return __uint_as_float((uint32_t)(w >> 32)); }
+
 // The queue is settled whenever it is touched (every entry has comp > now >=
 // its submit time: settle() lands comp <= now from the head after every time
 // step), so comp_i = max(comp_{i-1}, submit_i) + dur_i (engine.py:283-288)
@@ -555,13 +558,14 @@ DFI int64_t qcomp(const Pt& p, int i) {
 DFI QEntry q_load(const Pt& p, int i) {
     const int x = qphys(p, i);
     QEntry e;
-    e.ident = p.q_ident[x]; e.flags = p.q_flags[x]; e.score = p.q_score[x];
+    const uint64_t w = p.q_ent[x];
+    e.ident = qe_ident(w); e.flags = qe_flags(w); e.score = qe_score(w);
     if (!p.uniform) { e.submit = p.q_submit[x]; e.comp = p.q_comp[x]; }
     return e;
 }
 DFI void q_store(Pt& p, int i, const QEntry& e) {
     const int x = qphys(p, i);
-    p.q_ident[x] = e.ident; p.q_flags[x] = e.flags; p.q_score[x] = e.score;
+    p.q_ent[x] = qe_make(e.ident, e.flags, e.score);
     if (!p.uniform) { p.q_submit[x] = e.submit; p.q_comp[x] = e.comp; }
 }
 
@@ -609,7 +613,7 @@ DFI void retime(Pt& p, int from) {
         int x = 0;
         if (act) {
             x = qphys(p, i);
-            const int64_t d = pdur(p, (p.q_flags[x] >> 2) & 3);
+            const int64_t d = pdur(p, (qe_flags(p.q_ent[x]) >> 2) & 3);
             a = d;
             b = p.q_submit[x] + d;
         }
@@ -631,7 +635,7 @@ DFI void retime(Pt& p, int from) {
 DFI int q_find(const Pt& p, int ident) {
     for (int base = 0; base < p.qn; base += 32) {
         const int i = base + p.lane;
-        const bool hit = i < p.qn && p.q_ident[qphys(p, i)] == ident;
+        const bool hit = i < p.qn && qe_ident(p.q_ent[qphys(p, i)]) == ident;
         const unsigned m = __ballot_sync(FULL, hit);
         if (m) return base + __ffs(m) - 1;
     }
@@ -662,9 +666,10 @@ DFI void settle_uniform(Pt& p) {
         float score = 0.0f;
         if (act) {
             const int x = qphys(p, i);
-            ident = p.q_ident[x];
-            pf = p.q_flags[x] & 1;
-            score = p.q_score[x];
+            const uint64_t w = p.q_ent[x];
+            ident = qe_ident(w);
+            pf = qe_flags(w) & 1;
+            score = qe_score(w);
             slot = p.fs[p.fs_top - 1 - i];
             p.rs[ident] = rs_make(wp, slot);
             p.res_ident[slot] = (int16_t)ident;
@@ -706,9 +711,10 @@ DFI void settle(Pt& p) {                                                   // en
         const int h = p.qh;
         const int64_t comp = qcomp(p, 0);
         if (comp > p.now) break;
-        const int ident = p.q_ident[h];
-        const uint8_t fl = p.q_flags[h];
-        const float score = p.q_score[h];
+        const uint64_t w = p.q_ent[h];
+        const int ident = qe_ident(w);
+        const uint8_t fl = qe_flags(w);
+        const float score = qe_score(w);
         const int prec = (fl >> 2) & 3;
         const int64_t nb = peb(p, prec);
         if (p.fs_top <= 0) { p.err = -2; return; }
@@ -861,7 +867,7 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
         __syncwarp();
         int at = idx;
         if (idx == 0) {
-            if (p.lane == 0) p.q_flags[qphys(p, 0)] = e.flags;
+            if (p.lane == 0) p.q_ent[qphys(p, 0)] = qe_make(e.ident, e.flags, e.score);
             __syncwarp();
         } else {
             const bool inA = idx <= p.nA;
@@ -1085,9 +1091,7 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
         }
         if (st) {                                                      // reserve + channel.append
             const int x = qphys(p, p.qn + t);
-            p.q_ident[x] = (int16_t)(target * p.E + e);
-            p.q_flags[x] = (uint8_t)(1 | (wp << 2));
-            p.q_score[x] = sc;
+            p.q_ent[x] = qe_make((int16_t)(target * p.E + e), (uint8_t)(1 | (wp << 2)), sc);
             p.rs[target * p.E + e] = RS_INF;
         }
     }
@@ -1357,7 +1361,6 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     p.dem_summed_s = reinterpret_cast<double*>(base + lay.dem_summed);
     p.cnt = reinterpret_cast<uint16_t*>(base + lay.cnt);
     p.rscore = reinterpret_cast<float*>(base + lay.rscore);
-    p.q_score = reinterpret_cast<float*>(base + lay.q_score);
     p.pl = reinterpret_cast<int32_t*>(base + lay.pl);
     p.demmask = reinterpret_cast<uint32_t*>(base + lay.demmask);
     p.lsc = reinterpret_cast<float*>(base + lay.lsc);
@@ -1371,10 +1374,9 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     p.hist = reinterpret_cast<int16_t*>(base + lay.hist);
     p.res_ident = reinterpret_cast<int16_t*>(base + lay.res_ident);
     p.fs = reinterpret_cast<uint16_t*>(base + lay.fs);
-    p.q_ident = reinterpret_cast<int16_t*>(base + lay.q_ident);
+    p.q_ent = reinterpret_cast<uint64_t*>(base + lay.q_ent);
     p.ca_sel = reinterpret_cast<int16_t*>(base + lay.ca_sel);
     p.vict = reinterpret_cast<int16_t*>(base + lay.vict);
-    p.q_flags = base + lay.q_flags;
     p.tofetch = base + lay.tofetch;
     p.ca_mod = base + lay.ca_mod;
 
