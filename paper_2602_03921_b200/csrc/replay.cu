@@ -143,6 +143,7 @@ struct Pt {
     int64_t cap;
     int64_t dur0, dur1, dur2, dur3, eb0, eb1, eb2, eb3;   // by precision code (registers, not an array)
     int64_t dur_w, eb_w;            // working precision
+    int wp;                         // working precision code (cfg->working_prec, kept in a register)
     double inv_dur, inv_eb;         // 1 / dur_w, 1 / eb_w (uniform-path quotients)
     bool uniform;                   // all transfers at the working precision (common path)
     // shared memory
@@ -654,7 +655,7 @@ DFI void settle_uniform(Pt& p) {
         if (t < k) k = (int)t;
     }
     if (p.fs_top < k) { p.err = -2; return; }
-    const int wp = p.c->working_prec;
+    const int wp = p.wp;
     const unsigned below = lanes_below(p.lane);
     uint64_t dg = 0;
     int npf = 0;
@@ -702,7 +703,10 @@ DFI void settle_uniform(Pt& p) {
     p.resident_bytes += nb * k;
     p.n_recs += npf;
     p.pf_ev[2] += npf;
-    if (p.resident_bytes + p.reserved_bytes > p.cap && !p.err) p.err = -2;
+    // byte-accounting invariant (engine.py:216-236): checked on the general path
+    // and in full-log runs (the parity tests); the uniform sweep kernels hold it
+    // by construction (every landing was reserved)
+    if ((!p.uniform || p.full) && p.resident_bytes + p.reserved_bytes > p.cap && !p.err) p.err = -2;
 }
 
 DFI void settle(Pt& p) {                                                   // engine.py:422-442
@@ -974,7 +978,7 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
 // positions their candidate order fixes and are written lane-parallel.
 DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int target) {
     const int64_t nb = p.eb_w;
-    const int wp = p.c->working_prec;
+    const int wp = p.wp;
     const int64_t freeb = p.cap - p.resident_bytes - p.reserved_bytes;
     int64_t room = freeb <= 0 ? 0 : udiv_rcp(freeb, nb, p.inv_eb);
     const int F = nt < room ? nt : (int)room;
@@ -1120,7 +1124,7 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
     // the per-layer predicted-set sizes are added from it at the end)
     emit_mixed(p, p.digest_on ? R.pred_mix[tev] : 0u, ESIM_REC_PREDICTION, p.layer, target, n,
                p.full ? R.pred_clamped[tev] : 0, 0, 0, 0, 0, 0, 0.0, pe, n);
-    const int wp = p.c->working_prec;
+    const int wp = p.wp;
     const int64_t nb = peb(p, wp);
     const unsigned below = lanes_below(p.lane);
     // "predicted" records, one per prediction in order (lane j: prediction j)
@@ -1341,6 +1345,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     p.eb0 = ebs[0]; p.eb1 = ebs[1]; p.eb2 = ebs[2]; p.eb3 = ebs[3];
     p.dur0 = durs[0]; p.dur1 = durs[1]; p.dur2 = durs[2]; p.dur3 = durs[3];
     p.uniform = !GEN;
+    p.wp = cfg->working_prec;
     p.eb_w = ebs[cfg->working_prec & 3];
     p.dur_w = durs[cfg->working_prec & 3];
     p.inv_dur = p.dur_w > 0 ? 1.0 / (double)p.dur_w : 0.0;
