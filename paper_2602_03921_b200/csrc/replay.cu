@@ -49,26 +49,6 @@ constexpr int STATUS_QUEUE_OVERFLOW = -5;
 constexpr int STATUS_COUNT_OVERFLOW = -7;          // an LFU/LHU access count outgrew 16 bits
 constexpr int STATUS_SEQ_OVERFLOW = -8;            // > 2^31 policy stamps in one replay
 
-struct ReplayArgs {
-    const EsimConfig* cfg;
-    int n_points;
-    const EsimTraceDesc* traces;   // device array of descriptors (device pointers inside)
-    const EsimRouterOut* routers;
-    EsimCounters* counters;
-    int64_t* per_layer;            // [n][Lmax][ESIM_PL_FIELDS]
-    EsimRec* recs;
-    int64_t rec_cap;
-    int32_t* pexp;
-    int64_t pe_cap;
-    int N, S, Q, Lmax, Emax, Tmax, Kmax;  // smem sizing (max over points)
-    int has_cnt;                   // any LFU/LHU point (per-ident counts)
-    int warps_per_cta;
-    int point_bytes;
-    const int32_t* out_index;      // optional: output row of launch point pid (counters, per_layer, logs)
-    int* work;                     // optional: persistent launch, next point of the launch order
-    volatile int64_t* progress;    // optional (single point, streamed decisions): [0] events done
-                                   // (-1 on error), [1 + ev] records emitted through event ev
-};
 
 // lane-0 owned counters (shared memory)
 struct Ctr {                       // 32-bit counts: native ATOMS.ADD (64-bit is a CAS loop)
@@ -127,6 +107,29 @@ __host__ __device__ inline Layout make_layout(int N, int S, int Q, int L, int E,
     l.total = o;
     return l;
 }
+
+struct ReplayArgs {
+    const EsimConfig* cfg;
+    int n_points;
+    const EsimTraceDesc* traces;   // device array of descriptors (device pointers inside)
+    const EsimRouterOut* routers;
+    EsimCounters* counters;
+    int64_t* per_layer;            // [n][Lmax][ESIM_PL_FIELDS]
+    EsimRec* recs;
+    int64_t rec_cap;
+    int32_t* pexp;
+    int64_t pe_cap;
+    int N, S, Q, Lmax, Emax, Tmax, Kmax;  // smem sizing (max over points)
+    int has_cnt;                   // any LFU/LHU point (per-ident counts)
+    int warps_per_cta;
+    int point_bytes;
+    Layout lay;                    // per-point shared-memory layout (launch-uniform, kernel-parameter space:
+                                   // the smem pointers rematerialise from it instead of holding registers)
+    const int32_t* out_index;      // optional: output row of launch point pid (counters, per_layer, logs)
+    int* work;                     // optional: persistent launch, next point of the launch order
+    volatile int64_t* progress;    // optional (single point, streamed decisions): [0] events done
+                                   // (-1 on error), [1 + ev] records emitted through event ev
+};
 
 // packed directory word
 constexpr uint16_t RS_INF = 0x8000, RS_RES = 0x1000;
@@ -1316,7 +1319,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     const EsimTraceDesc tr = A.traces[cfg->trace_id];
     const EsimRouterOut R = A.routers[cfg->trace_id];
     const bool ca = GEN && cfg->routing == ESIM_ROUTE_CACHE_AWARE;
-    const Layout lay = make_layout(A.N, A.S, A.Q, A.Lmax, A.Emax, A.Tmax, A.Kmax, A.Tmax > 0, A.has_cnt != 0, GEN != 0);
+    const Layout& lay = A.lay;
 
     long long t_begin;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
@@ -1707,7 +1710,8 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
     a.N = N; a.S = S; a.Q = Q; a.Lmax = Lmax; a.Emax = Emax; a.Tmax = Tmax; a.Kmax = Kmax;
     a.has_cnt = has_cnt ? 1 : 0;
     a.warps_per_cta = warps_per_cta;
-    a.point_bytes = esim::make_layout(N, S, Q, Lmax, Emax, Tmax, Kmax, Tmax > 0, has_cnt, general).total;
+    a.lay = esim::make_layout(N, S, Q, Lmax, Emax, Tmax, Kmax, Tmax > 0, has_cnt, general);
+    a.point_bytes = a.lay.total;
     a.work = nullptr;
     const size_t smem = (size_t)a.point_bytes * warps_per_cta;
     int blocks = (n + warps_per_cta - 1) / warps_per_cta;
