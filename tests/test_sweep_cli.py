@@ -71,3 +71,30 @@ def test_sweep_cli_matches_reference_byte_for_byte(tmp_path, case):
     assert fails == [ln for ln in case["stderr"].splitlines() if ": FAILED: " in ln]
     got_csv = open(out_csv, newline="").read() if out_csv.exists() else None
     assert got_csv == case["csv"]
+
+
+@pytest.mark.gpu
+def test_sweep_cli_sharded_under_torchrun_matches_reference(tmp_path):
+    """`torchrun --nproc-per-node 2 -m paper_2602_03921_b200.cli sweep ...`: the
+    rows sharded over two ranks (gloo: they share the test box's one GPU),
+    results all-gathered, rank 0 writes -- stdout and CSV identical to the
+    reference CLI's single-process sweep."""
+    import socket
+    import subprocess
+    import sys
+    case = next(c for c in GOLD if c["name"] == "presets_olmoe")
+    p = _trace(tmp_path, case)
+    out_csv = tmp_path / "sharded.csv"
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(HERE)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "-m", "paper_2602_03921_b200.cli",
+           "sweep", "--trace", str(p), *case["sweep"], "--out", str(out_csv), "--jobs", "1"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "PYTHONPATH": root, "OMP_NUM_THREADS": "1"})
+    assert r.returncode == case["rc"], r.stderr[-2000:]
+    assert r.stdout.replace(str(tmp_path), "<DIR>") == case["stdout"]
+    assert open(out_csv, newline="").read() == case["csv"]
