@@ -84,7 +84,7 @@ def test_sweep_cli_sharded_under_torchrun_matches_reference(tmp_path):
     import sys
     case = next(c for c in GOLD if c["name"] == "presets_olmoe")
     p = _trace(tmp_path, case)
-    out_csv = tmp_path / "sharded.csv"
+    out_csv = tmp_path / (case["name"] + ".csv")
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
