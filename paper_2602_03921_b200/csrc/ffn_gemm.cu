@@ -700,7 +700,8 @@ constexpr int kDecQConv = 256;
 constexpr int kDecQThreads = 192 + kDecQConv;
 
 #ifndef DECQ_DIAG
-#define DECQ_DIAG 0                                       // A/B diagnostics: 1 no conversion, 2 no gemm1 MMAs, 3 phase stamps
+#define DECQ_DIAG 0   // A/B diagnostics: 1 no conversion, 2 no gemm1 MMAs, 3 phase stamps, 5 no conversion
+                      // and no proxy fence, 6 = 5 + no gemm1 MMAs (the hand-off skeleton)
 #endif
 #ifndef DECQ_AS
 #define DECQ_AS 4                                         // A (bf16) ring stages
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
                     tc_fence_after();
                     const uint64_t a = umma_desc(s.a[st]), b = umma_desc(s.xs[k]);
 #pragma unroll
-                    for (int kk = 0; kk < (DECQ_DIAG == 2 ? 0 : BK / 16); kk++)
+                    for (int kk = 0; kk < ((DECQ_DIAG == 2 || DECQ_DIAG == 6) ? 0 : BK / 16); kk++)
                         umma_bf16(tmem, a + 2 * kk, b + 2 * kk, idesc, (k | kk) ? 1u : 0u);
                     umma_commit(&s.empty[st]);
                 }
@@ -853,7 +854,7 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
                 if (kq >= AS) mbar_wait(&s.empty[st], ((kq / AS) - 1) & 1);
                 const uint32_t dst = smem_u32(s.a[st]);
 #pragma unroll
-                for (int i = 0; i < (DECQ_DIAG == 1 ? 0 : NI); i++) {
+                for (int i = 0; i < ((DECQ_DIAG == 1 || DECQ_DIAG >= 5) ? 0 : NI); i++) {
                     const int it = ct + kDecQConv * i, r = it >> 2, c0 = (it & 3) * 2;   // row, first 16-B chunk
                     uint32_t o[8];                         // bf16 pairs, element 2c in the low half
                     if (BITS == 8) {
@@ -893,7 +894,7 @@ __global__ void __launch_bounds__(kDecQThreads, 1) ffn_decode_q_kernel(const __g
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((c0 + 1) ^ (r & 7)) << 4)),
                                  "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]) : "memory");
                 }
-                fence_proxy_async_smem();                 // generic smem writes -> the tensor core's view
+                if (DECQ_DIAG < 5) fence_proxy_async_smem();   // generic smem writes -> the tensor core's view
                 __syncwarp();                             // the warp's codes read, its tile rows written + fenced
                 if (lane == 0) {
                     mbar_arrive(&s.qempty[qs]);

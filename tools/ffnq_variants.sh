@@ -1,8 +1,11 @@
 #!/bin/bash
-# quantised decode FFN: GPU tests (FFN + layer step) and the microbenchmark
+# quantised decode FFN A/B: production build vs diagnostic builds (lib/variants/libq_<name>.so)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_ffn.py tests/test_gpu_layer_step.py -q -p no:cacheprovider -x > gpurun_out/pytest_ffn.log 2>&1
-timeout 300 python tools/bench_ffn.py > gpurun_out/bench_ffn.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_decode_q -s 66 -c 1 -o gpurun_out/ffn_q4 -f python tools/bench_ffn.py > gpurun_out/ncu_q4.log 2>&1
-python tools/ncu_summary.py gpurun_out/ffn_q4.ncu-rep gpurun_out/ffn_q4_summary.json > /dev/null 2>&1
+cp paper_2602_03921_b200/lib/libspecmd_b200.so /tmp/base.so
+for v in base "$@"; do
+  if [ "$v" = base ]; then cp /tmp/base.so paper_2602_03921_b200/lib/libspecmd_b200.so;
+  else cp paper_2602_03921_b200/lib/variants/libq_$v.so paper_2602_03921_b200/lib/libspecmd_b200.so; fi
+  echo "== $v" >> gpurun_out/ffnq_var.log
+  timeout 300 python tools/bench_ffn.py 2>&1 | grep -E "^decode" | cut -c1-60 >> gpurun_out/ffnq_var.log
+done
