@@ -128,7 +128,7 @@ def layer_step_section(runs=2):
     out = {"config": "olmoe 16x64 top-8, SwiGLU H=2048 I=1024 bf16 (12,582,912 B/expert, 12.9 GB pinned store, "
                      "N(0,0.02) seed 0), cache 614,400,000 B -> 51 HBM slots, score:80 + fetch, "
                      "logical clock 5 GB/s / 2000 us (reference defaults), 64 prefill + 64 decode tokens",
-           "host_link_peak_gbs": peak, "host_link_peak_source": "pinned H2D 1 GiB x5, measured in this run"}
+           "host_link_peak_gbs": peak, "host_link_peak_source": "pinned H2D, best of 3 x (1 GiB x5), measured in this run"}
     eng = None
     for ev in ("ls", "lru"):
         cfg = SimConfig(model=spec, hardware=HardwareSpec(capacity_bytes=614_400_000), working_precision="fp16",

@@ -20,8 +20,10 @@ import numpy as np
 from .models import HardwareSpec
 
 
-def measure_link_gbs(nbytes: int = 1 << 30, reps: int = 5) -> float:
-    """Pinned host -> HBM copy bandwidth (GB/s) on a side stream."""
+def measure_link_gbs(nbytes: int = 1 << 30, reps: int = 5, trials: int = 3) -> float:
+    """Pinned host -> HBM copy bandwidth (GB/s) on a side stream: the best of
+    `trials` timings of `reps` back-to-back 1 GiB copies (the link's peak, not
+    an average over whatever else the host was doing)."""
     import torch
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
@@ -29,14 +31,17 @@ def measure_link_gbs(nbytes: int = 1 << 30, reps: int = 5) -> float:
     with torch.cuda.stream(s):
         d.copy_(h, non_blocking=True)
     s.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(s):
-        e0.record()
-        for _ in range(reps):
-            d.copy_(h, non_blocking=True)
-        e1.record()
-    s.synchronize()
-    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    best = 0.0
+    for _ in range(trials):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record()
+            for _ in range(reps):
+                d.copy_(h, non_blocking=True)
+            e1.record()
+        s.synchronize()
+        best = max(best, nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
 
 
 def _routing(tokens: int, top_k: int, experts: int, rng):
