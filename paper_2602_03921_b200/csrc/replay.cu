@@ -44,7 +44,6 @@ namespace esim {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint64_t FNV_OFFSET = 0xcbf29ce484222325ULL;
 constexpr uint64_t FNV_PRIME = 0x100000001b3ULL;
-constexpr uint64_t FNV_PRIME_MIX = 0xD6E8FEB86659FD93ULL;
 constexpr int STATUS_QUEUE_OVERFLOW = -5;
 constexpr int STATUS_COUNT_OVERFLOW = -7;          // an LFU/LHU access count outgrew 16 bits
 constexpr int STATUS_SEQ_OVERFLOW = -8;            // > 2^31 policy stamps in one replay
@@ -252,13 +251,15 @@ DFI void ps_add(Pt& p, int which, double x) {
 // record output + digest
 // digest: mix = sum_i w_i * K_i (mod 2^32) over the record's sixteen 32-bit
 // words (t0 skipped for predictions) + sum_j (e_j+1) * G*(j+1) over a
-// prediction's experts; x = (mix ^ idx*C) * P (idx = record index);
-// digest += x ^ (x >> 31). The index makes it order-sensitive, the sum keeps
-// the loop-carried chain one add. Zero/constant words fold at compile time.
+// prediction's experts; x = (mix ^ idx*C) * P mod 2^32 (idx = record index);
+// digest += x ^ (x >> 15), a 32-bit term summed into the 64-bit digest (all
+// 32-bit operations: the fold sits on every record's path). The index makes it
+// order-sensitive, the sum keeps the loop-carried chain one add. Zero/constant
+// words fold at compile time.
 // ---------------------------------------------------------------------------
 DFI uint64_t fold(uint32_t mix, int64_t idx) {
-    const uint64_t x = (uint64_t)(mix ^ ((uint32_t)idx * 0x85EBCA77u)) * FNV_PRIME_MIX;
-    return x ^ (x >> 31);
+    const uint32_t x = (mix ^ ((uint32_t)idx * 0x85EBCA77u)) * 0xC2B2AE3Du;
+    return (uint64_t)(x ^ (x >> 15));
 }
 
 // record with its digest word already mixed (premixed: from the router summary)
