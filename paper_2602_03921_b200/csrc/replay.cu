@@ -180,7 +180,8 @@ struct Pt {
     int64_t now, resident_bytes, reserved_bytes;
     int qh, qn, nA, fs_top;
     uint64_t seq;
-    uint64_t digest;
+    uint64_t digest;                // lane-partial sum of lane-parallel records' terms
+    uint64_t digest_u;              // warp-uniform records' terms (every lane holds the same sum)
     bool digest_on;
     uint32_t pf_ev[5];              // prefetch submitted/started/completed/skipped/dropped (registers)
     uint32_t n_evict, n_forced;
@@ -269,8 +270,7 @@ DFI void emit_mixed(Pt& p, uint32_t mix, int kind, int layer, int i0, int i1, in
         // order-sensitive through the record index, associative across records;
         // the digest is lane-partial (summed over the warp once, at the end), so a
         // warp-uniform record is added by lane 0 only
-        const uint64_t f = fold(mix, p.n_recs);
-        p.digest += p.lane == 0 ? f : 0ull;
+        p.digest_u += fold(mix, p.n_recs);            // warp-uniform part, added once at the end
     }
     if (p.full) {
         const int64_t n = p.n_recs, m = p.n_pe;
@@ -1406,7 +1406,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     p.now = 0; p.resident_bytes = 0; p.reserved_bytes = 0;
     p.qh = 0; p.qn = 0; p.nA = 0; p.fs_top = p.S; p.seq = 0; p.qc0 = 0;
     p.einv = ((1ull << 32) + (uint64_t)p.E - 1) / (uint64_t)p.E;
-    p.digest = p.lane == 0 ? FNV_OFFSET : 0ull; p.n_recs = 0; p.n_pe = 0;   // lane-partial sum
+    p.digest = 0ull; p.digest_u = FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
     p.n_evict = 0; p.n_forced = 0;
     p.lc_miss = p.lc_c0 = p.lc_c1 = p.lc_drop = p.lc_sub = 0;
     #pragma unroll
@@ -1592,6 +1592,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     __syncwarp();
     #pragma unroll
     for (int o = 16; o > 0; o >>= 1) p.digest += __shfl_xor_sync(FULL, p.digest, o);   // fold the lane partials
+    p.digest += p.digest_u;
     if (A.progress && p.lane == 0) {
         __threadfence_system();
         A.progress[0] = p.err ? -1 : (int64_t)tr.n_passes * p.L + 1;    // +1: final PassRec written
