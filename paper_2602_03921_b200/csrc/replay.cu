@@ -179,7 +179,7 @@ struct Pt {
     // warp-uniform scalars
     int64_t now, resident_bytes, reserved_bytes;
     int qh, qn, nA, fs_top;
-    uint64_t seq;
+    uint32_t seq;                   // policy stamp counter (< SEQ_LIMIT < 2^31: checked once per layer)
     uint64_t digest;                // lane-partial sum of lane-parallel records' terms
     uint64_t digest_u;              // warp-uniform records' terms (every lane holds the same sum)
     bool digest_on;
@@ -188,7 +188,8 @@ struct Pt {
     // this layer's access outcomes (registers; folded into the smem per-layer
     // counters once per layer): misses (fetch + wait) by class, drops, substitutions
     uint32_t lc_miss, lc_c0, lc_c1, lc_drop, lc_sub;
-    int64_t n_recs, n_pe;
+    int32_t n_recs;                 // records so far (< 2^31: a log of 2^31 x 64 B records cannot exist)
+    int64_t n_pe;
     int pass_id, layer;
     int err;
     // record output
@@ -258,7 +259,7 @@ DFI void ps_add(Pt& p, int which, double x) {
 // order-sensitive, the sum keeps the loop-carried chain one add. Zero/constant
 // words fold at compile time.
 // ---------------------------------------------------------------------------
-DFI uint64_t fold(uint32_t mix, int64_t idx) {
+DFI uint64_t fold(uint32_t mix, int32_t idx) {
     const uint32_t x = (mix ^ ((uint32_t)idx * 0x85EBCA77u)) * 0xC2B2AE3Du;
     return (uint64_t)(x ^ (x >> 15));
 }
@@ -332,7 +333,7 @@ DFI unsigned lanes_below(int lane) { return (1u << lane) - 1u; }
 // one record at absolute log index idx from this lane (batched phases: every
 // lane owns a record at a position fixed by prefix counts); returns its digest
 // term (0 when inactive) for the caller's one warp-sum per batch
-DFI uint64_t lane_rec(Pt& p, bool act, int64_t idx, int kind, int layer, int i0, int i1, int i2, int i3, int i4,
+DFI uint64_t lane_rec(Pt& p, bool act, int32_t idx, int kind, int layer, int i0, int i1, int i2, int i3, int i4,
                       int64_t t0, int64_t t1, int64_t t2, double x0) {
     if (!act) return 0;
     if (p.full) {
@@ -679,7 +680,7 @@ DFI void settle_uniform(Pt& p) {
             p.rs[ident] = rs_make(wp, slot);
             p.res_ident[slot] = (int16_t)ident;
             if (p.hist[ident] == -2) p.hist[ident] = -1;
-            const uint64_t st = p.seq + (uint64_t)i;            // note_admit, in pop order
+            const uint64_t st = (uint64_t)(p.seq + (uint32_t)i);   // note_admit, in pop order
             uint64_t nk = 0;
             if (p.pol == ESIM_EV_LRU) nk = st;
             else if (p.pol == ESIM_EV_LS) nk = LS_CURRENT | st;
@@ -696,7 +697,7 @@ DFI void settle_uniform(Pt& p) {
     if (p.full) err_fold(p);
     __syncwarp();
     const int64_t nb = p.eb_w;
-    p.seq += (uint64_t)k;
+    p.seq += (uint32_t)k;
     p.fs_top -= k;
     p.qh += k;
     if (p.qh >= p.Q) p.qh -= p.Q;
@@ -1070,7 +1071,7 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
     }
     const int started = F + r, dropped = nt - started;
     if (p.qn + started > p.Q) { p.err = STATUS_QUEUE_OVERFLOW; return; }
-    const int64_t base = p.n_recs;
+    const int32_t base = p.n_recs;
     uint64_t dg = 0;
     for (int b = 0; b < nt; b += 32) {
         const int t = b + p.lane;
@@ -1081,7 +1082,7 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
         const bool ev_rec = act && t >= F && t < started;
         const bool st = act && t < started;
         const bool dr = act && t >= started;
-        const int64_t ri = base + (t < F ? t : (t < started ? F + 2 * (t - F) : F + 2 * r + (t - started)));
+        const int32_t ri = base + (t < F ? t : (t < started ? F + 2 * (t - F) : F + 2 * r + (t - started)));
         int vid = 0, vslot = 0;
         if (ev_rec) { vslot = p.vict[t - F]; vid = p.res_ident[vslot]; }
         const int vl = ediv(p, vid);
@@ -1158,7 +1159,7 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
         if (p.pol == ESIM_EV_LS) {
             const bool touch = res && !(p.key[rs_slot(w)] & LS_CURRENT);
             const unsigned tm = __ballot_sync(FULL, touch);
-            if (touch) p.key[rs_slot(w)] = LS_CURRENT | (p.seq + __popc(tm & below));
+            if (touch) p.key[rs_slot(w)] = LS_CURRENT | (uint64_t)(p.seq + __popc(tm & below));
             p.seq += __popc(tm);
         }
         const unsigned hm = __ballot_sync(FULL, res || inf);
