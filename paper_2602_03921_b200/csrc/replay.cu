@@ -146,7 +146,7 @@ struct Pt {
     int64_t dur0, dur1, dur2, dur3, eb0, eb1, eb2, eb3;   // by precision code (registers, not an array)
     int64_t dur_w, eb_w;            // working precision
     int wp;                         // working precision code (cfg->working_prec, kept in a register)
-    double inv_dur, inv_eb;         // 1 / dur_w, 1 / eb_w (uniform-path quotients)
+    double inv_dur;                 // 1 / dur_w (uniform-path landing count)
     bool uniform;                   // all transfers at the working precision (common path)
     // shared memory
     uint64_t* key;
@@ -177,7 +177,8 @@ struct Pt {
     uint8_t* tofetch;
     uint8_t* ca_mod;
     // warp-uniform scalars
-    int64_t now, resident_bytes, reserved_bytes;
+    int64_t now, resident_bytes, reserved_bytes;   // general path: bytes
+    int32_t res_u, resv_u, cap_u;   // uniform path: resident / reserved experts and the experts capacity holds
     int qh, qn, nA, fs_top;
     uint32_t seq;                   // policy stamp counter (< SEQ_LIMIT < 2^31: checked once per layer)
     uint64_t digest;                // lane-partial sum of lane-parallel records' terms
@@ -218,6 +219,20 @@ DFI int64_t udiv_rcp(int64_t x, int64_t d, double inv) {
     if (q * d > x) q--;
     else if ((q + 1) * d <= x) q++;
     return q;
+}
+
+// Cache byte accounting (engine.py:188-255). On the uniform path every resident
+// or reserved entry is one working-precision expert, so it is counted in expert
+// units (32-bit) against cap_u = capacity / expert bytes -- exact: a fetch fits
+// iff units + 1 <= floor(capacity / bytes); the general path keeps bytes.
+DFI bool no_room(const Pt& p, int64_t nb) {
+    return p.uniform ? p.res_u + p.resv_u >= p.cap_u : p.cap - p.resident_bytes - p.reserved_bytes < nb;
+}
+DFI void reserve_add(Pt& p, int64_t nb, int n) {
+    if (p.uniform) p.resv_u += n; else p.reserved_bytes += nb * n;
+}
+DFI void resident_add(Pt& p, int64_t nb, int n) {
+    if (p.uniform) p.res_u += n; else p.resident_bytes += nb * n;
 }
 
 DFI int ediv(const Pt& p, int ident) {             // ident / E, exact for ident < 2^24
@@ -522,7 +537,7 @@ DFI int select_victim(Pt& p, bool forced) {
 DFI void evict(Pt& p, int slot, int cause, bool forced) {                 // engine.py:451-460
     const int ident = p.res_ident[slot];
     const int prec = rs_prec(p.rs[ident]);
-    p.resident_bytes -= peb(p, prec);
+    resident_add(p, peb(p, prec), -1);
     __syncwarp();
     if (p.lane == 0) {
         p.rs[ident] = 0;
@@ -704,14 +719,14 @@ DFI void settle_uniform(Pt& p) {
     p.qn -= k;
     p.qc0 += (int64_t)k * p.dur_w;
     p.nA = p.nA > k ? p.nA - k : 0;
-    p.reserved_bytes -= nb * k;
-    p.resident_bytes += nb * k;
+    reserve_add(p, nb, -k);
+    resident_add(p, nb, k);
     p.n_recs += npf;
     p.pf_ev[2] += npf;
     // byte-accounting invariant (engine.py:216-236): checked on the general path
     // and in full-log runs (the parity tests); the uniform sweep kernels hold it
     // by construction (every landing was reserved)
-    if ((!p.uniform || p.full) && p.resident_bytes + p.reserved_bytes > p.cap && !p.err) p.err = -2;
+    if (p.full && p.res_u + p.resv_u > p.cap_u && !p.err) p.err = -2;
 }
 
 DFI void settle(Pt& p) {                                                   // engine.py:422-442
@@ -760,12 +775,12 @@ DFI void advance_to(Pt& p, int64_t t) {
 // _fetch (engine.py:463-510): blocked us, or -1 for None
 DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
     const int64_t nb = peb(p, prec);
-    if (nb > p.cap) {
+    if (p.uniform ? p.cap_u < 1 : nb > p.cap) {
         if (!final) return -1;
         p.err = -1;
         return 0;
     }
-    while (p.cap - p.resident_bytes - p.reserved_bytes < nb && !p.err) {
+    while (no_room(p, nb) && !p.err) {
         const int v = select_victim(p, final);
         if (v >= 0) { evict(p, v, 0, final); continue; }
         if (!final) return -1;
@@ -773,7 +788,7 @@ DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
             const QEntry e = q_load(p, p.qn - 1);
             __syncwarp();
             p.qn--;
-            p.reserved_bytes -= peb(p, (e.flags >> 2) & 3);
+            reserve_add(p, peb(p, (e.flags >> 2) & 3), -1);
             if (p.lane == 0) p.rs[e.ident] = 0;
             __syncwarp();
             const int il = ediv(p, e.ident);
@@ -785,7 +800,7 @@ DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
         advance_to(p, nd > p.now ? nd : p.now);
     }
     if (p.err) return 0;
-    p.reserved_bytes += nb;
+    reserve_add(p, nb, 1);
     const int at = p.qn > 0 ? 1 + p.nA : 0;
     if (!q_open(p, at)) return 0;
     QEntry e;
@@ -984,8 +999,8 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
 DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int target) {
     const int64_t nb = p.eb_w;
     const int wp = p.wp;
-    const int64_t freeb = p.cap - p.resident_bytes - p.reserved_bytes;
-    int64_t room = freeb <= 0 ? 0 : udiv_rcp(freeb, nb, p.inv_eb);
+    int room = p.cap_u - p.res_u - p.resv_u;       // expert units (uniform path)
+    if (room < 0) room = 0;
     const int F = nt < room ? nt : (int)room;
     const int need = nt - F;
     int r = 0;
@@ -1110,8 +1125,8 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
     if (p.qn == 0 && started > 0) p.qc0 = p.now + p.dur_w;
     p.qn += started;
     p.fs_top += r;
-    p.resident_bytes -= nb * r;
-    p.reserved_bytes += nb * started;
+    resident_add(p, nb, -r);
+    reserve_add(p, nb, started);
     p.n_evict += r;
     p.pf_ev[1] += started;
     p.pf_ev[4] += dropped;
@@ -1182,14 +1197,14 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
         const float sc = ps[j];
         const int ident = target * p.E + e;
         bool refused = false;
-        while (p.cap - p.resident_bytes - p.reserved_bytes < nb) {
+        while (no_room(p, nb)) {
             const int v = select_victim(p, false);
             if (v < 0) { rec_prefetch(p, 4, target, e, p.now, sc, 3); refused = true; break; }
             evict(p, v, 1, false);
         }
         if (refused) continue;
         if (p.qn >= p.Q) { p.err = STATUS_QUEUE_OVERFLOW; return; }
-        p.reserved_bytes += nb;
+        reserve_add(p, nb, 1);
         QEntry q;
         q.ident = (int16_t)ident; q.flags = (uint8_t)(1 | (wp << 2)); q.score = sc; q.submit = p.now;
         int64_t start = p.now;
@@ -1354,7 +1369,6 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     p.eb_w = ebs[cfg->working_prec & 3];
     p.dur_w = durs[cfg->working_prec & 3];
     p.inv_dur = p.dur_w > 0 ? 1.0 / (double)p.dur_w : 0.0;
-    p.inv_eb = p.eb_w > 0 ? 1.0 / (double)p.eb_w : 0.0;
     // residents + queued transfers <= capacity / (smallest expert this point can admit):
     // only fetch_low / fetch_priority ever admit below the working precision
     if (p.miss != ESIM_MISS_FETCH_LOW && p.miss != ESIM_MISS_FETCH_PRIORITY) minb = peb(p, cfg->working_prec);
@@ -1405,6 +1419,9 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     }
     __syncwarp();
     p.now = 0; p.resident_bytes = 0; p.reserved_bytes = 0;
+    p.res_u = 0; p.resv_u = 0;
+    p.cap_u = p.uniform ? (int32_t)((p.eb_w > 0 ? p.cap / p.eb_w : 0) < 0x7FFFFFFF ? (p.eb_w > 0 ? p.cap / p.eb_w : 0)
+                                                                                  : 0x7FFFFFFF) : 0;
     p.qh = 0; p.qn = 0; p.nA = 0; p.fs_top = p.S; p.seq = 0; p.qc0 = 0;
     p.einv = ((1ull << 32) + (uint64_t)p.E - 1) / (uint64_t)p.E;
     p.digest = 0ull; p.digest_u = FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
