@@ -171,7 +171,7 @@ struct Pt {
     int16_t* hist;
     int16_t* res_ident;
     uint16_t* fs;
-    uint64_t* q_ent;                // channel ring: ident:16 | flags:8 (bits 16-23) | score f32 (bits 32-63)
+    uint2* q_ent;                   // channel ring: .x = ident:16 | flags:8 (bits 16-23), .y = score f32 bits
     int16_t* ca_sel;
     int16_t* vict;                  // sweep-2 victims in eviction order (uniform instances)
     uint8_t* tofetch;
@@ -559,12 +559,12 @@ DFI void evict(Pt& p, int slot, int cause, bool forced) {                 // eng
 // ---------------------------------------------------------------------------
 struct QEntry { int16_t ident; uint8_t flags; float score; int64_t submit, comp; };
 
-DFI uint64_t qe_make(int16_t ident, uint8_t flags, float score) {
-    return (uint64_t)(uint16_t)ident | ((uint64_t)flags << 16) | ((uint64_t)__float_as_uint(score) << 32);
+DFI uint2 qe_make(int16_t ident, uint8_t flags, float score) {         // one 8-byte smem access, 32-bit ops
+    return make_uint2((uint32_t)(uint16_t)ident | ((uint32_t)flags << 16), __float_as_uint(score));
 }
-DFI int16_t qe_ident(uint64_t w) { return (int16_t)(uint16_t)w; }
-DFI uint8_t qe_flags(uint64_t w) { return (uint8_t)(w >> 16); }
-DFI float qe_score(uint64_t w) { return __uint_as_float((uint32_t)(w >> 32)); }
+DFI int16_t qe_ident(uint2 w) { return (int16_t)(uint16_t)w.x; }
+DFI uint8_t qe_flags(uint2 w) { return (uint8_t)(w.x >> 16); }
+DFI float qe_score(uint2 w) { return __uint_as_float(w.y); }
 
 // The queue is settled whenever it is touched (every entry has comp > now >=
 // its submit time: settle() lands comp <= now from the head after every time
@@ -579,7 +579,7 @@ DFI int64_t qcomp(const Pt& p, int i) {
 DFI QEntry q_load(const Pt& p, int i) {
     const int x = qphys(p, i);
     QEntry e;
-    const uint64_t w = p.q_ent[x];
+    const uint2 w = p.q_ent[x];
     e.ident = qe_ident(w); e.flags = qe_flags(w); e.score = qe_score(w);
     if (!p.uniform) { e.submit = p.q_submit[x]; e.comp = p.q_comp[x]; }
     return e;
@@ -687,7 +687,7 @@ DFI void settle_uniform(Pt& p) {
         float score = 0.0f;
         if (act) {
             const int x = qphys(p, i);
-            const uint64_t w = p.q_ent[x];
+            const uint2 w = p.q_ent[x];
             ident = qe_ident(w);
             pf = qe_flags(w) & 1;
             score = qe_score(w);
@@ -735,7 +735,7 @@ DFI void settle(Pt& p) {                                                   // en
         const int h = p.qh;
         const int64_t comp = qcomp(p, 0);
         if (comp > p.now) break;
-        const uint64_t w = p.q_ent[h];
+        const uint2 w = p.q_ent[h];
         const int ident = qe_ident(w);
         const uint8_t fl = qe_flags(w);
         const float score = qe_score(w);
@@ -1398,7 +1398,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     p.hist = reinterpret_cast<int16_t*>(base + lay.hist);
     p.res_ident = reinterpret_cast<int16_t*>(base + lay.res_ident);
     p.fs = reinterpret_cast<uint16_t*>(base + lay.fs);
-    p.q_ent = reinterpret_cast<uint64_t*>(base + lay.q_ent);
+    p.q_ent = reinterpret_cast<uint2*>(base + lay.q_ent);
     p.ca_sel = reinterpret_cast<int16_t*>(base + lay.ca_sel);
     p.vict = reinterpret_cast<int16_t*>(base + lay.vict);
     p.tofetch = base + lay.tofetch;
