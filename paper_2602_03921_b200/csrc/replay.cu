@@ -671,8 +671,15 @@ DFI void settle_uniform(Pt& p) {
     if (p.qn == 0 || p.qc0 > p.now) return;
     int k = p.qn;
     if (p.dur_w > 0) {
-        const int64_t t = udiv_rcp(p.now - p.qc0, p.dur_w, p.inv_dur) + 1;
-        if (t < k) k = (int)t;
+        // entry i has landed iff i * dur <= now - qc0: one compare per lane for
+        // the usual <= 32 entries, the quotient beyond
+        const int64_t d = p.now - p.qc0;
+        if (p.qn <= 32) {
+            k = __popc(__ballot_sync(FULL, p.lane < p.qn && (int64_t)p.lane * p.dur_w <= d));
+        } else {
+            const int64_t t = udiv_rcp(d, p.dur_w, p.inv_dur) + 1;
+            if (t < k) k = (int)t;
+        }
     }
     if (p.fs_top < k) { p.err = -2; return; }
     const int wp = p.wp;
@@ -987,6 +994,43 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
     return 1;
 }
 
+// sweep 2's victims for <= 128 slots: the `need` smallest keys in ascending
+// order (LS: stale ones only), written to p.vict; K = the key width
+template <typename K>
+DFI int merge_victims(Pt& p, int need, K FREE, bool& refusals) {
+    K kk[4];
+    int ss[4];
+    #pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int sl = p.lane + 32 * j;
+        kk[j] = sl < p.S ? (sizeof(K) == 8 ? (K)p.key[sl] : (K)reinterpret_cast<const uint32_t*>(p.key)[2 * sl]) : FREE;
+        ss[j] = sl;
+    }
+    auto cx = [&](int a, int b) {
+        const bool sw = kk[b] < kk[a];
+        const K ka = kk[a], kb = kk[b];
+        const int sa = ss[a], sb = ss[b];
+        kk[a] = sw ? kb : ka; kk[b] = sw ? ka : kb;
+        ss[a] = sw ? sb : sa; ss[b] = sw ? sa : sb;
+    };
+    cx(0, 1); cx(2, 3); cx(0, 2); cx(1, 3); cx(1, 2);
+    int r = 0;
+    while (r < need) {
+        const K m = sizeof(K) == 8 ? (K)warp_min_u64((uint64_t)kk[0]) : (K)__reduce_min_sync(FULL, (uint32_t)kk[0]);
+        if (m == FREE) break;                                         // no resident left: no_space drops
+        if (p.pol == ESIM_EV_LS && ((uint64_t)m & LS_CURRENT)) { refusals = true; break; }
+        const int wl = __ffs(__ballot_sync(FULL, kk[0] == m)) - 1;
+        const int vs = __shfl_sync(FULL, ss[0], wl);
+        if (p.lane == 0) p.vict[r] = (int16_t)vs;
+        r++;
+        if (p.lane == wl) {
+            kk[0] = kk[1]; kk[1] = kk[2]; kk[2] = kk[3]; kk[3] = FREE;
+            ss[0] = ss[1]; ss[1] = ss[2]; ss[2] = ss[3];
+        }
+    }
+    return r;
+}
+
 // Watchdog sweep 2 (prefetch.py:199-221) for uniform instances under LRU / LS /
 // LFU / LHU, batched. Every candidate needs exactly one expert's bytes, so the
 // first `room` candidates start without evicting; each later one evicts the
@@ -1039,37 +1083,9 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
             // <= 4 slots per lane: each lane sorts its keys once (a 5-exchange
             // network in registers); the victims are then a 32-way merge of the
             // lanes' sorted lists -- the winner shifts its list instead of
-            // rescanning its slots for the next key
-            uint64_t kk[4];
-            int ss[4];
-            #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const int sl = p.lane + 32 * j;
-                const bool in = sl < p.S;
-                kk[j] = in ? (wide ? p.key[sl] : (uint64_t)k32[2 * sl]) : FREE;
-                ss[j] = sl;
-            }
-            auto cx = [&](int a, int b) {
-                const bool sw = kk[b] < kk[a];
-                const uint64_t ka = kk[a], kb = kk[b];
-                const int sa = ss[a], sb = ss[b];
-                kk[a] = sw ? kb : ka; kk[b] = sw ? ka : kb;
-                ss[a] = sw ? sb : sa; ss[b] = sw ? sa : sb;
-            };
-            cx(0, 1); cx(2, 3); cx(0, 2); cx(1, 3); cx(1, 2);
-            while (r < need) {
-                const uint64_t m = wide ? warp_min_u64(kk[0]) : (uint64_t)__reduce_min_sync(FULL, (uint32_t)kk[0]);
-                if (m == FREE) break;                                 // no resident left: no_space drops
-                if (p.pol == ESIM_EV_LS && (m & LS_CURRENT)) { refusals = true; break; }
-                const int wl = __ffs(__ballot_sync(FULL, kk[0] == m)) - 1;
-                const int vs = __shfl_sync(FULL, ss[0], wl);
-                if (p.lane == 0) p.vict[r] = (int16_t)vs;
-                r++;
-                if (p.lane == wl) {
-                    kk[0] = kk[1]; kk[1] = kk[2]; kk[2] = kk[3]; kk[3] = FREE;
-                    ss[0] = ss[1]; ss[1] = ss[2]; ss[2] = ss[3];
-                }
-            }
+            // rescanning its slots for the next key (LRU / LS: 32-bit keys)
+            if (wide) r = merge_victims<uint64_t>(p, need, KEY_FREE, refusals);
+            else r = merge_victims<uint32_t>(p, need, 0xFFFFFFFFu, refusals);
         } else {
             while (r < need) {
                 const uint64_t m = wide ? warp_min_u64(lk) : (uint64_t)__reduce_min_sync(FULL, (uint32_t)lk);
