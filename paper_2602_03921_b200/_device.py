@@ -293,7 +293,9 @@ class ReplayBatch:
         self.dtraces: dict = {}
         self.stream = stream
         streams = {}
+        from .engine import check_geometry
         for cfg, tr in zip(self.cfgs, self.traces):
+            check_geometry(cfg, tr)
             key = id(tr)
             if key not in self.dtraces:
                 self.dtraces[key] = getattr(tr, "_device", None) or DeviceTrace(tr.packed())

@@ -556,6 +556,8 @@ extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const Es
     P->prefix.assign(n_traces + 1, 0);
     for (int t = 0; t < n_traces; t++) {
         const EsimTraceDesc& d = traces[t];
+        if ((int64_t)d.n_events * d.experts >= ((int64_t)1 << 31))           // 32-bit event indices in the replay
+            return bail(fail(-1, "trace too long for the device replay: passes x layers x experts must be < 2^31"));
         P->small_off[t] = P->small_bytes;
         P->small_bytes += al256(d.n_passes * 4) * 2 + al256((d.n_events + 1) * 8);
         P->prefix[t + 1] = P->prefix[t] + d.n_events;

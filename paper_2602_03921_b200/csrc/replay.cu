@@ -1151,10 +1151,10 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
 }
 
 // _submit_prefetches + watchdog_step (engine.py:651-725, prefetch.py:163-221)
-DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int64_t tev) {
+DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int tev) {   // tev < 2^31 / E events
     const int target = p.layer + 1;
     const int n = R.n_pred[tev];
-    const int32_t* pe = R.pred_expert + tev * p.E;
+    const int32_t* pe = R.pred_expert + tev * p.E;      // 32-bit index products (< 2^31)
     const float* ps = R.pred_score + tev * p.E;
     // PredictionRec: fixed by the router output (digest word from the summary;
     // the per-layer predicted-set sizes are added from it at the end)
@@ -1475,7 +1475,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
         for (int l = 0; l < p.L && !p.err; l++) {
             p.layer = l;
             if (p.seq > SEQ_LIMIT) { p.err = STATUS_SEQ_OVERFLOW; break; }
-            const int64_t ev = (int64_t)pass * p.L + l;
+            const int ev = pass * p.L + l;                        // events and ev * E stay below 2^31
             settle(p);
             const int T = (int)(tr.row_offset[ev + 1] - tr.row_offset[ev]);
             int nd;

@@ -137,6 +137,8 @@ def check_geometry(config: SimConfig, trace) -> None:
         raise ConfigError(
             f"trace geometry (L={s.num_layers}, E={s.experts_per_layer}, k={s.top_k}) does not "
             f"match the model (L={m.num_layers}, E={m.experts_per_layer}, k={m.top_k})")
+    if trace.num_passes * s.num_layers * s.experts_per_layer >= 2**31:
+        raise ConfigError("trace too long for the device replay: passes x layers x experts must be < 2^31")
 
 
 @dataclass

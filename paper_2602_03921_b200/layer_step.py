@@ -292,6 +292,8 @@ class LayerStepEngine:
         """One request. keep_outputs: the last layer's hidden states of every
         pass (res.out); keep_layers: every layer's (res.layers, [events] list of
         [T, H] bf16 host tensors, events in (pass, layer) order)."""
+        from .engine import check_geometry
+        check_geometry(self.cfg, trace)
         torch = self.torch
         pk = trace.packed()
         cap = None
