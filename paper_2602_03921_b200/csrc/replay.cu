@@ -181,8 +181,8 @@ struct Pt {
     int32_t res_u, resv_u, cap_u;   // uniform path: resident / reserved experts and the experts capacity holds
     int qh, qn, nA, fs_top;
     uint32_t seq;                   // policy stamp counter (< SEQ_LIMIT < 2^31: checked once per layer)
-    uint64_t digest;                // lane-partial sum of lane-parallel records' terms
-    uint64_t digest_u;              // warp-uniform records' terms (every lane holds the same sum)
+    uint32_t digest;                // lane-partial sum (mod 2^32) of lane-parallel records' terms
+    uint32_t digest_u;              // warp-uniform records' terms (every lane holds the same sum)
     bool digest_on;
     uint32_t pf_ev[5];              // prefetch submitted/started/completed/skipped/dropped (registers)
     uint32_t n_evict, n_forced;
@@ -269,14 +269,14 @@ DFI void ps_add(Pt& p, int which, double x) {
 // digest: mix = sum_i w_i * K_i (mod 2^32) over the record's sixteen 32-bit
 // words (t0 skipped for predictions) + sum_j (e_j+1) * G*(j+1) over a
 // prediction's experts; x = (mix ^ idx*C) * P mod 2^32 (idx = record index);
-// digest += x ^ (x >> 15), a 32-bit term summed into the 64-bit digest (all
-// 32-bit operations: the fold sits on every record's path). The index makes it
+// digest += x ^ (x >> 15) mod 2^32 (all 32-bit operations: the fold sits on
+// every record's path). The index makes it
 // order-sensitive, the sum keeps the loop-carried chain one add. Zero/constant
 // words fold at compile time.
 // ---------------------------------------------------------------------------
-DFI uint64_t fold(uint32_t mix, int32_t idx) {
+DFI uint32_t fold(uint32_t mix, int32_t idx) {
     const uint32_t x = (mix ^ ((uint32_t)idx * 0x85EBCA77u)) * 0xC2B2AE3Du;
-    return (uint64_t)(x ^ (x >> 15));
+    return x ^ (x >> 15);
 }
 
 // record with its digest word already mixed (premixed: from the router summary)
@@ -320,7 +320,7 @@ DFI void emit_lanes(Pt& p, bool act, int rank, int cnt, int kind, int layer, int
                     int i4, int64_t t0, int64_t t1, int64_t t2, double x0) {
     if (cnt == 0) return;
     if (p.digest_on) {
-        uint64_t v = 0;
+        uint32_t v = 0;
         if (act) {
             v = fold(rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0), p.n_recs + rank);
         }
@@ -348,7 +348,7 @@ DFI unsigned lanes_below(int lane) { return (1u << lane) - 1u; }
 // one record at absolute log index idx from this lane (batched phases: every
 // lane owns a record at a position fixed by prefix counts); returns its digest
 // term (0 when inactive) for the caller's one warp-sum per batch
-DFI uint64_t lane_rec(Pt& p, bool act, int32_t idx, int kind, int layer, int i0, int i1, int i2, int i3, int i4,
+DFI uint32_t lane_rec(Pt& p, bool act, int32_t idx, int kind, int layer, int i0, int i1, int i2, int i3, int i4,
                       int64_t t0, int64_t t1, int64_t t2, double x0) {
     if (!act) return 0;
     if (p.full) {
@@ -365,7 +365,7 @@ DFI uint64_t lane_rec(Pt& p, bool act, int32_t idx, int kind, int layer, int i0,
     return p.digest_on ? fold(rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0), idx) : 0;
 }
 
-DFI void digest_add_warp(Pt& p, uint64_t v) {        // this lane's records of a batch (lane-partial digest)
+DFI void digest_add_warp(Pt& p, uint32_t v) {        // this lane's records of a batch (lane-partial digest)
     if (!p.digest_on) return;
     p.digest += v;
 }
@@ -684,7 +684,7 @@ DFI void settle_uniform(Pt& p) {
     if (p.fs_top < k) { p.err = -2; return; }
     const int wp = p.wp;
     const unsigned below = lanes_below(p.lane);
-    uint64_t dg = 0;
+    uint32_t dg = 0;
     int npf = 0;
     for (int b = 0; b < k; b += 32) {
         const int i = b + p.lane;
@@ -1103,7 +1103,7 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
     const int started = F + r, dropped = nt - started;
     if (p.qn + started > p.Q) { p.err = STATUS_QUEUE_OVERFLOW; return; }
     const int32_t base = p.n_recs;
-    uint64_t dg = 0;
+    uint32_t dg = 0;
     for (int b = 0; b < nt; b += 32) {
         const int t = b + p.lane;
         const bool act = t < nt;
@@ -1440,7 +1440,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
                                                                                   : 0x7FFFFFFF) : 0;
     p.qh = 0; p.qn = 0; p.nA = 0; p.fs_top = p.S; p.seq = 0; p.qc0 = 0;
     p.einv = ((1ull << 32) + (uint64_t)p.E - 1) / (uint64_t)p.E;
-    p.digest = 0ull; p.digest_u = FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
+    p.digest = 0u; p.digest_u = (uint32_t)FNV_OFFSET; p.n_recs = 0; p.n_pe = 0;
     p.n_evict = 0; p.n_forced = 0;
     p.lc_miss = p.lc_c0 = p.lc_c1 = p.lc_drop = p.lc_sub = 0;
     #pragma unroll
