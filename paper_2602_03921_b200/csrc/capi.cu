@@ -139,6 +139,11 @@ static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stri
     }
     if (s.S > 4095) return fail(-1, "more than 4095 resident experts per cache is not supported by the device directory");
     s.Q = queue_cap > 0 ? std::min(queue_cap, s.S + 1) : s.S + 1;
+    {                                  // the channel ring: a power of two (index wrap = one AND)
+        int q = 1;
+        while (q < s.Q) q <<= 1;
+        s.Q = q;
+    }
     s.Tmax = s.ca ? std::max(1, max_tokens) : 0;
     if (pl_stride < s.Lmax) return fail(-1, "per-layer stride smaller than num_layers");
     s.Lmax = pl_stride;

@@ -241,7 +241,7 @@ DFI int ediv(const Pt& p, int ident) {             // ident / E, exact for ident
 
 DFI int qphys(const Pt& p, int i) {
     int x = p.qh + i;
-    return x >= p.Q ? x - p.Q : x;
+    return x & (p.Q - 1);                          // Q is a power of two (replay_sizing)
 }
 
 // fire-and-forget shared-memory atomics: lane 0 never waits on a counter RMW
@@ -722,7 +722,7 @@ DFI void settle_uniform(Pt& p) {
     p.seq += (uint32_t)k;
     p.fs_top -= k;
     p.qh += k;
-    if (p.qh >= p.Q) p.qh -= p.Q;
+    p.qh &= p.Q - 1;
     p.qn -= k;
     p.qc0 += (int64_t)k * p.dur_w;
     p.nA = p.nA > k ? p.nA - k : 0;
@@ -752,7 +752,7 @@ DFI void settle(Pt& p) {                                                   // en
         const int slot = p.fs[p.fs_top - 1];
         __syncwarp();
         p.fs_top--;
-        p.qh = (p.qh + 1 == p.Q) ? 0 : p.qh + 1;
+        p.qh = (p.qh + 1) & (p.Q - 1);
         p.qn--;
         if (p.uniform) p.qc0 = comp + p.dur_w;       // the next entry's completion
         if (p.nA > 0) p.nA--;
