@@ -49,6 +49,9 @@ enum { ESIM_REC_ACCESS = 1, ESIM_REC_EVICT, ESIM_REC_PREFETCH, ESIM_REC_PREDICTI
 
 #define ESIM_FLAG_FULL_LOG 1   /* emit every EsimRec (else counters + digest only) */
 #define ESIM_FLAG_NO_DIGEST 2  /* skip the record-stream digest (counters only) */
+#define ESIM_FLAG_TIME32 4     /* caller-proven: the run's simulated clock stays below 2^31 us
+                                  (esim_time32_ok); launches whose points all carry it run
+                                  the 32-bit-clock replay kernels */
 #define ESIM_MAX_E 256         /* experts per layer supported by the device path */
 #define ESIM_MAX_K 16
 
@@ -156,6 +159,12 @@ const char *esim_last_error(void);
 int esim_host_register(void *ptr, size_t bytes);
 int esim_host_unregister(void *ptr);
 int esim_version(void);
+/* 1 if a replay of `cfg` over `trace` provably keeps its simulated clock below
+ * 2^31 us: trace events x compute_us + (demands + predictions) x the
+ * working-precision transfer time, with demands <= min(rows x top_k,
+ * events x experts) and predictions <= events x experts. The sweep plan sets
+ * ESIM_FLAG_TIME32 itself; a direct esim_replay_launch caller may set it. */
+int esim_time32_ok(const EsimConfig *cfg, const EsimTraceDesc *trace);
 /* Host-semantics switch: the builtin sum() of the interpreter the device
  * must match (RouteRec masses engine.py:630-631, report sums
  * metrics.py:168-180, 267-270): neumaier = 1 for CPython >= 3.12 (the

@@ -7,6 +7,7 @@ import numpy as np
 
 ESIM_FLAG_FULL_LOG = 1
 ESIM_FLAG_NO_DIGEST = 2
+ESIM_FLAG_TIME32 = 4
 ESIM_PL_FIELDS = 10
 ESIM_MAX_E = 256
 ESIM_MAX_K = 16

@@ -71,6 +71,7 @@ def lib():
         L.esim_version.restype = C.c_int
         L.esim_set_host_sum.argtypes = [i32]
         L.esim_miss_decide.argtypes = [vp, vp, vp, vp, vp]
+        L.esim_time32_ok.argtypes = [vp, vp]
         if L.esim_version() != 2:
             raise RuntimeError(f"{LIB_PATH}: C ABI version {L.esim_version()} != 2 (stale build)")
         _lib = L
@@ -320,6 +321,11 @@ class ReplayBatch:
             cc = cfg.to_c(skeys.index(skey), full_log)
             if not digest:
                 cc.flags |= _abi.ESIM_FLAG_NO_DIGEST
+            # common-path points whose simulated clock provably stays below 2^31 us
+            # replay on the 32-bit-clock kernels
+            if cc.miss == 0 and cc.routing == 0 and lib().esim_time32_ok(
+                    C.addressof(cc), C.addressof(self.sets[skeys.index(skey)][1].desc)):
+                cc.flags |= _abi.ESIM_FLAG_TIME32
             self.ccfg.append(cc)
         n = len(self.ccfg)
         self.Lmax = max(c.num_layers for c in self.ccfg)
@@ -330,7 +336,7 @@ class ReplayBatch:
         # in launch order)
         for i, c in enumerate(self.ccfg):
             general = c.miss != 0 or c.routing != 0
-            groups.setdefault((c.eviction, general), []).append(i)
+            groups.setdefault((c.eviction, general, bool(c.flags & _abi.ESIM_FLAG_TIME32)), []).append(i)
         # static order: longest estimated first (the trace's token-expert
         # selections); tune_order() re-sorts by measured replay times (opt-in)
         rows_k = {id(s_[1]): int(s_[1].pk.row_offset[-1]) * s_[1].pk.top_k for s_ in self.sets}

@@ -25,7 +25,7 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
                                     int policy, bool general, const int32_t* out_index = nullptr,
-                                    bool log_rt = true, int max_ctas = 0);
+                                    bool log_rt = true, int max_ctas = 0, bool time32 = false);
 int esim_replay_smem_bytes(int N, int S, int Q, int L, int E, int T, int K, bool ca, bool has_cnt, bool gen);
 
 static thread_local std::string g_err;
@@ -106,14 +106,29 @@ extern "C" int esim_router_launch(const EsimTraceDesc* tr, const EsimRouterOut* 
     return 0;
 }
 
-struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca, has_cnt; int policy; bool general; bool log_rt; };
+struct Sizing { int N, S, Q, Lmax, Emax, Tmax, Kmax; bool ca, has_cnt; int policy; bool general; bool log_rt; bool time32; };
+
+// the simulated clock's upper bound (see esim_time32_ok in the header)
+static bool time32_ok(const EsimConfig& c, const EsimTraceDesc& t) {
+    const int64_t bw = c.bandwidth, nb = c.expert_bytes[c.working_prec & 3];
+    const int64_t dur = (bw == 0 || nb == 0) ? 0 : (nb * 1000000 + bw - 1) / bw;
+    const int64_t ev = t.n_events, E = t.experts;
+    const int64_t dem = std::min<int64_t>((int64_t)t.n_rows_total * t.top_k, ev * E);
+    const int64_t lim = ((int64_t)1 << 31) - 1;
+    if (dur >= lim || c.compute_us >= lim || c.compute_us < 0) return false;
+    const double bound = (double)ev * (double)c.compute_us + (double)(dem + ev * E) * (double)dur;
+    return bound < (double)lim;
+}
+extern "C" int esim_time32_ok(const EsimConfig* cfg, const EsimTraceDesc* trace) {
+    return cfg && trace && time32_ok(*cfg, *trace) ? 1 : 0;
+}
 
 // queue_cap <= 0: the exact bound (resident slots + 1 entries: every queued
 // transfer holds a reservation of >= the smallest expert, so the channel can
 // never outgrow it). A positive cap trades shared memory for the risk of
 // status -5, which the caller resolves by re-launching with the bound.
 static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stride, int queue_cap, Sizing* z) {
-    Sizing s{0, 1, 2, 0, 0, 0, 0, false, false, n > 0 ? h[0].eviction : 0, false, false};
+    Sizing s{0, 1, 2, 0, 0, 0, 0, false, false, n > 0 ? h[0].eviction : 0, false, false, n > 0};
     for (int i = 0; i < n; i++) {
         const EsimConfig& c = h[i];
         if (c.experts > ESIM_MAX_E || c.top_k > ESIM_MAX_K) return fail(-1, "geometry exceeds device limits");
@@ -136,6 +151,7 @@ static int replay_sizing(const EsimConfig* h, int n, int max_tokens, int pl_stri
         if (c.eviction != s.policy) return fail(-1, "one replay launch replays one eviction policy (group the points)");
         if (c.miss != ESIM_MISS_FETCH || c.routing != ESIM_ROUTE_STANDARD) s.general = true;
         if (c.flags & (ESIM_FLAG_FULL_LOG | ESIM_FLAG_NO_DIGEST)) s.log_rt = true;   // else: digest-only kernel
+        if (!(c.flags & ESIM_FLAG_TIME32)) s.time32 = false;
     }
     if (s.S > 4095) return fail(-1, "more than 4095 resident experts per cache is not supported by the device directory");
     s.Q = queue_cap > 0 ? std::min(queue_cap, s.S + 1) : s.S + 1;
@@ -177,7 +193,7 @@ extern "C" int esim_replay_launch_ex(const EsimConfig* h_cfg, const EsimConfig* 
     cudaError_t e = esim_replay_launch_impl(d_cfg, n, d_traces, d_routers, d_counters, d_per_layer, d_recs, rec_cap,
                                             d_pexp, pe_cap, z.N, z.S, z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt,
                                             w, (cudaStream_t)stream, nullptr, z.policy, z.general, nullptr,
-                                            z.log_rt, max_ctas);
+                                            z.log_rt, max_ctas, z.time32);
     if (e != cudaSuccess) return cuda_fail(e, "replay launch");
     return 0;
 }
@@ -407,7 +423,8 @@ int slab_enqueue(SweepPlan* P, Slab& S, EsimCounters* counters, int64_t* per_lay
                                     (int64_t*)(base + P->pl_off), full ? (EsimRec*)(base + P->rec_off) : nullptr,
                                     P->rec_cap, full ? (int32_t*)(base + P->pe_off) : nullptr, P->pe_cap, z.N, z.S,
                                     z.Q, z.Lmax, z.Emax, z.Tmax, z.Kmax, z.has_cnt, w, S.gs[g], nullptr, z.policy,
-                                    z.general, (int32_t*)(base + P->idx_off) + b, z.log_rt, P->group_ctas[g]);
+                                    z.general, (int32_t*)(base + P->idx_off) + b, z.log_rt, P->group_ctas[g],
+                                    z.time32);
         if (e != cudaSuccess) return cuda_fail(e, "replay launch");
         cudaEventRecord(S.ge[g], S.gs[g]);
         cudaStreamWaitEvent(S.st, S.ge[g], 0);
@@ -517,7 +534,9 @@ extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const Es
     std::vector<int> order(n);
     for (int i = 0; i < n; i++) order[i] = i;
     auto gen_of = [&](int a) { return cfg[a].miss != ESIM_MISS_FETCH || cfg[a].routing != ESIM_ROUTE_STANDARD; };
-    auto grp_of = [&](int a) { return (gen_of(a) ? 16 : 0) + cfg[a].eviction; };
+    // common-path points whose clock provably stays below 2^31 us run the 32-bit-clock kernels
+    auto t32_of = [&](int a) { return !gen_of(a) && time32_ok(cfg[a], traces[cfg[a].trace_id]); };
+    auto grp_of = [&](int a) { return (gen_of(a) ? 32 : 0) + (t32_of(a) ? 16 : 0) + cfg[a].eviction; };
     auto cost_of = [&](int a) {
         const EsimTraceDesc& t = traces[cfg[a].trace_id];
         return (double)t.n_rows_total * t.top_k;
@@ -551,8 +570,10 @@ extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const Es
     }
     P->order = order;
     P->caller_cfg.assign(cfg, cfg + n);
+    for (int i = 0; i < n; i++)
+        if (t32_of(i)) P->caller_cfg[i].flags |= ESIM_FLAG_TIME32;
     P->pcfg.resize(n);
-    for (int i = 0; i < n; i++) P->pcfg[i] = cfg[order[i]];
+    for (int i = 0; i < n; i++) P->pcfg[i] = P->caller_cfg[order[i]];
     // slab layout: [small arrays of every trace][logits per trace][router outputs][tables][outputs]
     P->htr.assign(traces, traces + n_traces);
     P->small_off.resize(n_traces);

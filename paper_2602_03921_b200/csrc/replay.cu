@@ -30,6 +30,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 
 #include "../../include/specmd_b200.h"
@@ -137,21 +138,27 @@ DFI int rs_prec(uint16_t w) { return (w >> 13) & 3; }
 DFI int rs_slot(uint16_t w) { return w & 0x0FFF; }
 DFI uint16_t rs_make(int prec, int slot) { return (uint16_t)(RS_RES | (prec << 13) | slot); }
 
-struct Pt {
+// TM: the simulated-clock type -- int32_t when the host has bounded the run's
+// total time below 2^31 us (time32 launches), else int64_t
+template <typename TM>
+struct PtT {
+    using Tm = TM;
     const EsimConfig* c;
     int L, E, K, S, Q;
     int pol, lane;
     int miss;                       // ESIM_MISS_* (constant-folded in the simple specialisation)
     int64_t cap;
-    int64_t dur0, dur1, dur2, dur3, eb0, eb1, eb2, eb3;   // by precision code (registers, not an array)
-    int64_t dur_w, eb_w;            // working precision
+    TM dur0, dur1, dur2, dur3;      // transfer times by precision code (registers, not an array)
+    int64_t eb0, eb1, eb2, eb3;     // expert bytes by precision code
+    TM dur_w;                       // working precision
+    int64_t eb_w;
     int wp;                         // working precision code (cfg->working_prec, kept in a register)
     double inv_dur;                 // 1 / dur_w (uniform-path landing count)
     bool uniform;                   // all transfers at the working precision (common path)
     // shared memory
     uint64_t* key;
     int64_t *q_submit, *q_comp;     // non-uniform instances only
-    int64_t qc0;                    // uniform instances: completion time of the head entry
+    TM qc0;                         // uniform instances: completion time of the head entry
     uint64_t einv;                  // ceil(2^32 / E): ident / E as a multiply-high
     double* dsum;
     Ctr* ctr;
@@ -177,7 +184,8 @@ struct Pt {
     uint8_t* tofetch;
     uint8_t* ca_mod;
     // warp-uniform scalars
-    int64_t now, resident_bytes, reserved_bytes;   // general path: bytes
+    TM now;
+    int64_t resident_bytes, reserved_bytes;       // general path: bytes
     int32_t res_u, resv_u, cap_u;   // uniform path: resident / reserved experts and the experts capacity holds
     int qh, qn, nA, fs_top;
     uint32_t seq;                   // policy stamp counter (< SEQ_LIMIT < 2^31: checked once per layer)
@@ -203,10 +211,12 @@ struct Pt {
 
 // per-precision sizes; on the common path (miss=fetch) every transfer is at the working
 // precision, which `uniform` (a template constant after inlining) exploits
-DFI int64_t pdur(const Pt& p, int c) {
+template <class Pt>
+DFI typename Pt::Tm pdur(const Pt& p, int c) {
     if (p.uniform) return p.dur_w;
     return c == 0 ? p.dur0 : c == 1 ? p.dur1 : c == 2 ? p.dur2 : p.dur3;
 }
+template <class Pt>
 DFI int64_t peb(const Pt& p, int c) {
     if (p.uniform) return p.eb_w;
     return c == 0 ? p.eb0 : c == 1 ? p.eb1 : c == 2 ? p.eb2 : p.eb3;
@@ -225,33 +235,41 @@ DFI int64_t udiv_rcp(int64_t x, int64_t d, double inv) {
 // or reserved entry is one working-precision expert, so it is counted in expert
 // units (32-bit) against cap_u = capacity / expert bytes -- exact: a fetch fits
 // iff units + 1 <= floor(capacity / bytes); the general path keeps bytes.
+template <class Pt>
 DFI bool no_room(const Pt& p, int64_t nb) {
     return p.uniform ? p.res_u + p.resv_u >= p.cap_u : p.cap - p.resident_bytes - p.reserved_bytes < nb;
 }
+template <class Pt>
 DFI void reserve_add(Pt& p, int64_t nb, int n) {
     if (p.uniform) p.resv_u += n; else p.reserved_bytes += nb * n;
 }
+template <class Pt>
 DFI void resident_add(Pt& p, int64_t nb, int n) {
     if (p.uniform) p.res_u += n; else p.resident_bytes += nb * n;
 }
 
+template <class Pt>
 DFI int ediv(const Pt& p, int ident) {             // ident / E, exact for ident < 2^24
     return (int)(((uint64_t)(uint32_t)ident * p.einv) >> 32);
 }
 
+template <class Pt>
 DFI int qphys(const Pt& p, int i) {
     int x = p.qh + i;
     return x & (p.Q - 1);                          // Q is a power of two (replay_sizing)
 }
 
 // fire-and-forget shared-memory atomics: lane 0 never waits on a counter RMW
+template <class Pt>
 DFI void ctr_add(Pt& p, uint32_t& f, uint32_t v) {
     if (p.lane == 0) f += v;
 }
+template <class Pt>
 DFI void pl_add(Pt& p, int idx, int v) {
     if (p.lane == 0) p.pl[idx] += v;
 }
 
+template <class Pt>
 DFI void ps_add(Pt& p, int which, double x) {
     if (p.lane == 0) {
         double f = p.ctr->ps[2 * which], c = p.ctr->ps[2 * which + 1];
@@ -280,6 +298,7 @@ DFI uint32_t fold(uint32_t mix, int32_t idx) {
 }
 
 // record with its digest word already mixed (premixed: from the router summary)
+template <class Pt>
 DFI void emit_mixed(Pt& p, uint32_t mix, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0,
                     int64_t t1, int64_t t2, double x0, const int32_t* pe = nullptr, int npe = 0) {
     if (p.digest_on) {
@@ -308,6 +327,7 @@ DFI void emit_mixed(Pt& p, uint32_t mix, int kind, int layer, int i0, int i1, in
 }
 
 // record mixed here (digest.cuh; zero/constant words fold at compile time)
+template <class Pt>
 DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4, int64_t t0, int64_t t1,
               int64_t t2, double x0) {
     const uint32_t mix = p.digest_on ? rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0) : 0u;
@@ -316,6 +336,7 @@ DFI void emit(Pt& p, int kind, int layer, int i0, int i1, int i2, int i3, int i4
 
 // up to 32 records emitted at once, one per active lane (lane-varying fields),
 // in `rank` order after the records already emitted; cnt = number active
+template <class Pt>
 DFI void emit_lanes(Pt& p, bool act, int rank, int cnt, int kind, int layer, int i0, int i1, int i2, int i3,
                     int i4, int64_t t0, int64_t t1, int64_t t2, double x0) {
     if (cnt == 0) return;
@@ -348,6 +369,7 @@ DFI unsigned lanes_below(int lane) { return (1u << lane) - 1u; }
 // one record at absolute log index idx from this lane (batched phases: every
 // lane owns a record at a position fixed by prefix counts); returns its digest
 // term (0 when inactive) for the caller's one warp-sum per batch
+template <class Pt>
 DFI uint32_t lane_rec(Pt& p, bool act, int32_t idx, int kind, int layer, int i0, int i1, int i2, int i3, int i4,
                       int64_t t0, int64_t t1, int64_t t2, double x0) {
     if (!act) return 0;
@@ -365,16 +387,19 @@ DFI uint32_t lane_rec(Pt& p, bool act, int32_t idx, int kind, int layer, int i0,
     return p.digest_on ? fold(rec_mix(kind, p.pass_id, layer, i0, i1, i2, i3, i4, t0, t1, t2, x0), idx) : 0;
 }
 
+template <class Pt>
 DFI void digest_add_warp(Pt& p, uint32_t v) {        // this lane's records of a batch (lane-partial digest)
     if (!p.digest_on) return;
     p.digest += v;
 }
 
+template <class Pt>
 DFI void err_fold(Pt& p) {                       // a lane-local record-capacity error -> warp-uniform
     const int e = __reduce_min_sync(FULL, p.err);
     p.err = e;
 }
 
+template <class Pt>
 DFI void rec_prefetch(Pt& p, int ev, int target, int expert, int64_t t, float score, int reason) {
     emit(p, ESIM_REC_PREFETCH, p.layer, ev, target, expert, reason, 0, t, 0, 0, (double)score);
     p.pf_ev[ev]++;                  // ev is a compile-time constant at every call site
@@ -395,17 +420,20 @@ DFI uint64_t order_double(double d) {
     return (b >> 63) ? ~b : (b | (1ull << 63));
 }
 
+template <class Pt>
 DFI void set_key(Pt& p, int slot, uint64_t k) {
     if (p.lane == 0) p.key[slot] = k;
     __syncwarp();
 }
 
+template <class Pt>
 DFI void ls_touch(Pt& p, int slot) {                                  // eviction.py:245-250
     if (p.key[slot] & LS_CURRENT) return;                              // first touch fixed it
     __syncwarp();
     set_key(p, slot, LS_CURRENT | (p.seq++));
 }
 
+template <class Pt>
 DFI void note_admit(Pt& p, int slot, int ident) {
     uint64_t nk;
     switch (p.pol) {
@@ -418,6 +446,7 @@ DFI void note_admit(Pt& p, int slot, int ident) {
     set_key(p, slot, nk);
 }
 
+template <class Pt>
 DFI void note_access(Pt& p, int ident, int slot, bool has_gate, double gate, int prec) {
     switch (p.pol) {
     case ESIM_EV_LRU: set_key(p, slot, p.seq++); break;
@@ -455,6 +484,7 @@ DFI uint64_t warp_min_u64(uint64_t v) {         // two redux.sync (hi word, then
     return ((uint64_t)mhi << 32) | mlo;
 }
 
+template <class Pt>
 DFI int select_victim(Pt& p, bool forced) {
     const int c = p.layer;
     uint64_t best = ~0ull;
@@ -534,6 +564,7 @@ DFI int select_victim(Pt& p, bool forced) {
 // ---------------------------------------------------------------------------
 // cache
 // ---------------------------------------------------------------------------
+template <class Pt>
 DFI void evict(Pt& p, int slot, int cause, bool forced) {                 // engine.py:451-460
     const int ident = p.res_ident[slot];
     const int prec = rs_prec(p.rs[ident]);
@@ -571,11 +602,13 @@ DFI float qe_score(uint2 w) { return __uint_as_float(w.y); }
 // step), so comp_i = max(comp_{i-1}, submit_i) + dur_i (engine.py:283-288)
 // never idles for i >= 1. With one transfer size (the uniform instances) that
 // is comp_i = comp_0 + i * dur: only the head's completion time is stored.
-DFI int64_t qcomp(const Pt& p, int i) {
-    if (p.uniform) return p.qc0 + (int64_t)i * p.dur_w;
+template <class Pt>
+DFI typename Pt::Tm qcomp(const Pt& p, int i) {
+    if (p.uniform) return p.qc0 + (typename Pt::Tm)i * p.dur_w;
     return p.q_comp[qphys(p, i)];
 }
 
+template <class Pt>
 DFI QEntry q_load(const Pt& p, int i) {
     const int x = qphys(p, i);
     QEntry e;
@@ -584,6 +617,7 @@ DFI QEntry q_load(const Pt& p, int i) {
     if (!p.uniform) { e.submit = p.q_submit[x]; e.comp = p.q_comp[x]; }
     return e;
 }
+template <class Pt>
 DFI void q_store(Pt& p, int i, const QEntry& e) {
     const int x = qphys(p, i);
     p.q_ent[x] = qe_make(e.ident, e.flags, e.score);
@@ -591,6 +625,7 @@ DFI void q_store(Pt& p, int i, const QEntry& e) {
 }
 
 // open a hole at logical index `at` (shift [at, qn) right by one); false on overflow
+template <class Pt>
 DFI bool q_open(Pt& p, int at) {
     if (p.qn >= p.Q) { p.err = STATUS_QUEUE_OVERFLOW; return false; }
     for (int hi = p.qn; hi > at; hi -= 32) {
@@ -607,6 +642,7 @@ DFI bool q_open(Pt& p, int at) {
     return true;
 }
 
+template <class Pt>
 DFI void q_close(Pt& p, int at) {
     for (int lo = at + 1; lo < p.qn; lo += 32) {
         const int i = lo + p.lane;
@@ -622,6 +658,7 @@ DFI void q_close(Pt& p, int at) {
 
 // comp_i = max(comp_{i-1}, submit_i) + dur_i for i >= from >= 1 (engine.py:283-288):
 // a warp inclusive scan composing x -> max(x + a, b)
+template <class Pt>
 DFI void retime(Pt& p, int from) {
     if (p.uniform) return;                       // implied by qcomp()
     if (from < 1) from = 1;
@@ -653,6 +690,7 @@ DFI void retime(Pt& p, int from) {
     }
 }
 
+template <class Pt>
 DFI int q_find(const Pt& p, int ident) {
     for (int base = 0; base < p.qn; base += 32) {
         const int i = base + p.lane;
@@ -667,17 +705,19 @@ DFI int q_find(const Pt& p, int ident) {
 // the k entries landed by `now` are known up front and admitted lane-parallel:
 // slot = i-th pop of the free-slot stack, policy key stamp = seq + i, and the
 // prefetch "completed" records at the positions their order fixes.
+template <class Pt>
 DFI void settle_uniform(Pt& p) {
     if (p.qn == 0 || p.qc0 > p.now) return;
     int k = p.qn;
     if (p.dur_w > 0) {
         // entry i has landed iff i * dur <= now - qc0: one compare per lane for
         // the usual <= 32 entries, the quotient beyond
-        const int64_t d = p.now - p.qc0;
+        using Tm = typename Pt::Tm;
+        const Tm d = p.now - p.qc0;
         if (p.qn <= 32) {
-            k = __popc(__ballot_sync(FULL, p.lane < p.qn && (int64_t)p.lane * p.dur_w <= d));
+            k = __popc(__ballot_sync(FULL, p.lane < p.qn && (Tm)p.lane * p.dur_w <= d));
         } else {
-            const int64_t t = udiv_rcp(d, p.dur_w, p.inv_dur) + 1;
+            const int64_t t = udiv_rcp((int64_t)d, (int64_t)p.dur_w, p.inv_dur) + 1;
             if (t < k) k = (int)t;
         }
     }
@@ -712,7 +752,7 @@ DFI void settle_uniform(Pt& p) {
         const unsigned pm = __ballot_sync(FULL, pf);
         const int il = ediv(p, ident);
         dg += lane_rec(p, pf, p.n_recs + npf + __popc(pm & below), ESIM_REC_PREFETCH, p.layer, 2, il,
-                       ident - il * p.E, 0, 0, p.qc0 + (int64_t)i * p.dur_w, 0, 0, (double)score);
+                       ident - il * p.E, 0, 0, p.qc0 + (typename Pt::Tm)i * p.dur_w, 0, 0, (double)score);
         npf += __popc(pm);
     }
     digest_add_warp(p, dg);
@@ -724,7 +764,7 @@ DFI void settle_uniform(Pt& p) {
     p.qh += k;
     p.qh &= p.Q - 1;
     p.qn -= k;
-    p.qc0 += (int64_t)k * p.dur_w;
+    p.qc0 += (typename Pt::Tm)k * p.dur_w;
     p.nA = p.nA > k ? p.nA - k : 0;
     reserve_add(p, nb, -k);
     resident_add(p, nb, k);
@@ -736,11 +776,12 @@ DFI void settle_uniform(Pt& p) {
     if (p.full && p.res_u + p.resv_u > p.cap_u && !p.err) p.err = -2;
 }
 
+template <class Pt>
 DFI void settle(Pt& p) {                                                   // engine.py:422-442
     if (p.uniform) { settle_uniform(p); return; }
     while (p.qn > 0) {
         const int h = p.qh;
-        const int64_t comp = qcomp(p, 0);
+        const typename Pt::Tm comp = qcomp(p, 0);
         if (comp > p.now) break;
         const uint2 w = p.q_ent[h];
         const int ident = qe_ident(w);
@@ -774,12 +815,14 @@ DFI void settle(Pt& p) {                                                   // en
     }
 }
 
-DFI void advance_to(Pt& p, int64_t t) {
+template <class Pt>
+DFI void advance_to(Pt& p, typename Pt::Tm t) {
     p.now = t;
     settle(p);
 }
 
 // _fetch (engine.py:463-510): blocked us, or -1 for None
+template <class Pt>
 DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
     const int64_t nb = peb(p, prec);
     if (p.uniform ? p.cap_u < 1 : nb > p.cap) {
@@ -803,7 +846,7 @@ DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
             continue;
         }
         if (p.qn == 0) { p.err = -2; return 0; }
-        const int64_t nd = qcomp(p, 0);
+        const typename Pt::Tm nd = qcomp(p, 0);
         advance_to(p, nd > p.now ? nd : p.now);
     }
     if (p.err) return 0;
@@ -818,12 +861,13 @@ DFI int64_t do_fetch(Pt& p, int ident, float gate, int prec, bool final) {
     if (at == 0 && p.uniform) p.qc0 = e.comp;
     if (at > 0) p.nA++;
     retime(p, at);
-    const int64_t comp = qcomp(p, at);
-    const int64_t blocked = comp - p.now;
+    const typename Pt::Tm comp = qcomp(p, at);
+    const typename Pt::Tm blocked = comp - p.now;
     advance_to(p, comp);
     return blocked;
 }
 
+template <class Pt>
 DFI void access_rec(Pt& p, int expert, int tokens, int rank, int outcome, int mclass, int64_t blocked, double wd,
                     int prec, int sub) {
     emit(p, ESIM_REC_ACCESS, p.layer, expert, tokens, rank,
@@ -843,6 +887,7 @@ DFI void access_rec(Pt& p, int expert, int tokens, int rank, int outcome, int mc
 
 // the layer's access outcomes -> per-layer counters (totals[0..7] are their sums,
 // formed at the end); n = the layer's demands, blocked = their summed blocked time
+template <class Pt>
 DFI void flush_layer_counts(Pt& p, int layer, int n, int64_t blocked) {
     if (p.lane == 0) {
         int32_t* pl = p.pl + layer * ESIM_PL_FIELDS;
@@ -874,6 +919,7 @@ DFI float warp_nearest_rank(const float* v, int n, long rank, int lane) {
 }
 
 // _handle_demand + resolve_miss: outcome 0 hit 1 fetch 2 wait 3 drop 4 subst, -1 error
+template <class Pt>
 DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, int tokens, int nd,
                       int64_t& blocked, double& wd) {
     const EsimConfig* cfg = p.c;
@@ -912,7 +958,7 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
             retime(p, min(idx, at));
         }
         const int prec = (e.flags >> 2) & 3;
-        const int64_t comp = qcomp(p, at);
+        const typename Pt::Tm comp = qcomp(p, at);
         blocked = comp - p.now;
         advance_to(p, comp);
         const int slot = rs_slot(p.rs[ident]);
@@ -996,7 +1042,7 @@ DFI int handle_demand(Pt& p, int expert, int rank, float gate, double summed, in
 
 // sweep 2's victims for <= 128 slots: the `need` smallest keys in ascending
 // order (LS: stale ones only), written to p.vict; K = the key width
-template <typename K>
+template <typename K, class Pt>
 DFI int merge_victims(Pt& p, int need, K FREE, bool& refusals) {
     K kk[4];
     int ss[4];
@@ -1040,6 +1086,7 @@ DFI int merge_victims(Pt& p, int need, K FREE, bool& refusals) {
 // left the rest are dropped "no_space". The victims are extracted with one
 // warp min-reduction each; records (evict + started, or dropped) land at the
 // positions their candidate order fixes and are written lane-parallel.
+template <class Pt>
 DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int target) {
     const int64_t nb = p.eb_w;
     const int wp = p.wp;
@@ -1151,6 +1198,7 @@ DFI void sweep2_uniform(Pt& p, const int32_t* pe, const float* ps, int nt, int t
 }
 
 // _submit_prefetches + watchdog_step (engine.py:651-725, prefetch.py:163-221)
+template <class Pt>
 DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int tev) {   // tev < 2^31 / E events
     const int target = p.layer + 1;
     const int n = R.n_pred[tev];
@@ -1223,8 +1271,8 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int tev) {   // tev < 
         reserve_add(p, nb, 1);
         QEntry q;
         q.ident = (int16_t)ident; q.flags = (uint8_t)(1 | (wp << 2)); q.score = sc; q.submit = p.now;
-        int64_t start = p.now;
-        if (p.qn) { const int64_t tail = qcomp(p, p.qn - 1); start = p.now > tail ? p.now : tail; }
+        typename Pt::Tm start = p.now;
+        if (p.qn) { const typename Pt::Tm tail = qcomp(p, p.qn - 1); start = p.now > tail ? p.now : tail; }
         q.comp = start + pdur(p, wp);
         if (p.qn == 0 && p.uniform) p.qc0 = q.comp;
         const int at = p.qn;
@@ -1239,6 +1287,7 @@ DFI void submit_prefetches(Pt& p, const EsimRouterOut& R, int tev) {   // tev < 
 // ---- cache-aware routing inside the loop (routing.py:143-161) -------------
 // route one event with the cache-aware bias; fills the smem demand arrays
 // (indexed by expert) and dem_expert_s (sorted order); returns the demand count
+template <class Pt>
 DFI int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int64_t rows_before) {
     const int E = p.E, K = p.K, l = p.layer;
     const float* X = tr.logits + tr.row_offset[ev] * (int64_t)E;
@@ -1345,8 +1394,9 @@ constexpr int kPersistWarps = 12;
 // compile-time policy/miss constants delete the other policies' code from the kernel.
 // LOG: 0 = digest only, no record log (compile-time: the log-writing code is gone
 // from the kernel), 1 = per-point runtime flags (full log and/or digest)
-template <int POL, int GEN, int LOG>
+template <int POL, int GEN, int LOG, int T32>
 DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
+    using Tm = typename std::conditional<T32 != 0, int32_t, int64_t>::type;
     const int64_t orow = A.out_index ? A.out_index[pid] : pid;      // where this point's results go
     const EsimConfig* cfg = &A.cfg[pid];
     const EsimTraceDesc tr = A.traces[cfg->trace_id];
@@ -1356,7 +1406,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
 
     long long t_begin;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
-    Pt p;
+    PtT<Tm> p;
     p.c = cfg;
     p.L = cfg->num_layers; p.E = cfg->experts; p.K = cfg->top_k;
     const int N = p.L * p.E;
@@ -1379,7 +1429,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
         if (nb > 0 && nb < minb) minb = nb;
     }
     p.eb0 = ebs[0]; p.eb1 = ebs[1]; p.eb2 = ebs[2]; p.eb3 = ebs[3];
-    p.dur0 = durs[0]; p.dur1 = durs[1]; p.dur2 = durs[2]; p.dur3 = durs[3];
+    p.dur0 = (Tm)durs[0]; p.dur1 = (Tm)durs[1]; p.dur2 = (Tm)durs[2]; p.dur3 = (Tm)durs[3];
     p.uniform = !GEN;
     p.wp = cfg->working_prec;
     p.eb_w = ebs[cfg->working_prec & 3];
@@ -1603,7 +1653,7 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
             }
             }
             if (cfg->prefetch != ESIM_PF_NONE && l + 1 < p.L) submit_prefetches(p, R, ev + 1);
-            advance_to(p, p.now + cfg->compute_us);
+            advance_to(p, p.now + (Tm)cfg->compute_us);
             pblocked += blocked;
             if (A.progress && p.lane == 0) {             // publish this layer's decisions to the host
                 __threadfence_system();
@@ -1688,14 +1738,14 @@ DFI void replay_point(const ReplayArgs& A, const int pid, unsigned char* base) {
     }
 }
 
-template <int POL, int GEN, int LOG>
+template <int POL, int GEN, int LOG, int T32>
 __global__ void __launch_bounds__(GEN ? 128 : 32 * kPersistWarps, 1) replay_kernel(ReplayArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int wid = threadIdx.x >> 5;
     unsigned char* base = smem_raw + (size_t)wid * A.point_bytes;
     if (A.work == nullptr) {                         // one point per warp
         const int pid = blockIdx.x * A.warps_per_cta + wid;
-        if (pid < A.n_points) replay_point<POL, GEN, LOG>(A, pid, base);
+        if (pid < A.n_points) replay_point<POL, GEN, LOG, T32>(A, pid, base);
         return;
     }
     // persistent: every warp pulls the next point of the launch order (longest
@@ -1705,7 +1755,7 @@ __global__ void __launch_bounds__(GEN ? 128 : 32 * kPersistWarps, 1) replay_kern
         if ((threadIdx.x & 31) == 0) pid = atomicAdd(A.work, 1);
         pid = __shfl_sync(FULL, pid, 0);
         if (pid >= A.n_points) break;
-        replay_point<POL, GEN, LOG>(A, pid, base);
+        replay_point<POL, GEN, LOG, T32>(A, pid, base);
         __syncwarp();
     }
 }
@@ -1736,7 +1786,7 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
                                     int64_t pe_cap, int N, int S, int Q, int Lmax, int Emax, int Tmax, int Kmax,
                                     bool has_cnt, int warps_per_cta, cudaStream_t st, int64_t* progress,
                                     int policy, bool general, const int32_t* out_index, bool log_rt,
-                                    int max_ctas) {
+                                    int max_ctas, bool time32) {
     esim::ReplayArgs a;
     a.progress = progress;
     a.out_index = out_index;
@@ -1753,8 +1803,10 @@ cudaError_t esim_replay_launch_impl(const EsimConfig* d_cfg, int n, const EsimTr
     int blocks = (n + warps_per_cta - 1) / warps_per_cta;
     void (*k)(esim::ReplayArgs) = nullptr;
 #define ESIM_PICK(P)                                                                   \
-    case P: k = general ? esim::replay_kernel<P, 1, 1>                                 \
-                        : (log_rt ? esim::replay_kernel<P, 0, 1> : esim::replay_kernel<P, 0, 0>); break;
+    case P: k = general ? esim::replay_kernel<P, 1, 1, 0>                              \
+                        : (log_rt ? (time32 ? esim::replay_kernel<P, 0, 1, 1> : esim::replay_kernel<P, 0, 1, 0>) \
+                                  : (time32 ? esim::replay_kernel<P, 0, 0, 1> : esim::replay_kernel<P, 0, 0, 0>)); \
+        break;
     switch (policy) {
         ESIM_PICK(ESIM_EV_LRU) ESIM_PICK(ESIM_EV_LFU) ESIM_PICK(ESIM_EV_LHU)
         ESIM_PICK(ESIM_EV_FLD) ESIM_PICK(ESIM_EV_SB) ESIM_PICK(ESIM_EV_LS)
