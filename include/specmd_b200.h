@@ -464,6 +464,16 @@ int esim_ffn_experts_q(const void *d_slots, int64_t slot_bytes, int32_t bits, co
                        const int32_t *d_exec_slot, const int32_t *d_tok_index, const float *d_tok_weight,
                        float *d_y, int32_t n_exec, int32_t inter, int32_t hidden, void *stream);
 
+/* Decode layers (<= 4 tokens per expert) as a streaming GEMV straight from
+ * the slots (ffn_gemv.cu): bits 16 = bf16 slots, 8 / 4 / 2 = quantised codes
+ * + fp32 row scales (the layout above); x = the layer input [T][hidden]
+ * (no gather), d_tok_index / d_tok_weight [n_exec][npad] (-1 = no token),
+ * max_tok = the largest token count of any executed expert (1..4). */
+int esim_ffn_experts_gemv(const void *d_slots, int64_t slot_bytes, int32_t bits, const void *d_x,
+                          const int32_t *d_exec_slot, const int32_t *d_tok_index, const float *d_tok_weight,
+                          float *d_y, int32_t n_exec, int32_t npad, int32_t max_tok, int32_t inter, int32_t hidden,
+                          void *stream);
+
 #ifdef __cplusplus
 }
 #endif

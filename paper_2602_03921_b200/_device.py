@@ -51,6 +51,7 @@ def lib():
         L.esim_ffn_experts.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
         L.esim_ffn_experts_ex.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.esim_ffn_experts_q.argtypes = [vp, C.c_int64, i32, vp, vp, vp, vp, vp, i32, i32, i32, vp]
+        L.esim_ffn_experts_gemv.argtypes = [vp, C.c_int64, i32, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.esim_sweep_plan_create.argtypes = [vp, i32, vp, i32, i32, i64, i64, vp]
         L.esim_sweep_plan_run.argtypes = [vp, vp, vp, vp, vp]
         L.esim_sweep_plan_destroy.argtypes = [vp]

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libspecmd_b200.so")
-SOURCES = ["capi.cu", "router.cu", "replay.cu", "ffn_gemm.cu", "layer_step.cu", "policy.cu", "report.cu", "noise.cu", "trace_io.cu"]
+SOURCES = ["capi.cu", "router.cu", "replay.cu", "ffn_gemm.cu", "ffn_gemv.cu", "layer_step.cu", "policy.cu", "report.cu", "noise.cu", "trace_io.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

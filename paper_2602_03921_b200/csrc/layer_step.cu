@@ -45,6 +45,10 @@ extern "C" int esim_ffn_experts_ex(const void* d_w1_maps, const void* d_w2_maps,
                                    const void* d_act_map, const int32_t* d_exec_slot, const int32_t* d_tok_index,
                                    const float* d_tok_weight, void* d_act, float* d_y, int32_t n_exec, int32_t npad,
                                    int32_t I, int32_t H, int32_t max_tok, void* stream);
+extern "C" int esim_ffn_experts_gemv(const void* d_slots, int64_t slot_bytes, int32_t bits, const void* d_x,
+                                     const int32_t* d_exec_slot, const int32_t* d_tok_index,
+                                     const float* d_tok_weight, float* d_y, int32_t n_exec, int32_t npad,
+                                     int32_t max_tok, int32_t I, int32_t H, void* stream);
 extern "C" int esim_ffn_experts_q(const void* d_slots, int64_t slot_bytes, int32_t bits, const void* d_x_map,
                                   const int32_t* d_exec_slot, const int32_t* d_tok_index, const float* d_tok_weight,
                                   float* d_y, int32_t n_exec, int32_t I, int32_t H, void* stream);
@@ -212,6 +216,7 @@ struct Engine {
     int max_entries = 0;                 // FFN entries per flush: experts + token-count splits at 128
     char* scratch = nullptr;             // quantised: [max_entries][3*H*I] bf16 tile-major
     bool fused_dequant = true;           // decode flushes over one quantised precision: ffn_decode_q_kernel
+    bool decode_gemv = true;             // decode flushes over one precision: ffn_gemv_kernel (ESIM_FFN_DECODE=tc: off)
     // per-run device scratch
     void* dev_scratch = nullptr;
     size_t dev_scratch_bytes = 0;
@@ -272,6 +277,7 @@ extern "C" int esim_ls_create(const EsimLSParams* p, void** handle) {
     }
     g->mask = p->prec_mask ? p->prec_mask : 1 << p->weight_format;
     if (const char* v = getenv("ESIM_LS_SCRATCH_DEQUANT")) g->fused_dequant = v[0] != '1';   // A/B switch
+    if (const char* v = getenv("ESIM_FFN_DECODE")) g->decode_gemv = !(v[0] == 't' && v[1] == 'c');
     const size_t bf16_bytes = (size_t)3 * H * I * 2;
     for (int pc = 0; pc < 4; pc++) {
         if (!(g->mask >> pc & 1)) continue;
@@ -624,16 +630,28 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
             table_next += E + 3 * g->max_entries;
             for (int e = 0; e < E; e++) tpos[e] = pos_of_expert[e];
             for (int i = 0; i < n_exec; i++) CK(cudaStreamWaitEvent(g->comp_st, g->landed[pend_slot[i]], 0));
-            // decode-like flush whose slots all hold one quantised precision: the FFN
-            // dequantises in shared memory (no scratch round trip)
-            int fused_bits = 0;
-            if (g->fused_dequant && npad == 16 && maxtok <= 4 && H / 128 <= 16) {
+            // decode flush (<= 4 tokens per expert) whose slots all hold one
+            // precision: the streaming GEMV reads the slots directly (bf16 or
+            // quantised codes, no gather, no scratch); ESIM_FFN_DECODE=tc selects
+            // the tcgen05 decode kernels instead (quantised: dequant fused into
+            // the A operand; bf16: the per-slice kernel below)
+            int fused_bits = 0, gemv_bits = 0;
+            if (npad == 16 && maxtok <= 4) {
                 const int pc = slot_prec[pend_slot[0]];
-                bool uniform = pc > 0;
+                bool uniform = true;
                 for (int i = 1; i < n_exec && uniform; i++) uniform = slot_prec[pend_slot[i]] == pc;
-                if (uniform) fused_bits = 16 >> pc;
+                if (uniform && g->decode_gemv) gemv_bits = 16 >> pc;
+                else if (uniform && pc > 0 && g->fused_dequant && H / 128 <= 16) fused_bits = 16 >> pc;
             }
-            if (fused_bits) {
+            if (gemv_bits) {
+                for (int i = 0; i < n_exec; i++) tslot[i] = pend_slot[i];
+                build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
+                                                                       g->tok_index, g->tok_weight);
+                if (esim_ffn_experts_gemv(g->slots, (int64_t)g->slot_bytes, gemv_bits, g->x, tslot, g->tok_index,
+                                          g->tok_weight, g->y, n_exec, npad, std::max(1, maxtok), I, H, g->comp_st))
+                    return ls_fail(-3, "gemv ffn launch failed");
+                fused_bits = -1;                        // done: skip the tcgen05 paths below
+            } else if (fused_bits) {
                 for (int i = 0; i < n_exec; i++) tslot[i] = pend_slot[i];
                 build_tables_kernel<<<1, 256, n_exec * 4, g->comp_st>>>(rs, rw, layer_rows, K, tpos, n_exec, npad,
                                                                        g->tok_index, g->tok_weight);

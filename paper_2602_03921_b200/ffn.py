@@ -76,38 +76,58 @@ class ExpertSlots:
         return self.buf[slot * self.expert_elems:(slot + 1) * self.expert_elems]
 
     def run_layer(self, x, exec_slot, tok_index, tok_weight, npad: int, stream=None, residual: bool = True,
-                  max_tok: int | None = None) -> None:
+                  max_tok: int | None = None, decode: str = "gemv") -> None:
         """x[T,H] bf16 (device, updated in place: x += MoE(x)). exec_slot int32
         [n_exec] (device), tok_index int32 [n_exec*npad], tok_weight f32 (device).
-        max_tok: the largest token count of an executed expert (<= 4 selects the
-        fused decode kernel); None = npad (the two-phase kernel)."""
+        max_tok: the largest token count of an executed expert; <= 4 is a decode
+        layer: decode="gemv" streams it straight from the slots (ffn_gemv.cu),
+        "tc" runs the fused tcgen05 decode kernel; None = npad (the two-phase
+        tcgen05 kernel)."""
         n_exec = int(exec_slot.numel())
         if n_exec > self.max_exec:
             raise ValueError("more executed experts than staged")
+        if decode not in ("gemv", "tc"):
+            raise ValueError(f"unknown decode kernel {decode!r}")
         st = stream or _stream()
         L = lib()
-        _check(L.esim_ffn_gather(x.data_ptr(), tok_index.data_ptr(), self.xg.data_ptr(), n_exec, npad, self.H, st),
-               "gather")
-        _check(L.esim_ffn_experts_ex(self.w1_maps.data_ptr(), self.w2_maps.data_ptr(), self.x_maps[npad].data_ptr(),
-                                     self.act_maps[npad].data_ptr(), exec_slot.data_ptr(), tok_index.data_ptr(),
-                                     tok_weight.data_ptr(), self.act.data_ptr(), self.y.data_ptr(), n_exec, npad,
-                                     self.I, self.H, npad if max_tok is None else max_tok, st), "ffn experts")
+        if decode == "gemv" and max_tok is not None and 1 <= max_tok <= 4:
+            _check(L.esim_ffn_experts_gemv(self.buf.data_ptr(), self.expert_bytes, 16, x.data_ptr(),
+                                           exec_slot.data_ptr(), tok_index.data_ptr(), tok_weight.data_ptr(),
+                                           self.y.data_ptr(), n_exec, npad, max_tok, self.I, self.H, st),
+                   "gemv ffn experts")
+        else:
+            _check(L.esim_ffn_gather(x.data_ptr(), tok_index.data_ptr(), self.xg.data_ptr(), n_exec, npad, self.H,
+                                     st), "gather")
+            _check(L.esim_ffn_experts_ex(self.w1_maps.data_ptr(), self.w2_maps.data_ptr(),
+                                         self.x_maps[npad].data_ptr(), self.act_maps[npad].data_ptr(),
+                                         exec_slot.data_ptr(), tok_index.data_ptr(), tok_weight.data_ptr(),
+                                         self.act.data_ptr(), self.y.data_ptr(), n_exec, npad, self.I, self.H,
+                                         npad if max_tok is None else max_tok, st), "ffn experts")
         if residual:
             T = x.numel() // self.H
             _check(L.esim_ffn_residual(x.data_ptr(), self.y.data_ptr(), T * self.H, st), "residual")
 
     def run_layer_quant(self, qslots, slot_bytes: int, bits: int, x, exec_slot, tok_index, tok_weight,
-                        stream=None) -> None:
+                        stream=None, decode: str = "gemv", max_tok: int = 4) -> None:
         """Decode-like layer (<= 4 tokens per expert, npad 16) over quantised
         slots: qslots uint8 (device) holding tile-major codes of `bits` then
         fp32 row scales per slot (slot_bytes apart, layer_step.cu's format);
-        y += MoE(x) with the dequantisation fused into the FFN
-        (ffn_decode_q_kernel). No residual."""
+        y += MoE(x) with the dequantisation fused into the FFN: decode="gemv"
+        (ffn_gemv.cu, codes converted in registers) or "tc"
+        (ffn_decode_q_kernel, codes converted into the tcgen05 A operand).
+        No residual."""
         n_exec = int(exec_slot.numel())
         if n_exec > self.max_exec:
             raise ValueError("more executed experts than staged")
+        if decode not in ("gemv", "tc"):
+            raise ValueError(f"unknown decode kernel {decode!r}")
         st = stream or _stream()
         L = lib()
+        if decode == "gemv":
+            _check(L.esim_ffn_experts_gemv(qslots.data_ptr(), slot_bytes, bits, x.data_ptr(), exec_slot.data_ptr(),
+                                           tok_index.data_ptr(), tok_weight.data_ptr(), self.y.data_ptr(), n_exec,
+                                           16, max_tok, self.I, self.H, st), "gemv quantised ffn experts")
+            return
         _check(L.esim_ffn_gather(x.data_ptr(), tok_index.data_ptr(), self.xg.data_ptr(), n_exec, 16, self.H, st),
                "gather")
         _check(L.esim_ffn_experts_q(qslots.data_ptr(), slot_bytes, bits, self.x_maps[16].data_ptr(),

@@ -11,7 +11,7 @@ H, I = 2048, 1024
 TOL = 1e-2
 
 
-def _case(T, K, n_exp, npad_expected, seed, fused, H=H, I=I):
+def _case(T, K, n_exp, npad_expected, seed, fused, H=H, I=I, decode="tc"):
     import torch
     from paper_2602_03921_b200.ffn import ExpertSlots, expert_matrices, npad_for, routing_tables
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -32,7 +32,7 @@ def _case(T, K, n_exp, npad_expected, seed, fused, H=H, I=I):
     slots.y.zero_()
     mt = int(counts.max()) if fused else None          # <= 4 tokens: fused decode kernel
     slots.run_layer(x, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad, residual=False,
-                    max_tok=mt)
+                    max_tok=mt, decode=decode)
     torch.cuda.synchronize()
     y = slots.y[:T * H].view(T, H).float()
     ref = torch.zeros(T, H, device="cuda")
@@ -51,7 +51,8 @@ def _case(T, K, n_exp, npad_expected, seed, fused, H=H, I=I):
     assert err <= TOL, f"max rel err {err:.3e}"
     # residual path: x += y
     x2 = x.clone()
-    slots.run_layer(x2, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad, max_tok=mt)
+    slots.run_layer(x2, exec_slot, torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), npad, max_tok=mt,
+                    decode=decode)
     torch.cuda.synchronize()
     assert torch.isfinite(x2.float()).all()
     return err
@@ -64,10 +65,13 @@ def test_ffn_matches_torch_fp32(T, K, n_exp, npad, seed):
     _case(T, K, n_exp, npad, seed, fused=False)
 
 
-@pytest.mark.parametrize("T,K,n_exp,seed", [(1, 8, 8, 10), (1, 8, 64, 11), (3, 4, 8, 12), (4, 2, 3, 13)])
-def test_ffn_decode_kernel_matches_torch_fp32(T, K, n_exp, seed):
-    """The fused per-slice decode kernel (<= 4 tokens per expert)."""
-    _case(T, K, n_exp, 16, seed, fused=True)
+@pytest.mark.parametrize("decode", ["tc", "gemv"])
+@pytest.mark.parametrize("T,K,n_exp,seed", [(1, 8, 8, 10), (1, 8, 64, 11), (3, 4, 8, 12), (4, 2, 3, 13),
+                                            (2, 8, 8, 14)])
+def test_ffn_decode_kernel_matches_torch_fp32(T, K, n_exp, seed, decode):
+    """Decode layers (<= 4 tokens per expert): the fused per-slice tcgen05
+    kernel ("tc") and the streaming GEMV over the slots ("gemv")."""
+    _case(T, K, n_exp, 16, seed, fused=True, decode=decode)
 
 
 # BASELINE.json configs[2]: Mixtral-8x7B experts, H=4096, I=14336 (352 MB bf16
@@ -80,6 +84,14 @@ def test_ffn_mixtral_shape_matches_torch_fp32(T, K, n_exp, npad, seed, fused):
     _case(T, K, n_exp, npad, seed, fused=fused, H=4096, I=14336)
 
 
+@pytest.mark.parametrize("T,K,n_exp,seed,H_,I_", [(1, 2, 2, 34, 4096, 14336), (2, 2, 4, 35, 4096, 14336),
+                                                  (1, 4, 4, 44, 2048, 1408), (1, 1, 1, 45, 2048, 5632)])
+def test_ffn_gemv_decode_other_shapes(T, K, n_exp, seed, H_, I_):
+    """The GEMV decode kernel at the Mixtral (configs[2]) and Qwen (configs[3])
+    expert shapes."""
+    _case(T, K, n_exp, 16, seed, fused=True, H=H_, I=I_, decode="gemv")
+
+
 # configs[3]: Qwen1.5-MoE routed experts (I = 1408) and its shared expert (I = 5632)
 @pytest.mark.parametrize("T,K,n_exp,npad,seed,fused,inter", [(1, 4, 4, 16, 40, True, 1408), (64, 4, 24, 32, 41, False, 1408),
                                                              (1, 1, 1, 16, 42, True, 5632), (64, 1, 1, 64, 43, False, 5632)])
@@ -87,9 +99,10 @@ def test_ffn_qwen_shapes_match_torch_fp32(T, K, n_exp, npad, seed, fused, inter)
     _case(T, K, n_exp, npad, seed, fused=fused, H=2048, I=inter)
 
 
+@pytest.mark.parametrize("decode", ["tc", "gemv"])
 @pytest.mark.parametrize("bits,T,K,n_exp,seed", [(8, 1, 8, 8, 20), (4, 1, 8, 64, 21), (2, 3, 4, 16, 22),
-                                                 (4, 4, 8, 40, 23)])
-def test_ffn_quantised_decode_kernel_matches_torch_fp32(bits, T, K, n_exp, seed):
+                                                 (4, 4, 8, 40, 23), (2, 1, 8, 8, 24), (8, 2, 8, 8, 25)])
+def test_ffn_quantised_decode_kernel_matches_torch_fp32(bits, T, K, n_exp, seed, decode):
     """ffn_decode_q_kernel: quantised slots (codes + fp32 row scales), the
     dequantisation fused into the A operand; 64 experts x 16 units puts
     several units on every CTA (ring phases wrap across units)."""
@@ -113,11 +126,12 @@ def test_ffn_quantised_decode_kernel_matches_torch_fp32(bits, T, K, n_exp, seed)
     row_sel = np.stack([rng.choice(n_exp, size=K, replace=False) for _ in range(T)]).astype(np.int32)
     row_w = rng.uniform(0.01, 0.3, size=(T, K)).astype(np.float32)
     slot_of = rng.permutation(n_slots)[:n_exp]
-    assert np.bincount(row_sel.ravel()).max() <= 4
+    mt = int(np.bincount(row_sel.ravel()).max())
+    assert mt <= 4
     ti, tw = routing_tables(row_sel, row_w, {e: (e, e) for e in range(n_exp)}, 16)
     slots.y.zero_()
     slots.run_layer_quant(q, slot_bytes, bits, x, torch.tensor(slot_of, dtype=torch.int32, device="cuda"),
-                          torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda())
+                          torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), decode=decode, max_tok=mt)
     torch.cuda.synchronize()
     y = slots.y[:T * H].view(T, H).float()
     ref = torch.zeros(T, H, device="cuda")

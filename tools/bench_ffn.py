@@ -25,23 +25,25 @@ for name, T, K, n_exp in (("prefill64", 64, 8, 28), ("decode", 1, 8, 8), ("prefi
     ti, tw = routing_tables(row_sel, row_w, {e: (e, e) for e in range(n_exp)}, npad)
     ti, tw = torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda()
     es = torch.arange(n_exp, dtype=torch.int32, device="cuda")
-    for _ in range(3):
-        slots.run_layer(x, es, ti, tw, npad, residual=False, max_tok=mt)
-    torch.cuda.synchronize()
-    n = 30
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
-    for i in range(n):
-        flush.zero_()
-        ev[i][0].record()
-        slots.run_layer(x, es, ti, tw, npad, residual=False, max_tok=mt)
-        ev[i][1].record()
-    torch.cuda.synchronize()
-    ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
-    byt = n_exp * 3 * H * I * 2
-    flops = 2 * 3 * H * I * int(row_sel.size)
-    out[name] = {"ms": ms, "npad": npad, "n_exec": n_exp, "weight_gbs": byt / ms / 1e6,
-                 "frac_of_hbm_peak": byt / ms / 1e6 / peak, "tflops": flops / ms / 1e9}
-    print(name, out[name], flush=True)
+    for impl in (("tc", "gemv") if mt <= 4 else ("tc",)):
+        for _ in range(3):
+            slots.run_layer(x, es, ti, tw, npad, residual=False, max_tok=mt, decode=impl)
+        torch.cuda.synchronize()
+        n = 30
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for i in range(n):
+            flush.zero_()
+            ev[i][0].record()
+            slots.run_layer(x, es, ti, tw, npad, residual=False, max_tok=mt, decode=impl)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+        byt = n_exp * 3 * H * I * 2
+        flops = 2 * 3 * H * I * int(row_sel.size)
+        key = name if impl == "tc" else name + "_gemv"
+        out[key] = {"ms": ms, "npad": npad, "n_exec": n_exp, "weight_gbs": byt / ms / 1e6,
+                    "frac_of_hbm_peak": byt / ms / 1e6 / peak, "tflops": flops / ms / 1e9}
+        print(key, out[key], flush=True)
 # decode over quantised slots (ffn_decode_q_kernel, dequantisation fused into the
 # A operand): algorithmic bytes = codes + fp32 row scales per executed expert
 for bits in (8, 4, 2):
@@ -62,22 +64,23 @@ for bits in (8, 4, 2):
         ti, tw = torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda()
         x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
         es = torch.arange(n_exp, dtype=torch.int32, device="cuda")
-        for _ in range(3):
-            slots.run_layer_quant(qbuf, sb, bits, x, es, ti, tw)
-        torch.cuda.synchronize()
-        n = 30
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
-        for i in range(n):
-            flush.zero_()
-            ev[i][0].record()
-            slots.run_layer_quant(qbuf, sb, bits, x, es, ti, tw)
-            ev[i][1].record()
-        torch.cuda.synchronize()
-        ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
-        byt = n_exp * per
-        name = f"decode_int{bits}_{n_exp}experts"
-        out[name] = {"ms": ms, "n_exec": n_exp, "quant_bytes_per_expert": per, "quant_gbs": byt / ms / 1e6,
-                     "frac_of_hbm_peak": byt / ms / 1e6 / peak,
-                     "bf16_equivalent_gbs": n_exp * 3 * H * I * 2 / ms / 1e6}
-        print(name, out[name], flush=True)
+        for impl in ("tc", "gemv"):
+            for _ in range(3):
+                slots.run_layer_quant(qbuf, sb, bits, x, es, ti, tw, decode=impl, max_tok=1)
+            torch.cuda.synchronize()
+            n = 30
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+            for i in range(n):
+                flush.zero_()
+                ev[i][0].record()
+                slots.run_layer_quant(qbuf, sb, bits, x, es, ti, tw, decode=impl, max_tok=1)
+                ev[i][1].record()
+            torch.cuda.synchronize()
+            ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+            byt = n_exp * per
+            name = f"decode_int{bits}_{n_exp}experts" + ("_gemv" if impl == "gemv" else "")
+            out[name] = {"ms": ms, "n_exec": n_exp, "quant_bytes_per_expert": per, "quant_gbs": byt / ms / 1e6,
+                         "frac_of_hbm_peak": byt / ms / 1e6 / peak,
+                         "bf16_equivalent_gbs": n_exp * 3 * H * I * 2 / ms / 1e6}
+            print(name, out[name], flush=True)
 json.dump(out, open("gpurun_out/bench_ffn.json", "w"), indent=1)
