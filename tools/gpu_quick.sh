@@ -1,9 +1,10 @@
 #!/bin/bash
-# One GPU session: gpu tests, smoke, bench line (no profiler).
+# One GPU session: gpu tests, smoke, bench line, FFN microbenchmark (no profiler).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider --durations=15 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log
+timeout 600 python tools/bench_ffn.py > gpurun_out/bench_ffn.log 2>&1; echo "bench_ffn exit $?" >> gpurun_out/bench_ffn.log
 echo done
