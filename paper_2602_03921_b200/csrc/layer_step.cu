@@ -606,6 +606,12 @@ extern "C" int esim_ls_run(void* handle, const EsimTraceDesc* trace_dev, const i
         shared_tables_kernel<<<(n_ent * npad + 7) / 8, 256, 0, g->comp_st>>>(
             (const __nv_bfloat16*)g->x, g->shared_gate + (size_t)layer * H, T, H, npad, n_ent, layer, g->s_tok_index,
             g->s_tok_weight, g->s_exec);
+        if (T <= 4 && g->decode_gemv) {              // decode: the GEMV straight from the layer's weights
+            if (esim_ffn_experts_gemv(g->shared_w, (int64_t)3 * H * g->Is * 2, 16, g->x, g->s_exec, g->s_tok_index,
+                                      g->s_tok_weight, g->y, n_ent, npad, T, g->Is, H, g->comp_st))
+                return ls_fail(-3, "shared expert gemv launch failed");
+            return 0;
+        }
         if (esim_ffn_gather(g->x, g->s_tok_index, g->xg, n_ent, npad, H, g->comp_st) ||
             esim_ffn_experts_ex(g->sw1_maps, g->sw2_maps, g->x_maps[npad_index(npad)], g->sact_maps[npad_index(npad)],
                                 g->s_exec, g->s_tok_index, g->s_tok_weight, g->sact, g->y, n_ent, npad, g->Is, H,

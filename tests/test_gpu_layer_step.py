@@ -1,5 +1,6 @@
 """Physical layer step: HBM cache slots filled by copy-engine H2D copies
-driven by the device decision stream, tcgen05 FFN per layer.
+driven by the device decision stream, tcgen05 FFN per prefill layer and the
+streaming GEMV per decode layer.
 
 * outputs == a no-cache PyTorch fp32 reference of the same MoE forward
   (bf16 activations between layers), max error <= 1e-2 of max |x|;
@@ -103,10 +104,20 @@ def test_layer_step_cache_aware_routing(oracle_lib):
 
 
 def test_layer_step_quantised_scratch_path(oracle_lib, monkeypatch):
-    """The dequantise-to-scratch path for decode flushes too (the fused
-    ffn_decode_q_kernel is the default there): same reference, same bar."""
+    """The dequantise-to-scratch path for decode flushes too (the GEMV, then
+    the fused ffn_decode_q_kernel, are the defaults there): same reference,
+    same bar."""
+    monkeypatch.setenv("ESIM_FFN_DECODE", "tc")
     monkeypatch.setenv("ESIM_LS_SCRATCH_DEQUANT", "1")
     _run_case("ls", 7, "fetch", 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=3, prec="int4")
+
+
+@pytest.mark.parametrize("prec", ["fp16", "int4"])
+def test_layer_step_tcgen05_decode_path(prec, oracle_lib, monkeypatch):
+    """ESIM_FFN_DECODE=tc: decode flushes on the tcgen05 kernels (bf16 per-slice
+    decode kernel / fused-dequant ffn_decode_q_kernel) instead of the GEMV."""
+    monkeypatch.setenv("ESIM_FFN_DECODE", "tc")
+    _run_case("ls", 7, "fetch", 1024, oracle_lib, experts=16, top_k=4, prefill=8, decode=3, prec=prec)
 
 
 @pytest.mark.parametrize("eviction,cap_experts,miss,working,ladder",
