@@ -433,9 +433,15 @@ static cudaError_t launch(const GemvArgs& a, cudaStream_t st) {
     lc.stream = st;
     cudaLaunchAttribute at[1];
     cudaError_t e;
+    // the smem opt-in is raised once per instantiation (to the largest request so far)
+    static int set_pair = 0, set_one = 0;
     if (pair) {
-        e = cudaFuncSetAttribute(ffn_gemv_kernel<BITS, NTOK, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
+        if ((int)smem > set_pair) {
+            e = cudaFuncSetAttribute(ffn_gemv_kernel<BITS, NTOK, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+            if (e != cudaSuccess) return e;
+            set_pair = (int)smem;
+        }
         lc.gridDim = dim3(2 * units);
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = 2;
@@ -445,8 +451,12 @@ static cudaError_t launch(const GemvArgs& a, cudaStream_t st) {
         lc.numAttrs = 1;
         return cudaLaunchKernelEx(&lc, ffn_gemv_kernel<BITS, NTOK, 2>, a);
     }
-    e = cudaFuncSetAttribute(ffn_gemv_kernel<BITS, NTOK, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    if ((int)smem > set_one) {
+        e = cudaFuncSetAttribute(ffn_gemv_kernel<BITS, NTOK, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return e;
+        set_one = (int)smem;
+    }
     lc.gridDim = dim3(units);
     return cudaLaunchKernelEx(&lc, ffn_gemv_kernel<BITS, NTOK, 1>, a);
 }

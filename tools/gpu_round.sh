@@ -21,6 +21,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_
 python tools/ncu_summary.py gpurun_out/ffn_prefill_full.ncu-rep gpurun_out/ffn_prefill_summary.json > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:router_persistent -s 32 -c 1 -o gpurun_out/router_full -f python tools/ncu_replay.py 8 > gpurun_out/ncu_router.log 2>&1
 python tools/ncu_summary.py gpurun_out/router_full.ncu-rep gpurun_out/router_summary.json > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ffn_gemv --launch-skip 92 --launch-count 1 -o gpurun_out/ffn_gemv_full -f python tools/probe_gemv_variants.py paper_2602_03921_b200/lib/libspecmd_b200.so > gpurun_out/ncu_gemv.log 2>&1
+python tools/ncu_summary.py gpurun_out/ffn_gemv_full.ncu-rep gpurun_out/ffn_gemv_summary.json > /dev/null 2>&1
 timeout 300 python tools/bench_ffn.py > gpurun_out/bench_ffn.log 2>&1
+timeout 300 python tools/probe_gemv_variants.py paper_2602_03921_b200/lib/libspecmd_b200.so > gpurun_out/pgv.log 2>&1
 rm -f gpurun_out/*.ncu-rep
 echo done
