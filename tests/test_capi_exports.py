@@ -40,3 +40,26 @@ def test_struct_sizes_match_the_header():
     from paper_2602_03921_b200.layer_step import EsimLSParams, EsimLSResult
     assert ctypes.sizeof(EsimLSParams) == 9 * 4           # incl. weight_format, prec_mask
     assert ctypes.sizeof(EsimLSResult) == 4 * 8 + 9 * 8
+
+
+def test_gemv_decode_rejects_bad_geometry_before_any_device_work():
+    """esim_ffn_experts_gemv validates its arguments on the host (-1, no CUDA
+    call): unknown bit width, I not a multiple of 64, H not a multiple of 128
+    or above 8192, 0 or > 4 tokens per expert, npad below max_tok, unaligned
+    slot stride; no executed experts is a no-op (0)."""
+    from paper_2602_03921_b200 import build
+    lib = ctypes.CDLL(build.build())
+    f = lib.esim_ffn_experts_gemv
+    vp, i32 = ctypes.c_void_p, ctypes.c_int32
+    f.argtypes = [vp, ctypes.c_int64, i32, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
+    ok = dict(sb=3 * 2048 * 1024 * 2, bits=16, n=8, npad=16, mt=1, I=1024, H=2048)
+
+    def call(**kw):
+        a = dict(ok, **kw)
+        return f(None, a["sb"], a["bits"], None, None, None, None, None, a["n"], a["npad"], a["mt"], a["I"], a["H"],
+                 None)
+
+    assert call(n=0) == 0
+    for bad in (dict(bits=3), dict(bits=1), dict(I=1000), dict(H=2112), dict(H=16384), dict(mt=0), dict(mt=5),
+                dict(npad=2, mt=4), dict(sb=3 * 2048 * 1024 * 2 + 8)):
+        assert call(**bad) == -1, bad
