@@ -146,3 +146,74 @@ def test_ffn_quantised_decode_kernel_matches_torch_fp32(bits, T, K, n_exp, seed,
                     ref[t] += float(row_w[t, j]) * out[t]
     err = (y - ref).abs().max().item() / ref.abs().max().item()
     assert err <= TOL, f"max rel err {err:.3e}"
+
+
+def _gemv_reference(q_or_w, bits, H, I, x, row_sel, row_w, slot_of, n_exp):
+    import torch
+    from paper_2602_03921_b200.ffn import expert_matrices
+    from paper_2602_03921_b200.layer_step import dequant_expert
+    T = x.shape[0]
+    ref = torch.zeros(T, H, device="cuda")
+    xf = x.float()
+    for e in range(n_exp):
+        if bits == 16:
+            w1, wd = expert_matrices(q_or_w[int(slot_of[e])].float(), H, I)
+        else:
+            w1, wd = dequant_expert(q_or_w[int(slot_of[e])], bits, H, I)
+        out = (torch.nn.functional.silu(xf @ w1[:I].T) * (xf @ w1[I:].T)) @ wd.T
+        for t in range(T):
+            for j in range(row_sel.shape[1]):
+                if row_sel[t, j] == e:
+                    ref[t] += float(row_w[t, j]) * out[t]
+    return ref
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_ffn_gemv_random_geometries(case):
+    """The decode GEMV over random shapes (H a multiple of 128 from 128 to
+    4096, I a multiple of 64 from 64 to 3008, 1-64 experts, 1-4 tokens per
+    expert, bf16 / int8 / int4 / int2 slots): partial ring chunks, single-tile
+    blocks, CTA-pair and single-CTA units, against fp32 torch (1e-2 of max |y|)."""
+    import torch
+    from paper_2602_03921_b200.ffn import ExpertSlots, routing_tables
+    rng = np.random.default_rng(1000 + case)
+    H_ = int(rng.integers(1, 33)) * 128
+    I_ = int(rng.integers(1, 48)) * 64
+    bits = int(rng.choice([16, 8, 4, 2]))
+    n_exp = int(rng.integers(1, 65))
+    K = int(rng.integers(1, min(n_exp, 8) + 1))
+    T = int(rng.integers(1, 5))
+    g = torch.Generator(device="cuda").manual_seed(case)
+    n_slots = n_exp + 1
+    nq, ns = 3 * H_ * I_, 2 * I_ + H_
+    if bits == 16:
+        sb = nq * 2
+        buf = (torch.randn(n_slots, nq, generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+        flat = buf.view(torch.uint8).view(-1)
+        refw = buf
+    else:
+        per = nq * bits // 8 + 4 * ns
+        sb = (per + 255) // 256 * 256
+        q = torch.zeros(n_slots, sb, dtype=torch.uint8, device="cuda")
+        q[:, :nq * bits // 8] = torch.randint(0, 256, (n_slots, nq * bits // 8), generator=g, device="cuda",
+                                              dtype=torch.int32).to(torch.uint8)
+        qmax = {8: 127, 4: 7, 2: 1}[bits]
+        sc = (0.5 + torch.rand(n_slots, ns, generator=g, device="cuda")) * (0.02 / qmax)
+        q[:, nq * bits // 8:per] = sc.view(torch.uint8).view(n_slots, ns * 4)
+        flat = q.view(-1)
+        refw = q
+    x = torch.randn(T, H_, generator=g, device="cuda").to(torch.bfloat16)
+    row_sel = np.stack([rng.choice(n_exp, size=K, replace=False) for _ in range(T)]).astype(np.int32)
+    row_w = rng.uniform(0.01, 0.3, size=(T, K)).astype(np.float32)
+    slot_of = rng.permutation(n_slots)[:n_exp]
+    mt = int(np.bincount(row_sel.ravel()).max())
+    ti, tw = routing_tables(row_sel, row_w, {e: (e, e) for e in range(n_exp)}, 16)
+    slots = ExpertSlots(1, H_, I_, max_tokens=T, max_exec=n_exp)
+    slots.y.zero_()
+    slots.run_layer_quant(flat, sb, bits, x, torch.tensor(slot_of, dtype=torch.int32, device="cuda"),
+                          torch.from_numpy(ti).cuda(), torch.from_numpy(tw).cuda(), decode="gemv", max_tok=mt)
+    torch.cuda.synchronize()
+    y = slots.y[:T * H_].view(T, H_).float()
+    ref = _gemv_reference(refw, bits, H_, I_, x, row_sel, row_w, slot_of, n_exp)
+    err = (y - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= TOL, f"H={H_} I={I_} bits={bits} experts={n_exp} K={K} T={T}: max rel err {err:.3e}"
