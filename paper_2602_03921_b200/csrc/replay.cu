@@ -1388,7 +1388,10 @@ DFI int route_cache_aware(Pt& p, const EsimTraceDesc& tr, int64_t ev, int T, int
 // (registers <= 65536 / (32 * 12) = 170 per thread): an SM then only ever runs
 // one policy's kernel -- two policies' ~80 KB instruction streams sharing an SM
 // thrash its instruction cache -- and its warps pull points longest-first.
-constexpr int kPersistWarps = 12;
+#ifndef REPLAY_WARPS
+#define REPLAY_WARPS 12
+#endif
+constexpr int kPersistWarps = REPLAY_WARPS;
 // POL: eviction policy; GEN: 0 = the common case (miss=fetch, standard routing) with every
 // other miss/routing path compiled out, 1 = all paths. Every helper is force-inlined, so the
 // compile-time policy/miss constants delete the other policies' code from the kernel.
