@@ -17,6 +17,9 @@ roofline = replay kernel: 48 B algorithmic per demanded access (SURVEY.md
            section 8(d)) / its CUDA-event time vs measured HBM peak
 cpu_baseline / --impl reference = the C oracle (oracle/, a restatement of
            the reference simulator) on this box's host cores
+stock_reference = the unmodified reference (`expertsim`, pip-installed in
+           baseline/_ref) on one host core over a bounded sample, its CSV rows
+           compared byte for byte with the device's for the same points
 
 Also reported: `layer_step` (physical OLMoE bf16 prefill+decode with the
 0.6 GB cache, configs[1]) when --layer-step is given or by default at N=1.
@@ -31,6 +34,8 @@ import subprocess
 import sys
 import threading
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -268,7 +273,60 @@ def run_reference(args, rank, world):
             "cpu_baseline": {"value": value, "unit": "accesses/s", "cores": threads, "kind": "port",
                              "sample": f"C5 grid x {args.seeds} seeds ({acc} demanded accesses) per step"},
             "e2e": {"value": value, "unit": "accesses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.no_stock:
+        line["stock_reference"] = stock_reference(args.stock_seconds)
     print(json.dumps(line), flush=True)
+
+
+def stock_reference(budget_s: float = 12.0, cfgs=None, device_rows=None):
+    """The unmodified reference simulator (`expertsim`, installed once with
+    pip --target baseline/_ref from /root/reference; it travels to the GPU box
+    with the repo) timed on this host on a bounded sample of the bench
+    workload: the C5 grid points of the OLMoE seed-1 trace in grid order, one
+    core, until `budget_s` is spent. With `cfgs` / `device_rows` (the device's
+    CSV rows of the same points, sweep.csv_text) the reference's own
+    emit(report, "csv") rows are compared with them byte for byte."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "expertsim")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref /root/reference)"}
+    import importlib
+    import tempfile
+    sys.path.insert(0, ref)
+    try:
+        es_engine = importlib.import_module("expertsim.engine")
+        es_models = importlib.import_module("expertsim.models")
+        es_trace = importlib.import_module("expertsim.trace")
+        es_metrics = importlib.import_module("expertsim.metrics")
+    finally:
+        sys.path.remove(ref)
+    from paper_2602_03921_b200.sweep import C5_BANDWIDTHS, C5_CAPACITIES, C5_EVICTIONS
+    from itertools import product
+    spec = es_models.builtin_spec("olmoe")
+    tr = es_trace.generate_synthetic(spec, seed=1, prefill_tokens=64, decode_tokens=64, affinity=0.6, skew=1.0)
+    pts = list(product(C5_EVICTIONS, C5_CAPACITIES, C5_BANDWIDTHS))
+    acc, n, t_run = 0, 0, 0.0
+    rows_match = None
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "ref.csv")
+        for ev, cap, bw in pts:
+            hw = es_models.HardwareSpec(capacity_fraction=cap, bandwidth_bytes_per_sec=bw)
+            cfg = es_engine.SimConfig(model=spec, hardware=hw, eviction=ev, working_precision="int4",
+                                      prefetch="score", percentile=80.0, miss="fetch", seed=0)
+            t0 = time.perf_counter()
+            rep = es_engine.run_simulation(cfg, tr)
+            t_run += time.perf_counter() - t0
+            acc += int(rep["totals"]["demanded"])
+            es_metrics.emit(rep, "csv", path)
+            n += 1
+            if t_run >= budget_s:
+                break
+        with open(path, newline="") as fh:
+            ref_csv = fh.read()
+    if device_rows is not None:
+        rows_match = ref_csv == device_rows(n)
+    return {"value": acc / t_run, "unit": "accesses/s", "cores": 1, "kind": "reference (stock expertsim, "
+            "baseline/_ref)", "sample": f"{n} C5 points of the OLMoE seed-1 trace ({acc} demanded accesses) in "
+            f"{t_run:.1f} s", "csv_rows_identical_to_device": rows_match}
 
 
 def self_launch(n: int) -> int:
@@ -293,6 +351,8 @@ def main():
     ap.add_argument("--cpu-seeds", type=int, default=8, help="cpu_baseline sample (1 thread)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-layer-step", action="store_true")
+    ap.add_argument("--no-stock", action="store_true", help="skip the stock-reference (baseline/_ref) leg")
+    ap.add_argument("--stock-seconds", type=float, default=12.0, help="stock-reference sample budget (1 core)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return self_launch(args.gpus)
@@ -451,6 +511,7 @@ def main():
         cs, pl_ = grid.wait()
         csv_out = csv_text(cfgs, cs, pl_)
         e2r_ms = 1e3 * (time.perf_counter() - t0) / args.steps
+        last_cs, last_pl = list(cs), np.array(pl_)     # the last step's results (the stock-reference check)
         te = torch.tensor([e2e_ms, e2r_ms], dtype=torch.float64, device=gdev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -517,6 +578,13 @@ def main():
             dev_by.setdefault(c.model.name, []).append(int(r.counters.digest))
         line["parity"] = {"points_checked": 108 * nshared,
                           "digest_mismatches": _count_mismatch(cfgs, digests, ccs, args.seeds, args.cpu_seeds)}
+        if not args.no_stock:
+            # the unmodified reference on this host, its CSV rows vs the device's (untimed leg)
+            rows = None
+            if e2e:
+                from paper_2602_03921_b200.sweep import csv_text as _csv
+                rows = lambda k: _csv(cfgs[:k], last_cs[:k], last_pl[:k])
+            line["stock_reference"] = stock_reference(args.stock_seconds, cfgs, rows)
         if not args.no_layer_step:
             line["layer_step"] = layer_step_section()
     print(json.dumps(line), flush=True)
