@@ -57,4 +57,16 @@ out["slowest_configs"] = [{"cfg": list(k), "ms": m, "recs": rc, "demanded": dm, 
                           for m, k, rc, dm in slow[:15]]
 out["all_configs"] = [{"cfg": list(k), "ms": m, "recs": rc, "demanded": dm} for m, k, rc, dm in slow]
 out["fastest_configs"] = [{"cfg": list(k), "ms": m, "recs": rc, "demanded": dm} for m, k, rc, dm in slow[-5:]]
+# occupancy: points in flight over the step (per SM group of each policy launch)
+t_end = max(r["t1"] for r in rows)
+span = (t_end - t00) / 1e6
+busy = sum((r["t1"] - r["t0"]) for r in rows) / 1e6
+slots = len(set(r["sm"] for r in rows)) * 12
+grid_t = np.linspace(0, span, 201)
+act = [sum(1 for r in rows if (r["t0"] - t00) / 1e6 <= t < (r["t1"] - t00) / 1e6) for t in grid_t]
+full = 0.9 * slots
+tail_start = next((grid_t[i] for i in range(len(act)) if i > 10 and act[i] < full), span)
+out["occupancy"] = {"span_ms": span, "warp_ms_busy": busy, "warp_slots": slots,
+                    "utilisation": busy / (span * slots), "tail_from_ms": tail_start,
+                    "active_points_at_pct": {str(p): act[int(p * 2)] for p in (10, 25, 50, 75, 90, 95, 99)}}
 print(json.dumps(out, indent=1, default=float))
