@@ -283,6 +283,33 @@ def rec_capacity(pk) -> tuple[int, int]:
     return 64 + pk.n_events * (6 + 12 * pk.experts) + rows * pk.top_k * 2, pk.n_events * pk.experts
 
 
+# Relative replay cost per demanded access of the common-path kernel by
+# eviction policy (ESIM_EV_* order: lru lfu lhu fld sb ls), a static property
+# of the kernels (LFU keeps access counts, LS the stale class): the concurrent
+# policy launches split the SMs by estimated work x this factor.
+POLICY_COST = (0.94, 0.98, 0.98, 1.0, 1.0, 1.0)
+
+
+def sm_shares(work, sms: int) -> list:
+    """SMs per concurrent launch in proportion to `work`, at least one each,
+    summing to exactly `sms` when there are at most `sms` launches (largest
+    remainder), so no SM idles and none is oversubscribed."""
+    tot = float(sum(work)) or 1.0
+    if len(work) > sms:
+        return [1] * len(work)
+    raw = [sms * w / tot for w in work]
+    out = [max(1, int(r)) for r in raw]
+    order = sorted(range(len(work)), key=lambda i: -(raw[i] - int(raw[i])))
+    k = 0
+    while sum(out) < sms:
+        out[order[k % len(order)]] += 1
+        k += 1
+    while sum(out) > sms:
+        j = max(range(len(out)), key=lambda i: out[i] - raw[i])
+        out[j] -= 1
+    return out
+
+
 class ReplayBatch:
     """A set of grid points staged on the device for (repeated) replay.
 
@@ -349,8 +376,8 @@ class ReplayBatch:
         # concurrent group launches split the SMs by estimated work (persistent
         # common-path launches: one CTA per SM, policies never share an SM)
         sms = _torch().cuda.get_device_properties(0).multi_processor_count
-        gw = [sum(tcost[i] for i in g) for g in self.groups]
-        self.group_ctas = [max(1, round(sms * w / max(1, sum(gw)))) for w in gw]
+        gw = [sum(tcost[i] for i in g) * POLICY_COST[self.ccfg[g[0]].eviction] for g in self.groups]
+        self.group_ctas = sm_shares(gw, sms)
         self.order = [i for g in self.groups for i in g]
         harr = (_abi.EsimConfig * n)(*[self.ccfg[i] for i in self.order])
         self.h_cfg = harr

@@ -558,15 +558,44 @@ extern "C" int esim_sweep_plan_create(const EsimConfig* cfg, int32_t n, const Es
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // relative replay cost per access by policy (ESIM_EV_* order; the kernels'
+        // own property: LFU keeps counts, LS the stale class) -- _device.POLICY_COST
+        static const double kPolicyCost[6] = {0.94, 0.98, 0.98, 1.0, 1.0, 1.0};
         std::vector<double> gw;
         double tw = 0;
         for (auto& gr : P->groups) {
             double w = 0;
             for (int i = gr.first; i < gr.second; i++) w += cost_of(order[i]);
+            const int ev = cfg[order[gr.first]].eviction;
+            w *= (ev >= 0 && ev < 6) ? kPolicyCost[ev] : 1.0;
             gw.push_back(w);
             tw += w;
         }
-        for (double w : gw) P->group_ctas.push_back(std::max(1, (int)std::lround(sms * w / (tw > 0 ? tw : 1))));
+        // shares summing to exactly the SM count (largest remainder, >= 1 each)
+        const int ng = (int)gw.size();
+        std::vector<double> raw(ng);
+        std::vector<int> sh(ng);
+        int tot = 0;
+        for (int g = 0; g < ng; g++) {
+            raw[g] = sms * gw[g] / (tw > 0 ? tw : 1);
+            sh[g] = std::max(1, (int)raw[g]);
+            tot += sh[g];
+        }
+        if (ng <= sms) {
+            std::vector<int> ord(ng);
+            for (int g = 0; g < ng; g++) ord[g] = g;
+            std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+                return raw[a] - (int)raw[a] > raw[b] - (int)raw[b];
+            });
+            for (int k = 0; tot < sms; k++, tot++) sh[ord[k % ng]]++;
+            while (tot > sms) {
+                int j = 0;
+                for (int g = 1; g < ng; g++) if (sh[g] - raw[g] > sh[j] - raw[j]) j = g;
+                sh[j]--;
+                tot--;
+            }
+        }
+        for (int g = 0; g < ng; g++) P->group_ctas.push_back(sh[g]);
     }
     P->order = order;
     P->caller_cfg.assign(cfg, cfg + n);
