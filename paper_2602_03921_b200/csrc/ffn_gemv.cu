@@ -41,7 +41,7 @@ constexpr int NT = GEMV_NT; // compute threads per CTA (+ one producer warp)
 #define GEMV_STAGES 4           // ring chunks in flight per CTA (two CTAs fit an SM)
 #endif
 #ifndef GEMV_PAIR_UNITS
-#define GEMV_PAIR_UNITS 148     // at most this many units: a CTA pair per unit
+#define GEMV_PAIR_UNITS -1      // at most this many units: a CTA pair per unit (-1: the device's SM count)
 #endif
 #ifndef GEMV_CHUNK
 #define GEMV_CHUNK 16384        // bytes per ring chunk (one bulk copy; holds whole w1 tiles)
@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(NT + 32) ffn_gemv_kernel(const __grid_constant
         cluster_wait();
     }
 }
+#undef GSTAMP
 
 template <int BITS, int NTOK>
 static size_t gemv_smem(int H) {
@@ -426,7 +427,14 @@ static cudaError_t launch(const GemvArgs& a, cudaStream_t st) {
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     const int units = a.n_exec * (a.I / 64);
     // fewer units than SMs: split each across a CTA pair (cluster), both SMs' worth of warps
-    const bool pair = units <= GEMV_PAIR_UNITS && (a.H / 64) % 2 == 0;
+    static int pair_units = -1;
+    if (pair_units < 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        pair_units = GEMV_PAIR_UNITS >= 0 ? GEMV_PAIR_UNITS : sms;
+    }
+    const bool pair = units <= pair_units && (a.H / 64) % 2 == 0;
     cudaLaunchConfig_t lc{};
     lc.blockDim = dim3(NT + 32);
     lc.dynamicSmemBytes = smem;
