@@ -256,18 +256,16 @@ def _config_prefix(cfg) -> str:
     hit = _CFG_PREFIX.get(id(cfg))
     if hit is not None and hit[0] is cfg:
         return hit[1]
-    p = None
-    if p is None:
-        import io
-        echo = cfg.echo()
-        vals = []
-        for key in sorted(echo):
-            v = echo[key]
-            vals.extend(v[sub] for sub in sorted(v)) if isinstance(v, dict) else vals.append(v)
-        buf = io.StringIO()
-        csv.writer(buf).writerow(vals)
-        p = buf.getvalue()[:-2] + ","
-        _CFG_PREFIX[id(cfg)] = (cfg, p)
+    import io
+    echo = cfg.echo()
+    vals = []
+    for key in sorted(echo):
+        v = echo[key]
+        vals.extend(v[sub] for sub in sorted(v)) if isinstance(v, dict) else vals.append(v)
+    buf = io.StringIO()
+    csv.writer(buf).writerow(vals)
+    p = buf.getvalue()[:-2] + ","
+    _CFG_PREFIX[id(cfg)] = (cfg, p)
     return p
 
 
